@@ -1,0 +1,337 @@
+"""Pins for the oracle's RNG and genetic operators (Alg. 1, §3.1, Table 3)
+and for end-to-end behaviour (planted recovery, brute-force agreement).
+CPU only."""
+import math
+
+import numpy as np
+import pytest
+
+from conftest import golden
+import workloads
+
+
+def _kats():
+    for line in open(golden("philox_kat.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        v = [int(x, 16) for x in line.split()]
+        yield v[:4], v[4:6], v[6:10]
+
+
+@pytest.mark.parametrize("ctr,key,out", list(_kats()))
+def test_philox_kat(orc, ctr, key, out):
+    assert list(orc.philox(ctr, key)) == out
+
+
+def test_canonicalize_invariants(orc):
+    rng = np.random.default_rng(1)
+    lab = rng.integers(0, 30, (200, 30)).astype(np.int32)
+    can = orc.canonicalize(lab)
+    assert np.array_equal(orc.canonicalize(can), can)          # idempotent
+    assert (can[:, 0] == 0).all()                              # first label 0
+    for p in range(200):
+        # each new label is exactly one more than the running max (contiguous)
+        mx = -1
+        for v in can[p]:
+            assert v <= mx + 1
+            mx = max(mx, v)
+        # same equivalence relation as the input
+        a, b = lab[p], can[p]
+        assert np.array_equal(a[:, None] == a[None, :], b[:, None] == b[None, :])
+
+
+def test_init_population_valid_and_uniform(orc):
+    N, P = 10, 20000
+    pop = orc.init_population(seed=7, N=N, P=P)
+    assert np.array_equal(orc.canonicalize(pop), pop)
+    # number of distinct labels of N uniform draws over N values:
+    # E[K] = N (1 - (1 - 1/N)^N)
+    K = pop.max(1) + 1
+    EK = N * (1 - (1 - 1 / N) ** N)
+    assert abs(K.mean() - EK) < 0.02
+    # distinct seeds / islands / offsets give different streams
+    assert not np.array_equal(orc.init_population(8, N, 50), pop[:50])
+    assert not np.array_equal(orc.init_population(7, N, 50, island=1), pop[:50])
+    assert np.array_equal(orc.init_population(7, N, 50, p_off=50), pop[50:100])
+
+
+def _copies(sel, P):
+    return np.bincount(sel, minlength=P)
+
+
+def test_sus_equal_fitness_each_once(orc):
+    """fitnesses [1,1,1,1], 4 pointers -> each selected exactly once."""
+    for seed in range(20):
+        _, sel = orc.select([1.0, 1.0, 1.0, 1.0], E=0, scaling=1, seed=seed)
+        assert list(_copies(sel, 4)) == [1, 1, 1, 1]
+
+
+def test_sus_three_to_one(orc):
+    """S:155 shape: fitness mass 3:1.  With equally spaced pointers the heavy
+    individual gets floor or ceil of its expected M*3/4 copies, and over many
+    spins exactly that expectation (Baker's SUS property)."""
+    L = [3.0, 1.0] * 4            # P = 8, M = 8 -> expected 1.5 and 0.5
+    tot = np.zeros(8)
+    for seed in range(400):
+        _, sel = orc.select(L, E=0, scaling=1, seed=seed)
+        c = _copies(sel, 8)
+        assert c.sum() == 8
+        assert all(v in (1, 2) for v in c[0::2]) and all(v in (0, 1) for v in c[1::2])
+        tot += c
+    assert abs(tot[0::2].mean() / 400 - 1.5) < 0.08
+
+
+def test_sus_one_holds_all_mass(orc):
+    """one individual holds all the fitness -> every parent is it."""
+    _, sel = orc.select([0.0, 0.0, 5.0, 0.0, 0.0, 0.0], E=0, scaling=1, seed=3)
+    assert (sel == 2).all()
+
+
+def test_sus_zero_fitness_uniform_fallback(orc):
+    """all-zero fitness falls back to uniform selection."""
+    tot = np.zeros(10)
+    for seed in range(300):
+        _, sel = orc.select(np.zeros(10), E=0, scaling=1, seed=seed)
+        tot += _copies(sel, 10)
+    assert tot.min() > 0.7 * tot.mean()
+
+
+def test_rank_scaling_order_only(orc):
+    """RANK scaling (Q9) depends on the order of L only."""
+    rng = np.random.default_rng(5)
+    L = rng.random(64)
+    o1, s1 = orc.select(L, E=4, scaling=0, seed=9)
+    o2, s2 = orc.select(np.exp(10 * L), E=4, scaling=0, seed=9)
+    assert np.array_equal(o1, o2) and np.array_equal(s1, s2)
+    # expected copies proportional to 1/sqrt(rank)
+    tot = np.zeros(64)
+    for seed in range(300):
+        o, s = orc.select(L, E=4, scaling=0, seed=seed)
+        tot += _copies(s, 64)
+    w = 1 / np.sqrt(np.arange(1, 65))
+    want = 60 * 300 * w / w.sum()
+    got = tot[o]
+    assert np.abs(got - want).max() < 0.05 * want.max() + 3
+
+
+def test_order_ties_lowest_index(orc):
+    o = orc.order([1.0, 2.0, 2.0, 0.5, 2.0])
+    assert list(o) == [1, 2, 4, 0, 3]
+
+
+def test_tournament_properties(orc):
+    L = np.array([5.0, 1.0])
+    worst = 0
+    n = 0
+    for seed in range(300):
+        _, sel = orc.select(L, E=0, selection=1, tour_k=2, seed=seed)
+        worst += (sel == 1).sum()
+        n += sel.size
+    assert abs(worst / n - 0.25) < 0.05          # both candidates worst w.p. 1/4
+    _, sel = orc.select(np.arange(16.0), E=0, selection=1, tour_k=1, seed=1)
+    assert sel.min() >= 0 and sel.max() < 16
+
+
+def test_mates_is_permutation(orc):
+    for M in (2, 10, 1000):
+        s = orc.mates(M, seed=4, gen=3)
+        assert np.array_equal(np.sort(s), np.arange(M))
+
+
+def _breed_setup(orc, N=12, P=20, seed=0):
+    rng = np.random.default_rng(seed)
+    pop = orc.canonicalize(rng.integers(0, 4, (P, N)).astype(np.int32))
+    C = np.eye(N)
+    for i in range(N):
+        for j in range(N):
+            if i != j:
+                C[i, j] = 0.3 if (i % 3) == (j % 3) else 0.0
+    L, top = orc.evaluate(C, pop)
+    return pop, L, top
+
+
+def test_breed_no_crossover_no_mutation_copies(orc):
+    pop, L, top = _breed_setup(orc)
+    P, E = pop.shape[0], 3
+    o, sel = orc.select(L, E=E, seed=2)
+    sig = orc.mates(len(sel), seed=2)
+    nxt = orc.breed(pop, top, o, E, sel, sig, p_c=0.0, p_m=0.0, p_kb=0.9, seed=2)
+    for e in range(E):
+        assert np.array_equal(nxt[e], pop[o[e]])
+    for k in range((P - E) // 2 + 1):
+        for c in range(2):
+            slot = E + 2 * k + c
+            if slot < P:
+                assert np.array_equal(nxt[slot], pop[sel[sig[2 * k + c]]])
+
+
+def test_breed_one_point_reduction(orc):
+    """with p_kb = 0 every crossover is classic one-point."""
+    pop, L, top = _breed_setup(orc, N=16, P=30, seed=1)
+    P, N, E = 30, 16, 0
+    o, sel = orc.select(L, E=E, seed=5)
+    sig = orc.mates(len(sel), seed=5)
+    nxt = orc.breed(pop, top, o, E, sel, sig, p_c=1.0, p_m=0.0, p_kb=0.0, seed=5)
+    for k in range(P // 2):
+        a, b = pop[sel[sig[2 * k]]], pop[sel[sig[2 * k + 1]]]
+        ok = False
+        for cut in range(1, N):
+            A = orc.canonicalize(np.concatenate([a[:cut], b[cut:]]))
+            B = orc.canonicalize(np.concatenate([b[:cut], a[cut:]]))
+            if np.array_equal(nxt[2 * k], A) and np.array_equal(nxt[2 * k + 1], B):
+                ok = True
+                break
+        assert ok
+
+
+def test_breed_identical_parents(orc):
+    """identical parents give offspring equal to the parents (both the
+    KB and the one-point path)."""
+    N, P = 14, 10
+    base = orc.canonicalize(np.array([0, 1, 0, 2, 1, 2, 3, 3, 0, 1, 4, 4, 2, 0], np.int32))
+    pop = np.tile(base, (P, 1))
+    L = np.ones(P)
+    top = np.full(P, 1, np.int32)
+    for pkb in (0.0, 1.0):
+        o, sel = orc.select(L, E=2, seed=3)
+        sig = orc.mates(len(sel), seed=3)
+        nxt = orc.breed(pop, top, o, 2, sel, sig, p_c=1.0, p_m=0.0, p_kb=pkb, seed=3)
+        assert (nxt == base).all()
+
+
+def test_breed_kb_transplant(orc):
+    """Q12 reconstruction: child A = a with b's top cluster moved to a
+    fresh cluster."""
+    N = 8
+    a = np.array([0, 0, 0, 0, 1, 1, 1, 1], np.int32)
+    b = np.array([0, 1, 0, 1, 0, 1, 0, 1], np.int32)
+    pop = np.stack([a, b])
+    top = np.array([1, 0], np.int32)     # a's top = cluster 1, b's top = cluster 0
+    nxt = orc.breed(pop, top, np.array([0, 1], np.int32), 0, np.array([0, 1], np.int32),
+                    np.array([0, 1], np.int32), p_c=1.0, p_m=0.0, p_kb=1.0, seed=1)
+    want_A = orc.canonicalize(np.where(b == 0, 8, a))
+    want_B = orc.canonicalize(np.where(a == 1, 8, b))
+    assert np.array_equal(nxt[0], want_A) and np.array_equal(nxt[1], want_B)
+
+
+def test_mutation_full_rate_redraws(orc):
+    """p_m = 1 replaces every gene with a uniform label: children become
+    (canonical) uniform random partitions."""
+    N, P = 10, 4000
+    pop = np.zeros((P, N), np.int32)
+    L = np.ones(P)
+    top = np.full(P, -1, np.int32)
+    o, sel = orc.select(L, E=0, seed=8)
+    sig = orc.mates(len(sel), seed=8)
+    nxt = orc.breed(pop, top, o, 0, sel, sig, p_c=0.0, p_m=1.0, p_kb=0.0, seed=8)
+    K = nxt.max(1) + 1
+    EK = N * (1 - (1 - 1 / N) ** N)
+    assert abs(K.mean() - EK) < 0.05
+
+
+def test_mutation_rate_binomial(orc):
+    """p_m = 0.1 over 18 genes.  Starting from the all-distinct
+    partition, a gene is unaffected iff it was not mutated, so the number of
+    genes whose label changed is ~ mutated count * (1 - 1/N)."""
+    N, P = 18, 6000
+    base = np.arange(N, dtype=np.int32)
+    pop = np.tile(base, (P, 1))
+    o, sel = orc.select(np.ones(P), E=0, seed=9)
+    sig = orc.mates(len(sel), seed=9)
+    nxt = orc.breed(pop, np.full(P, -1, np.int32), o, 0, sel, sig, p_c=0.0, p_m=0.1,
+                    p_kb=0.0, seed=9)
+    # a mutated gene joins an existing singleton's label (prob (N-1)/N) ->
+    # the number of clusters drops by the number of effective merges
+    merges = N - (nxt.max(1) + 1)
+    assert 0.8 * 1.8 * (N - 1) / N * 0.85 < merges.mean() < 1.8
+
+
+def test_run_elitism_monotone_and_recovery_C1(orc):
+    """C1 (BASELINE configs[0]): N=18, 3 planted clusters, P=128, 100
+    generations -> the planted partition is recovered, best L never drops."""
+    X, planted = workloads.noh_returns(workloads.CONFIGS["C1"])
+    C = orc.pearson(X)
+    Lp, _ = orc.log_likelihood(C, planted)
+    rec = 0
+    for seed in range(1, 6):
+        pr = orc.default_params(pop=128, max_gens=100, tol=-1.0, seed=seed, p_m=0.1)
+        r = orc.run(C, pr)
+        h = r["history"]
+        assert all(b >= a for a, b in zip(h, h[1:]))
+        assert r["gens_run"] == 100
+        assert r["best_L"] <= Lp + 1e-9 or not np.array_equal(r["best_labels"], planted)
+        rec += np.array_equal(r["best_labels"], planted)
+    assert rec >= 4
+
+
+def test_run_matches_brute_force_small(orc):
+    """SPEC acceptance 2 shape: GA best == exhaustive max on small
+    planted/noise instances, never above it."""
+    hits = 0
+    for s in range(6):
+        spec = workloads.PlantedSpec((3, 2), (0.8, 0.7), 60, 3000 + s, singletons=3)
+        X, _ = workloads.noh_returns(spec)
+        C = orc.pearson(X)
+        _, Lb, _ = orc.brute_force(C)
+        r = orc.run(C, orc.default_params(pop=256, max_gens=60, seed=s + 1))
+        assert r["best_L"] <= Lb + 1e-9
+        hits += abs(r["best_L"] - Lb) <= 1e-9 * max(1.0, Lb)
+    assert hits >= 5
+
+
+def test_run_stall_termination(orc):
+    C = np.eye(8)
+    r = orc.run(C, orc.default_params(pop=32, max_gens=400, tol=1e-5, stall_gens=50, seed=3))
+    assert r["reason"] == 1 and r["gens_run"] == 51 and r["best_L"] == 0.0
+
+
+def test_islands_migration_keeps_global_best(orc):
+    X, planted = workloads.noh_returns(workloads.CONFIGS["C1"])
+    C = orc.pearson(X)
+    pr = orc.default_params(pop=64, max_gens=40, tol=-1.0, seed=11, n_islands=3,
+                            migrate_every=5, migrants=4)
+    r = orc.run(C, pr)
+    h = r["history"]
+    assert all(b >= a for a, b in zip(h, h[1:]))
+    assert r["gens_run"] == 40
+
+
+def test_migrate_rule(orc):
+    N = 4
+    pops = [np.full((5, N), g, np.int32) for g in range(2)]
+    for g in range(2):
+        pops[g][:, 0] = np.arange(5)
+    Ls = [np.array([1.0, 5.0, 3.0, 2.0, 0.5]), np.array([4.0, 0.1, 5.0, 0.2, 0.3])]
+    tops = [np.zeros(5, np.int32), np.ones(5, np.int32)]
+    p, L, t = orc.migrate(pops, Ls, tops, migrants=2)
+    # global top-2 by (L desc, island asc, rank asc): (5.0, isl0, idx1), (5.0, isl1, idx2)
+    # island 0 worst two: idx4 (0.5) then idx0 (1.0)
+    assert L[0][4] == 5.0 and p[0][4][0] == 1 and p[0][4][1] == 0
+    assert L[0][0] == 5.0 and p[0][0][0] == 2 and p[0][0][1] == 1
+    # island 1 worst two: idx1 (0.1), idx3 (0.2)
+    assert L[1][1] == 5.0 and p[1][1][1] == 0 and t[1][1] == 0
+    assert L[1][3] == 5.0 and p[1][3][1] == 1 and t[1][3] == 1
+
+
+def test_pearson_vs_numpy(orc):
+    X, _ = workloads.noh_returns(workloads.CONFIGS["C3"])
+    C = orc.pearson(X)
+    np.testing.assert_allclose(C, np.corrcoef(X, rowvar=False), rtol=0, atol=1e-12)
+    assert np.array_equal(C, C.T) and (np.diag(C) == 1.0).all()
+    assert np.abs(C).max() <= 1.0 + 1e-12
+
+
+def test_pearson_zero_variance(orc):
+    X = np.random.default_rng(0).standard_normal((50, 4))
+    X[:, 2] = 3.0
+    with pytest.raises(ValueError):
+        orc.pearson(X)
+
+
+def test_noh_planted_correlation(orc):
+    """within-cluster population correlation is g^2."""
+    spec = workloads.PlantedSpec((30,), (0.8,), 20000, 5, shuffle=False)
+    X, _ = workloads.noh_returns(spec)
+    C = orc.pearson(X)
+    off = C[~np.eye(30, dtype=bool)]
+    assert abs(off.mean() - 0.64) < 0.01
