@@ -1,0 +1,233 @@
+/*
+ * pga.h — C ABI of the B200-native Giada–Marsili parallel genetic algorithm
+ * (Hendricks, Gebbie & Wilcox, arXiv:1403.4099).
+ *
+ * Citation keys: P:n = PAPER.md line n; S:n = SPEC.md line n; Q<k> = the
+ * reading listed in DESIGN.md §3.  Every entry point below cites the passage
+ * that defines the operation it computes.
+ *
+ * Conventions (all entry points):
+ *  - Return 0 (PGA_OK) or a negative PGA_E* code.  Nothing throws, nothing
+ *    calls exit().  pga_last_error() gives a thread-local message.
+ *  - Pointers are HOST pointers unless the name ends in _device / the
+ *    argument is documented as device memory.  Caller buffers are borrowed
+ *    only for the duration of the call; outputs are caller-allocated.
+ *  - Labels at this boundary are int32 cluster indices 1..N (Eq. 9, P:194-198,
+ *    K = N) unless documented as 0-based uint16 device labels.
+ *  - A pga_ctx is bound to one CUDA device (one island of the island model)
+ *    and must be used by one host thread at a time.  Any CUDA failure returns
+ *    PGA_EDEVICE; the ctx must then be destroyed.
+ *  - There is no CPU fallback: without a CUDA device every call that needs
+ *    one returns PGA_EDEVICE.  Argument validation happens first, so invalid
+ *    arguments return PGA_EINVAL even without a device.
+ */
+#ifndef PGA_H
+#define PGA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    PGA_OK = 0,
+    PGA_EINVAL = -1,    /* invalid argument (message says which) */
+    PGA_ENOMEM = -2,    /* device or pinned allocation failed */
+    PGA_EDEVICE = -3,   /* CUDA error or no device */
+    PGA_ENUMERIC = -4,  /* zero-variance / non-finite column in pga_correlation */
+    PGA_ESTATE = -5     /* call not valid in the ctx's current state */
+};
+
+enum { PGA_SEL_SUS = 0, PGA_SEL_TOURNAMENT = 1 };   /* P:128; Q10 */
+enum { PGA_SCALE_RANK = 0, PGA_SCALE_NONE = 1 };    /* Alg. 1; Q9 */
+enum { PGA_REASON_MAX_GENS = 0, PGA_REASON_STALLED = 1 };
+
+typedef struct pga_ctx pga_ctx;
+
+/* GA parameters.  Defaults (pga_params_default) are Table 3. */
+typedef struct {
+    int32_t  pop_size;      /* individuals on THIS island (this GPU); >= 2, default 1000 */
+    int32_t  elite;         /* elites copied unchanged, 0 <= elite < pop_size, default 10 */
+    double   p_crossover;   /* per pair (Q11), default 0.9 */
+    double   p_mutation;    /* per gene, random replacement (Q13), default 0.1 */
+    double   p_kb;          /* share of crossovers that are knowledge-based (Q11/Q12), default 0.9 */
+    double   tol;           /* stall tolerance on best L (Q16), default 1e-5; < 0 disables */
+    int32_t  stall_gens;    /* default 50 */
+    int32_t  max_gens;      /* default 400 */
+    int32_t  selection;     /* PGA_SEL_SUS (default) or PGA_SEL_TOURNAMENT */
+    int32_t  tournament_k;  /* 1..4, default 2 */
+    int32_t  scaling;       /* PGA_SCALE_RANK (default) or PGA_SCALE_NONE */
+    int32_t  device;        /* CUDA device ordinal, default 0 */
+    int32_t  island;        /* this island's id, 0 <= island < n_islands */
+    int32_t  n_islands;     /* islands in the run (1 = single population) */
+    int32_t  migrate_every; /* migration period M in generations (Q21), default 10 */
+    int32_t  migrants;      /* E_m migrants per island per migration, default 10 */
+    uint64_t seed;          /* Philox key (Q18) */
+} pga_params;
+
+/* Fill *out with the Table 3 defaults.  Host only; no device needed. */
+int pga_params_default(pga_params *out);
+
+/* Create a context on p->device: copies the N x N correlation matrix C
+ * (row-major fp64, host) to the device and allocates the population.
+ * C must be exactly symmetric, |C_ii - 1| <= 1e-12, |C_ij| <= 1 + 1e-9,
+ * finite (Eq. 7; reading Q4); otherwise PGA_EINVAL.  2 <= N <= 16384.
+ * The ctx owns its copy of C; the caller's buffer may be freed on return. */
+int pga_create(const double *C, int32_t N, const pga_params *p, pga_ctx **out);
+
+/* Free everything owned by ctx.  NULL-safe. */
+void pga_destroy(pga_ctx *ctx);
+
+/* Thread-local message describing the last failure on this thread. */
+const char *pga_last_error(void);
+
+/* ---------------------------------------------------------------------
+ * Fitness: Eq. 5 (n_s), Eq. 6 (c_s), Eq. 8 (L_c), with readings
+ * Q1 (natural log), Q2 (c_s <= n_s contributes 0), Q3 (c_s clamped to
+ * n_s^2 - 1e-9).
+ * ------------------------------------------------------------------- */
+
+/* labels: host int32 [P][N] row-major, values 1..N (any labelling, not
+ * necessarily canonical).  out_L: host fp64 [P].  Any P >= 1 (processed in
+ * chunks of the ctx's population capacity).  Values outside 1..N -> PGA_EINVAL. */
+int pga_evaluate(pga_ctx *ctx, const int32_t *labels, int64_t P, double *out_L);
+
+/* Device fast path, stream-ordered on `stream` (cudaStream_t, NULL = the
+ * ctx's stream):  labels_dev: device uint16 [P][N] row-major, 0-based values
+ * < N (unchecked);  L_dev: device fp64 [P];  top_dev: device uint16 [P] or
+ * NULL — label of the cluster with the largest Eq. 8 summand, 0xFFFF if none.
+ * 1 <= P <= the ctx's capacity (pop_size rounded up to 64). */
+int pga_evaluate_device(pga_ctx *ctx, const uint16_t *labels_dev, int64_t P,
+                        double *L_dev, uint16_t *top_dev, void *stream);
+
+/* ---------------------------------------------------------------------
+ * Genetic algorithm (Alg. 1; operators §3.1; DESIGN.md
+ * §3 "GA step" fixes every unspecified detail).  The population stays
+ * resident on the device; each call below is stream-ordered and the whole
+ * generation runs in this library's kernels.
+ * ------------------------------------------------------------------- */
+
+/* Create the initial population from `seed` (Alg. 1 "Create initial
+ * population"; Q8) and reset generation, stall and best state. */
+int pga_init(pga_ctx *ctx, uint64_t seed);
+
+/* Phase A of one generation: evaluate fitness of all individuals, then
+ * (unless this is a migration generation of a multi-island run) update the
+ * state and statistics and the termination test (Alg. 1).
+ * *is_migration (may be NULL) is set to 1 when the caller must exchange
+ * migrants (pga_export_migrants / all-gather / pga_import_migrants) before
+ * phase B.  Asynchronous: does not wait for the device. */
+int pga_gen_evaluate(pga_ctx *ctx, int32_t *is_migration);
+
+/* Phase B: isolate fittest, elitism, scaling, selection, crossover,
+ * mutation, replacement (Alg. 1), then advance the generation.
+ * A no-op on the device once the termination flag is set. */
+int pga_gen_breed(pga_ctx *ctx);
+
+/* One full generation on a single island (phase A + phase B).  *done is set
+ * to 1 if the termination criteria are met (this synchronises the stream).
+ * PGA_ESTATE if no population exists or n_islands > 1. */
+int pga_generation(pga_ctx *ctx, int32_t *done);
+
+/* Whole GA run on a single island: pga_init(seed), then generations until
+ * termination or `gens` generations (gens <= 0: max_gens).  Outputs (host):
+ * best_labels [N] canonical 1-based, best_L, gens_run, reason
+ * (PGA_REASON_*).  Any output pointer may be NULL. */
+int pga_run(pga_ctx *ctx, int32_t gens, uint64_t seed, int32_t *best_labels,
+            double *best_L, int32_t *gens_run, int32_t *reason);
+
+/* Poll the device state (synchronises the stream).  Any pointer may be NULL.
+ * best_labels: host int32 [N], 1-based canonical labels of the best
+ * individual seen so far. */
+int pga_get_state(pga_ctx *ctx, int32_t *generation, int32_t *done, int32_t *reason,
+                  double *best_L, double *mean_L, int32_t *best_labels);
+
+/* Per-generation best L, host fp64 [n] for generations 0..n-1 (n <= gens run). */
+int pga_get_history(pga_ctx *ctx, double *best_L, int32_t n);
+
+/* Copy the population out (host int32 [pop_size][N], 1-based) and, if L is
+ * not NULL, the fitness of the last evaluation (host fp64 [pop_size]). */
+int pga_get_population(pga_ctx *ctx, int32_t *labels, double *L);
+
+/* Replace the population (host int32 [pop_size][N], values 1..N; stored
+ * canonicalised) and set the generation counter (resume, S:N/A). */
+int pga_set_population(pga_ctx *ctx, const int32_t *labels, int32_t generation);
+
+/* ---------------------------------------------------------------------
+ * Island migration (P:147 ZLL2012; reading Q21).  A record
+ * is {fp64 L, uint16 top, uint16 labels[N]} padded to pga_migrant_bytes().
+ * ------------------------------------------------------------------- */
+
+/* Bytes of one island's send buffer (migrants records). */
+int pga_migrant_bytes(pga_ctx *ctx, int64_t *bytes);
+
+/* After pga_gen_evaluate reported a migration generation: write this
+ * island's top-`migrants` records (L desc, index asc) to dev_send (device,
+ * pga_migrant_bytes()).  Stream-ordered. */
+int pga_export_migrants(pga_ctx *ctx, void *dev_send);
+
+/* dev_recv: device buffer holding n_islands send buffers back to back in
+ * island order (an all-gather).  The global top-`migrants` under (L desc,
+ * island asc, rank asc) replace this island's worst (L asc, index desc); then
+ * the statistics / termination step of phase A runs.  Stream-ordered. */
+int pga_import_migrants(pga_ctx *ctx, const void *dev_recv, int32_t n_islands);
+
+/* The ctx's cudaStream_t (for ordering collectives with the library). */
+int pga_get_stream(pga_ctx *ctx, void **stream);
+
+/* ---------------------------------------------------------------------
+ * Eq. 7, Pearson correlation with per-column centring (Q5):
+ * returns: host fp64 [T][N] row-major (T observations of N assets).
+ * C_out: host fp64 [N][N]; exactly symmetric, unit diagonal.  Zero-variance
+ * or non-finite column -> PGA_ENUMERIC.  T >= 2, N >= 1.  Uses `device`.
+ * ------------------------------------------------------------------- */
+int pga_correlation(const double *returns, int32_t T, int32_t N, double *C_out, int32_t device);
+
+/* Device variant, stream-ordered: X_dev [T][N], C_dev [N][N] (device fp64).
+ * Zero variance is reported through *status_dev (device int32, set to
+ * nonzero) instead of a return code. */
+int pga_correlation_device(const double *X_dev, int32_t T, int32_t N, double *C_dev,
+                           int32_t *status_dev, void *stream);
+
+/* ---------------------------------------------------------------------
+ * Operator test hooks: run ONE operator of DESIGN.md §3's GA step on
+ * explicit host inputs, so the CUDA kernels can be compared bit-for-bit with
+ * the oracle given identical inputs.  All arrays are host memory; labels
+ * here are 0-based int32; `gen`/`island` select the Philox stream.
+ * ------------------------------------------------------------------- */
+
+/* Isolate fittest + scaling + selection: order_out [P] (indices
+ * by L desc, index asc) and sel_out [M] parents, M = 2*ceil((P-elite)/2). */
+int pga_op_select(const double *L, int64_t P, const pga_params *p, int32_t gen,
+                  int32_t island, int32_t *order_out, int32_t *sel_out);
+
+/* Mate pairing: sigma_out [M], the slot permutation (Philox keys, ties by slot). */
+int pga_op_mates(int64_t M, const pga_params *p, int32_t gen, int32_t island,
+                 int32_t *sigma_out);
+
+/* Elitism + crossover + mutation + canonicalisation + replacement
+ * (P:130-136): pop [P][N] canonical 0-based parents, top [P] (-1 = none),
+ * order [P], sel [M], sigma [M]; next_out [P][N] 0-based canonical.
+ * p_off = global index of slot 0 (island offset). */
+int pga_op_breed(const int32_t *pop, const int32_t *top, const int32_t *order,
+                 int64_t P, int32_t N, const int32_t *sel, const int32_t *sigma,
+                 const pga_params *p, int32_t gen, int32_t island, int64_t p_off,
+                 int32_t *next_out);
+
+/* First-occurrence canonical form (Q7), in place, labels [P][N] 0-based < 2N. */
+int pga_op_canonicalize(int32_t *labels, int64_t P, int32_t N, int32_t device);
+
+/* Initial population (Q8): out [P][N] 0-based canonical. */
+int pga_op_init(uint64_t seed, int32_t N, int64_t P, int64_t p_off, int32_t island,
+                int32_t device, int32_t *out);
+
+/* Number of this library's kernel launches issued so far in this process
+ * (for the bench's gpu_launches claim). */
+int64_t pga_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PGA_H */

@@ -1,0 +1,288 @@
+"""Thin ctypes binding of libpga.so (include/pga.h) — argument marshalling only.
+
+Every function here has the name of the C entry point it wraps and does no
+arithmetic of the method: it converts numpy / torch arguments to pointers,
+calls the library and turns negative return codes into ``PgaError``.  There
+is no CPU fallback: if libpga.so is missing or no CUDA device exists the
+calls fail loudly.
+"""
+from __future__ import annotations
+
+import ctypes as ct
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpga.so")
+
+PGA_OK, PGA_EINVAL, PGA_ENOMEM, PGA_EDEVICE, PGA_ENUMERIC, PGA_ESTATE = 0, -1, -2, -3, -4, -5
+PGA_SEL_SUS, PGA_SEL_TOURNAMENT = 0, 1
+PGA_SCALE_RANK, PGA_SCALE_NONE = 0, 1
+_CODES = {-1: "PGA_EINVAL", -2: "PGA_ENOMEM", -3: "PGA_EDEVICE", -4: "PGA_ENUMERIC", -5: "PGA_ESTATE"}
+
+
+class PgaError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__("%s: %s" % (_CODES.get(code, code), msg))
+        self.code = code
+
+
+class pga_params(ct.Structure):
+    _fields_ = [
+        ("pop_size", ct.c_int32), ("elite", ct.c_int32), ("p_crossover", ct.c_double),
+        ("p_mutation", ct.c_double), ("p_kb", ct.c_double), ("tol", ct.c_double),
+        ("stall_gens", ct.c_int32), ("max_gens", ct.c_int32), ("selection", ct.c_int32),
+        ("tournament_k", ct.c_int32), ("scaling", ct.c_int32), ("device", ct.c_int32),
+        ("island", ct.c_int32), ("n_islands", ct.c_int32), ("migrate_every", ct.c_int32),
+        ("migrants", ct.c_int32), ("seed", ct.c_uint64),
+    ]
+
+
+_lib = None
+
+_SIGS = {
+    "pga_params_default": (ct.c_int, [ct.c_void_p]),
+    "pga_create": (ct.c_int, [ct.c_void_p, ct.c_int32, ct.c_void_p, ct.c_void_p]),
+    "pga_destroy": (None, [ct.c_void_p]),
+    "pga_last_error": (ct.c_char_p, []),
+    "pga_evaluate": (ct.c_int, [ct.c_void_p, ct.c_void_p, ct.c_int64, ct.c_void_p]),
+    "pga_evaluate_device": (ct.c_int, [ct.c_void_p, ct.c_void_p, ct.c_int64, ct.c_void_p,
+                                       ct.c_void_p, ct.c_void_p]),
+    "pga_init": (ct.c_int, [ct.c_void_p, ct.c_uint64]),
+    "pga_gen_evaluate": (ct.c_int, [ct.c_void_p, ct.c_void_p]),
+    "pga_gen_breed": (ct.c_int, [ct.c_void_p]),
+    "pga_generation": (ct.c_int, [ct.c_void_p, ct.c_void_p]),
+    "pga_run": (ct.c_int, [ct.c_void_p, ct.c_int32, ct.c_uint64, ct.c_void_p, ct.c_void_p,
+                           ct.c_void_p, ct.c_void_p]),
+    "pga_get_state": (ct.c_int, [ct.c_void_p] + [ct.c_void_p] * 6),
+    "pga_get_history": (ct.c_int, [ct.c_void_p, ct.c_void_p, ct.c_int32]),
+    "pga_get_population": (ct.c_int, [ct.c_void_p, ct.c_void_p, ct.c_void_p]),
+    "pga_set_population": (ct.c_int, [ct.c_void_p, ct.c_void_p, ct.c_int32]),
+    "pga_migrant_bytes": (ct.c_int, [ct.c_void_p, ct.c_void_p]),
+    "pga_export_migrants": (ct.c_int, [ct.c_void_p, ct.c_void_p]),
+    "pga_import_migrants": (ct.c_int, [ct.c_void_p, ct.c_void_p, ct.c_int32]),
+    "pga_get_stream": (ct.c_int, [ct.c_void_p, ct.c_void_p]),
+    "pga_correlation": (ct.c_int, [ct.c_void_p, ct.c_int32, ct.c_int32, ct.c_void_p, ct.c_int32]),
+    "pga_correlation_device": (ct.c_int, [ct.c_void_p, ct.c_int32, ct.c_int32, ct.c_void_p,
+                                          ct.c_void_p, ct.c_void_p]),
+    "pga_op_select": (ct.c_int, [ct.c_void_p, ct.c_int64, ct.c_void_p, ct.c_int32, ct.c_int32,
+                                 ct.c_void_p, ct.c_void_p]),
+    "pga_op_mates": (ct.c_int, [ct.c_int64, ct.c_void_p, ct.c_int32, ct.c_int32, ct.c_void_p]),
+    "pga_op_breed": (ct.c_int, [ct.c_void_p, ct.c_void_p, ct.c_void_p, ct.c_int64, ct.c_int32,
+                                ct.c_void_p, ct.c_void_p, ct.c_void_p, ct.c_int32, ct.c_int32,
+                                ct.c_int64, ct.c_void_p]),
+    "pga_op_canonicalize": (ct.c_int, [ct.c_void_p, ct.c_int64, ct.c_int32, ct.c_int32]),
+    "pga_op_init": (ct.c_int, [ct.c_uint64, ct.c_int32, ct.c_int64, ct.c_int64, ct.c_int32,
+                               ct.c_int32, ct.c_void_p]),
+    "pga_launch_count": (ct.c_int64, []),
+}
+
+
+def lib():
+    """Load libpga.so (no fallback: raises if it is missing)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError("libpga.so not built: run `python -m paper_1403_4099_b200.build` "
+                              "(there is no CPU fallback)")
+        l = ct.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(l, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = l
+    return _lib
+
+
+def _check(rc):
+    if rc != PGA_OK:
+        raise PgaError(rc, lib().pga_last_error().decode())
+    return rc
+
+
+def _p(a):
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data_as(ct.c_void_p)
+    if hasattr(a, "data_ptr"):  # torch tensor (device pointer)
+        return ct.c_void_p(a.data_ptr())
+    return a
+
+
+def _c(a, dt):
+    return np.ascontiguousarray(a, dtype=dt)
+
+
+def pga_params_default(**kw) -> pga_params:
+    p = pga_params()
+    _check(lib().pga_params_default(ct.byref(p)))
+    for k, v in kw.items():
+        if not hasattr(p, k):
+            raise AttributeError(k)
+        setattr(p, k, v)
+    return p
+
+
+def pga_create(C, params: pga_params):
+    C = _c(C, np.float64)
+    ctx = ct.c_void_p()
+    _check(lib().pga_create(_p(C), C.shape[0], ct.byref(params), ct.byref(ctx)))
+    return ctx
+
+
+def pga_destroy(ctx):
+    lib().pga_destroy(ctx)
+
+
+def pga_evaluate(ctx, labels_1based) -> np.ndarray:
+    lab = _c(labels_1based, np.int32)
+    if lab.ndim == 1:
+        lab = lab[None, :]
+    L = np.zeros(lab.shape[0], np.float64)
+    _check(lib().pga_evaluate(ctx, _p(lab), lab.shape[0], _p(L)))
+    return L
+
+
+def pga_evaluate_device(ctx, labels_dev, L_dev, top_dev=None, stream=None):
+    """labels_dev: torch uint16-compatible (int16) CUDA tensor [P][N] 0-based."""
+    P = labels_dev.shape[0]
+    _check(lib().pga_evaluate_device(ctx, _p(labels_dev), P, _p(L_dev), _p(top_dev),
+                                     None if stream is None else ct.c_void_p(stream)))
+
+
+def pga_init(ctx, seed: int):
+    _check(lib().pga_init(ctx, seed))
+
+
+def pga_gen_evaluate(ctx) -> bool:
+    m = ct.c_int32(0)
+    _check(lib().pga_gen_evaluate(ctx, ct.byref(m)))
+    return bool(m.value)
+
+
+def pga_gen_breed(ctx):
+    _check(lib().pga_gen_breed(ctx))
+
+
+def pga_generation(ctx) -> bool:
+    d = ct.c_int32(0)
+    _check(lib().pga_generation(ctx, ct.byref(d)))
+    return bool(d.value)
+
+
+def pga_run(ctx, gens: int, seed: int, N: int):
+    best = np.zeros(N, np.int32)
+    L = ct.c_double(0)
+    g = ct.c_int32(0)
+    r = ct.c_int32(0)
+    _check(lib().pga_run(ctx, gens, seed, _p(best), ct.byref(L), ct.byref(g), ct.byref(r)))
+    return dict(best_labels=best, best_L=L.value, gens_run=g.value, reason=r.value)
+
+
+def pga_get_state(ctx, N: int):
+    gen, done, reason = ct.c_int32(), ct.c_int32(), ct.c_int32()
+    best, mean = ct.c_double(), ct.c_double()
+    lab = np.zeros(N, np.int32)
+    _check(lib().pga_get_state(ctx, ct.byref(gen), ct.byref(done), ct.byref(reason),
+                               ct.byref(best), ct.byref(mean), _p(lab)))
+    return dict(generation=gen.value, done=done.value, reason=reason.value, best_L=best.value,
+                mean_L=mean.value, best_labels=lab)
+
+
+def pga_get_history(ctx, n: int) -> np.ndarray:
+    h = np.zeros(n, np.float64)
+    _check(lib().pga_get_history(ctx, _p(h), n))
+    return h
+
+
+def pga_get_population(ctx, P: int, N: int):
+    lab = np.zeros((P, N), np.int32)
+    L = np.zeros(P, np.float64)
+    _check(lib().pga_get_population(ctx, _p(lab), _p(L)))
+    return lab, L
+
+
+def pga_set_population(ctx, labels_1based, generation: int = 0):
+    lab = _c(labels_1based, np.int32)
+    _check(lib().pga_set_population(ctx, _p(lab), generation))
+
+
+def pga_migrant_bytes(ctx) -> int:
+    b = ct.c_int64(0)
+    _check(lib().pga_migrant_bytes(ctx, ct.byref(b)))
+    return b.value
+
+
+def pga_export_migrants(ctx, dev_send):
+    _check(lib().pga_export_migrants(ctx, _p(dev_send)))
+
+
+def pga_import_migrants(ctx, dev_recv, n_islands: int):
+    _check(lib().pga_import_migrants(ctx, _p(dev_recv), n_islands))
+
+
+def pga_get_stream(ctx) -> int:
+    s = ct.c_void_p()
+    _check(lib().pga_get_stream(ctx, ct.byref(s)))
+    return s.value or 0
+
+
+def pga_correlation(returns, device: int = 0) -> np.ndarray:
+    X = _c(returns, np.float64)
+    T, N = X.shape
+    C = np.zeros((N, N), np.float64)
+    _check(lib().pga_correlation(_p(X), T, N, _p(C), device))
+    return C
+
+
+def pga_correlation_device(X_dev, C_dev, status_dev, stream=None):
+    T, N = X_dev.shape
+    _check(lib().pga_correlation_device(_p(X_dev), T, N, _p(C_dev), _p(status_dev),
+                                        None if stream is None else ct.c_void_p(stream)))
+
+
+def pga_op_select(L, params: pga_params, gen: int = 0, island: int = 0):
+    L = _c(L, np.float64)
+    P = L.shape[0]
+    M = 2 * ((P - params.elite + 1) // 2)
+    order = np.zeros(P, np.int32)
+    sel = np.zeros(M, np.int32)
+    _check(lib().pga_op_select(_p(L), P, ct.byref(params), gen, island, _p(order), _p(sel)))
+    return order, sel
+
+
+def pga_op_mates(M: int, params: pga_params, gen: int = 0, island: int = 0):
+    sigma = np.zeros(M, np.int32)
+    _check(lib().pga_op_mates(M, ct.byref(params), gen, island, _p(sigma)))
+    return sigma
+
+
+def pga_op_breed(pop, top, order, sel, sigma, params: pga_params, gen=0, island=0, p_off=0):
+    pop = _c(pop, np.int32)
+    P, N = pop.shape
+    nxt = np.zeros_like(pop)
+    _check(lib().pga_op_breed(_p(pop), _p(_c(top, np.int32)), _p(_c(order, np.int32)), P, N,
+                              _p(_c(sel, np.int32)), _p(_c(sigma, np.int32)), ct.byref(params),
+                              gen, island, p_off, _p(nxt)))
+    return nxt
+
+
+def pga_op_canonicalize(labels, device: int = 0):
+    lab = np.array(labels, dtype=np.int32, copy=True, order="C")
+    two = lab.ndim == 2
+    if not two:
+        lab = lab[None, :]
+    _check(lib().pga_op_canonicalize(_p(lab), lab.shape[0], lab.shape[1], device))
+    return lab if two else lab[0]
+
+
+def pga_op_init(seed: int, N: int, P: int, p_off: int = 0, island: int = 0, device: int = 0):
+    out = np.zeros((P, N), np.int32)
+    _check(lib().pga_op_init(seed, N, P, p_off, island, device, _p(out)))
+    return out
+
+
+def pga_launch_count() -> int:
+    return lib().pga_launch_count()

@@ -1,0 +1,736 @@
+// api.cu — the C ABI declared in include/pga.h.  Argument validation, the
+// per-island runtime (buffers, stream, CUDA graph of one generation) and the
+// host<->device marshalling.  Every step of the method runs in the kernels of
+// fitness.cu / ga.cu / corr.cu; nothing here computes on the host beyond
+// label base conversion (1-based <-> 0-based) at the boundary.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "pga_internal.cuh"
+
+namespace pga {
+
+static thread_local std::string g_err;
+static std::atomic<int64_t> g_launches{0};
+
+void set_error(const std::string &m) { g_err = m; }
+int fail(int code, const std::string &m) {
+    g_err = m;
+    return code;
+}
+int cuda_fail(cudaError_t e, const char *what) {
+    g_err = std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e);
+    return PGA_EDEVICE;
+}
+void count_launch(int n) { g_launches += n; }
+
+// declared in ga.cu / fitness.cu
+int launch_init_raw(uint64_t seed, int N, int ldn, int64_t P, int64_t Pcap, int64_t p_off,
+                    uint32_t island, uint16_t *CM, uint16_t *GM, int32_t *out32, cudaStream_t s);
+int run_select_ops(const double *L, int64_t P, const pga_params &p, int32_t gen, int32_t island,
+                   int32_t *order, int32_t *sel, uint64_t *keys_in, uint64_t *keys_out,
+                   int32_t *idx_in, uint64_t *q, uint64_t *prefix, void *tmp, size_t tmp_bytes,
+                   const int32_t *done, cudaStream_t s, const int32_t *gen_ptr, bool sorted);
+int run_mates(int64_t M, const pga_params &p, int32_t gen, int32_t island, uint32_t *k_in,
+              uint32_t *k_out, int32_t *m_in, int32_t *sigma, void *tmp, size_t tmp_bytes,
+              const int32_t *done, cudaStream_t s, const int32_t *gen_ptr);
+int launch_breed_hook(const int32_t *pop, const int32_t *top, const int32_t *order, int64_t P,
+                      int N, const int32_t *sel, const int32_t *sigma, const pga_params &p,
+                      int32_t gen, int32_t island, int64_t p_off, int32_t *next, cudaStream_t s);
+int launch_set_pop(pga_ctx *c, const int32_t *lab32, int par, cudaStream_t s);
+
+static int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+static int check_params(const pga_params *p) {
+    if (!p) return fail(PGA_EINVAL, "params is NULL");
+    if (p->pop_size < 2) return fail(PGA_EINVAL, "pop_size must be >= 2 (S:113)");
+    if (p->pop_size > (1 << 26)) return fail(PGA_EINVAL, "pop_size too large");
+    if (p->elite < 0 || p->elite >= p->pop_size)
+        return fail(PGA_EINVAL, "elite must satisfy 0 <= elite < pop_size (S:113)");
+    auto prob = [](double x) { return std::isfinite(x) && x >= 0.0 && x <= 1.0; };
+    if (!prob(p->p_crossover) || !prob(p->p_mutation) || !prob(p->p_kb))
+        return fail(PGA_EINVAL, "probabilities must lie in [0, 1]");
+    if (!std::isfinite(p->tol)) return fail(PGA_EINVAL, "tol must be finite");
+    if (p->stall_gens < 1) return fail(PGA_EINVAL, "stall_gens must be >= 1");
+    if (p->max_gens < 1) return fail(PGA_EINVAL, "max_gens must be >= 1");
+    if (p->selection != PGA_SEL_SUS && p->selection != PGA_SEL_TOURNAMENT)
+        return fail(PGA_EINVAL, "selection must be PGA_SEL_SUS or PGA_SEL_TOURNAMENT");
+    if (p->tournament_k < 1 || p->tournament_k > 4) return fail(PGA_EINVAL, "tournament_k must be 1..4");
+    if (p->scaling != PGA_SCALE_RANK && p->scaling != PGA_SCALE_NONE)
+        return fail(PGA_EINVAL, "scaling must be PGA_SCALE_RANK or PGA_SCALE_NONE");
+    if (p->n_islands < 1 || p->n_islands > 8) return fail(PGA_EINVAL, "n_islands must be 1..8");
+    if (p->island < 0 || p->island >= p->n_islands) return fail(PGA_EINVAL, "island out of range");
+    if (p->device < 0) return fail(PGA_EINVAL, "device must be >= 0");
+    if (p->n_islands > 1) {
+        if (p->migrate_every < 1) return fail(PGA_EINVAL, "migrate_every must be >= 1");
+        if (p->migrants < 1 || p->migrants > 256 || p->migrants > p->pop_size)
+            return fail(PGA_EINVAL, "migrants must be 1..min(256, pop_size)");
+    }
+    return PGA_OK;
+}
+
+static int check_corr(const double *C, int32_t N) {
+    if (!C) return fail(PGA_EINVAL, "C is NULL");
+    if (N < 2 || N > 16384) return fail(PGA_EINVAL, "N must be in [2, 16384]");
+    for (int64_t i = 0; i < N; ++i) {
+        for (int64_t j = 0; j < N; ++j) {
+            const double v = C[i * N + j];
+            if (!std::isfinite(v)) return fail(PGA_EINVAL, "C has a non-finite entry");
+            if (i == j) {
+                if (std::fabs(v - 1.0) > 1e-12) return fail(PGA_EINVAL, "C_ii must be 1 (+-1e-12)");
+            } else {
+                if (std::fabs(v) > 1.0 + 1e-9) return fail(PGA_EINVAL, "|C_ij| must be <= 1 + 1e-9");
+                if (v != C[j * N + i]) return fail(PGA_EINVAL, "C must be exactly symmetric (Q4)");
+            }
+        }
+    }
+    return PGA_OK;
+}
+
+}  // namespace pga
+
+using namespace pga;
+
+namespace {
+
+struct Graphs {
+    cudaGraphExec_t gen = nullptr;
+};
+
+void free_ctx(pga_ctx *c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    void *ptrs[] = {c->C, c->diag, c->pop[0], c->pop[1], c->popT[0], c->popT[1], c->V, c->L,
+                    c->top, c->keys_in, c->keys_out, c->idx_in, c->order, c->q, c->prefix,
+                    c->sel, c->mkeys_in, c->mkeys_out, c->m_in, c->sigma, c->cub_tmp, c->st,
+                    c->best_labels, c->history, c->stage_i32, c->evCM, c->evGM, c->evL};
+    for (void *p : ptrs)
+        if (p) cudaFree(p);
+    if (c->h_st) cudaFreeHost(c->h_st);
+    if (c->stream) cudaStreamDestroy(c->stream);
+}
+
+int ensure_device(int dev) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) return fail(PGA_EDEVICE, "no CUDA device available (libpga has no CPU fallback)");
+    if (dev >= n) return fail(PGA_EINVAL, "device ordinal out of range");
+    PGA_CUDA(cudaSetDevice(dev));
+    return PGA_OK;
+}
+
+template <typename T>
+int dalloc(T **p, size_t count) {
+    cudaError_t e = cudaMalloc((void **)p, sizeof(T) * (count ? count : 1));
+    if (e != cudaSuccess) return fail(PGA_ENOMEM, std::string("cudaMalloc failed: ") + cudaGetErrorString(e));
+    return PGA_OK;
+}
+
+#define TRY(x)                 \
+    do {                       \
+        int _rc = (x);         \
+        if (_rc) return _rc;   \
+    } while (0)
+
+int reset_state(pga_ctx *c, int32_t max_gens) {
+    DevState h{};
+    h.gen = 0;
+    h.best_ever = -1.0;
+    *c->h_st = h;
+    PGA_CUDA(cudaMemcpyAsync(c->st, c->h_st, sizeof(DevState), cudaMemcpyHostToDevice, c->stream));
+    PGA_CUDA(cudaStreamSynchronize(c->stream));
+    (void)max_gens;
+    return PGA_OK;
+}
+
+int read_state(pga_ctx *c) {
+    PGA_CUDA(cudaMemcpyAsync(c->h_st, c->st, sizeof(DevState), cudaMemcpyDeviceToHost, c->stream));
+    PGA_CUDA(cudaStreamSynchronize(c->stream));
+    return PGA_OK;
+}
+
+int ensure_history(pga_ctx *c, int32_t n) {
+    if (n <= c->hist_cap) return PGA_OK;
+    double *h = nullptr;
+    TRY(dalloc(&h, (size_t)n));
+    PGA_CUDA(cudaMemsetAsync(h, 0, sizeof(double) * n, c->stream));
+    if (c->history) {
+        PGA_CUDA(cudaMemcpyAsync(h, c->history, sizeof(double) * c->hist_cap, cudaMemcpyDeviceToDevice, c->stream));
+        PGA_CUDA(cudaStreamSynchronize(c->stream));
+        cudaFree(c->history);
+    }
+    c->history = h;
+    c->hist_cap = n;
+    return PGA_OK;
+}
+
+FitBufs ga_bufs(pga_ctx *c) {
+    FitBufs b;
+    b.cm0 = c->pop[0];
+    b.cm1 = c->pop[1];
+    b.gm0 = c->popT[0];
+    b.gm1 = c->popT[1];
+    b.gen = &c->st->gen;
+    b.done = &c->st->done;
+    return b;
+}
+
+bool is_migration_gen(const pga_ctx *c, int32_t g) {
+    return c->p.n_islands > 1 && ((g + 1) % c->p.migrate_every == 0);
+}
+
+int phase_a(pga_ctx *c, int32_t g, int32_t *is_mig) {
+    TRY(launch_fitness(c, ga_bufs(c), c->P, c->L, c->top, c->stream));
+    const bool mig = is_migration_gen(c, g);
+    if (is_mig) *is_mig = mig ? 1 : 0;
+    if (mig) {
+        TRY(launch_sort_order(c, c->stream));
+        c->pending_migration = true;
+    } else {
+        TRY(launch_stats(c, c->p.n_islands > 1 ? 1 : 0, c->stream));
+    }
+    return PGA_OK;
+}
+
+int phase_b(pga_ctx *c) {
+    TRY(launch_sort_order(c, c->stream));
+    TRY(launch_select_breed(c, c->stream));
+    return PGA_OK;
+}
+
+// one single-island generation, captured once into a CUDA graph
+int run_one_generation(pga_ctx *c, Graphs &g, bool use_graph) {
+    if (!use_graph) {
+        TRY(phase_a(c, 0, nullptr));
+        return phase_b(c);
+    }
+    if (!g.gen) {
+        cudaGraph_t graph;
+        PGA_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        int rc = phase_a(c, 0, nullptr);
+        if (!rc) rc = phase_b(c);
+        cudaError_t e = cudaStreamEndCapture(c->stream, &graph);
+        if (rc) return rc;
+        if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
+        e = cudaGraphInstantiate(&g.gen, graph, 0);
+        cudaGraphDestroy(graph);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+    }
+    PGA_CUDA(cudaGraphLaunch(g.gen, c->stream));
+    count_launch(0);
+    return PGA_OK;
+}
+
+void to_one_based(const std::vector<uint16_t> &src, int32_t *dst, size_t n) {
+    for (size_t i = 0; i < n; ++i) dst[i] = (int32_t)src[i] + 1;
+}
+
+struct HookBufs {
+    std::vector<void *> ptrs;
+    ~HookBufs() {
+        for (void *p : ptrs) cudaFree(p);
+    }
+    template <typename T>
+    int get(T **p, size_t n) {
+        int rc = dalloc(p, n);
+        if (!rc) ptrs.push_back((void *)*p);
+        return rc;
+    }
+};
+
+int ensure_eval_bufs(pga_ctx *c) {
+    if (c->evCM) return PGA_OK;
+    TRY(dalloc(&c->evCM, (size_t)c->Pcap * c->ldn));
+    TRY(dalloc(&c->evGM, (size_t)c->N * c->Pcap));
+    TRY(dalloc(&c->evL, (size_t)c->Pcap));
+    PGA_CUDA(cudaMemsetAsync(c->evCM, 0, sizeof(uint16_t) * (size_t)c->Pcap * c->ldn, c->stream));
+    PGA_CUDA(cudaMemsetAsync(c->evGM, 0, sizeof(uint16_t) * (size_t)c->N * c->Pcap, c->stream));
+    PGA_CUDA(cudaStreamSynchronize(c->stream));
+    return PGA_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// ABI
+// ===========================================================================
+extern "C" {
+
+const char *pga_last_error(void) { return g_err.c_str(); }
+
+int64_t pga_launch_count(void) { return g_launches.load(); }
+
+int pga_params_default(pga_params *o) {
+    if (!o) return fail(PGA_EINVAL, "out is NULL");
+    std::memset(o, 0, sizeof(*o));
+    o->pop_size = 1000;   // Table 3 context
+    o->elite = 10;
+    o->p_crossover = 0.9;
+    o->p_mutation = 0.1;
+    o->p_kb = 0.9;
+    o->tol = 1e-5;
+    o->stall_gens = 50;
+    o->max_gens = 400;
+    o->selection = PGA_SEL_SUS;
+    o->tournament_k = 2;
+    o->scaling = PGA_SCALE_RANK;
+    o->device = 0;
+    o->island = 0;
+    o->n_islands = 1;
+    o->migrate_every = 10;
+    o->migrants = 10;
+    o->seed = 1;
+    return PGA_OK;
+}
+
+struct pga_graphs_holder;
+
+int pga_create(const double *C, int32_t N, const pga_params *p, pga_ctx **out) {
+    if (!out) return fail(PGA_EINVAL, "out is NULL");
+    *out = nullptr;
+    TRY(check_params(p));
+    TRY(check_corr(C, N));
+    TRY(ensure_device(p->device));
+    pga_ctx *c = new pga_ctx();
+    c->device = p->device;
+    c->p = *p;
+    c->N = N;
+    c->ldn = (int32_t)round_up(N, 8);
+    c->ldc = (int32_t)round_up(N, 8);
+    c->P = p->pop_size;
+    c->Pcap = round_up(p->pop_size, CB);
+    auto bail = [&](int rc) {
+        free_ctx(c);
+        delete c;
+        return rc;
+    };
+    cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return bail(cuda_fail(e, "cudaStreamCreate"));
+    const size_t cm = (size_t)c->Pcap * c->ldn, gm = (size_t)N * c->Pcap;
+    int rc = 0;
+    rc = rc ? rc : dalloc(&c->C, (size_t)N * c->ldc);
+    rc = rc ? rc : dalloc(&c->diag, (size_t)N);
+    for (int b = 0; b < 2 && !rc; ++b) {
+        rc = rc ? rc : dalloc(&c->pop[b], cm);
+        rc = rc ? rc : dalloc(&c->popT[b], gm);
+    }
+    rc = rc ? rc : dalloc(&c->V, cm);
+    rc = rc ? rc : dalloc(&c->L, (size_t)c->Pcap);
+    rc = rc ? rc : dalloc(&c->top, (size_t)c->Pcap);
+    rc = rc ? rc : dalloc(&c->keys_in, (size_t)c->Pcap);
+    rc = rc ? rc : dalloc(&c->keys_out, (size_t)c->Pcap);
+    rc = rc ? rc : dalloc(&c->idx_in, (size_t)c->Pcap);
+    rc = rc ? rc : dalloc(&c->order, (size_t)c->Pcap);
+    rc = rc ? rc : dalloc(&c->q, (size_t)c->Pcap);
+    rc = rc ? rc : dalloc(&c->prefix, (size_t)c->Pcap);
+    rc = rc ? rc : dalloc(&c->sel, (size_t)c->Pcap + 2);
+    rc = rc ? rc : dalloc(&c->mkeys_in, (size_t)c->Pcap + 2);
+    rc = rc ? rc : dalloc(&c->mkeys_out, (size_t)c->Pcap + 2);
+    rc = rc ? rc : dalloc(&c->m_in, (size_t)c->Pcap + 2);
+    rc = rc ? rc : dalloc(&c->sigma, (size_t)c->Pcap + 2);
+    rc = rc ? rc : dalloc(&c->st, 1);
+    rc = rc ? rc : dalloc(&c->best_labels, (size_t)c->ldn);
+    if (rc) return bail(rc);
+    c->cub_tmp_bytes = cub_tmp_needed(c->Pcap + 2);
+    rc = dalloc((unsigned char **)&c->cub_tmp, c->cub_tmp_bytes);
+    if (rc) return bail(rc);
+    e = cudaMallocHost((void **)&c->h_st, sizeof(DevState));
+    if (e != cudaSuccess) return bail(fail(PGA_ENOMEM, "cudaMallocHost failed"));
+    // population buffers: zero so padding chromosomes hold valid labels
+    for (int b = 0; b < 2; ++b) {
+        e = cudaMemsetAsync(c->pop[b], 0, sizeof(uint16_t) * cm, c->stream);
+        if (e == cudaSuccess) e = cudaMemsetAsync(c->popT[b], 0, sizeof(uint16_t) * gm, c->stream);
+        if (e != cudaSuccess) return bail(cuda_fail(e, "cudaMemset"));
+    }
+    // C -> padded device layout, plus its diagonal
+    {
+        std::vector<double> diag(N);
+        for (int i = 0; i < N; ++i) diag[i] = C[(int64_t)i * N + i];
+        e = cudaMemsetAsync(c->C, 0, sizeof(double) * (size_t)N * c->ldc, c->stream);
+        if (e == cudaSuccess)
+            e = cudaMemcpy2DAsync(c->C, sizeof(double) * c->ldc, C, sizeof(double) * N,
+                                  sizeof(double) * N, N, cudaMemcpyHostToDevice, c->stream);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(c->diag, diag.data(), sizeof(double) * N, cudaMemcpyHostToDevice, c->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+        if (e != cudaSuccess) return bail(cuda_fail(e, "copy C"));
+    }
+    rc = prepare_fitness(N);
+    if (rc) return bail(rc);
+    rc = ensure_history(c, p->max_gens);
+    if (rc) return bail(rc);
+    {
+        const int64_t rec = round_up(16 + 2 * (int64_t)N, 16);
+        c->mig_bytes = rec * (p->n_islands > 1 ? p->migrants : 1);
+    }
+    rc = reset_state(c, p->max_gens);
+    if (rc) return bail(rc);
+    *out = c;
+    return PGA_OK;
+}
+
+void pga_destroy(pga_ctx *c) {
+    if (!c) return;
+    free_ctx(c);
+    delete c;
+}
+
+int pga_get_stream(pga_ctx *c, void **stream) {
+    if (!c || !stream) return fail(PGA_EINVAL, "NULL argument");
+    *stream = (void *)c->stream;
+    return PGA_OK;
+}
+
+int pga_evaluate(pga_ctx *c, const int32_t *labels, int64_t P, double *out_L) {
+    if (!c || !labels || !out_L) return fail(PGA_EINVAL, "NULL argument");
+    if (P < 1) return fail(PGA_EINVAL, "P must be >= 1");
+    PGA_CUDA(cudaSetDevice(c->device));
+    if (!c->stage_i32) TRY(dalloc(&c->stage_i32, (size_t)c->Pcap * c->N));
+    TRY(ensure_eval_bufs(c));
+    const int32_t zero = 0;
+    for (int64_t p0 = 0; p0 < P; p0 += c->Pcap) {
+        const int64_t n = (P - p0 < c->Pcap) ? (P - p0) : c->Pcap;
+        PGA_CUDA(cudaMemcpyAsync(&c->st->pack_error, &zero, sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
+        PGA_CUDA(cudaMemcpyAsync(c->stage_i32, labels + p0 * c->N, sizeof(int32_t) * (size_t)n * c->N,
+                                 cudaMemcpyHostToDevice, c->stream));
+        TRY(launch_pack(c, nullptr, c->stage_i32, n, c->N, c->evCM, c->evGM, c->stream));
+        FitBufs b{c->evCM, c->evCM, c->evGM, c->evGM, nullptr, nullptr};
+        TRY(launch_fitness(c, b, n, c->evL, nullptr, c->stream));
+        int32_t perr = 0;
+        PGA_CUDA(cudaMemcpyAsync(out_L + p0, c->evL, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+        PGA_CUDA(cudaMemcpyAsync(&perr, &c->st->pack_error, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+        PGA_CUDA(cudaStreamSynchronize(c->stream));
+        if (perr) return fail(PGA_EINVAL, "labels must lie in 1..N (Eq. 9)");
+    }
+    return PGA_OK;
+}
+
+int pga_evaluate_device(pga_ctx *c, const uint16_t *labels_dev, int64_t P, double *L_dev,
+                        uint16_t *top_dev, void *stream) {
+    if (!c || !labels_dev || !L_dev) return fail(PGA_EINVAL, "NULL argument");
+    if (P < 1 || P > c->Pcap) return fail(PGA_EINVAL, "P must be in [1, capacity]");
+    cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+    if (!c->evCM) {
+        PGA_CUDA(cudaSetDevice(c->device));
+        TRY(ensure_eval_bufs(c));
+    }
+    TRY(launch_pack(c, labels_dev, nullptr, P, c->N, c->evCM, c->evGM, s));
+    FitBufs b{c->evCM, c->evCM, c->evGM, c->evGM, nullptr, nullptr};
+    return launch_fitness(c, b, P, L_dev, top_dev, s);
+}
+
+int pga_init(pga_ctx *c, uint64_t seed) {
+    if (!c) return fail(PGA_EINVAL, "ctx is NULL");
+    PGA_CUDA(cudaSetDevice(c->device));
+    c->p.seed = seed;
+    TRY(reset_state(c, c->p.max_gens));
+    TRY(launch_init(c, seed, c->stream));
+    c->has_pop = true;
+    c->host_gen = 0;
+    c->pending_migration = false;
+    return PGA_OK;
+}
+
+int pga_gen_evaluate(pga_ctx *c, int32_t *is_migration) {
+    if (!c) return fail(PGA_EINVAL, "ctx is NULL");
+    if (!c->has_pop) return fail(PGA_ESTATE, "no population: call pga_init first");
+    if (c->pending_migration) return fail(PGA_ESTATE, "migration pending: call pga_import_migrants");
+    PGA_CUDA(cudaSetDevice(c->device));
+    return phase_a(c, c->host_gen, is_migration);
+}
+
+int pga_gen_breed(pga_ctx *c) {
+    if (!c) return fail(PGA_EINVAL, "ctx is NULL");
+    if (!c->has_pop) return fail(PGA_ESTATE, "no population: call pga_init first");
+    if (c->pending_migration) return fail(PGA_ESTATE, "migration pending: call pga_import_migrants");
+    PGA_CUDA(cudaSetDevice(c->device));
+    TRY(phase_b(c));
+    c->host_gen += 1;
+    return PGA_OK;
+}
+
+int pga_generation(pga_ctx *c, int32_t *done) {
+    if (!c) return fail(PGA_EINVAL, "ctx is NULL");
+    if (c->p.n_islands > 1) return fail(PGA_ESTATE, "pga_generation is single-island; use pga_gen_evaluate/breed");
+    TRY(pga_gen_evaluate(c, nullptr));
+    TRY(pga_gen_breed(c));
+    if (done) {
+        TRY(read_state(c));
+        *done = c->h_st->done;
+    }
+    return PGA_OK;
+}
+
+int pga_run(pga_ctx *c, int32_t gens, uint64_t seed, int32_t *best_labels, double *best_L,
+            int32_t *gens_run, int32_t *reason) {
+    if (!c) return fail(PGA_EINVAL, "ctx is NULL");
+    if (c->p.n_islands > 1) return fail(PGA_ESTATE, "pga_run is single-island; drive islands with pga_gen_evaluate/breed");
+    PGA_CUDA(cudaSetDevice(c->device));
+    const int32_t saved_max = c->p.max_gens;
+    const int32_t maxg = gens > 0 ? gens : c->p.max_gens;
+    TRY(ensure_history(c, maxg));
+    c->p.max_gens = maxg;
+    int rc = pga_init(c, seed);
+    Graphs g;
+    int32_t launched = 0;
+    const int32_t batch = 8;
+    while (!rc) {
+        for (int k = 0; k < batch && launched < maxg && !rc; ++k, ++launched)
+            rc = run_one_generation(c, g, true);
+        if (rc) break;
+        rc = read_state(c);
+        if (rc) break;
+        if (c->h_st->done || launched >= maxg) break;
+    }
+    if (g.gen) cudaGraphExecDestroy(g.gen);
+    c->p.max_gens = saved_max;
+    if (rc) return rc;
+    c->host_gen = c->h_st->gen;
+    if (best_L) *best_L = c->h_st->best_ever;
+    if (gens_run) *gens_run = c->h_st->gen + 1;
+    if (reason) *reason = c->h_st->reason;
+    if (best_labels) {
+        std::vector<uint16_t> h(c->N);
+        PGA_CUDA(cudaMemcpy(h.data(), c->best_labels, sizeof(uint16_t) * c->N, cudaMemcpyDeviceToHost));
+        to_one_based(h, best_labels, c->N);
+    }
+    return PGA_OK;
+}
+
+int pga_get_state(pga_ctx *c, int32_t *generation, int32_t *done, int32_t *reason, double *best_L,
+                  double *mean_L, int32_t *best_labels) {
+    if (!c) return fail(PGA_EINVAL, "ctx is NULL");
+    PGA_CUDA(cudaSetDevice(c->device));
+    TRY(read_state(c));
+    if (generation) *generation = c->h_st->gen;
+    if (done) *done = c->h_st->done;
+    if (reason) *reason = c->h_st->reason;
+    if (best_L) *best_L = c->h_st->best_ever;
+    if (mean_L) *mean_L = c->h_st->mean;
+    if (best_labels) {
+        std::vector<uint16_t> h(c->N);
+        PGA_CUDA(cudaMemcpy(h.data(), c->best_labels, sizeof(uint16_t) * c->N, cudaMemcpyDeviceToHost));
+        to_one_based(h, best_labels, c->N);
+    }
+    return PGA_OK;
+}
+
+int pga_get_history(pga_ctx *c, double *best_L, int32_t n) {
+    if (!c || !best_L) return fail(PGA_EINVAL, "NULL argument");
+    if (n < 0 || n > c->hist_cap) return fail(PGA_EINVAL, "n exceeds the history capacity");
+    PGA_CUDA(cudaSetDevice(c->device));
+    PGA_CUDA(cudaStreamSynchronize(c->stream));
+    PGA_CUDA(cudaMemcpy(best_L, c->history, sizeof(double) * n, cudaMemcpyDeviceToHost));
+    return PGA_OK;
+}
+
+int pga_get_population(pga_ctx *c, int32_t *labels, double *L) {
+    if (!c || !labels) return fail(PGA_EINVAL, "NULL argument");
+    if (!c->has_pop) return fail(PGA_ESTATE, "no population");
+    PGA_CUDA(cudaSetDevice(c->device));
+    TRY(read_state(c));
+    const int par = c->h_st->gen & 1;
+    std::vector<uint16_t> h((size_t)c->P * c->ldn);
+    PGA_CUDA(cudaMemcpy(h.data(), c->pop[par], sizeof(uint16_t) * h.size(), cudaMemcpyDeviceToHost));
+    for (int64_t p = 0; p < c->P; ++p)
+        for (int i = 0; i < c->N; ++i) labels[p * c->N + i] = (int32_t)h[p * c->ldn + i] + 1;
+    if (L) PGA_CUDA(cudaMemcpy(L, c->L, sizeof(double) * c->P, cudaMemcpyDeviceToHost));
+    return PGA_OK;
+}
+
+int pga_set_population(pga_ctx *c, const int32_t *labels, int32_t generation) {
+    if (!c || !labels) return fail(PGA_EINVAL, "NULL argument");
+    if (generation < 0) return fail(PGA_EINVAL, "generation must be >= 0");
+    for (int64_t k = 0; k < c->P * (int64_t)c->N; ++k)
+        if (labels[k] < 1 || labels[k] > c->N) return fail(PGA_EINVAL, "labels must lie in 1..N (Eq. 9)");
+    PGA_CUDA(cudaSetDevice(c->device));
+    TRY(reset_state(c, c->p.max_gens));
+    if (!c->stage_i32) TRY(dalloc(&c->stage_i32, (size_t)c->Pcap * c->N));
+    PGA_CUDA(cudaMemcpyAsync(c->stage_i32, labels, sizeof(int32_t) * (size_t)c->P * c->N,
+                             cudaMemcpyHostToDevice, c->stream));
+    TRY(launch_set_pop(c, c->stage_i32, generation & 1, c->stream));
+    c->h_st->gen = generation;
+    PGA_CUDA(cudaMemcpyAsync(&c->st->gen, &c->h_st->gen, sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
+    PGA_CUDA(cudaStreamSynchronize(c->stream));
+    c->has_pop = true;
+    c->host_gen = generation;
+    c->pending_migration = false;
+    return PGA_OK;
+}
+
+int pga_migrant_bytes(pga_ctx *c, int64_t *bytes) {
+    if (!c || !bytes) return fail(PGA_EINVAL, "NULL argument");
+    *bytes = c->mig_bytes;
+    return PGA_OK;
+}
+
+int pga_export_migrants(pga_ctx *c, void *dev_send) {
+    if (!c || !dev_send) return fail(PGA_EINVAL, "NULL argument");
+    if (!c->pending_migration) return fail(PGA_ESTATE, "not a migration generation");
+    PGA_CUDA(cudaSetDevice(c->device));
+    return launch_export(c, dev_send, c->stream);
+}
+
+int pga_import_migrants(pga_ctx *c, const void *dev_recv, int32_t n_islands) {
+    if (!c || !dev_recv) return fail(PGA_EINVAL, "NULL argument");
+    if (!c->pending_migration) return fail(PGA_ESTATE, "not a migration generation");
+    if (n_islands != c->p.n_islands) return fail(PGA_EINVAL, "n_islands differs from the ctx's");
+    PGA_CUDA(cudaSetDevice(c->device));
+    TRY(launch_import(c, dev_recv, n_islands, c->stream));
+    TRY(launch_stats(c, 2, c->stream));
+    c->pending_migration = false;
+    return PGA_OK;
+}
+
+int pga_correlation(const double *returns, int32_t T, int32_t N, double *C_out, int32_t device) {
+    if (!returns || !C_out) return fail(PGA_EINVAL, "NULL argument");
+    if (T < 2 || N < 1) return fail(PGA_EINVAL, "need T >= 2 and N >= 1");
+    TRY(ensure_device(device));
+    cudaStream_t s;
+    PGA_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    double *X = nullptr, *C = nullptr;
+    int32_t *st = nullptr;
+    int rc = dalloc(&X, (size_t)T * N);
+    rc = rc ? rc : dalloc(&C, (size_t)N * N);
+    rc = rc ? rc : dalloc(&st, 1);
+    int32_t hst = 0;
+    if (!rc) {
+        cudaError_t e = cudaMemcpyAsync(X, returns, sizeof(double) * (size_t)T * N, cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess) e = cudaMemsetAsync(st, 0, sizeof(int32_t), s);
+        rc = (e == cudaSuccess) ? launch_corr(X, T, N, C, st, s) : cuda_fail(e, "H2D returns");
+        if (!rc) {
+            e = cudaMemcpyAsync(C_out, C, sizeof(double) * (size_t)N * N, cudaMemcpyDeviceToHost, s);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(&hst, st, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+            if (e != cudaSuccess) rc = cuda_fail(e, "pga_correlation");
+        }
+    }
+    cudaFree(X);
+    cudaFree(C);
+    cudaFree(st);
+    cudaStreamDestroy(s);
+    if (!rc && hst) rc = fail(PGA_ENUMERIC, "zero-variance or non-finite column in returns");
+    return rc;
+}
+
+int pga_correlation_device(const double *X_dev, int32_t T, int32_t N, double *C_dev,
+                           int32_t *status_dev, void *stream) {
+    if (!X_dev || !C_dev || !status_dev) return fail(PGA_EINVAL, "NULL argument");
+    if (T < 2 || N < 1) return fail(PGA_EINVAL, "need T >= 2 and N >= 1");
+    return launch_corr(X_dev, T, N, C_dev, status_dev, (cudaStream_t)stream);
+}
+
+int pga_op_select(const double *L, int64_t P, const pga_params *p, int32_t gen, int32_t island,
+                  int32_t *order_out, int32_t *sel_out) {
+    if (!L || !order_out || !sel_out || !p) return fail(PGA_EINVAL, "NULL argument");
+    if (P < 2 || p->elite < 0 || p->elite >= P) return fail(PGA_EINVAL, "need P >= 2 and 0 <= elite < P");
+    if (p->tournament_k < 1 || p->tournament_k > 4) return fail(PGA_EINVAL, "tournament_k must be 1..4");
+    TRY(ensure_device(p->device));
+    const int64_t M = 2 * ((P - p->elite + 1) / 2);
+    HookBufs hb;
+    double *dL;
+    int32_t *dorder, *dsel, *didx;
+    uint64_t *k1, *k2, *q, *pre;
+    void *tmp;
+    const size_t tb = cub_tmp_needed(P + 2);
+    TRY(hb.get(&dL, P));
+    TRY(hb.get(&dorder, P));
+    TRY(hb.get(&dsel, M));
+    TRY(hb.get(&didx, P));
+    TRY(hb.get(&k1, P));
+    TRY(hb.get(&k2, P));
+    TRY(hb.get(&q, P));
+    TRY(hb.get(&pre, P));
+    TRY(hb.get((unsigned char **)&tmp, tb));
+    PGA_CUDA(cudaMemcpy(dL, L, sizeof(double) * P, cudaMemcpyHostToDevice));
+    TRY(run_select_ops(dL, P, *p, gen, island, dorder, dsel, k1, k2, didx, q, pre, tmp, tb, nullptr,
+                       0, nullptr, false));
+    PGA_CUDA(cudaDeviceSynchronize());
+    PGA_CUDA(cudaMemcpy(order_out, dorder, sizeof(int32_t) * P, cudaMemcpyDeviceToHost));
+    PGA_CUDA(cudaMemcpy(sel_out, dsel, sizeof(int32_t) * M, cudaMemcpyDeviceToHost));
+    return PGA_OK;
+}
+
+int pga_op_mates(int64_t M, const pga_params *p, int32_t gen, int32_t island, int32_t *sigma_out) {
+    if (!p || !sigma_out) return fail(PGA_EINVAL, "NULL argument");
+    if (M < 1) return fail(PGA_EINVAL, "M must be >= 1");
+    TRY(ensure_device(p->device));
+    HookBufs hb;
+    uint32_t *k1, *k2;
+    int32_t *m1, *sig;
+    void *tmp;
+    const size_t tb = cub_tmp_needed(M + 2);
+    TRY(hb.get(&k1, M));
+    TRY(hb.get(&k2, M));
+    TRY(hb.get(&m1, M));
+    TRY(hb.get(&sig, M));
+    TRY(hb.get((unsigned char **)&tmp, tb));
+    TRY(run_mates(M, *p, gen, island, k1, k2, m1, sig, tmp, tb, nullptr, 0, nullptr));
+    PGA_CUDA(cudaDeviceSynchronize());
+    PGA_CUDA(cudaMemcpy(sigma_out, sig, sizeof(int32_t) * M, cudaMemcpyDeviceToHost));
+    return PGA_OK;
+}
+
+int pga_op_breed(const int32_t *pop, const int32_t *top, const int32_t *order, int64_t P, int32_t N,
+                 const int32_t *sel, const int32_t *sigma, const pga_params *p, int32_t gen,
+                 int32_t island, int64_t p_off, int32_t *next_out) {
+    if (!pop || !top || !order || !sel || !sigma || !p || !next_out) return fail(PGA_EINVAL, "NULL argument");
+    if (P < 2 || N < 2 || p->elite < 0 || p->elite >= P) return fail(PGA_EINVAL, "bad sizes");
+    TRY(ensure_device(p->device));
+    const int64_t M = 2 * ((P - p->elite + 1) / 2);
+    HookBufs hb;
+    int32_t *dpop, *dtop, *dord, *dsel, *dsig, *dnext;
+    TRY(hb.get(&dpop, (size_t)P * N));
+    TRY(hb.get(&dtop, P));
+    TRY(hb.get(&dord, P));
+    TRY(hb.get(&dsel, M));
+    TRY(hb.get(&dsig, M));
+    TRY(hb.get(&dnext, (size_t)P * N));
+    PGA_CUDA(cudaMemcpy(dpop, pop, sizeof(int32_t) * P * N, cudaMemcpyHostToDevice));
+    PGA_CUDA(cudaMemcpy(dtop, top, sizeof(int32_t) * P, cudaMemcpyHostToDevice));
+    PGA_CUDA(cudaMemcpy(dord, order, sizeof(int32_t) * P, cudaMemcpyHostToDevice));
+    PGA_CUDA(cudaMemcpy(dsel, sel, sizeof(int32_t) * M, cudaMemcpyHostToDevice));
+    PGA_CUDA(cudaMemcpy(dsig, sigma, sizeof(int32_t) * M, cudaMemcpyHostToDevice));
+    TRY(launch_breed_hook(dpop, dtop, dord, P, N, dsel, dsig, *p, gen, island, p_off, dnext, 0));
+    PGA_CUDA(cudaDeviceSynchronize());
+    PGA_CUDA(cudaMemcpy(next_out, dnext, sizeof(int32_t) * P * N, cudaMemcpyDeviceToHost));
+    return PGA_OK;
+}
+
+int pga_op_canonicalize(int32_t *labels, int64_t P, int32_t N, int32_t device) {
+    if (!labels) return fail(PGA_EINVAL, "NULL argument");
+    if (P < 1 || N < 1) return fail(PGA_EINVAL, "bad sizes");
+    for (int64_t k = 0; k < P * (int64_t)N; ++k)
+        if (labels[k] < 0 || labels[k] > 2 * N) return fail(PGA_EINVAL, "labels must lie in 0..2N");
+    TRY(ensure_device(device));
+    HookBufs hb;
+    int32_t *d;
+    TRY(hb.get(&d, (size_t)P * N));
+    PGA_CUDA(cudaMemcpy(d, labels, sizeof(int32_t) * P * N, cudaMemcpyHostToDevice));
+    TRY(launch_canonicalize_i32(d, P, N, 0));
+    PGA_CUDA(cudaDeviceSynchronize());
+    PGA_CUDA(cudaMemcpy(labels, d, sizeof(int32_t) * P * N, cudaMemcpyDeviceToHost));
+    return PGA_OK;
+}
+
+int pga_op_init(uint64_t seed, int32_t N, int64_t P, int64_t p_off, int32_t island, int32_t device,
+                int32_t *out) {
+    if (!out) return fail(PGA_EINVAL, "NULL argument");
+    if (P < 1 || N < 2) return fail(PGA_EINVAL, "bad sizes");
+    TRY(ensure_device(device));
+    HookBufs hb;
+    int32_t *d;
+    TRY(hb.get(&d, (size_t)P * N));
+    TRY(launch_init_raw(seed, N, N, P, P, p_off, (uint32_t)island, nullptr, nullptr, d, 0));
+    PGA_CUDA(cudaDeviceSynchronize());
+    PGA_CUDA(cudaMemcpy(out, d, sizeof(int32_t) * P * N, cudaMemcpyDeviceToHost));
+    return PGA_OK;
+}
+
+}  // extern "C"

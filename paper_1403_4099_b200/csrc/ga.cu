@@ -1,0 +1,701 @@
+// ga.cu — the per-generation GA operators of Alg. 1 on device:
+// initial population, state & statistics, termination, isolate fittest,
+// elitism, scaling, SUS / tournament selection, mate pairing, crossover
+// (knowledge-based or one-point), mutation, canonicalisation, replacement,
+// and elite migration between islands.  DESIGN.md §3 fixes every detail the
+// paper leaves open (readings Q7-Q21); the Philox stream layout makes every
+// operator bit-reproducible.
+#include <cuda_runtime.h>
+#include <cub/cub.cuh>
+
+#include "pga_internal.cuh"
+
+namespace {
+
+using namespace pgad;
+
+// ---------------------------------------------------------------------------
+// warp-cooperative first-occurrence canonicalisation (Q7)
+// The caller streams genes in order, 32 per step; `table` (per warp, smem,
+// >= max label + 1 entries, initialised to 0xFFFF) maps old -> new labels.
+// ---------------------------------------------------------------------------
+struct Canon {
+    uint16_t *table;
+    int next;
+    __device__ __forceinline__ uint32_t step(uint32_t s, bool valid, int lane) {
+        const uint32_t key = valid ? s : (0x10000u + (uint32_t)lane);
+        const unsigned m = __match_any_sync(0xFFFFFFFFu, key);
+        const bool leader = (__ffs(m) - 1) == lane;
+        const bool fresh = valid && leader && table[s] == 0xFFFF;
+        const unsigned bal = __ballot_sync(0xFFFFFFFFu, fresh);
+        if (fresh) table[s] = (uint16_t)(next + __popc(bal & lanemask_lt()));
+        next += __popc(bal);
+        __syncwarp();
+        return valid ? (uint32_t)table[s] : 0u;
+    }
+};
+
+__device__ __forceinline__ void table_reset(uint16_t *table, int n, int lane) {
+    for (int k = lane; k < n; k += 32) table[k] = 0xFFFF;
+    __syncwarp();
+}
+
+// ---------------------------------------------------------------------------
+// k_init: warp per chromosome.  gene i of chromosome p_global:
+// scale(Philox(INIT; i>>2, p_global)[i&3], N), generation field 0xFFFFFFFF.
+// ---------------------------------------------------------------------------
+__global__ void k_init(uint64_t seed, int N, int ldn, int64_t P, int64_t Pcap, int64_t p_off,
+                       uint32_t island, uint16_t *CM, uint16_t *GM, int32_t *out32) {
+    extern __shared__ uint16_t tables[];
+    const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t p = (int64_t)blockIdx.x * nw + warp;
+    if (p >= P) return;
+    uint16_t *table = tables + (size_t)warp * (N + 1);
+    table_reset(table, N + 1, lane);
+    Canon cn{table, 0};
+    for (int base = 0; base < N; base += 32) {
+        const int i = base + lane;
+        const bool valid = i < N;
+        uint32_t s = 0;
+        if (valid) {
+            const U4 u = draw(seed, pga::TAG_INIT, island, 0xFFFFFFFFu, (uint32_t)(i >> 2),
+                              (uint32_t)(p_off + p));
+            s = scale_u32(word(u, i & 3), (uint32_t)N);
+        }
+        const uint32_t c = cn.step(s, valid, lane);
+        if (valid) {
+            if (CM) CM[p * ldn + i] = (uint16_t)c;
+            if (GM) GM[(int64_t)i * Pcap + p] = (uint16_t)c;
+            if (out32) out32[p * N + i] = (int32_t)c;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// k_canon_i32: canonicalise int32 labels in place (test hook), warp per row.
+// ---------------------------------------------------------------------------
+__global__ void k_canon_i32(int32_t *lab, int64_t P, int N, int tab) {
+    extern __shared__ uint16_t tables[];
+    const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t p = (int64_t)blockIdx.x * nw + warp;
+    if (p >= P) return;
+    uint16_t *table = tables + (size_t)warp * tab;
+    table_reset(table, tab, lane);
+    Canon cn{table, 0};
+    for (int base = 0; base < N; base += 32) {
+        const int i = base + lane;
+        const bool valid = i < N;
+        const uint32_t s = valid ? (uint32_t)lab[p * N + i] : 0u;
+        const uint32_t c = cn.step(s, valid, lane);
+        if (valid) lab[p * N + i] = (int32_t)c;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// k_stats: one block.  best (lowest index on ties), mean, stall counter,
+// termination flag, best-ever labels, history (Alg. 1; Q16, Q17).
+// mode 0: single island, update stall every generation
+// mode 1: multi-island non-migration generation: statistics only
+// mode 2: multi-island migration generation: stall on the (global) best
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024)
+k_stats(const double *__restrict__ L, int64_t P, const uint16_t *CM0, const uint16_t *CM1,
+        int ldn, int N, pga::DevState *st, uint16_t *best_labels, double *history,
+        int hist_cap, double tol, int stall_gens, int max_gens, int mode, int migrate_every) {
+    __shared__ double sb[32], ss[32];
+    __shared__ int si[32];
+    if (st->done) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double best = -1.0, sum = 0.0;
+    int bi = 0x7FFFFFFF;
+    for (int64_t i = tid; i < P; i += blockDim.x) {
+        const double v = L[i];
+        sum += v;
+        if (v > best) {  // ascending i per thread -> first max kept
+            best = v;
+            bi = (int)i;
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const double ob = __shfl_xor_sync(0xFFFFFFFFu, best, off);
+        const int oi = __shfl_xor_sync(0xFFFFFFFFu, bi, off);
+        sum += __shfl_xor_sync(0xFFFFFFFFu, sum, off);
+        if (ob > best || (ob == best && oi < bi)) {
+            best = ob;
+            bi = oi;
+        }
+    }
+    if (lane == 0) {
+        sb[warp] = best;
+        si[warp] = bi;
+        ss[warp] = sum;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        const int nw = blockDim.x >> 5;
+        best = lane < nw ? sb[lane] : -1.0;
+        bi = lane < nw ? si[lane] : 0x7FFFFFFF;
+        sum = lane < nw ? ss[lane] : 0.0;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const double ob = __shfl_xor_sync(0xFFFFFFFFu, best, off);
+            const int oi = __shfl_xor_sync(0xFFFFFFFFu, bi, off);
+            sum += __shfl_xor_sync(0xFFFFFFFFu, sum, off);
+            if (ob > best || (ob == best && oi < bi)) {
+                best = ob;
+                bi = oi;
+            }
+        }
+        if (lane == 0) {
+            const int g = st->gen;
+            st->best = best;
+            st->best_idx = bi;
+            st->mean = sum / (double)P;
+            if (g < hist_cap) history[g] = best;
+            if (mode == 0) {
+                if (g > 0) st->stall = (best - st->prev_best < tol) ? st->stall + 1 : 0;
+                st->prev_best = best;
+            } else if (mode == 2) {
+                if (g + 1 > migrate_every)
+                    st->stall = (best - st->prev_best < tol) ? st->stall + migrate_every : 0;
+                st->prev_best = best;
+            }
+            int done = 0;
+            if (tol >= 0.0 && st->stall >= stall_gens) {
+                done = 1;
+                st->reason = PGA_REASON_STALLED;
+            }
+            if (g + 1 >= max_gens) done = 1;
+            st->done = done;
+            si[0] = (best > st->best_ever) ? 1 : 0;
+            if (si[0]) st->best_ever = best;
+        }
+    }
+    __syncthreads();
+    if (si[0]) {
+        const uint16_t *CM = (st->gen & 1) ? CM1 : CM0;
+        for (int i = tid; i < N; i += blockDim.x) best_labels[i] = CM[(int64_t)bi * ldn + i];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// selection
+// ---------------------------------------------------------------------------
+__global__ void k_sort_keys(const double *__restrict__ L, int64_t P, uint64_t *keys, int32_t *idx,
+                            const int32_t *done) {
+    if (done && *done) return;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P) return;
+    double v = L[i];
+    if (v == 0.0) v = 0.0;  // -0 -> +0
+    // ascending key order == (L desc); L >= 0 so the raw bits are monotone.
+    keys[i] = ~(uint64_t)__double_as_longlong(v);
+    idx[i] = (int32_t)i;
+}
+
+__device__ __forceinline__ int ceil_log2_d(int64_t x) {
+    int b = 0;
+    while (((int64_t)1 << b) < x) ++b;
+    return b;
+}
+
+// q_i = floor(2^B * w_i / w_max), w = 1/sqrt(rank) (RANK) or L (NONE)
+__global__ void k_weights(const double *__restrict__ L, const int32_t *__restrict__ order, int64_t P,
+                          int scaling, uint64_t *q, const int32_t *done) {
+    if (done && *done) return;
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= P) return;
+    const int i = order[r];
+    const int B = 62 - ceil_log2_d(P);
+    double w, wmax;
+    if (scaling == PGA_SCALE_RANK) {
+        w = 1.0 / sqrt((double)(r + 1));
+        wmax = 1.0;
+    } else {
+        w = L[i];
+        wmax = L[order[0]];
+    }
+    uint64_t qi = 0;
+    if (wmax > 0.0) {
+        const double x = w / wmax;
+        if (x > 0.0) qi = (uint64_t)floor(ldexp(x, B));
+    }
+    q[i] = qi;
+}
+
+__global__ void k_sus(const uint64_t *__restrict__ prefix, const double *__restrict__ L,
+                      const int32_t *__restrict__ order, int64_t P, int64_t M, int scaling,
+                      uint64_t seed, uint32_t gen, uint32_t island, int32_t *sel,
+                      const int32_t *done, const int32_t *gen_ptr) {
+    if (done && *done) return;
+    const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= M) return;
+    if (gen_ptr) gen = (uint32_t)*gen_ptr;
+    const double wmax = (scaling == PGA_SCALE_RANK) ? 1.0 : L[order[0]];
+    if (!(wmax > 0.0)) {  // all-zero fitness: uniform fallback
+        const U4 u = draw(seed, pga::TAG_SUS, island, gen, (uint32_t)m, 0u);
+        sel[m] = (int32_t)scale_u32(u.x, (uint32_t)P);
+        return;
+    }
+    const uint64_t Q = prefix[P - 1];
+    const uint64_t step = Q / (uint64_t)M;
+    const U4 u = draw(seed, pga::TAG_SUS, island, gen, 0u, 0xFFFFFFFFu);
+    const uint64_t x = ((uint64_t)u.x << 32) | (uint64_t)u.y;
+    const uint64_t start = __umul64hi(x, step);
+    const uint64_t ptr = start + (uint64_t)m * step;
+    // min{i : prefix[i] > ptr}
+    int64_t lo = 0, hi = P - 1;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (prefix[mid] > ptr) hi = mid;
+        else lo = mid + 1;
+    }
+    sel[m] = (int32_t)lo;
+}
+
+__global__ void k_tournament(const double *__restrict__ L, int64_t P, int64_t M, int k,
+                             uint64_t seed, uint32_t gen, uint32_t island, int32_t *sel,
+                             const int32_t *done, const int32_t *gen_ptr) {
+    if (done && *done) return;
+    const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= M) return;
+    if (gen_ptr) gen = (uint32_t)*gen_ptr;
+    const U4 u = draw(seed, pga::TAG_TOUR, island, gen, (uint32_t)m, 0u);
+    int best = (int)scale_u32(u.x, (uint32_t)P);
+    for (int t = 1; t < k; ++t) {
+        const int c = (int)scale_u32(word(u, t), (uint32_t)P);
+        if (L[c] > L[best] || (L[c] == L[best] && c < best)) best = c;
+    }
+    sel[m] = best;
+}
+
+__global__ void k_mate_keys(int64_t M, uint64_t seed, uint32_t gen, uint32_t island, uint32_t *keys,
+                            int32_t *idx, const int32_t *done, const int32_t *gen_ptr) {
+    if (done && *done) return;
+    const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= M) return;
+    if (gen_ptr) gen = (uint32_t)*gen_ptr;
+    const U4 u = draw(seed, pga::TAG_PERM, island, gen, (uint32_t)(m >> 2), 0u);
+    keys[m] = word(u, (int)(m & 3));
+    idx[m] = (int32_t)m;
+}
+
+
+// ---------------------------------------------------------------------------
+// k_breed: warp per output slot o.  o < E: copy elite order[o];
+// else child c of pair k = (o - E) / 2.  Crossover, mutation, canonicalise,
+// write both layouts (and an optional int32 copy for the test hook).
+// ---------------------------------------------------------------------------
+struct BreedArgs {
+    const uint16_t *cm_in0, *cm_in1;   // parents (chromosome-major), by gen parity
+    uint16_t *cm_out0, *cm_out1;       // children written to the other buffer
+    uint16_t *gm_out0, *gm_out1;
+    const int32_t *i32_in;             // hook: int32 parents [P][N] (instead of cm_in)
+    int32_t *i32_out;                  // hook: int32 children [P][N]
+    const uint16_t *top16;             // KB top labels (0xFFFF none)
+    const int32_t *top32;              // hook: int32 tops (-1 none)
+    const int32_t *order, *sel, *sigma;
+    int64_t P, Pcap, p_off;
+    int N, ldn, E;
+    uint64_t thr_c, thr_m, thr_kb;
+    uint64_t seed;
+    uint32_t gen, island;
+    const int32_t *done, *gen_ptr;
+};
+
+__device__ __forceinline__ uint32_t parent_gene(const BreedArgs &a, const uint16_t *cm, int64_t p,
+                                                int i) {
+    return a.i32_in ? (uint32_t)a.i32_in[p * a.N + i] : (uint32_t)cm[p * a.ldn + i];
+}
+
+__device__ __forceinline__ int parent_top(const BreedArgs &a, int64_t p) {
+    if (a.top32) return a.top32[p];
+    const uint16_t t = a.top16[p];
+    return t == 0xFFFF ? -1 : (int)t;
+}
+
+__global__ void k_breed(BreedArgs a) {
+    if (a.done && *a.done) return;
+    extern __shared__ uint16_t tables[];
+    const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t o = (int64_t)blockIdx.x * nw + warp;
+    if (o >= a.P) return;
+    const uint32_t gen = a.gen_ptr ? (uint32_t)*a.gen_ptr : a.gen;
+    const int par = a.gen_ptr ? (int)(gen & 1u) : 0;
+    const uint16_t *cm_in = par ? a.cm_in1 : a.cm_in0;
+    uint16_t *cm_out = par ? a.cm_out0 : a.cm_out1;
+    uint16_t *gm_out = par ? a.gm_out0 : a.gm_out1;
+    const int N = a.N;
+    uint16_t *table = tables + (size_t)warp * (N + 1);
+    table_reset(table, N + 1, lane);
+    Canon cn{table, 0};
+
+    int mode = 0;          // 0 copy, 1 KB, 2 one-point
+    int64_t pa = 0, pb = 0;
+    int kb_top = -1, cut = 0, child = 0;
+    bool mutate = false;
+    if (o < a.E) {
+        pa = a.order[o];
+    } else {
+        const int64_t k = (o - a.E) >> 1;
+        child = (int)((o - a.E) & 1);
+        const int64_t ia = a.sel[a.sigma[2 * k]], ib = a.sel[a.sigma[2 * k + 1]];
+        pa = child ? ib : ia;   // the parent whose genes child keeps
+        pb = child ? ia : ib;   // the other parent
+        const U4 x = draw(a.seed, pga::TAG_XO, a.island, gen, (uint32_t)k, 0u);
+        if ((uint64_t)x.x >= a.thr_c) {
+            mode = 0;
+        } else if ((uint64_t)x.y < a.thr_kb) {
+            mode = 1;
+            kb_top = parent_top(a, pb);
+        } else {
+            mode = 2;
+            cut = 1 + (int)scale_u32(x.z, (uint32_t)(N - 1));
+        }
+        mutate = true;
+    }
+    const uint32_t og = (uint32_t)(a.p_off + o);
+    for (int base = 0; base < N; base += 32) {
+        const int i = base + lane;
+        const bool valid = i < N;
+        uint32_t s = 0;
+        if (valid) {
+            s = parent_gene(a, cm_in, pa, i);
+            if (mode == 1) {
+                if (kb_top >= 0 && (int)parent_gene(a, cm_in, pb, i) == kb_top) s = (uint32_t)N;
+            } else if (mode == 2) {
+                if (i >= cut) s = parent_gene(a, cm_in, pb, i);
+            }
+            if (mutate && a.thr_m) {
+                const U4 u = draw(a.seed, pga::TAG_MUT, a.island, gen, (uint32_t)(i >> 2), og);
+                if ((uint64_t)word(u, i & 3) < a.thr_m) {
+                    const U4 v = draw(a.seed, pga::TAG_MUTV, a.island, gen, (uint32_t)(i >> 2), og);
+                    s = scale_u32(word(v, i & 3), (uint32_t)N);
+                }
+            }
+        }
+        const uint32_t c = cn.step(s, valid, lane);
+        if (valid) {
+            if (a.i32_out) {
+                a.i32_out[o * N + i] = (int32_t)c;
+            } else {
+                cm_out[o * a.ldn + i] = (uint16_t)c;
+                gm_out[(int64_t)i * a.Pcap + o] = (uint16_t)c;
+            }
+        }
+    }
+}
+
+// k_set_pop: int32 1-based labels (validated on the host) -> canonical
+// u16 in both layouts of buffer `par`.
+__global__ void k_set_pop(const int32_t *__restrict__ lab, int64_t P, int N, int ldn, int64_t Pcap,
+                          uint16_t *CM, uint16_t *GM) {
+    extern __shared__ uint16_t tables[];
+    const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t p = (int64_t)blockIdx.x * nw + warp;
+    if (p >= P) return;
+    uint16_t *table = tables + (size_t)warp * (N + 1);
+    table_reset(table, N + 1, lane);
+    Canon cn{table, 0};
+    for (int base = 0; base < N; base += 32) {
+        const int i = base + lane;
+        const bool valid = i < N;
+        const uint32_t s = valid ? (uint32_t)(lab[p * N + i] - 1) : 0u;
+        const uint32_t c = cn.step(s, valid, lane);
+        if (valid) {
+            CM[p * ldn + i] = (uint16_t)c;
+            GM[(int64_t)i * Pcap + p] = (uint16_t)c;
+        }
+    }
+}
+
+__global__ void k_advance(pga::DevState *st) {
+    if (!st->done) st->gen += 1;
+}
+
+// ---------------------------------------------------------------------------
+// migration (Q21).  Record: fp64 L | u16 top | u16 pad[3] | u16 labels[N],
+// padded to a multiple of 16 bytes.
+// ---------------------------------------------------------------------------
+__global__ void k_export(const double *__restrict__ L, const uint16_t *__restrict__ top,
+                         const int32_t *__restrict__ order, const uint16_t *CM0,
+                         const uint16_t *CM1, const pga::DevState *st, int ldn, int N, int Em,
+                         int64_t rec_bytes, unsigned char *out) {
+    const int r = blockIdx.x;
+    if (r >= Em) return;
+    const uint16_t *CM = (st->gen & 1) ? CM1 : CM0;
+    const int p = order[r];
+    unsigned char *rec = out + (int64_t)r * rec_bytes;
+    if (threadIdx.x == 0) {
+        *reinterpret_cast<double *>(rec) = L[p];
+        reinterpret_cast<uint16_t *>(rec + 8)[0] = top[p];
+    }
+    uint16_t *lab = reinterpret_cast<uint16_t *>(rec + 16);
+    for (int i = threadIdx.x; i < N; i += blockDim.x) lab[i] = CM[(int64_t)p * ldn + i];
+}
+
+// one block: choose the global top Em of G*Em candidates by (L desc, island
+// asc, rank asc), then replace this island's Em worst (order[P-1-r]).
+__global__ void k_import(const unsigned char *__restrict__ in, int G, int Em, int64_t rec_bytes,
+                         const int32_t *__restrict__ order, int64_t P, double *L, uint16_t *top,
+                         uint16_t *CM0, uint16_t *CM1, uint16_t *GM0, uint16_t *GM1,
+                         const pga::DevState *st, int ldn, int N, int64_t Pcap) {
+    __shared__ int chosen[256];
+    const int total = G * Em;
+    if (threadIdx.x == 0) {
+        // selection by repeated scans (total <= 8 * 256); strict '>' keeps
+        // the earliest (island, rank) among equal L.
+        unsigned char used[2048];
+        for (int j = 0; j < total; ++j) used[j] = 0;
+        for (int r = 0; r < Em; ++r) {
+            int b = -1;
+            double bl = 0.0;
+            for (int j = 0; j < total; ++j) {
+                if (used[j]) continue;
+                const double v = *reinterpret_cast<const double *>(in + (int64_t)j * rec_bytes);
+                if (b < 0 || v > bl) {
+                    b = j;
+                    bl = v;
+                }
+            }
+            used[b] = 1;
+            chosen[r] = b;
+        }
+    }
+    __syncthreads();
+    const int par = st->gen & 1;
+    uint16_t *CM = par ? CM1 : CM0;
+    uint16_t *GM = par ? GM1 : GM0;
+    for (int r = 0; r < Em; ++r) {
+        const unsigned char *rec = in + (int64_t)chosen[r] * rec_bytes;
+        const int64_t w = order[P - 1 - r];
+        const uint16_t *lab = reinterpret_cast<const uint16_t *>(rec + 16);
+        for (int i = threadIdx.x; i < N; i += blockDim.x) {
+            CM[w * ldn + i] = lab[i];
+            GM[(int64_t)i * Pcap + w] = lab[i];
+        }
+        if (threadIdx.x == 0) {
+            L[w] = *reinterpret_cast<const double *>(rec);
+            top[w] = reinterpret_cast<const uint16_t *>(rec + 8)[0];
+        }
+    }
+}
+
+}  // namespace
+
+namespace pga {
+
+static int breed_warps(int N) {
+    const size_t per = (size_t)(N + 1) * sizeof(uint16_t);
+    int w = (int)((48 * 1024) / per);
+    return w < 1 ? 1 : (w > 8 ? 8 : w);
+}
+
+int launch_canonicalize_i32(int32_t *lab, int64_t P, int32_t N, cudaStream_t s) {
+    const int tab = 2 * N + 1;
+    int w = (int)((48 * 1024) / ((size_t)tab * 2));
+    w = w < 1 ? 1 : (w > 8 ? 8 : w);
+    k_canon_i32<<<(unsigned)((P + w - 1) / w), 32 * w, (size_t)w * tab * 2, s>>>(lab, P, N, tab);
+    PGA_LAUNCHED();
+    return PGA_OK;
+}
+
+int launch_init_raw(uint64_t seed, int N, int ldn, int64_t P, int64_t Pcap, int64_t p_off,
+                    uint32_t island, uint16_t *CM, uint16_t *GM, int32_t *out32, cudaStream_t s) {
+    const int w = breed_warps(N);
+    k_init<<<(unsigned)((P + w - 1) / w), 32 * w, (size_t)w * (N + 1) * 2, s>>>(
+        seed, N, ldn, P, Pcap, p_off, island, CM, GM, out32);
+    PGA_LAUNCHED();
+    return PGA_OK;
+}
+
+int launch_set_pop(pga_ctx *c, const int32_t *lab32, int par, cudaStream_t s) {
+    const int w = breed_warps(c->N);
+    k_set_pop<<<(unsigned)((c->P + w - 1) / w), 32 * w, (size_t)w * (c->N + 1) * 2, s>>>(
+        lab32, c->P, c->N, c->ldn, c->Pcap, c->pop[par], c->popT[par]);
+    PGA_LAUNCHED();
+    return PGA_OK;
+}
+
+int launch_init(pga_ctx *c, uint64_t seed, cudaStream_t s) {
+    return launch_init_raw(seed, c->N, c->ldn, c->P, c->Pcap, (int64_t)c->p.island * c->P,
+                           (uint32_t)c->p.island, c->pop[0], c->popT[0], nullptr, s);
+}
+
+int launch_stats(pga_ctx *c, int mode, cudaStream_t s) {
+    k_stats<<<1, 1024, 0, s>>>(c->L, c->P, c->pop[0], c->pop[1], c->ldn, c->N, c->st,
+                               c->best_labels, c->history, c->hist_cap, c->p.tol,
+                               c->p.stall_gens, c->p.max_gens, mode, c->p.migrate_every);
+    PGA_LAUNCHED();
+    return PGA_OK;
+}
+
+size_t cub_tmp_needed(int64_t P) {
+    size_t a = 0, b = 0, d = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, a, (uint64_t *)nullptr, (uint64_t *)nullptr,
+                                    (int32_t *)nullptr, (int32_t *)nullptr, (int)P);
+    cub::DeviceScan::InclusiveSum(nullptr, b, (uint64_t *)nullptr, (uint64_t *)nullptr, (int)P);
+    cub::DeviceRadixSort::SortPairs(nullptr, d, (uint32_t *)nullptr, (uint32_t *)nullptr,
+                                    (int32_t *)nullptr, (int32_t *)nullptr, (int)(P + 1));
+    size_t m = a > b ? a : b;
+    return (m > d ? m : d) + 256;
+}
+
+// order = indices by (L desc, idx asc)
+static int sort_order(const double *L, int64_t P, int32_t *order, uint64_t *keys_in,
+                      uint64_t *keys_out, int32_t *idx_in, void *tmp, size_t tmp_bytes,
+                      const int32_t *done, cudaStream_t s) {
+    const unsigned nb = (unsigned)((P + 255) / 256);
+    k_sort_keys<<<nb, 256, 0, s>>>(L, P, keys_in, idx_in, done);
+    PGA_LAUNCHED();
+    size_t tb = tmp_bytes;
+    PGA_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, keys_in, keys_out, idx_in, order, (int)P, 0,
+                                             64, s));
+    count_launch();
+    return PGA_OK;
+}
+
+int run_select_ops(const double *L, int64_t P, const pga_params &p, int32_t gen, int32_t island,
+                   int32_t *order, int32_t *sel, uint64_t *keys_in, uint64_t *keys_out,
+                   int32_t *idx_in, uint64_t *q, uint64_t *prefix, void *tmp, size_t tmp_bytes,
+                   const int32_t *done, cudaStream_t s, const int32_t *gen_ptr, bool sorted) {
+    const int64_t M = 2 * ((P - p.elite + 1) / 2);
+    const unsigned nb = (unsigned)((P + 255) / 256);
+    int rc;
+    if (!sorted) {
+        rc = sort_order(L, P, order, keys_in, keys_out, idx_in, tmp, tmp_bytes, done, s);
+        if (rc) return rc;
+    }
+    if (p.selection == PGA_SEL_TOURNAMENT) {
+        k_tournament<<<(unsigned)((M + 255) / 256), 256, 0, s>>>(L, P, M, p.tournament_k, p.seed,
+                                                                (uint32_t)gen, (uint32_t)island,
+                                                                sel, done, gen_ptr);
+        PGA_LAUNCHED();
+        return PGA_OK;
+    }
+    k_weights<<<nb, 256, 0, s>>>(L, order, P, p.scaling, q, done);
+    PGA_LAUNCHED();
+    size_t tb = tmp_bytes;
+    PGA_CUDA(cub::DeviceScan::InclusiveSum(tmp, tb, q, prefix, (int)P, s));
+    count_launch();
+    k_sus<<<(unsigned)((M + 255) / 256), 256, 0, s>>>(prefix, L, order, P, M, p.scaling, p.seed,
+                                                      (uint32_t)gen, (uint32_t)island, sel, done,
+                                                      gen_ptr);
+    PGA_LAUNCHED();
+    return PGA_OK;
+}
+
+int run_mates(int64_t M, const pga_params &p, int32_t gen, int32_t island, uint32_t *k_in,
+              uint32_t *k_out, int32_t *m_in, int32_t *sigma, void *tmp, size_t tmp_bytes,
+              const int32_t *done, cudaStream_t s, const int32_t *gen_ptr) {
+    k_mate_keys<<<(unsigned)((M + 255) / 256), 256, 0, s>>>(M, p.seed, (uint32_t)gen,
+                                                            (uint32_t)island, k_in, m_in, done,
+                                                            gen_ptr);
+    PGA_LAUNCHED();
+    size_t tb = tmp_bytes;
+    PGA_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, k_in, k_out, m_in, sigma, (int)M, 0, 32, s));
+    count_launch();
+    return PGA_OK;
+}
+
+static void fill_breed(BreedArgs &a, const pga_params &p, int64_t P, int N) {
+    a.thr_c = 0;
+    a.P = P;
+    a.N = N;
+    a.E = p.elite;
+    a.seed = p.seed;
+    a.island = (uint32_t)p.island;
+    auto thr = [](double x) -> uint64_t {
+        if (x >= 1.0) return (uint64_t)1 << 32;
+        if (x <= 0.0) return 0;
+        return (uint64_t)llrint(x * 4294967296.0);
+    };
+    a.thr_c = thr(p.p_crossover);
+    a.thr_m = thr(p.p_mutation);
+    a.thr_kb = thr(p.p_kb);
+}
+
+int launch_breed_hook(const int32_t *pop, const int32_t *top, const int32_t *order, int64_t P,
+                      int N, const int32_t *sel, const int32_t *sigma, const pga_params &p,
+                      int32_t gen, int32_t island, int64_t p_off, int32_t *next, cudaStream_t s) {
+    BreedArgs a{};
+    fill_breed(a, p, P, N);
+    a.i32_in = pop;
+    a.i32_out = next;
+    a.top32 = top;
+    a.order = order;
+    a.sel = sel;
+    a.sigma = sigma;
+    a.p_off = p_off;
+    a.gen = (uint32_t)gen;
+    a.island = (uint32_t)island;
+    a.ldn = N;
+    a.Pcap = P;
+    const int w = breed_warps(N);
+    k_breed<<<(unsigned)((P + w - 1) / w), 32 * w, (size_t)w * (N + 1) * 2, s>>>(a);
+    PGA_LAUNCHED();
+    return PGA_OK;
+}
+
+int launch_sort_order(pga_ctx *c, cudaStream_t s) {
+    return sort_order(c->L, c->P, c->order, c->keys_in, c->keys_out, c->idx_in, c->cub_tmp,
+                      c->cub_tmp_bytes, &c->st->done, s);
+}
+
+// Phase B of a generation, after launch_sort_order.
+int launch_select_breed(pga_ctx *c, cudaStream_t s) {
+    const pga_params &p = c->p;
+    const int32_t *done = &c->st->done;
+    const int32_t *genp = &c->st->gen;
+    int rc = run_select_ops(c->L, c->P, p, 0, p.island, c->order, c->sel, c->keys_in, c->keys_out,
+                            c->idx_in, c->q, c->prefix, c->cub_tmp, c->cub_tmp_bytes, done, s,
+                            genp, true);
+    if (rc) return rc;
+    const int64_t M = 2 * ((c->P - p.elite + 1) / 2);
+    rc = run_mates(M, p, 0, p.island, c->mkeys_in, c->mkeys_out, c->m_in, c->sigma, c->cub_tmp,
+                   c->cub_tmp_bytes, done, s, genp);
+    if (rc) return rc;
+    BreedArgs a{};
+    fill_breed(a, p, c->P, c->N);
+    a.cm_in0 = c->pop[0];
+    a.cm_in1 = c->pop[1];
+    a.cm_out0 = c->pop[0];
+    a.cm_out1 = c->pop[1];
+    a.gm_out0 = c->popT[0];
+    a.gm_out1 = c->popT[1];
+    a.top16 = c->top;
+    a.order = c->order;
+    a.sel = c->sel;
+    a.sigma = c->sigma;
+    a.Pcap = c->Pcap;
+    a.p_off = (int64_t)p.island * c->P;
+    a.ldn = c->ldn;
+    a.done = done;
+    a.gen_ptr = genp;
+    const int w = breed_warps(c->N);
+    k_breed<<<(unsigned)((c->P + w - 1) / w), 32 * w, (size_t)w * (c->N + 1) * 2, s>>>(a);
+    PGA_LAUNCHED();
+    k_advance<<<1, 1, 0, s>>>(c->st);
+    PGA_LAUNCHED();
+    return PGA_OK;
+}
+
+int launch_export(pga_ctx *c, void *dev_send, cudaStream_t s) {
+    k_export<<<c->p.migrants, 128, 0, s>>>(c->L, c->top, c->order, c->pop[0], c->pop[1], c->st,
+                                           c->ldn, c->N, c->p.migrants, c->mig_bytes / c->p.migrants,
+                                           (unsigned char *)dev_send);
+    PGA_LAUNCHED();
+    return PGA_OK;
+}
+
+int launch_import(pga_ctx *c, const void *dev_recv, int32_t G, cudaStream_t s) {
+    k_import<<<1, 256, 0, s>>>((const unsigned char *)dev_recv, G, c->p.migrants,
+                               c->mig_bytes / c->p.migrants, c->order, c->P, c->L, c->top,
+                               c->pop[0], c->pop[1], c->popT[0], c->popT[1], c->st, c->ldn, c->N,
+                               c->Pcap);
+    PGA_LAUNCHED();
+    return PGA_OK;
+}
+
+}  // namespace pga

@@ -1,0 +1,198 @@
+// pga_internal.cuh — shared internals of libpga.so (product path).
+// Nothing here is shared with oracle/ (independence rule).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+
+#include "../../include/pga.h"
+
+namespace pga {
+
+// ---------------------------------------------------------------------------
+// Error plumbing: thread-local last error, return codes.
+// ---------------------------------------------------------------------------
+void set_error(const std::string &msg);
+int fail(int code, const std::string &msg);
+int cuda_fail(cudaError_t e, const char *what);
+void count_launch(int n = 1);
+
+#define PGA_CUDA(call)                                                     \
+    do {                                                                   \
+        cudaError_t _e = (call);                                           \
+        if (_e != cudaSuccess) return ::pga::cuda_fail(_e, #call);         \
+    } while (0)
+
+#define PGA_LAUNCHED()                                                     \
+    do {                                                                   \
+        ::pga::count_launch();                                             \
+        cudaError_t _e = cudaGetLastError();                               \
+        if (_e != cudaSuccess) return ::pga::cuda_fail(_e, "kernel launch");\
+    } while (0)
+
+// Philox stream tags (RNG layout).
+enum : uint32_t {
+    TAG_INIT = 1, TAG_SUS = 2, TAG_PERM = 3, TAG_TOUR = 4, TAG_XO = 5, TAG_MUT = 6, TAG_MUTV = 7
+};
+
+constexpr int TI = 8;          // rows per sweep work item
+constexpr int CB = 64;         // chromosomes per sweep warp (2 per lane)
+
+// Device-resident GA state (one island).  Read/written only by kernels.
+struct DevState {
+    int32_t gen;          // generation about to be / being evaluated
+    int32_t stall;
+    int32_t done;
+    int32_t reason;
+    int32_t best_idx;     // argmax of the last evaluated generation
+    int32_t pad0;
+    double best;          // best L of the last evaluated generation
+    double prev_best;
+    double best_ever;
+    double mean;
+    int32_t pack_error;   // set by k_pack when a label is out of range
+    int32_t pad1;
+};
+
+struct Migrant;  // layout documented in api.cu
+
+}  // namespace pga
+
+// The context (opaque at the ABI).
+struct pga_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    pga_params p{};
+    int32_t N = 0;
+    int32_t ldn = 0;       // padded gene stride of chromosome-major labels / V
+    int32_t ldc = 0;       // padded row stride of C
+    int64_t P = 0;         // pop_size (island)
+    int64_t Pcap = 0;      // capacity rounded up to CB
+    // correlation matrix
+    double *C = nullptr;
+    double *diag = nullptr;
+    // population: chromosome-major [Pcap][ldn] and gene-major [N][Pcap], double buffered
+    uint16_t *pop[2] = {nullptr, nullptr};
+    uint16_t *popT[2] = {nullptr, nullptr};
+    // fitness scratch/output
+    double *V = nullptr;   // [Pcap][ldn] per-gene fold inputs C_ii + 2 r'_i
+    double *L = nullptr;   // [Pcap]
+    uint16_t *top = nullptr;
+    // selection scratch
+    uint64_t *keys_in = nullptr, *keys_out = nullptr;
+    int32_t *idx_in = nullptr, *order = nullptr;
+    uint64_t *q = nullptr, *prefix = nullptr;
+    int32_t *sel = nullptr;
+    uint32_t *mkeys_in = nullptr, *mkeys_out = nullptr;
+    int32_t *m_in = nullptr, *sigma = nullptr;
+    void *cub_tmp = nullptr;
+    size_t cub_tmp_bytes = 0;
+    // state
+    pga::DevState *st = nullptr;
+    uint16_t *best_labels = nullptr;   // [ldn]
+    double *history = nullptr;         // [hist_cap]
+    int32_t hist_cap = 0;
+    // staging for pga_evaluate / pga_evaluate_device (never the GA buffers)
+    int32_t *stage_i32 = nullptr;      // device [Pcap][N]
+    uint16_t *evCM = nullptr, *evGM = nullptr;
+    double *evL = nullptr;
+    // migration scratch
+    int64_t mig_bytes = 0;
+    // host mirror
+    bool has_pop = false;
+    bool pending_migration = false;
+    int32_t host_gen = 0;              // host-side count of launched generations
+    // pinned host
+    pga::DevState *h_st = nullptr;
+};
+
+namespace pga {
+
+// Launch wrappers implemented in the .cu files (all stream-ordered).
+// Population buffers for a fitness launch: kernels pick buffer (*gen & 1)
+// when gen != nullptr (GA double buffer), else buffer 0.
+struct FitBufs {
+    const uint16_t *cm0, *cm1, *gm0, *gm1;
+    const int32_t *gen;
+    const int32_t *done;
+};
+int launch_pack(pga_ctx *c, const uint16_t *lab16, const int32_t *lab32, int64_t P, int ld_in,
+                uint16_t *CM, uint16_t *GM, cudaStream_t s);
+int prepare_fitness(int N);
+int launch_fitness(pga_ctx *c, const FitBufs &b, int64_t P, double *L, uint16_t *top,
+                   cudaStream_t s);
+int launch_init(pga_ctx *c, uint64_t seed, cudaStream_t s);
+int launch_stats(pga_ctx *c, int is_migration_check, cudaStream_t s);
+int launch_sort_order(pga_ctx *c, cudaStream_t s);
+int launch_select_breed(pga_ctx *c, cudaStream_t s);
+int launch_export(pga_ctx *c, void *dev_send, cudaStream_t s);
+int launch_import(pga_ctx *c, const void *dev_recv, int32_t G, cudaStream_t s);
+int launch_canonicalize_i32(int32_t *lab, int64_t P, int32_t N, cudaStream_t s);
+int launch_corr(const double *X, int32_t T, int32_t N, double *C, int32_t *status,
+                cudaStream_t s);
+
+size_t cub_tmp_needed(int64_t P);
+
+}  // namespace pga
+
+// ---------------------------------------------------------------------------
+// Device helpers
+// ---------------------------------------------------------------------------
+namespace pgad {
+
+// Philox4x32-10 (Salmon et al. SC'11), the product's own implementation.
+struct U4 {
+    uint32_t x, y, z, w;
+};
+
+__device__ __forceinline__ U4 philox(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                                      uint32_t k0, uint32_t k1) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        uint32_t lo0 = 0xD2511F53u * c0;
+        uint32_t hi0 = __umulhi(0xD2511F53u, c0);
+        uint32_t lo1 = 0xCD9E8D57u * c2;
+        uint32_t hi1 = __umulhi(0xCD9E8D57u, c2);
+        uint32_t n0 = hi1 ^ c1 ^ k0;
+        uint32_t n2 = hi0 ^ c3 ^ k1;
+        c0 = n0;
+        c1 = lo1;
+        c2 = n2;
+        c3 = lo0;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    return U4{c0, c1, c2, c3};
+}
+
+// counter = (c0, c1, gen, tag | island << 8), key = (seed_lo, seed_hi)
+__device__ __forceinline__ U4 draw(uint64_t seed, uint32_t tag, uint32_t island, uint32_t gen,
+                                    uint32_t c0, uint32_t c1) {
+    return philox(c0, c1, gen, tag | (island << 8), (uint32_t)seed, (uint32_t)(seed >> 32));
+}
+
+__device__ __forceinline__ uint32_t word(const U4 &u, int i) {
+    return i == 0 ? u.x : i == 1 ? u.y : i == 2 ? u.z : u.w;
+}
+
+__device__ __forceinline__ uint32_t scale_u32(uint32_t x, uint32_t n) {
+    return (uint32_t)(((uint64_t)x * (uint64_t)n) >> 32);
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// Summand of Eq. 8 for one cluster with readings Q2/Q3.
+__device__ __forceinline__ double cluster_term(int n_s, double c_s) {
+    const double n = (double)n_s;
+    if (n_s < 2 || !(c_s > n)) return 0.0;
+    const double n2 = n * n;
+    const double ch = fmin(c_s, n2 - 1e-9);
+    return log(n / ch) + (n - 1.0) * log((n2 - n) / (n2 - ch));
+}
+
+}  // namespace pgad
