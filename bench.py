@@ -1,0 +1,374 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 Giada–Marsili PGA hot path (BASELINE.json config 4).
+
+A step is one GA generation of the whole hot path (SURVEY §8(a) a3-a11:
+fitness sweep + fold, statistics/termination, isolate fittest, elitism,
+scaling, SUS selection, mating, crossover, mutation, canonicalisation,
+replacement; plus the elite migration all-gather every 10 generations when
+N > 1) over the C4 workload: N = 500 assets, P = 65536 chromosomes in total,
+sharded as islands over the ranks (strong scaling).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl pga|reference]
+
+Prints ONE JSON line on rank 0.  `--impl reference` times the CPU oracle
+(the reference arm of this tier) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads  # noqa: E402
+
+CONFIG = "C4"
+P_TOTAL = 65536
+SEED = 2024
+SM_COUNT = 148
+FP64_LANES_PER_SM = 64           # DFMA lanes / clk / SM (B200: 37 TF fp64 = 148*64*2*1.965G)
+
+METRIC = ("GA generation throughput, nominal pair-updates/s (N^2 * P per generation; "
+          "fitness + all operators), BASELINE config 4")
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md clocks line)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpus):
+        self.gpus = gpus
+        self.proc = None
+        self.path = os.path.join("/tmp", "pga_clocks_%d.csv" % os.getpid())
+
+    def start(self):
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "--query-gpu=" + self.FIELDS, "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.close()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                idx = int(parts[0])
+            except ValueError:
+                continue
+            if idx not in self.gpus:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                pass
+            for n, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle timing (cpu_baseline and --impl reference)
+# ---------------------------------------------------------------------------
+def oracle_generation(orc, C, pop, params, gen):
+    L, top = orc.evaluate(C, pop, nthreads=os.cpu_count() or 1)
+    return orc.step(params, pop, L, top, gen)
+
+
+def oracle_rate(C, planted, target_s=10.0, max_P=16384):
+    """Time the oracle's full generation (evaluate on all host cores + the
+    single-threaded operators) on a bounded sample population; return
+    (nominal pair-updates/s, sample size, seconds)."""
+    import oracle as orc
+    orc.build()
+    N = C.shape[0]
+    P = 256
+    while True:
+        pop = orc.canonicalize(workloads.population_mix(SEED, planted, P))
+        params = orc.default_params(pop=P, elite=10, p_m=2.0 / N, tol=-1.0, seed=SEED)
+        t = time.perf_counter()
+        oracle_generation(orc, C, pop, params, 0)
+        dt = time.perf_counter() - t
+        if dt >= 0.5 * target_s or P >= max_P:
+            return N * N * P / dt, P, dt
+        P = int(min(max_P, max(P * 2, P * target_s / max(dt, 1e-3))))
+        P = max(64, P // 64 * 64)
+
+
+def run_reference(args):
+    rank = env_int("RANK", 0)
+    if rank != 0:
+        return 0
+    import oracle as orc
+    orc.build()
+    X, planted = workloads.noh_returns(workloads.CONFIGS[CONFIG])
+    C = orc.pearson(X)
+    N = C.shape[0]
+    K, W = args.steps, args.warmup
+    # size each step so the whole run stays within ~3 minutes
+    budget = 150.0 / max(1, K + W)
+    P = 256
+    pop = orc.canonicalize(workloads.population_mix(SEED, planted, P))
+    params = orc.default_params(pop=P, elite=10, p_m=2.0 / N, tol=-1.0, seed=SEED)
+    t = time.perf_counter()
+    oracle_generation(orc, C, pop, params, 0)
+    dt = time.perf_counter() - t
+    P = int(max(64, min(P_TOTAL, P * budget / max(dt, 1e-3))) // 64 * 64)
+    pop = orc.canonicalize(workloads.population_mix(SEED, planted, P))
+    params = orc.default_params(pop=P, elite=10, p_m=2.0 / N, tol=-1.0, seed=SEED)
+    for g in range(W):
+        pop = oracle_generation(orc, C, pop, params, g)
+    t = time.perf_counter()
+    for g in range(K):
+        pop = oracle_generation(orc, C, pop, params, W + g)
+    dt = time.perf_counter() - t
+    ms = 1000.0 * dt / max(1, K)
+    value = N * N * P / (ms / 1000.0)
+    cores = os.cpu_count() or 1
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "pair-updates/s",
+        "n_gpus": args.gpus, "steps": K, "warmup": W, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (Noh-model returns, seed 50004)",
+        "config": {"workload": "C4 (N=500; oracle on a bounded sample of P=%d chromosomes per "
+                               "generation)" % P, "N": N, "population": P},
+        "cpu_baseline": {"value": value, "unit": "pair-updates/s", "cores": cores,
+                         "kind": "oracle",
+                         "sample": "%d-chromosome C4 population, full generation (evaluate on %d "
+                                   "threads + single-threaded operators)" % (P, cores)},
+        "e2e": {"value": value, "unit": "pair-updates/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="pga", choices=["pga", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    import paper_1403_4099_b200 as pga
+    from paper_1403_4099_b200.islands import GpuIsland, IslandRunner
+
+    rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    K, W = args.steps, args.warmup
+
+    X, planted = workloads.noh_returns(workloads.CONFIGS[CONFIG])
+    N = X.shape[1]
+    C = pga.pga_correlation(X, device=local)        # Eq. 7 on the device
+    P_local = P_TOTAL // world
+    params = pga.pga_params_default(
+        pop_size=P_local, elite=10, p_mutation=2.0 / N, tol=-1.0, max_gens=W + K + 2,
+        device=local, island=rank, n_islands=world, migrate_every=10, migrants=10, seed=SEED)
+
+    eng = GpuIsland(C, params)
+    runner = IslandRunner(eng)
+    eng.init(SEED)
+    stream = eng.stream
+    for _ in range(W):
+        runner.step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(list(range(torch.cuda.device_count())) if world > 1 else [local])
+    if rank == 0:
+        clocks.start()
+        time.sleep(0.3)
+    pga.pga_profile_enable(eng.ctx, True)
+    launches0 = pga.pga_launch_count()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev0.record(stream)
+    for _ in range(K):
+        runner.step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    launches = pga.pga_launch_count() - launches0
+    ms = ev0.elapsed_time(ev1)
+    prof = pga.pga_profile_read(eng.ctx)
+    pga.pga_profile_enable(eng.ctx, False)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    clk = clocks.stop() if rank == 0 else None
+    st = eng.state()
+
+    ms_step = ms / K
+    nominal = float(N) * N * P_TOTAL
+    executed_local = N * (N - 1) / 2.0 * P_local
+    value = nominal / (ms_step / 1000.0)
+
+    # roofline of the dominant kernel (k_sweep), from live CUDA events
+    sweep_ms = prof["sweep_ms"] / max(1, prof["count"])
+    fold_ms = prof["fold_ms"] / max(1, prof["count"])
+    gen_ms = prof["gen_ms"] / max(1, prof["count"])
+    achieved = executed_local / (sweep_ms / 1000.0)
+    peaks = measured_peaks()
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    peak = FP64_LANES_PER_SM * SM_COUNT * sm_max * 1e6
+    traffic = None
+    try:
+        tj = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        traffic = tj.get("k_sweep", {}).get("dram_bytes_per_launch")
+    except Exception:
+        pass
+
+    # end-to-end through the public API from host memory (rank-local), see DESIGN.md §7
+    e2e = None
+    if not args.no_e2e:
+        eng.close()
+        e2e = e2e_run(pga, torch, dist, C, params, world, min(K, 200), planted)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v, Ps, dt = oracle_rate(C, planted)
+        cpu = {"value": v, "unit": "pair-updates/s", "cores": os.cpu_count() or 1,
+               "kind": "oracle",
+               "sample": "%d-chromosome C4 population, one full oracle generation (evaluate on "
+                         "%d host threads + single-threaded operators), %.1f s"
+                         % (Ps, os.cpu_count() or 1, dt)}
+    if eng.ctx is not None:
+        eng.close()
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "pair-updates/s", "n_gpus": world,
+            "steps": K, "warmup": W, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (Noh-model returns T=2000, seed 50004; Pearson C on device)",
+            "config": {"workload": "C4: N=500, P=65536 total (%d per GPU), 1 step = 1 generation"
+                                   % P_local, "N": N, "population": P_TOTAL,
+                       "population_per_gpu": P_local, "parallelism": "islands x%d" % world,
+                       "migration": "every 10 generations, 10 elites, NCCL all-gather",
+                       "l2": "working set > L2 (two population layouts x2 buffers + 264 MB "
+                             "fold scratch per GPU); no flush"},
+            "evals_per_s": P_TOTAL / (ms_step / 1000.0),
+            "gens_per_s": 1000.0 / ms_step,
+            "executed_pair_updates_per_s": executed_local * world / (ms_step / 1000.0),
+            "kernel_ms_per_generation": {"k_sweep": sweep_ms, "k_fold": fold_ms,
+                                         "generation": gen_ms},
+            "roofline": {"bound": "alu", "kernel": "k_sweep", "achieved": achieved,
+                         "peak": peak, "unit": "pair-updates/s", "frac": achieved / peak,
+                         "traffic": traffic,
+                         "work_per_launch": "%d chromosomes x N(N-1)/2 = %.4g executed pair-updates"
+                                            % (P_local, executed_local),
+                         "peak_basis": "1 DFMA per executed pair; 64 FP64 lanes/clk/SM x 148 SMs "
+                                       "x %.0f MHz (sm_max_mhz)" % sm_max,
+                         "frac_at_measured_clock": (achieved / (FP64_LANES_PER_SM * SM_COUNT *
+                                                    clk["sm_mhz"] * 1e6))
+                         if clk and clk.get("sm_mhz") else None},
+            "gpu_launches": int(launches),
+            "clocks": clk,
+            "best_L": st["best_L"],
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def e2e_run(pga, torch, dist, C, params, world, K, planted):
+    """Same metric through the public API with HOST buffers: C copied from
+    pinned host memory (pga_create), K generations, and every step a
+    device->host read of the step's result (best L, mean L, best labels)."""
+    from paper_1403_4099_b200.islands import GpuIsland, IslandRunner
+    N = C.shape[0]
+    Cp = torch.from_numpy(np.ascontiguousarray(C)).pin_memory()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    eng = GpuIsland(Cp.numpy(), params)
+    runner = IslandRunner(eng)
+    eng.init(SEED + 1)
+    for _ in range(K):
+        runner.step()
+        st = eng.state()                 # D2H of the step's result (syncs)
+    bestL, best, _ = runner.global_best()
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
+    eng.close()
+    value = float(N) * N * P_TOTAL * K / dt
+    d2h = 56 + 2 * N          # DevState + best labels (u16)
+    return {"value": value, "unit": "pair-updates/s", "h2d_bytes_per_step": N * N * 8 / K,
+            "d2h_bytes_per_step": d2h, "steps": K, "seconds": dt,
+            "includes": "pga_create from pinned host C + init + K generations + per-step state "
+                        "read + final global best gather"}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

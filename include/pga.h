@@ -146,9 +146,12 @@ int pga_get_state(pga_ctx *ctx, int32_t *generation, int32_t *done, int32_t *rea
 /* Per-generation best L, host fp64 [n] for generations 0..n-1 (n <= gens run). */
 int pga_get_history(pga_ctx *ctx, double *best_L, int32_t n);
 
-/* Copy the population out (host int32 [pop_size][N], 1-based) and, if L is
- * not NULL, the fitness of the last evaluation (host fp64 [pop_size]). */
-int pga_get_population(pga_ctx *ctx, int32_t *labels, double *L);
+/* Copy the current population out (host int32 [pop_size][N], 1-based).  If
+ * not NULL, L (host fp64 [pop_size]) and top (host int32 [pop_size], 0-based
+ * label of the cluster with the largest Eq. 8 summand, -1 if none) receive
+ * the results of the LAST EVALUATION, i.e. of the parents of the current
+ * population once a generation has bred. */
+int pga_get_population(pga_ctx *ctx, int32_t *labels, double *L, int32_t *top);
 
 /* Replace the population (host int32 [pop_size][N], values 1..N; stored
  * canonicalised) and set the generation counter (resume, S:N/A). */
@@ -225,6 +228,16 @@ int pga_op_init(uint64_t seed, int32_t N, int64_t P, int64_t p_off, int32_t isla
 /* Number of this library's kernel launches issued so far in this process
  * (for the bench's gpu_launches claim). */
 int64_t pga_launch_count(void);
+
+/* Kernel timing with CUDA events on the ctx's stream (measurement only).
+ * pga_profile_enable(ctx, 1) starts recording, for every generation launched
+ * through pga_gen_evaluate / pga_gen_breed, the duration of the pair-sweep
+ * kernel, of the fold kernel and of the whole generation; 0 stops and clears.
+ * pga_profile_read synchronises and returns the SUMS in milliseconds and the
+ * number of generations recorded. */
+int pga_profile_enable(pga_ctx *ctx, int32_t on);
+int pga_profile_read(pga_ctx *ctx, double *sweep_ms, double *fold_ms, double *gen_ms,
+                     int32_t *count);
 
 #ifdef __cplusplus
 }

@@ -57,7 +57,10 @@ _SIGS = {
                            ct.c_void_p, ct.c_void_p]),
     "pga_get_state": (ct.c_int, [ct.c_void_p] + [ct.c_void_p] * 6),
     "pga_get_history": (ct.c_int, [ct.c_void_p, ct.c_void_p, ct.c_int32]),
-    "pga_get_population": (ct.c_int, [ct.c_void_p, ct.c_void_p, ct.c_void_p]),
+    "pga_get_population": (ct.c_int, [ct.c_void_p, ct.c_void_p, ct.c_void_p, ct.c_void_p]),
+    "pga_profile_enable": (ct.c_int, [ct.c_void_p, ct.c_int32]),
+    "pga_profile_read": (ct.c_int, [ct.c_void_p, ct.c_void_p, ct.c_void_p, ct.c_void_p,
+                                    ct.c_void_p]),
     "pga_set_population": (ct.c_int, [ct.c_void_p, ct.c_void_p, ct.c_int32]),
     "pga_migrant_bytes": (ct.c_int, [ct.c_void_p, ct.c_void_p]),
     "pga_export_migrants": (ct.c_int, [ct.c_void_p, ct.c_void_p]),
@@ -197,11 +200,23 @@ def pga_get_history(ctx, n: int) -> np.ndarray:
     return h
 
 
-def pga_get_population(ctx, P: int, N: int):
+def pga_get_population(ctx, P: int, N: int, with_top: bool = False):
     lab = np.zeros((P, N), np.int32)
     L = np.zeros(P, np.float64)
-    _check(lib().pga_get_population(ctx, _p(lab), _p(L)))
-    return lab, L
+    top = np.zeros(P, np.int32)
+    _check(lib().pga_get_population(ctx, _p(lab), _p(L), _p(top)))
+    return (lab, L, top) if with_top else (lab, L)
+
+
+def pga_profile_enable(ctx, on: bool = True):
+    _check(lib().pga_profile_enable(ctx, 1 if on else 0))
+
+
+def pga_profile_read(ctx):
+    s, f, g = ct.c_double(), ct.c_double(), ct.c_double()
+    n = ct.c_int32()
+    _check(lib().pga_profile_read(ctx, ct.byref(s), ct.byref(f), ct.byref(g), ct.byref(n)))
+    return dict(sweep_ms=s.value, fold_ms=f.value, gen_ms=g.value, count=n.value)
 
 
 def pga_set_population(ctx, labels_1based, generation: int = 0):

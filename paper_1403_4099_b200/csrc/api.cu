@@ -113,6 +113,7 @@ void free_ctx(pga_ctx *c) {
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (c->h_st) cudaFreeHost(c->h_st);
+    for (cudaEvent_t e : c->prof_ev) cudaEventDestroy(e);
     if (c->stream) cudaStreamDestroy(c->stream);
 }
 
@@ -185,8 +186,19 @@ bool is_migration_gen(const pga_ctx *c, int32_t g) {
     return c->p.n_islands > 1 && ((g + 1) % c->p.migrate_every == 0);
 }
 
+cudaEvent_t *prof_slot(pga_ctx *c) {
+    if (!c->prof) return nullptr;
+    while (c->prof_ev.size() < c->prof_used + 4) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+        c->prof_ev.push_back(e);
+    }
+    return &c->prof_ev[c->prof_used];
+}
+
 int phase_a(pga_ctx *c, int32_t g, int32_t *is_mig) {
-    TRY(launch_fitness(c, ga_bufs(c), c->P, c->L, c->top, c->stream));
+    cudaEvent_t *ev = prof_slot(c);
+    TRY(launch_fitness(c, ga_bufs(c), c->P, c->L, c->top, c->stream, ev));
     const bool mig = is_migration_gen(c, g);
     if (is_mig) *is_mig = mig ? 1 : 0;
     if (mig) {
@@ -201,6 +213,10 @@ int phase_a(pga_ctx *c, int32_t g, int32_t *is_mig) {
 int phase_b(pga_ctx *c) {
     TRY(launch_sort_order(c, c->stream));
     TRY(launch_select_breed(c, c->stream));
+    if (c->prof && c->prof_ev.size() >= c->prof_used + 4) {
+        PGA_CUDA(cudaEventRecord(c->prof_ev[c->prof_used + 3], c->stream));
+        c->prof_used += 4;
+    }
     return PGA_OK;
 }
 
@@ -530,7 +546,7 @@ int pga_get_history(pga_ctx *c, double *best_L, int32_t n) {
     return PGA_OK;
 }
 
-int pga_get_population(pga_ctx *c, int32_t *labels, double *L) {
+int pga_get_population(pga_ctx *c, int32_t *labels, double *L, int32_t *top) {
     if (!c || !labels) return fail(PGA_EINVAL, "NULL argument");
     if (!c->has_pop) return fail(PGA_ESTATE, "no population");
     PGA_CUDA(cudaSetDevice(c->device));
@@ -541,6 +557,41 @@ int pga_get_population(pga_ctx *c, int32_t *labels, double *L) {
     for (int64_t p = 0; p < c->P; ++p)
         for (int i = 0; i < c->N; ++i) labels[p * c->N + i] = (int32_t)h[p * c->ldn + i] + 1;
     if (L) PGA_CUDA(cudaMemcpy(L, c->L, sizeof(double) * c->P, cudaMemcpyDeviceToHost));
+    if (top) {
+        std::vector<uint16_t> t(c->P);
+        PGA_CUDA(cudaMemcpy(t.data(), c->top, sizeof(uint16_t) * c->P, cudaMemcpyDeviceToHost));
+        for (int64_t p = 0; p < c->P; ++p) top[p] = t[p] == 0xFFFF ? -1 : (int32_t)t[p];
+    }
+    return PGA_OK;
+}
+
+int pga_profile_enable(pga_ctx *c, int32_t on) {
+    if (!c) return fail(PGA_EINVAL, "ctx is NULL");
+    c->prof = on != 0;
+    c->prof_used = 0;
+    return PGA_OK;
+}
+
+int pga_profile_read(pga_ctx *c, double *sweep_ms, double *fold_ms, double *gen_ms, int32_t *count) {
+    if (!c) return fail(PGA_EINVAL, "ctx is NULL");
+    PGA_CUDA(cudaSetDevice(c->device));
+    PGA_CUDA(cudaStreamSynchronize(c->stream));
+    double s = 0, f = 0, g = 0;
+    int32_t n = 0;
+    for (size_t k = 0; k + 4 <= c->prof_used; k += 4) {
+        float a = 0, b = 0, d = 0;
+        PGA_CUDA(cudaEventElapsedTime(&a, c->prof_ev[k], c->prof_ev[k + 1]));
+        PGA_CUDA(cudaEventElapsedTime(&b, c->prof_ev[k + 1], c->prof_ev[k + 2]));
+        PGA_CUDA(cudaEventElapsedTime(&d, c->prof_ev[k], c->prof_ev[k + 3]));
+        s += a;
+        f += b;
+        g += d;
+        ++n;
+    }
+    if (sweep_ms) *sweep_ms = s;
+    if (fold_ms) *fold_ms = f;
+    if (gen_ms) *gen_ms = g;
+    if (count) *count = n;
     return PGA_OK;
 }
 

@@ -296,19 +296,22 @@ int prepare_fitness(int N) {
 }
 
 int launch_fitness(pga_ctx *c, const FitBufs &b, int64_t P, double *L, uint16_t *top,
-                   cudaStream_t s) {
+                   cudaStream_t s, cudaEvent_t *ev) {
     const int N = c->N;
     const int nRB = (N + TI - 1) / TI;
     const int nCB = (int)((P + CB - 1) / CB);
     const int nQ = (nCB + SWEEP_WARPS - 1) / SWEEP_WARPS;
+    if (ev) PGA_CUDA(cudaEventRecord(ev[0], s));
     k_sweep<<<(unsigned)(nRB * nQ), SWEEP_WARPS * 32, 0, s>>>(
         c->C, c->ldc, c->diag, reinterpret_cast<const uint32_t *>(b.gm0),
         reinterpret_cast<const uint32_t *>(b.gm1), b.gen, N, c->Pcap, nCB, nQ, c->V, c->ldn, b.done);
     PGA_LAUNCHED();
+    if (ev) PGA_CUDA(cudaEventRecord(ev[1], s));
     const int fw = fold_warps(N);
     k_fold<<<(unsigned)((P + fw - 1) / fw), fw * 32, fold_smem(N), s>>>(
         b.cm0, b.cm1, b.gen, c->ldn, c->V, N, P, L, top, b.done);
     PGA_LAUNCHED();
+    if (ev) PGA_CUDA(cudaEventRecord(ev[2], s));
     return PGA_OK;
 }
 

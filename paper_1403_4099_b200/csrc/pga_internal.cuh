@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string>
+#include <vector>
 
 #include "../../include/pga.h"
 
@@ -105,6 +106,10 @@ struct pga_ctx {
     int32_t host_gen = 0;              // host-side count of launched generations
     // pinned host
     pga::DevState *h_st = nullptr;
+    // profiling (pga_profile_enable): per generation 4 events
+    bool prof = false;
+    std::vector<cudaEvent_t> prof_ev;   // groups of 4: gen start, sweep end, fold end, gen end
+    size_t prof_used = 0;
 };
 
 namespace pga {
@@ -120,8 +125,10 @@ struct FitBufs {
 int launch_pack(pga_ctx *c, const uint16_t *lab16, const int32_t *lab32, int64_t P, int ld_in,
                 uint16_t *CM, uint16_t *GM, cudaStream_t s);
 int prepare_fitness(int N);
+// ev (optional): 3 events recorded before the sweep, between sweep and
+// fold, and after the fold.
 int launch_fitness(pga_ctx *c, const FitBufs &b, int64_t P, double *L, uint16_t *top,
-                   cudaStream_t s);
+                   cudaStream_t s, cudaEvent_t *ev = nullptr);
 int launch_init(pga_ctx *c, uint64_t seed, cudaStream_t s);
 int launch_stats(pga_ctx *c, int is_migration_check, cudaStream_t s);
 int launch_sort_order(pga_ctx *c, cudaStream_t s);

@@ -22,6 +22,11 @@ def pga():
     return p
 
 
+def _par(pga, P, **kw):
+    kw.setdefault("elite", min(10, P - 1))
+    return pga.pga_params_default(pop_size=P, **kw)
+
+
 def _assert_L(Lg, Lo):
     err = np.abs(np.asarray(Lg) - np.asarray(Lo)) / np.maximum(1.0, np.abs(Lo))
     assert err.max() <= TOL, "max rel err %g at %d" % (err.max(), int(err.argmax()))
@@ -50,7 +55,7 @@ def test_fitness_parity_random(pga, orc, N, P):
     C = _rand_C(orc, N, seed=N * 1000 + P)
     planted = orc.canonicalize(np.random.default_rng(N).integers(0, max(1, N // 4), N))
     lab = workloads.population_mix(N + P, planted, P)
-    params = pga.pga_params_default(pop_size=max(P, 2))
+    params = _par(pga, max(P, 2))
     ctx = pga.pga_create(C, params)
     try:
         Lg = pga.pga_evaluate(ctx, lab + 1)
@@ -64,7 +69,7 @@ def test_fitness_parity_random(pga, orc, N, P):
 def test_fitness_adversarial(pga, orc, N):
     C = _rand_C(orc, N, seed=7 + N)
     lab = workloads.adversarial_population(N)
-    ctx = pga.pga_create(C, pga.pga_params_default(pop_size=8))
+    ctx = pga.pga_create(C, _par(pga, 8))
     try:
         Lg = pga.pga_evaluate(ctx, lab + 1)
         # identity matrix -> every partition 0; perfectly correlated
@@ -78,14 +83,14 @@ def test_fitness_adversarial(pga, orc, N):
 
 def test_fitness_identity_and_clamp(pga, orc):
     N = 12
-    ctx = pga.pga_create(np.eye(N), pga.pga_params_default(pop_size=8))
+    ctx = pga.pga_create(np.eye(N), _par(pga, 8))
     try:
         lab = np.random.default_rng(1).integers(1, N + 1, (8, N))
         assert (pga.pga_evaluate(ctx, lab) == 0.0).all()
     finally:
         pga.pga_destroy(ctx)
     C = np.ones((6, 6))
-    ctx = pga.pga_create(C, pga.pga_params_default(pop_size=4))
+    ctx = pga.pga_create(C, _par(pga, 4))
     try:
         lab = np.array([[1] * 6, [1, 1, 1, 2, 2, 2], [1, 2, 3, 4, 5, 6]])
         Lg = pga.pga_evaluate(ctx, lab)
@@ -97,7 +102,7 @@ def test_fitness_identity_and_clamp(pga, orc):
 
 
 def test_fitness_label_range_rejected(pga, orc):
-    ctx = pga.pga_create(np.eye(5), pga.pga_params_default(pop_size=4))
+    ctx = pga.pga_create(np.eye(5), _par(pga, 4))
     try:
         with pytest.raises(pga.PgaError):
             pga.pga_evaluate(ctx, np.array([[1, 2, 6, 1, 1]]))
@@ -111,7 +116,7 @@ def test_fitness_chunking_beyond_capacity(pga, orc):
     N, P = 20, 300
     C = _rand_C(orc, N, seed=3)
     lab = np.random.default_rng(2).integers(0, 6, (P, N))
-    ctx = pga.pga_create(C, pga.pga_params_default(pop_size=64))
+    ctx = pga.pga_create(C, _par(pga, 64))
     try:
         Lg = pga.pga_evaluate(ctx, lab + 1)
     finally:
@@ -125,7 +130,7 @@ def test_fitness_top_label(pga, orc):
     C = _rand_C(orc, N, seed=11)
     planted = orc.canonicalize(np.random.default_rng(4).integers(0, 6, N))
     lab = orc.canonicalize(workloads.population_mix(5, planted, P))
-    ctx = pga.pga_create(C, pga.pga_params_default(pop_size=P))
+    ctx = pga.pga_create(C, _par(pga, P))
     try:
         dl = torch.from_numpy(lab.astype(np.int16)).cuda()
         L = torch.zeros(P, dtype=torch.float64, device="cuda")
@@ -158,7 +163,7 @@ def test_fitness_full_size_sampled(pga, orc, cfg, P, sample):
     C, planted = _corr(orc, workloads.CONFIGS[cfg])
     N = C.shape[0]
     lab = workloads.population_mix(99, planted, P)
-    ctx = pga.pga_create(C, pga.pga_params_default(pop_size=P))
+    ctx = pga.pga_create(C, _par(pga, P))
     try:
         dl = torch.from_numpy(lab.astype(np.int16)).cuda()
         L = torch.zeros(P, dtype=torch.float64, device="cuda")
@@ -204,7 +209,7 @@ def test_op_select(pga, orc, P, E, selection, scaling):
     rng = np.random.default_rng(P + 7 * selection + scaling)
     L = np.round(rng.random(P) * 50, 3)          # include exact ties
     L[rng.integers(0, P, max(1, P // 10))] = 0.0
-    params = pga.pga_params_default(pop_size=P, elite=E, selection=selection, scaling=scaling,
+    params = _par(pga, P, elite=E, selection=selection, scaling=scaling,
                                     tournament_k=3, seed=12345)
     og, sg = pga.pga_op_select(L, params, gen=17, island=2)
     oo, so = orc.select(L, E, selection=selection, tour_k=3, scaling=scaling, seed=12345,
@@ -214,7 +219,7 @@ def test_op_select(pga, orc, P, E, selection, scaling):
 
 
 def test_op_select_zero_fitness_fallback(pga, orc):
-    params = pga.pga_params_default(pop_size=50, elite=2, scaling=1, seed=3)
+    params = _par(pga, 50, elite=2, scaling=1, seed=3)
     og, sg = pga.pga_op_select(np.zeros(50), params, gen=1)
     oo, so = orc.select(np.zeros(50), 2, scaling=1, seed=3, gen=1)
     assert np.array_equal(sg, so)
@@ -236,7 +241,7 @@ def test_op_breed(pga, orc, N, P, pc, pm, pkb):
     pop = orc.canonicalize(rng.integers(0, max(2, N // 3), (P, N)))
     L, top = orc.evaluate(C, pop)
     E = min(10, P - 1)
-    params = pga.pga_params_default(pop_size=P, elite=E, p_crossover=pc, p_mutation=pm, p_kb=pkb,
+    params = _par(pga, P, elite=E, p_crossover=pc, p_mutation=pm, p_kb=pkb,
                                     seed=2024)
     o, sel = orc.select(L, E, seed=2024, gen=5, island=1)
     sig = orc.mates(len(sel), seed=2024, gen=5, island=1)
@@ -272,27 +277,64 @@ def _gpu_steps(pga, C, params, gens):
     return r, hist, pop - 1, L
 
 
-@pytest.mark.parametrize("cfg,P,gens,pm", [("C1", 128, 30, 0.1), ("C3", 512, 12, 0.02)])
-def test_generation_trajectory_matches_oracle(pga, orc, cfg, P, gens, pm):
-    """Same seed, same Philox streams: the GPU run and the oracle run produce
-    the same best-L history and the same final best partition (they could only
-    diverge on a last-bit near-tie of two distinct L values, which these
-    seeds do not hit)."""
-    C, planted = _corr(orc, workloads.CONFIGS[cfg])
-    params = pga.pga_params_default(pop_size=P, max_gens=gens, tol=-1.0, p_mutation=pm, seed=5)
-    r, hist, _, _ = _gpu_steps(pga, C, params, gens)
-    op = orc.default_params(pop=P, max_gens=gens, tol=-1.0, p_m=pm, seed=5)
-    ro = orc.run(C, op)
-    assert r["gens_run"] == ro["gens_run"] == gens
-    _assert_L(hist, ro["history"])
-    assert np.array_equal(r["best_labels"] - 1, ro["best_labels"])
+@pytest.mark.parametrize("cfg,P,gens,pm", [("C1", 128, 25, 0.1), ("C3", 512, 8, 0.02),
+                                           ("C4", 1024, 3, 0.004)])
+def test_generation_lockstep(pga, orc, cfg, P, gens, pm):
+    """Generation by generation: (a) the GPU's fitness of the resident
+    population matches the oracle's, and (b) given the GPU's own fitness
+    vector and top labels, the oracle's operators produce bit-for-bit the
+    population the GPU bred.  (Free-running GPU and oracle trajectories may
+    drift apart after a last-bit near-tie of two distinct L values flips a
+    rank; (a)+(b) is the equivalence that holds at every step.)"""
+    C, _ = _corr(orc, workloads.CONFIGS[cfg])
+    N = C.shape[0]
+    params = _par(pga, P, max_gens=gens + 1, tol=-1.0, p_mutation=pm, seed=5)
+    op = orc.default_params(pop=P, max_gens=gens + 1, tol=-1.0, p_m=pm, seed=5)
+    ctx = pga.pga_create(C, params)
+    try:
+        pga.pga_init(ctx, 5)
+        pop, _ = pga.pga_get_population(ctx, P, N)
+        assert np.array_equal(pop - 1, orc.init_population(5, N, P))
+        for g in range(gens):
+            pga.pga_generation(ctx)
+            nxt, L, top = pga.pga_get_population(ctx, P, N, with_top=True)
+            Lo, _ = orc.evaluate(C, pop - 1, nthreads=8)
+            _assert_L(L, Lo)
+            want = orc.step(op, pop - 1, L, top, gen=g)
+            assert np.array_equal(nxt - 1, want), "generation %d" % g
+            pop = nxt
+    finally:
+        pga.pga_destroy(ctx)
+
+
+def test_graph_run_equals_stepwise(pga, orc):
+    """pga_run (CUDA-graph replay) and pga_generation calls are the same
+    computation: bit-identical populations and histories."""
+    C, _ = _corr(orc, workloads.CONFIGS["C1"])
+    N, P, G = C.shape[0], 128, 37
+    params = _par(pga, P, max_gens=G, tol=-1.0, seed=8)
+    ctx = pga.pga_create(C, params)
+    try:
+        r = pga.pga_run(ctx, G, 8, N)
+        popA, LA = pga.pga_get_population(ctx, P, N)
+        hA = pga.pga_get_history(ctx, G)
+        pga.pga_init(ctx, 8)
+        for _ in range(G):
+            pga.pga_generation(ctx)
+        popB, LB = pga.pga_get_population(ctx, P, N)
+        hB = pga.pga_get_history(ctx, G)
+        stB = pga.pga_get_state(ctx, N)
+    finally:
+        pga.pga_destroy(ctx)
+    assert np.array_equal(popA, popB) and np.array_equal(LA, LB) and np.array_equal(hA, hB)
+    assert r["best_L"] == stB["best_L"] and np.array_equal(r["best_labels"], stB["best_labels"])
 
 
 def test_run_recovers_planted_C1(pga, orc):
     C, planted = _corr(orc, workloads.CONFIGS["C1"])
     ok = 0
     for seed in range(1, 11):
-        params = pga.pga_params_default(pop_size=128, max_gens=100, tol=-1.0, seed=seed)
+        params = _par(pga, 128, max_gens=100, tol=-1.0, seed=seed)
         r, _, _, _ = _gpu_steps(pga, C, params, 100)
         ok += np.array_equal(r["best_labels"] - 1, planted)
     assert ok >= 9
@@ -302,7 +344,7 @@ def test_run_recovers_planted_C3_device_pearson(pga, orc):
     X, planted = workloads.noh_returns(workloads.CONFIGS["C3"])
     C = pga.pga_correlation(X)                # C computed on device (config 3)
     assert np.abs(C - orc.pearson(X)).max() <= 1e-12
-    params = pga.pga_params_default(pop_size=4096, max_gens=500, tol=-1.0,
+    params = _par(pga, 4096, max_gens=500, tol=-1.0,
                                     p_mutation=2.0 / 100, seed=3)
     r, hist, pop, L = _gpu_steps(pga, C, params, 500)
     assert np.array_equal(r["best_labels"] - 1, planted)
@@ -318,7 +360,7 @@ def test_run_C2_matches_brute_force(pga, orc):
     C = orc.pearson(X)
     best, Lb, count = orc.brute_force(C)
     assert count == 115975
-    params = pga.pga_params_default(pop_size=1024, seed=1)   # Table 3 termination
+    params = _par(pga, 1024, seed=1)   # Table 3 termination
     r, _, _, _ = _gpu_steps(pga, C, params, 0)
     assert r["best_L"] <= Lb + TOL * max(1, Lb)
     assert abs(r["best_L"] - Lb) <= TOL * max(1, Lb)
@@ -326,14 +368,14 @@ def test_run_C2_matches_brute_force(pga, orc):
 
 def test_run_deterministic(pga, orc):
     C, _ = _corr(orc, workloads.CONFIGS["C1"])
-    params = pga.pga_params_default(pop_size=256, max_gens=40, tol=-1.0, seed=9)
+    params = _par(pga, 256, max_gens=40, tol=-1.0, seed=9)
     a = _gpu_steps(pga, C, params, 40)
     b = _gpu_steps(pga, C, params, 40)
     assert np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2]) and np.array_equal(a[3], b[3])
 
 
 def test_stall_termination(pga, orc):
-    params = pga.pga_params_default(pop_size=64, max_gens=400, tol=1e-5, stall_gens=50, seed=3)
+    params = _par(pga, 64, max_gens=400, tol=1e-5, stall_gens=50, seed=3)
     r, _, _, _ = _gpu_steps(pga, np.eye(8), params, 0)
     ro = orc.run(np.eye(8), orc.default_params(pop=64, seed=3))
     assert r["reason"] == 1 == ro["reason"]
@@ -344,7 +386,7 @@ def test_set_get_population_roundtrip(pga, orc):
     C = _rand_C(orc, 30, seed=1)
     P = 100
     lab = np.random.default_rng(3).integers(1, 31, (P, 30))
-    ctx = pga.pga_create(C, pga.pga_params_default(pop_size=P, seed=4))
+    ctx = pga.pga_create(C, _par(pga, P, seed=4))
     try:
         pga.pga_set_population(ctx, lab, generation=3)
         got, _ = pga.pga_get_population(ctx, P, 30)
