@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpga.so")
+LIB_PATH = os.environ.get("PGA_LIB") or os.path.join(_HERE, "libpga.so")
 
 PGA_OK, PGA_EINVAL, PGA_ENOMEM, PGA_EDEVICE, PGA_ENUMERIC, PGA_ESTATE = 0, -1, -2, -3, -4, -5
 PGA_SEL_SUS, PGA_SEL_TOURNAMENT = 0, 1

@@ -31,18 +31,24 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
+    target = out or LIB
+    if out is None and not force and not _stale():
         return LIB
-    tmp = LIB + ".tmp%d" % os.getpid()
-    cmd = [NVCC] + FLAGS + ["-o", tmp] + [os.path.join(CSRC, s) for s in SOURCES]
+    tmp = target + ".tmp%d" % os.getpid()
+    cmd = [NVCC] + FLAGS + ["-D" + d for d in defines] + ["-o", tmp] + \
+        [os.path.join(CSRC, s) for s in SOURCES]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd, cwd=CSRC)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
-    print(LIB)
+    args = sys.argv[1:]
+    out = None
+    defs = [a[2:] for a in args if a.startswith("-D")]
+    if "-o" in args:
+        out = args[args.index("-o") + 1]
+    print(build(force="--force" in args, verbose=True, out=out, defines=defs))

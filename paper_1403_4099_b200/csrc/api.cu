@@ -109,7 +109,8 @@ void free_ctx(pga_ctx *c) {
     void *ptrs[] = {c->C, c->diag, c->pop[0], c->pop[1], c->popT[0], c->popT[1], c->V, c->L,
                     c->top, c->keys_in, c->keys_out, c->idx_in, c->order, c->q, c->prefix,
                     c->sel, c->mkeys_in, c->mkeys_out, c->m_in, c->sigma, c->cub_tmp, c->st,
-                    c->best_labels, c->history, c->stage_i32, c->evCM, c->evGM, c->evL};
+                    c->best_labels, c->history, c->stage_i32, c->evCM, c->evGM, c->evL,
+                    c->counters};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (c->h_st) cudaFreeHost(c->h_st);
@@ -175,8 +176,8 @@ FitBufs ga_bufs(pga_ctx *c) {
     FitBufs b;
     b.cm0 = c->pop[0];
     b.cm1 = c->pop[1];
-    b.gm0 = c->popT[0];
-    b.gm1 = c->popT[1];
+    b.tm0 = &c->tmLab[0];
+    b.tm1 = &c->tmLab[1];
     b.gen = &c->st->gen;
     b.done = &c->st->done;
     return b;
@@ -268,6 +269,7 @@ int ensure_eval_bufs(pga_ctx *c) {
     PGA_CUDA(cudaMemsetAsync(c->evCM, 0, sizeof(uint16_t) * (size_t)c->Pcap * c->ldn, c->stream));
     PGA_CUDA(cudaMemsetAsync(c->evGM, 0, sizeof(uint16_t) * (size_t)c->N * c->Pcap, c->stream));
     PGA_CUDA(cudaStreamSynchronize(c->stream));
+    TRY(make_label_tmap(&c->tmLabEv, c->evGM, c->N, c->Pcap));
     return PGA_OK;
 }
 
@@ -317,7 +319,7 @@ int pga_create(const double *C, int32_t N, const pga_params *p, pga_ctx **out) {
     c->device = p->device;
     c->p = *p;
     c->N = N;
-    c->ldn = (int32_t)round_up(N, 8);
+    c->ldn = (int32_t)round_up(N, 16);   // fitness tiles write 16 rows per warp
     c->ldc = (int32_t)round_up(N, 8);
     c->P = p->pop_size;
     c->Pcap = round_up(p->pop_size, CB);
@@ -352,7 +354,10 @@ int pga_create(const double *C, int32_t N, const pga_params *p, pga_ctx **out) {
     rc = rc ? rc : dalloc(&c->sigma, (size_t)c->Pcap + 2);
     rc = rc ? rc : dalloc(&c->st, 1);
     rc = rc ? rc : dalloc(&c->best_labels, (size_t)c->ldn);
+    rc = rc ? rc : dalloc(&c->counters, (size_t)(c->Pcap / CB));
     if (rc) return bail(rc);
+    e = cudaMemsetAsync(c->counters, 0, sizeof(uint32_t) * (size_t)(c->Pcap / CB), c->stream);
+    if (e != cudaSuccess) return bail(cuda_fail(e, "cudaMemset counters"));
     c->cub_tmp_bytes = cub_tmp_needed(c->Pcap + 2);
     rc = dalloc((unsigned char **)&c->cub_tmp, c->cub_tmp_bytes);
     if (rc) return bail(rc);
@@ -378,6 +383,9 @@ int pga_create(const double *C, int32_t N, const pga_params *p, pga_ctx **out) {
         if (e != cudaSuccess) return bail(cuda_fail(e, "copy C"));
     }
     rc = prepare_fitness(N);
+    if (!rc) rc = make_c_tmap(&c->tmC, c->C, N, c->ldc);
+    if (!rc) rc = make_label_tmap(&c->tmLab[0], c->popT[0], N, c->Pcap);
+    if (!rc) rc = make_label_tmap(&c->tmLab[1], c->popT[1], N, c->Pcap);
     if (rc) return bail(rc);
     rc = ensure_history(c, p->max_gens);
     if (rc) return bail(rc);
@@ -416,7 +424,7 @@ int pga_evaluate(pga_ctx *c, const int32_t *labels, int64_t P, double *out_L) {
         PGA_CUDA(cudaMemcpyAsync(c->stage_i32, labels + p0 * c->N, sizeof(int32_t) * (size_t)n * c->N,
                                  cudaMemcpyHostToDevice, c->stream));
         TRY(launch_pack(c, nullptr, c->stage_i32, n, c->N, c->evCM, c->evGM, c->stream));
-        FitBufs b{c->evCM, c->evCM, c->evGM, c->evGM, nullptr, nullptr};
+        FitBufs b{c->evCM, c->evCM, &c->tmLabEv, &c->tmLabEv, nullptr, nullptr};
         TRY(launch_fitness(c, b, n, c->evL, nullptr, c->stream));
         int32_t perr = 0;
         PGA_CUDA(cudaMemcpyAsync(out_L + p0, c->evL, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
@@ -437,7 +445,7 @@ int pga_evaluate_device(pga_ctx *c, const uint16_t *labels_dev, int64_t P, doubl
         TRY(ensure_eval_bufs(c));
     }
     TRY(launch_pack(c, labels_dev, nullptr, P, c->N, c->evCM, c->evGM, s));
-    FitBufs b{c->evCM, c->evCM, c->evGM, c->evGM, nullptr, nullptr};
+    FitBufs b{c->evCM, c->evCM, &c->tmLabEv, &c->tmLabEv, nullptr, nullptr};
     return launch_fitness(c, b, P, L_dev, top_dev, s);
 }
 

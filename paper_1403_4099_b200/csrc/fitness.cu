@@ -1,19 +1,16 @@
 // fitness.cu — batched Giada–Marsili fitness (Eq. 5, 6, 8).
 //
-// Two kernels per evaluation:
-//   k_sweep  the O(N^2 P) masked pair sweep.  One warp = 64 chromosomes
-//            (two per lane) x TI = 8 rows i0..i0+7; it walks the columns j > i
-//            of its rows and accumulates r'_i = sum_{j>i, s_j = s_i} C_ij in
-//            fp64.  The label test is a packed fp16 compare (labels are stored
-//            as raw 16-bit patterns, exact and never NaN for N < 31744) whose
-//            1.0h/0.0h result, placed in the high word of a double, is exactly
-//            2^-63 or 0; one DFMA then adds C_ij * 2^-63 or 0.  Per pair: one
-//            HSET2 + one DFMA.  Output V[p][i] = C_ii + 2 r'_i.
-//   k_fold   warp per chromosome: n_s by __match_any_sync/popc (exact),
+// One kernel per evaluation (k_fitness, below):
+//   sweep    the O(N^2 P) masked pair sweep: every row i of every
+//            chromosome accumulates r'_i = sum_{j>i, s_j = s_i} C_ij in fp64
+//            (3 SASS instructions per pair, see k_fitness).  V = C_ii + 2 r'_i.
+//   fold     warp per chromosome (fused, last CTA per chromosome block): n_s by __match_any_sync/popc (exact),
 //            c_s = sum_{i in s} V[p][i] in a fixed order (pointer-jumping
 //            group sums, no float atomics -> deterministic), then Eq. 8 with
 //            readings Q1-Q3, L = 1/2 sum f_s and top = argmax f_s.
 #include <cuda_runtime.h>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_fp16.h>
 
 #include "pga_internal.cuh"
@@ -21,16 +18,6 @@
 namespace {
 
 using namespace pgad;
-
-__device__ __forceinline__ uint32_t heq(uint32_t a, uint32_t b) {
-    uint32_t d;
-    asm("set.eq.f16x2.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
-    return d;
-}
-
-// high word = 0x3C00xxxx pattern from heq (low half is always 0 by
-// construction) -> the double 2^-63 or +0.
-__device__ __forceinline__ double mask_d(uint32_t h) { return __hiloint2double((int)h, 0); }
 
 // ---------------------------------------------------------------------------
 // k_pack: caller labels -> the two internal layouts.
@@ -75,198 +62,330 @@ __global__ void k_pack(const uint16_t *__restrict__ lab16, const int32_t *__rest
 }
 
 // ---------------------------------------------------------------------------
-// k_sweep
-// grid.x = nRB (row blocks, ascending = longest first) * nQ; block = 4 warps,
-// warp w handles chromosome block cb = q*4 + w of row block rb.
+// k_fitness: TMA-pipelined pair sweep + fused fold.
+//
+// CTA tile = 32 chromosomes (one per lane) x RT = 64 rows (four consumer
+// warps x 16 rows).  A producer warp streams the tile's columns j in chunks
+// of KC through NSTAGE shared-memory stages with TMA (cp.async.bulk.tensor,
+// mbarrier complete_tx): per stage the gene-major labels [KC][32] u16 and
+// the C strip [KC][RT] fp64 (C is symmetric, so C[j][i0..i0+RT) is the
+// contiguous row segment).  Out-of-range rows/columns are zero-filled by TMA
+// and never match (row labels NaN) or are never visited.
+//
+// Inner step (two rows r, r+1 of one chromosome against column j):
+//   ld.shared.v4  {lo_r, hi_r, lo_r1, hi_r1} = C[j][r..r+1]   (broadcast)
+//   HSETP2        p|q = (s_r, s_r1) == (s_j, s_j)   packed fp16 compare of
+//                 the raw 16-bit labels (exact, never NaN for labels < 31744)
+//   SEL x2        hi := p ? hi : 0  (in place)
+//   DADD x2       acc_r += {lo, hi}
+// A non-match adds the positive denormal {lo, 0} < 2^-1022, which rounds away
+// against any normal accumulator and cannot change V = C_ii + 2 acc.
+// CTAs are ordered chromosome-block-major; the last CTA to finish a block
+// (atomic counter, threadfence pattern) folds its chromosomes while V is
+// still in L2.
 // ---------------------------------------------------------------------------
-constexpr int SWEEP_WARPS = 4;
+constexpr int KC = 32;                  // columns per stage
+constexpr int NSTAGE = 3;
+constexpr int CW = 4;                   // consumer warps
+constexpr int WR = 16;                  // rows per consumer warp
+constexpr int RT = CW * WR;             // rows per CTA tile
+constexpr int LAB_BYTES = KC * pga::CB * 2;
+constexpr int CST_BYTES = KC * RT * 8;
+constexpr int STAGE_BYTES = LAB_BYTES + CST_BYTES;
+constexpr int FIT_THREADS = (CW + 1) * 32;
+static_assert(KC % WR == 0, "a warp's rows must not straddle two chunks");
 
-__global__ void __launch_bounds__(SWEEP_WARPS * 32)
-k_sweep(const double *__restrict__ C, int ldc, const double *__restrict__ diag,
-        const uint32_t *__restrict__ GM0, const uint32_t *__restrict__ GM1,
-        const int32_t *__restrict__ gen_ptr,  // gene-major labels as u32 pairs [N][Pcap/2]
-        int N, int64_t Pcap, int nCB, int nQ, double *__restrict__ V, int ldn,
-        const int32_t *__restrict__ done_flag) {
-    if (done_flag && *done_flag) return;
-    const uint32_t *GM32 = (gen_ptr && (*gen_ptr & 1)) ? GM1 : GM0;
-    const int rb = blockIdx.x / nQ;
-    const int q = blockIdx.x - rb * nQ;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int cb = q * SWEEP_WARPS + warp;
-    if (cb >= nCB) return;
-    const int i0 = rb * pga::TI;
-    const int64_t half = Pcap >> 1;
-    const uint32_t *lab = GM32 + (int64_t)cb * 32 + lane;   // + j * half
-
-    // row labels, in the compare layout: (s_i << 16) | NaN
-    uint32_t rowA[pga::TI], rowB[pga::TI];
-#pragma unroll
-    for (int r = 0; r < pga::TI; ++r) {
-        const int i = i0 + r;
-        uint32_t w = 0xFFFFFFFFu;
-        if (i < N) w = __ldg(lab + (int64_t)i * half);
-        rowA[r] = (w << 16) | 0x7FFFu;
-        rowB[r] = (w & 0xFFFF0000u) | 0x7FFFu;
-        if (i >= N) rowA[r] = rowB[r] = 0xFFFF7FFFu;   // NaN halves never match
-    }
-    double accA[pga::TI], accB[pga::TI];
-#pragma unroll
-    for (int r = 0; r < pga::TI; ++r) accA[r] = accB[r] = 0.0;
-
-    // diagonal block: columns i0+1 .. i0+7, rows r < t only (pairs j > i)
-#pragma unroll
-    for (int t = 1; t < pga::TI; ++t) {
-        const int j = i0 + t;
-        if (j < N) {
-            const uint32_t w = __ldg(lab + (int64_t)j * half);
-            const uint32_t a = w << 16;
-            const double *cj = C + (int64_t)j * ldc + i0;
-#pragma unroll
-            for (int r = 0; r < t; ++r) {
-                const double c = __ldg(cj + r);
-                accA[r] = fma(c, mask_d(heq(a, rowA[r])), accA[r]);
-                accB[r] = fma(c, mask_d(heq(w, rowB[r])), accB[r]);
-            }
-        }
-    }
-
-    // main loop over full columns j >= i0 + TI
-    int j = i0 + pga::TI;
-#pragma unroll 1
-    for (; j + 1 < N; j += 2) {
-        const uint32_t w0 = __ldg(lab + (int64_t)j * half);
-        const uint32_t w1 = __ldg(lab + (int64_t)(j + 1) * half);
-        const double2 *c0p = reinterpret_cast<const double2 *>(C + (int64_t)j * ldc + i0);
-        const double2 *c1p = reinterpret_cast<const double2 *>(C + (int64_t)(j + 1) * ldc + i0);
-        double2 c0[4], c1[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            c0[k] = __ldg(c0p + k);
-            c1[k] = __ldg(c1p + k);
-        }
-        const uint32_t a0 = w0 << 16, a1 = w1 << 16;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            accA[2 * k] = fma(c0[k].x, mask_d(heq(a0, rowA[2 * k])), accA[2 * k]);
-            accB[2 * k] = fma(c0[k].x, mask_d(heq(w0, rowB[2 * k])), accB[2 * k]);
-            accA[2 * k + 1] = fma(c0[k].y, mask_d(heq(a0, rowA[2 * k + 1])), accA[2 * k + 1]);
-            accB[2 * k + 1] = fma(c0[k].y, mask_d(heq(w0, rowB[2 * k + 1])), accB[2 * k + 1]);
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            accA[2 * k] = fma(c1[k].x, mask_d(heq(a1, rowA[2 * k])), accA[2 * k]);
-            accB[2 * k] = fma(c1[k].x, mask_d(heq(w1, rowB[2 * k])), accB[2 * k]);
-            accA[2 * k + 1] = fma(c1[k].y, mask_d(heq(a1, rowA[2 * k + 1])), accA[2 * k + 1]);
-            accB[2 * k + 1] = fma(c1[k].y, mask_d(heq(w1, rowB[2 * k + 1])), accB[2 * k + 1]);
-        }
-    }
-    if (j < N) {
-        const uint32_t w0 = __ldg(lab + (int64_t)j * half);
-        const double2 *c0p = reinterpret_cast<const double2 *>(C + (int64_t)j * ldc + i0);
-        const uint32_t a0 = w0 << 16;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const double2 c = __ldg(c0p + k);
-            accA[2 * k] = fma(c.x, mask_d(heq(a0, rowA[2 * k])), accA[2 * k]);
-            accB[2 * k] = fma(c.x, mask_d(heq(w0, rowB[2 * k])), accB[2 * k]);
-            accA[2 * k + 1] = fma(c.y, mask_d(heq(a0, rowA[2 * k + 1])), accA[2 * k + 1]);
-            accB[2 * k + 1] = fma(c.y, mask_d(heq(w0, rowB[2 * k + 1])), accB[2 * k + 1]);
-        }
-    }
-
-    // epilogue: V[p][i] = C_ii + 2 * 2^63 * acc   (exact rescale)
-    const double two64 = 18446744073709551616.0;  // 2 * 2^63
-    const int64_t pA = (int64_t)cb * pga::CB + 2 * lane;
-    double *vA = V + pA * ldn + i0;
-    double *vB = vA + ldn;
-#pragma unroll
-    for (int r = 0; r < pga::TI; r += 2) {
-        double d0 = 0.0, d1 = 0.0;
-        if (i0 + r < N) d0 = __ldg(diag + i0 + r);
-        if (i0 + r + 1 < N) d1 = __ldg(diag + i0 + r + 1);
-        reinterpret_cast<double2 *>(vA)[r >> 1] = make_double2(fma(two64, accA[r], d0), fma(two64, accA[r + 1], d1));
-        reinterpret_cast<double2 *>(vB)[r >> 1] = make_double2(fma(two64, accB[r], d0), fma(two64, accB[r + 1], d1));
-    }
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *tm, int x, int y, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_u32(dst)),
+        "l"((uint64_t)tm), "r"(x), "r"(y), "r"(smem_u32(bar))
+        : "memory");
 }
 
-// ---------------------------------------------------------------------------
-// k_fold: one warp per chromosome.  smem per warp: cs[N] fp64, ns[N] int32.
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(128)
-k_fold(const uint16_t *__restrict__ CM0, const uint16_t *__restrict__ CM1,
-       const int32_t *__restrict__ gen_ptr, int ldn, const double *__restrict__ V, int N, int64_t P,
-       double *__restrict__ Lout, uint16_t *__restrict__ topout,
-       const int32_t *__restrict__ done_flag) {
-    if (done_flag && *done_flag) return;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int nw = blockDim.x >> 5;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint16_t *CM = (gen_ptr && (*gen_ptr & 1)) ? CM1 : CM0;
-    double *cs = reinterpret_cast<double *>(smem_raw) + (size_t)warp * N;
-    int32_t *ns = reinterpret_cast<int32_t *>(reinterpret_cast<double *>(smem_raw) + (size_t)nw * N) +
-                  (size_t)warp * N;
-    const int64_t p = (int64_t)blockIdx.x * nw + warp;
-    if (p >= P) return;
-    for (int k = lane; k < N; k += 32) {
-        cs[k] = 0.0;
-        ns[k] = 0;
-    }
+struct FitArgs {
+    int N, ldn, nRT, nCB, fold_warps;
+    int64_t P;
+    const double *diag;
+    double *V;
+    const uint16_t *cm0, *cm1;
+    double *L;
+    uint16_t *top;
+    const int32_t *gen, *done;
+    uint32_t *counters;
+};
+
+// Two rows (packed labels rp) against one column (col = s_j | s_j << 16);
+// caddr = shared address of C[j][r], C[j][r+1].
+__device__ __forceinline__ void pair2(uint32_t caddr, uint32_t rp, uint32_t col, double &a0, double &a1) {
+    asm("{\n\t.reg .pred p, q;\n\t.reg .b32 l0, h0, l1, h1;\n\t.reg .b64 d0, d1;\n\t"
+        "ld.shared.v4.u32 {l0, h0, l1, h1}, [%2];\n\t"
+        "setp.eq.f16x2 p|q, %3, %4;\n\t"
+        "selp.b32 h0, h0, 0, p;\n\t"
+        "selp.b32 h1, h1, 0, q;\n\t"
+        "mov.b64 d0, {l0, h0};\n\t"
+        "mov.b64 d1, {l1, h1};\n\t"
+        "add.f64 %0, %0, d0;\n\t"
+        "add.f64 %1, %1, d1;\n\t}"
+        : "+d"(a0), "+d"(a1)
+        : "r"(caddr), "r"(rp), "r"(col));
+}
+
+// 16 pair updates: rows 0..15 of this lane's chromosome against column j.
+__device__ __forceinline__ void pairs16(uint32_t caddr, uint32_t w, const uint32_t (&rp)[WR / 2],
+                                        double (&acc)[WR]) {
+    const uint32_t col = w | (w << 16);
+#pragma unroll
+    for (int q = 0; q < WR / 2; ++q) pair2(caddr + 16 * q, rp[q], col, acc[2 * q], acc[2 * q + 1]);
+}
+
+// Fold (warp-wide) of NC chromosomes at once (independent chains -> ILP):
+// n_s by match_any/popc, c_s by deterministic pointer-jumping group sums
+// (fixed order of additions, no float atomics), then Eq. 8 (Q1-Q3).
+template <int NC>
+__device__ __forceinline__ void fold_multi(const uint16_t *const (&lab)[NC], const double *const (&v)[NC],
+                                           int N, double *const (&cs)[NC], int32_t *const (&ns)[NC],
+                                           int lane, double *const (&L_out)[NC],
+                                           uint16_t *const (&top_out)[NC]) {
+#pragma unroll
+    for (int q = 0; q < NC; ++q)
+        for (int k = lane; k < N; k += 32) {
+            cs[q][k] = 0.0;
+            ns[q][k] = 0;
+        }
     __syncwarp();
-    const uint16_t *lab = CM + p * ldn;
-    const double *v = V + p * ldn;
     for (int base = 0; base < N; base += 32) {
         const int i = base + lane;
         const bool valid = i < N;
-        const uint32_t s = valid ? (uint32_t)lab[i] : (0x10000u + (uint32_t)lane);
-        double sum = valid ? v[i] : 0.0;
-        const unsigned m = __match_any_sync(0xFFFFFFFFu, s);
-        // next member of my group after me (32 = none)
-        const unsigned after = (lane == 31) ? 0u : (m & ~((2u << lane) - 1u));
-        int nxt = after ? (__ffs(after) - 1) : 32;
+        uint32_t s[NC];
+        double sum[NC];
+        unsigned m[NC];
+        int nxt[NC];
+#pragma unroll
+        for (int q = 0; q < NC; ++q) {
+            s[q] = valid ? (uint32_t)lab[q][i] : (0x10000u + (uint32_t)lane);
+            sum[q] = valid ? __ldcg(v[q] + i) : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < NC; ++q) {
+            m[q] = __match_any_sync(0xFFFFFFFFu, s[q]);
+            const unsigned after = (lane == 31) ? 0u : (m[q] & ~((2u << lane) - 1u));
+            nxt[q] = after ? (__ffs(after) - 1) : 32;
+        }
 #pragma unroll
         for (int step = 0; step < 5; ++step) {
-            const double o = __shfl_sync(0xFFFFFFFFu, sum, nxt & 31);
-            const int on = __shfl_sync(0xFFFFFFFFu, nxt, nxt & 31);
-            if (nxt < 32) {
-                sum += o;
-                nxt = on;
+#pragma unroll
+            for (int q = 0; q < NC; ++q) {
+                const double o = __shfl_sync(0xFFFFFFFFu, sum[q], nxt[q] & 31);
+                const int on = __shfl_sync(0xFFFFFFFFu, nxt[q], nxt[q] & 31);
+                if (nxt[q] < 32) {
+                    sum[q] += o;
+                    nxt[q] = on;
+                }
             }
         }
-        const int leader = __ffs(m) - 1;
-        if (valid && lane == leader) {
-            cs[s] += sum;
-            ns[s] += __popc(m);
-        }
+#pragma unroll
+        for (int q = 0; q < NC; ++q)
+            if (valid && lane == __ffs(m[q]) - 1) {
+                cs[q][s[q]] += sum[q];
+                ns[q][s[q]] += __popc(m[q]);
+            }
         __syncwarp();
     }
-    // Eq. 8 over clusters k = lane, lane+32, ...
-    double fsum = 0.0, fbest = 0.0;
-    int kbest = 0x7FFFFFFF;
-    for (int k = lane; k < N; k += 32) {
-        const int n = ns[k];
-        if (n >= 2) {
-            const double f = cluster_term(n, cs[k]);
-            fsum += f;
-            if (f > fbest) {
-                fbest = f;
-                kbest = k;
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+        double fsum = 0.0, fbest = 0.0;
+        int kbest = 0x7FFFFFFF;
+        for (int k = lane; k < N; k += 32) {
+            const int n = ns[q][k];
+            if (n >= 2) {
+                const double f = cluster_term(n, cs[q][k]);
+                fsum += f;
+                if (f > fbest) {
+                    fbest = f;
+                    kbest = k;
+                }
+            }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            fsum += __shfl_xor_sync(0xFFFFFFFFu, fsum, off);
+            const double of = __shfl_xor_sync(0xFFFFFFFFu, fbest, off);
+            const int ok = __shfl_xor_sync(0xFFFFFFFFu, kbest, off);
+            if (of > fbest || (of == fbest && ok < kbest)) {
+                fbest = of;
+                kbest = ok;
+            }
+        }
+        if (lane == 0) {
+            *L_out[q] = 0.5 * fsum;
+            if (top_out[q]) *top_out[q] = (fbest > 0.0) ? (uint16_t)kbest : (uint16_t)0xFFFF;
+        }
+    }
+    __syncwarp();
+}
+
+__global__ void __launch_bounds__(FIT_THREADS)
+k_fitness(const __grid_constant__ CUtensorMap tmLab0, const __grid_constant__ CUtensorMap tmLab1,
+          const __grid_constant__ CUtensorMap tmC, FitArgs a) {
+    if (a.done && *a.done) return;
+    const int par = (a.gen && (*a.gen & 1)) ? 1 : 0;
+    const CUtensorMap *tmLab = par ? &tmLab1 : &tmLab0;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    // keep the shared address space visible to ptxas (LDS, not generic LD)
+    unsigned char *smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + NSTAGE * STAGE_BYTES);
+    uint64_t *empty = full + NSTAGE;
+    __shared__ int s_last;
+
+    const int N = a.N;
+    const int cb = blockIdx.x / a.nRT, rt = blockIdx.x - (blockIdx.x / a.nRT) * a.nRT;
+    const int i0 = rt * RT;
+    const int nchunks = (N - i0 + KC - 1) / KC;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+    if (tid == 0) {
+        for (int s = 0; s < NSTAGE; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], CW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == CW) {
+        // ---------------- producer ----------------
+        if (lane == 0) {
+            for (int k = 0; k < nchunks; ++k) {
+                const int s = k % NSTAGE;
+                if (k >= NSTAGE) mbar_wait(&empty[s], (uint32_t)((k / NSTAGE - 1) & 1));
+                unsigned char *st = smem + s * STAGE_BYTES;
+                mbar_expect_tx(&full[s], STAGE_BYTES);
+                tma_load_2d(st, tmLab, cb * pga::CB, i0 + k * KC, &full[s]);
+                tma_load_2d(st + LAB_BYTES, &tmC, i0, i0 + k * KC, &full[s]);
+            }
+        }
+    } else {
+        // ---------------- consumers ----------------
+        const int i0w = i0 + WR * warp;     // first row of this warp
+        const int lw = WR * warp;           // its local column in chunk 0
+        const bool active = i0w < N;
+        uint32_t rp[WR / 2];
+        double acc[WR];
+#pragma unroll
+        for (int r = 0; r < WR; ++r) acc[r] = 0.0;
+        // this warp's rows are the columns lw..lw+15, i.e. chunk kw at local
+        // column lw0 (KC is a multiple of WR); earlier chunks hold only
+        // columns j < i0w and are skipped by this warp.
+        const int kw = lw / KC, lw0 = lw - kw * KC;
+        uint32_t rl[WR];
+        for (int k = 0; k < nchunks; ++k) {
+            const int s = k % NSTAGE;
+            mbar_wait(&full[s], (uint32_t)((k / NSTAGE) & 1));
+            const unsigned char *st = smem + s * STAGE_BYTES;
+            const uint16_t *labs = reinterpret_cast<const uint16_t *>(st) + lane;
+            const double *cst = reinterpret_cast<const double *>(st + LAB_BYTES) + lw;
+            const uint32_t cbase = smem_u32(cst);
+            const int jbase = i0 + k * KC;
+            int t = 0;
+            const int tend = min(KC, N - jbase);
+            if (active && k >= kw) {
+                if (k == kw) {
+                    // this lane's labels of the warp's rows
+#pragma unroll
+                    for (int r = 0; r < WR; ++r)
+                        rl[r] = (i0w + r < N) ? (uint32_t)labs[(lw0 + r) * pga::CB] : 0x7FFFu;
+#pragma unroll
+                    for (int q = 0; q < WR / 2; ++q) rp[q] = rl[2 * q] | (rl[2 * q + 1] << 16);
+                    // diagonal block: local columns lw0+1 .. lw0+15, rows r < d
+#pragma unroll
+                    for (int d = 1; d < WR; ++d) {
+                        const int lc = lw0 + d;
+                        if (jbase + lc < N) {
+                            const uint32_t sj = labs[lc * pga::CB];
+                            const double *cj = cst + lc * RT;
+#pragma unroll
+                            for (int r = 0; r < d; ++r)
+                                if (rl[r] == sj) acc[r] += cj[r];
+                        }
+                    }
+                    t = lw0 + WR;
+                }
+#pragma unroll 1
+                for (; t + 1 < tend; t += 2) {
+                    const uint32_t w0 = labs[t * pga::CB], w1 = labs[(t + 1) * pga::CB];
+                    pairs16(cbase + t * RT * 8, w0, rp, acc);
+                    pairs16(cbase + (t + 1) * RT * 8, w1, rp, acc);
+                }
+                if (t < tend) pairs16(cbase + t * RT * 8, labs[t * pga::CB], rp, acc);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
+        if (active) {
+            const int64_t p = (int64_t)cb * pga::CB + lane;
+            double *vp = a.V + p * a.ldn + i0w;
+#pragma unroll
+            for (int r = 0; r < WR; r += 2) {
+                const double d0 = (i0w + r < N) ? a.diag[i0w + r] : 0.0;
+                const double d1 = (i0w + r + 1 < N) ? a.diag[i0w + r + 1] : 0.0;
+                reinterpret_cast<double2 *>(vp)[r >> 1] = make_double2(fma(2.0, acc[r], d0), fma(2.0, acc[r + 1], d1));
             }
         }
     }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-        fsum += __shfl_xor_sync(0xFFFFFFFFu, fsum, off);
-        const double of = __shfl_xor_sync(0xFFFFFFFFu, fbest, off);
-        const int ok = __shfl_xor_sync(0xFFFFFFFFu, kbest, off);
-        if (of > fbest || (of == fbest && ok < kbest)) {
-            fbest = of;
-            kbest = ok;
+
+    // ---------------- fused fold (last CTA of the chromosome block) ----------------
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        const unsigned prev = atomicAdd(&a.counters[cb], 1u);
+        s_last = (prev == (unsigned)(a.nRT - 1));
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (warp < a.fold_warps) {
+        // two chromosomes per warp per pass
+        const uint16_t *CM = par ? a.cm1 : a.cm0;
+        double *csb = reinterpret_cast<double *>(smem) + (size_t)warp * 2 * N;
+        int32_t *nsb = reinterpret_cast<int32_t *>(reinterpret_cast<double *>(smem) + (size_t)a.fold_warps * 2 * N) +
+                       (size_t)warp * 2 * N;
+        for (int q = 2 * warp; q < pga::CB; q += 2 * a.fold_warps) {
+            const int64_t p = (int64_t)cb * pga::CB + q;
+            if (p >= a.P) break;
+            const int64_t p2 = (p + 1 < a.P) ? p + 1 : p;   // duplicate work if odd tail
+            const uint16_t *lab[2] = {CM + p * a.ldn, CM + p2 * a.ldn};
+            const double *vv[2] = {a.V + p * a.ldn, a.V + p2 * a.ldn};
+            double *cs[2] = {csb, csb + N};
+            int32_t *ns[2] = {nsb, nsb + N};
+            double *Lo[2] = {&a.L[p], &a.L[p2]};
+            uint16_t *to[2] = {a.top ? &a.top[p] : nullptr, a.top ? &a.top[p2] : nullptr};
+            fold_multi<2>(lab, vv, N, cs, ns, lane, Lo, to);
         }
     }
-    if (lane == 0) {
-        Lout[p] = 0.5 * fsum;
-        if (topout) topout[p] = (fbest > 0.0) ? (uint16_t)kbest : (uint16_t)0xFFFF;
-    }
+    if (tid == 0) a.counters[cb] = 0u;
 }
 
 }  // namespace
@@ -281,37 +400,91 @@ int launch_pack(pga_ctx *c, const uint16_t *lab16, const int32_t *lab32, int64_t
     return PGA_OK;
 }
 
-int fold_warps(int N) {
-    const size_t per = (size_t)N * (sizeof(double) + sizeof(int32_t));
-    int w = (int)((200 * 1024) / per);
-    return w < 1 ? 1 : (w > 4 ? 4 : w);
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+static int get_encode() {
+    if (g_encode) return PGA_OK;
+    cudaDriverEntryPointQueryResult q;
+    void *fn = nullptr;
+    PGA_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess) return fail(PGA_EDEVICE, "cuTensorMapEncodeTiled unavailable");
+    g_encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+    return PGA_OK;
 }
 
-size_t fold_smem(int N) { return (size_t)fold_warps(N) * N * (sizeof(double) + sizeof(int32_t)); }
+// labels: gene-major [N][Pcap] u16, box {64, KC}
+int make_label_tmap(CUtensorMap *tm, const uint16_t *GM, int N, int64_t Pcap) {
+    if (get_encode()) return PGA_EDEVICE;
+    cuuint64_t dims[2] = {(cuuint64_t)Pcap, (cuuint64_t)N};
+    cuuint64_t strides[1] = {(cuuint64_t)Pcap * 2};
+    cuuint32_t box[2] = {(cuuint32_t)CB, (cuuint32_t)KC};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = g_encode(tm, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, (void *)GM, dims, strides, box, es,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(PGA_EDEVICE, "cuTensorMapEncodeTiled (labels) failed");
+    return PGA_OK;
+}
+
+// C: [N][ldc] fp64, box {RT, KC}
+int make_c_tmap(CUtensorMap *tm, const double *C, int N, int ldc) {
+    if (get_encode()) return PGA_EDEVICE;
+    cuuint64_t dims[2] = {(cuuint64_t)ldc, (cuuint64_t)N};
+    cuuint64_t strides[1] = {(cuuint64_t)ldc * 8};
+    cuuint32_t box[2] = {(cuuint32_t)RT, (cuuint32_t)KC};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = g_encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void *)C, dims, strides, box, es,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(PGA_EDEVICE, "cuTensorMapEncodeTiled (C) failed");
+    return PGA_OK;
+}
+
+int fold_warps(int N) {
+    const size_t per = 2 * (size_t)N * (sizeof(double) + sizeof(int32_t));
+    int w = (int)((size_t)(NSTAGE * STAGE_BYTES) / per);
+    if (w < 1) w = 1;
+    return w > CW + 1 ? CW + 1 : w;
+}
+
+size_t fitness_smem(int N) {
+    const size_t fold = (size_t)fold_warps(N) * 2 * N * (sizeof(double) + sizeof(int32_t));
+    const size_t pipe = (size_t)NSTAGE * STAGE_BYTES;
+    return (fold > pipe ? fold : pipe) + 2 * NSTAGE * sizeof(uint64_t) + 128;
+}
 
 int prepare_fitness(int N) {
-    PGA_CUDA(cudaFuncSetAttribute(k_fold, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)fold_smem(N)));
+    PGA_CUDA(cudaFuncSetAttribute(k_fitness, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)fitness_smem(N)));
     return PGA_OK;
 }
 
 int launch_fitness(pga_ctx *c, const FitBufs &b, int64_t P, double *L, uint16_t *top,
                    cudaStream_t s, cudaEvent_t *ev) {
     const int N = c->N;
-    const int nRB = (N + TI - 1) / TI;
-    const int nCB = (int)((P + CB - 1) / CB);
-    const int nQ = (nCB + SWEEP_WARPS - 1) / SWEEP_WARPS;
+    FitArgs a;
+    a.N = N;
+    a.ldn = c->ldn;
+    a.nRT = (N + RT - 1) / RT;
+    a.nCB = (int)((P + CB - 1) / CB);
+    a.fold_warps = fold_warps(N);
+    a.P = P;
+    a.diag = c->diag;
+    a.V = c->V;
+    a.cm0 = b.cm0;
+    a.cm1 = b.cm1;
+    a.L = L;
+    a.top = top;
+    a.gen = b.gen;
+    a.done = b.done;
+    a.counters = c->counters;
     if (ev) PGA_CUDA(cudaEventRecord(ev[0], s));
-    k_sweep<<<(unsigned)(nRB * nQ), SWEEP_WARPS * 32, 0, s>>>(
-        c->C, c->ldc, c->diag, reinterpret_cast<const uint32_t *>(b.gm0),
-        reinterpret_cast<const uint32_t *>(b.gm1), b.gen, N, c->Pcap, nCB, nQ, c->V, c->ldn, b.done);
+    k_fitness<<<(unsigned)(a.nRT * a.nCB), FIT_THREADS, fitness_smem(N), s>>>(*b.tm0, *b.tm1, c->tmC, a);
     PGA_LAUNCHED();
-    if (ev) PGA_CUDA(cudaEventRecord(ev[1], s));
-    const int fw = fold_warps(N);
-    k_fold<<<(unsigned)((P + fw - 1) / fw), fw * 32, fold_smem(N), s>>>(
-        b.cm0, b.cm1, b.gen, c->ldn, c->V, N, P, L, top, b.done);
-    PGA_LAUNCHED();
-    if (ev) PGA_CUDA(cudaEventRecord(ev[2], s));
+    if (ev) {
+        PGA_CUDA(cudaEventRecord(ev[1], s));
+        PGA_CUDA(cudaEventRecord(ev[2], s));
+    }
     return PGA_OK;
 }
 

@@ -2,6 +2,7 @@
 // Nothing here is shared with oracle/ (independence rule).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string>
@@ -37,8 +38,7 @@ enum : uint32_t {
     TAG_INIT = 1, TAG_SUS = 2, TAG_PERM = 3, TAG_TOUR = 4, TAG_XO = 5, TAG_MUT = 6, TAG_MUTV = 7
 };
 
-constexpr int TI = 8;          // rows per sweep work item
-constexpr int CB = 64;         // chromosomes per sweep warp (2 per lane)
+constexpr int CB = 32;         // chromosomes per fitness CTA tile (one per lane)
 
 // Device-resident GA state (one island).  Read/written only by kernels.
 struct DevState {
@@ -98,6 +98,9 @@ struct pga_ctx {
     int32_t *stage_i32 = nullptr;      // device [Pcap][N]
     uint16_t *evCM = nullptr, *evGM = nullptr;
     double *evL = nullptr;
+    // TMA descriptors (sweep) and fold counters
+    CUtensorMap tmC{}, tmLab[2]{}, tmLabEv{};
+    uint32_t *counters = nullptr;      // [Pcap / CB]
     // migration scratch
     int64_t mig_bytes = 0;
     // host mirror
@@ -118,10 +121,13 @@ namespace pga {
 // Population buffers for a fitness launch: kernels pick buffer (*gen & 1)
 // when gen != nullptr (GA double buffer), else buffer 0.
 struct FitBufs {
-    const uint16_t *cm0, *cm1, *gm0, *gm1;
+    const uint16_t *cm0, *cm1;       // chromosome-major (fold)
+    const CUtensorMap *tm0, *tm1;    // gene-major TMA maps (sweep)
     const int32_t *gen;
     const int32_t *done;
 };
+int make_label_tmap(CUtensorMap *tm, const uint16_t *GM, int N, int64_t Pcap);
+int make_c_tmap(CUtensorMap *tm, const double *C, int N, int ldc);
 int launch_pack(pga_ctx *c, const uint16_t *lab16, const int32_t *lab32, int64_t P, int ld_in,
                 uint16_t *CM, uint16_t *GM, cudaStream_t s);
 int prepare_fitness(int N);
