@@ -176,6 +176,8 @@ FitBufs ga_bufs(pga_ctx *c) {
     FitBufs b;
     b.cm0 = c->pop[0];
     b.cm1 = c->pop[1];
+    b.gm0 = c->popT[0];
+    b.gm1 = c->popT[1];
     b.tm0 = &c->tmLab[0];
     b.tm1 = &c->tmLab[1];
     b.gen = &c->st->gen;
@@ -424,7 +426,7 @@ int pga_evaluate(pga_ctx *c, const int32_t *labels, int64_t P, double *out_L) {
         PGA_CUDA(cudaMemcpyAsync(c->stage_i32, labels + p0 * c->N, sizeof(int32_t) * (size_t)n * c->N,
                                  cudaMemcpyHostToDevice, c->stream));
         TRY(launch_pack(c, nullptr, c->stage_i32, n, c->N, c->evCM, c->evGM, c->stream));
-        FitBufs b{c->evCM, c->evCM, &c->tmLabEv, &c->tmLabEv, nullptr, nullptr};
+        FitBufs b{c->evCM, c->evCM, c->evGM, c->evGM, &c->tmLabEv, &c->tmLabEv, nullptr, nullptr};
         TRY(launch_fitness(c, b, n, c->evL, nullptr, c->stream));
         int32_t perr = 0;
         PGA_CUDA(cudaMemcpyAsync(out_L + p0, c->evL, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
@@ -445,7 +447,7 @@ int pga_evaluate_device(pga_ctx *c, const uint16_t *labels_dev, int64_t P, doubl
         TRY(ensure_eval_bufs(c));
     }
     TRY(launch_pack(c, labels_dev, nullptr, P, c->N, c->evCM, c->evGM, s));
-    FitBufs b{c->evCM, c->evCM, &c->tmLabEv, &c->tmLabEv, nullptr, nullptr};
+    FitBufs b{c->evCM, c->evCM, c->evGM, c->evGM, &c->tmLabEv, &c->tmLabEv, nullptr, nullptr};
     return launch_fitness(c, b, P, L_dev, top_dev, s);
 }
 

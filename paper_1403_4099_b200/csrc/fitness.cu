@@ -127,10 +127,11 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *tm, in
 
 struct FitArgs {
     int N, ldn, nRT, nCB, fold_warps;
-    int64_t P;
+    int64_t P, Pcap;
     const double *diag;
-    double *V;
+    double *V;                      // [Pcap][ldn]: V[p][i] = C_ii + 2 r'_i
     const uint16_t *cm0, *cm1;
+    const uint16_t *gm0, *gm1;      // gene-major labels [N][Pcap]
     double *L;
     uint16_t *top;
     const int32_t *gen, *done;
@@ -176,6 +177,17 @@ __device__ __forceinline__ void fold_multi(const uint16_t *const (&lab)[NC], con
             ns[q][k] = 0;
         }
     __syncwarp();
+    // software pipeline: loads of chunk c+2 are issued while chunk c folds
+    uint32_t s_n1[NC], s_n2[NC];
+    double v_n1[NC], v_n2[NC];
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+        const int i1 = lane, i2 = 32 + lane;
+        s_n1[q] = (i1 < N) ? (uint32_t)lab[q][i1] : (0x10000u + (uint32_t)lane);
+        v_n1[q] = (i1 < N) ? __ldcg(v[q] + i1) : 0.0;
+        s_n2[q] = (i2 < N) ? (uint32_t)lab[q][i2] : (0x10000u + (uint32_t)lane);
+        v_n2[q] = (i2 < N) ? __ldcg(v[q] + i2) : 0.0;
+    }
     for (int base = 0; base < N; base += 32) {
         const int i = base + lane;
         const bool valid = i < N;
@@ -185,8 +197,13 @@ __device__ __forceinline__ void fold_multi(const uint16_t *const (&lab)[NC], con
         int nxt[NC];
 #pragma unroll
         for (int q = 0; q < NC; ++q) {
-            s[q] = valid ? (uint32_t)lab[q][i] : (0x10000u + (uint32_t)lane);
-            sum[q] = valid ? __ldcg(v[q] + i) : 0.0;
+            s[q] = s_n1[q];
+            sum[q] = v_n1[q];
+            s_n1[q] = s_n2[q];
+            v_n1[q] = v_n2[q];
+            const int i3 = base + 64 + lane;
+            s_n2[q] = (i3 < N) ? (uint32_t)lab[q][i3] : (0x10000u + (uint32_t)lane);
+            v_n2[q] = (i3 < N) ? __ldcg(v[q] + i3) : 0.0;
         }
 #pragma unroll
         for (int q = 0; q < NC; ++q) {
@@ -367,22 +384,32 @@ k_fitness(const __grid_constant__ CUtensorMap tmLab0, const __grid_constant__ CU
     if (!s_last) return;
     __threadfence();
     if (warp < a.fold_warps) {
-        // two chromosomes per warp per pass
+        // NCF chromosomes per warp per pass (independent chains -> ILP)
+        constexpr int NCF = 2;
         const uint16_t *CM = par ? a.cm1 : a.cm0;
-        double *csb = reinterpret_cast<double *>(smem) + (size_t)warp * 2 * N;
-        int32_t *nsb = reinterpret_cast<int32_t *>(reinterpret_cast<double *>(smem) + (size_t)a.fold_warps * 2 * N) +
-                       (size_t)warp * 2 * N;
-        for (int q = 2 * warp; q < pga::CB; q += 2 * a.fold_warps) {
+        double *csb = reinterpret_cast<double *>(smem) + (size_t)warp * NCF * N;
+        int32_t *nsb = reinterpret_cast<int32_t *>(reinterpret_cast<double *>(smem) + (size_t)a.fold_warps * NCF * N) +
+                       (size_t)warp * NCF * N;
+        for (int q = NCF * warp; q < pga::CB; q += NCF * a.fold_warps) {
             const int64_t p = (int64_t)cb * pga::CB + q;
             if (p >= a.P) break;
-            const int64_t p2 = (p + 1 < a.P) ? p + 1 : p;   // duplicate work if odd tail
-            const uint16_t *lab[2] = {CM + p * a.ldn, CM + p2 * a.ldn};
-            const double *vv[2] = {a.V + p * a.ldn, a.V + p2 * a.ldn};
-            double *cs[2] = {csb, csb + N};
-            int32_t *ns[2] = {nsb, nsb + N};
-            double *Lo[2] = {&a.L[p], &a.L[p2]};
-            uint16_t *to[2] = {a.top ? &a.top[p] : nullptr, a.top ? &a.top[p2] : nullptr};
-            fold_multi<2>(lab, vv, N, cs, ns, lane, Lo, to);
+            const uint16_t *lab[NCF];
+            const double *vv[NCF];
+            double *cs[NCF];
+            int32_t *ns[NCF];
+            double *Lo[NCF];
+            uint16_t *to[NCF];
+#pragma unroll
+            for (int c = 0; c < NCF; ++c) {
+                const int64_t pc = (p + c < a.P) ? p + c : p;   // duplicate work at an odd tail
+                lab[c] = CM + pc * a.ldn;
+                vv[c] = a.V + pc * a.ldn;
+                cs[c] = csb + c * N;
+                ns[c] = nsb + c * N;
+                Lo[c] = &a.L[pc];
+                to[c] = a.top ? &a.top[pc] : nullptr;
+            }
+            fold_multi<NCF>(lab, vv, N, cs, ns, lane, Lo, to);
         }
     }
     if (tid == 0) a.counters[cb] = 0u;
@@ -469,6 +496,9 @@ int launch_fitness(pga_ctx *c, const FitBufs &b, int64_t P, double *L, uint16_t 
     a.nCB = (int)((P + CB - 1) / CB);
     a.fold_warps = fold_warps(N);
     a.P = P;
+    a.Pcap = c->Pcap;
+    a.gm0 = b.gm0;
+    a.gm1 = b.gm1;
     a.diag = c->diag;
     a.V = c->V;
     a.cm0 = b.cm0;

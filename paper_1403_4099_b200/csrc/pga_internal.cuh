@@ -77,7 +77,7 @@ struct pga_ctx {
     uint16_t *pop[2] = {nullptr, nullptr};
     uint16_t *popT[2] = {nullptr, nullptr};
     // fitness scratch/output
-    double *V = nullptr;   // [Pcap][ldn] per-gene fold inputs C_ii + 2 r'_i
+    double *V = nullptr;   // [Pcap][ldn] fold inputs C_ii + 2 r'_i
     double *L = nullptr;   // [Pcap]
     uint16_t *top = nullptr;
     // selection scratch
@@ -121,7 +121,8 @@ namespace pga {
 // Population buffers for a fitness launch: kernels pick buffer (*gen & 1)
 // when gen != nullptr (GA double buffer), else buffer 0.
 struct FitBufs {
-    const uint16_t *cm0, *cm1;       // chromosome-major (fold)
+    const uint16_t *cm0, *cm1;       // chromosome-major
+    const uint16_t *gm0, *gm1;       // gene-major (fold)
     const CUtensorMap *tm0, *tm1;    // gene-major TMA maps (sweep)
     const int32_t *gen;
     const int32_t *done;
