@@ -44,6 +44,7 @@ int launch_breed_hook(const int32_t *pop, const int32_t *top, const int32_t *ord
                       int N, const int32_t *sel, const int32_t *sigma, const pga_params &p,
                       int32_t gen, int32_t island, int64_t p_off, int32_t *next, cudaStream_t s);
 int launch_set_pop(pga_ctx *c, const int32_t *lab32, int par, cudaStream_t s);
+int prepare_breed(int N);
 
 static int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
@@ -385,6 +386,7 @@ int pga_create(const double *C, int32_t N, const pga_params *p, pga_ctx **out) {
         if (e != cudaSuccess) return bail(cuda_fail(e, "copy C"));
     }
     rc = prepare_fitness(N);
+    if (!rc) rc = prepare_breed(N);
     if (!rc) rc = make_c_tmap(&c->tmC, c->C, N, c->ldc);
     if (!rc) rc = make_label_tmap(&c->tmLab[0], c->popT[0], N, c->Pcap);
     if (!rc) rc = make_label_tmap(&c->tmLab[1], c->popT[1], N, c->Pcap);
@@ -744,6 +746,7 @@ int pga_op_breed(const int32_t *pop, const int32_t *top, const int32_t *order, i
     if (!pop || !top || !order || !sel || !sigma || !p || !next_out) return fail(PGA_EINVAL, "NULL argument");
     if (P < 2 || N < 2 || p->elite < 0 || p->elite >= P) return fail(PGA_EINVAL, "bad sizes");
     TRY(ensure_device(p->device));
+    TRY(prepare_breed(N));
     const int64_t M = 2 * ((P - p->elite + 1) / 2);
     HookBufs hb;
     int32_t *dpop, *dtop, *dord, *dsel, *dsig, *dnext;

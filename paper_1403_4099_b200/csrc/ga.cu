@@ -104,6 +104,7 @@ k_stats(const double *__restrict__ L, int64_t P, const uint16_t *CM0, const uint
         int hist_cap, double tol, int stall_gens, int max_gens, int mode, int migrate_every) {
     __shared__ double sb[32], ss[32];
     __shared__ int si[32];
+    __shared__ int s_improved, s_bi;
     if (st->done) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     double best = -1.0, sum = 0.0;
@@ -168,14 +169,17 @@ k_stats(const double *__restrict__ L, int64_t P, const uint16_t *CM0, const uint
             }
             if (g + 1 >= max_gens) done = 1;
             st->done = done;
-            si[0] = (best > st->best_ever) ? 1 : 0;
-            if (si[0]) st->best_ever = best;
+            const int improved = (best > st->best_ever) ? 1 : 0;
+            if (improved) st->best_ever = best;
+            s_improved = improved;
+            s_bi = bi;               // broadcast the block-wide argmax
         }
     }
     __syncthreads();
-    if (si[0]) {
+    if (s_improved) {
         const uint16_t *CM = (st->gen & 1) ? CM1 : CM0;
-        for (int i = tid; i < N; i += blockDim.x) best_labels[i] = CM[(int64_t)bi * ldn + i];
+        const int b = s_bi;
+        for (int i = tid; i < N; i += blockDim.x) best_labels[i] = CM[(int64_t)b * ldn + i];
     }
 }
 
@@ -315,75 +319,135 @@ __device__ __forceinline__ int parent_top(const BreedArgs &a, int64_t p) {
     return t == 0xFFFF ? -1 : (int)t;
 }
 
-__global__ void k_breed(BreedArgs a) {
+// CTA = BW warps x BC children (BS = BW*BC consecutive output slots).  Genes
+// are processed in chunks of 128: each lane draws ONE Philox block for 4
+// consecutive genes (the oracle's layout Philox(MUT; i>>2, o)[i&3]) and the
+// 4-bit mutation mask is redistributed with one shuffle per 32 genes; the
+// children's canonical genes go to CM directly (coalesced) and through a
+// shared-memory tile [128][BS] to the gene-major layout (BS*2-byte rows).
+constexpr int BW = 16, BC = 1, BS = BW * BC, GCH = 128;
+
+struct ChildPlan {
+    int64_t pa, pb;
+    int mode, kb_top, cut;
+    bool mutate, valid;
+    uint32_t og;
+};
+
+__device__ __forceinline__ ChildPlan plan_child(const BreedArgs &a, int64_t o, uint32_t gen) {
+    ChildPlan c{};
+    c.valid = o < a.P;
+    if (!c.valid) return c;
+    c.og = (uint32_t)(a.p_off + o);
+    if (o < a.E) {
+        c.pa = a.order[o];
+        c.mode = 0;
+        c.mutate = false;
+        return c;
+    }
+    const int64_t k = (o - a.E) >> 1;
+    const int child = (int)((o - a.E) & 1);
+    const int64_t ia = a.sel[a.sigma[2 * k]], ib = a.sel[a.sigma[2 * k + 1]];
+    c.pa = child ? ib : ia;   // the parent whose genes the child keeps
+    c.pb = child ? ia : ib;   // the other parent
+    const U4 x = draw(a.seed, pga::TAG_XO, a.island, gen, (uint32_t)k, 0u);
+    c.kb_top = -1;
+    if ((uint64_t)x.x >= a.thr_c) {
+        c.mode = 0;
+    } else if ((uint64_t)x.y < a.thr_kb) {
+        c.mode = 1;
+        c.kb_top = parent_top(a, c.pb);
+    } else {
+        c.mode = 2;
+        c.cut = 1 + (int)scale_u32(x.z, (uint32_t)(a.N - 1));
+    }
+    c.mutate = a.thr_m != 0;
+    return c;
+}
+
+__global__ void __launch_bounds__(BW * 32, 2) k_breed(BreedArgs a) {
     if (a.done && *a.done) return;
-    extern __shared__ uint16_t tables[];
-    const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t o = (int64_t)blockIdx.x * nw + warp;
-    if (o >= a.P) return;
+    extern __shared__ uint16_t sm16[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int N = a.N;
     const uint32_t gen = a.gen_ptr ? (uint32_t)*a.gen_ptr : a.gen;
     const int par = a.gen_ptr ? (int)(gen & 1u) : 0;
     const uint16_t *cm_in = par ? a.cm_in1 : a.cm_in0;
     uint16_t *cm_out = par ? a.cm_out0 : a.cm_out1;
     uint16_t *gm_out = par ? a.gm_out0 : a.gm_out1;
-    const int N = a.N;
-    uint16_t *table = tables + (size_t)warp * (N + 1);
-    table_reset(table, N + 1, lane);
-    Canon cn{table, 0};
+    uint16_t *tile = sm16;                               // [GCH][BS]
+    uint16_t *tables = sm16 + GCH * BS;                  // [BS][N+1]
+    const int64_t o0 = (int64_t)blockIdx.x * BS;
 
-    int mode = 0;          // 0 copy, 1 KB, 2 one-point
-    int64_t pa = 0, pb = 0;
-    int kb_top = -1, cut = 0, child = 0;
-    bool mutate = false;
-    if (o < a.E) {
-        pa = a.order[o];
-    } else {
-        const int64_t k = (o - a.E) >> 1;
-        child = (int)((o - a.E) & 1);
-        const int64_t ia = a.sel[a.sigma[2 * k]], ib = a.sel[a.sigma[2 * k + 1]];
-        pa = child ? ib : ia;   // the parent whose genes child keeps
-        pb = child ? ia : ib;   // the other parent
-        const U4 x = draw(a.seed, pga::TAG_XO, a.island, gen, (uint32_t)k, 0u);
-        if ((uint64_t)x.x >= a.thr_c) {
-            mode = 0;
-        } else if ((uint64_t)x.y < a.thr_kb) {
-            mode = 1;
-            kb_top = parent_top(a, pb);
-        } else {
-            mode = 2;
-            cut = 1 + (int)scale_u32(x.z, (uint32_t)(N - 1));
-        }
-        mutate = true;
+    ChildPlan cp[BC];
+    Canon cn[BC];
+#pragma unroll
+    for (int c = 0; c < BC; ++c) {
+        const int slot = warp * BC + c;
+        cp[c] = plan_child(a, o0 + slot, gen);
+        cn[c].table = tables + (size_t)slot * (N + 1);
+        cn[c].next = 0;
+        table_reset(cn[c].table, N + 1, lane);
     }
-    const uint32_t og = (uint32_t)(a.p_off + o);
-    for (int base = 0; base < N; base += 32) {
-        const int i = base + lane;
-        const bool valid = i < N;
-        uint32_t s = 0;
-        if (valid) {
-            s = parent_gene(a, cm_in, pa, i);
-            if (mode == 1) {
-                if (kb_top >= 0 && (int)parent_gene(a, cm_in, pb, i) == kb_top) s = (uint32_t)N;
-            } else if (mode == 2) {
-                if (i >= cut) s = parent_gene(a, cm_in, pb, i);
+    for (int base = 0; base < N; base += GCH) {
+#pragma unroll
+        for (int c = 0; c < BC; ++c) {
+            const ChildPlan &p = cp[c];
+            const int slot = warp * BC + c;
+            // batch this chunk's parent loads (memory-level parallelism)
+            uint32_t ga[GCH / 32], gb[GCH / 32];
+#pragma unroll
+            for (int sc = 0; sc < GCH / 32; ++sc) {
+                const int i = base + 32 * sc + lane;
+                const bool valid = p.valid && i < N;
+                ga[sc] = valid ? parent_gene(a, cm_in, p.pa, i) : 0u;
+                gb[sc] = (valid && p.mode != 0) ? parent_gene(a, cm_in, p.pb, i) : 0u;
             }
-            if (mutate && a.thr_m) {
-                const U4 u = draw(a.seed, pga::TAG_MUT, a.island, gen, (uint32_t)(i >> 2), og);
-                if ((uint64_t)word(u, i & 3) < a.thr_m) {
-                    const U4 v = draw(a.seed, pga::TAG_MUTV, a.island, gen, (uint32_t)(i >> 2), og);
+            // mutation mask of genes base+4*lane .. base+4*lane+3
+            uint32_t mbits = 0;
+            if (p.valid && p.mutate && base + 4 * lane < N) {
+                const U4 u = draw(a.seed, pga::TAG_MUT, a.island, gen, (uint32_t)((base >> 2) + lane), p.og);
+                mbits = ((uint64_t)u.x < a.thr_m ? 1u : 0u) | ((uint64_t)u.y < a.thr_m ? 2u : 0u) |
+                        ((uint64_t)u.z < a.thr_m ? 4u : 0u) | ((uint64_t)u.w < a.thr_m ? 8u : 0u);
+            }
+#pragma unroll
+            for (int sc = 0; sc < GCH / 32; ++sc) {
+                const int i = base + 32 * sc + lane;
+                const bool valid = p.valid && i < N;
+                const uint32_t mb = __shfl_sync(0xFFFFFFFFu, mbits, 8 * sc + (lane >> 2));
+                uint32_t s = ga[sc];
+                if (p.mode == 1) {
+                    if (p.kb_top >= 0 && (int)gb[sc] == p.kb_top) s = (uint32_t)N;
+                } else if (p.mode == 2) {
+                    if (i >= p.cut) s = gb[sc];
+                }
+                if (valid && ((mb >> (lane & 3)) & 1u)) {
+                    const U4 v = draw(a.seed, pga::TAG_MUTV, a.island, gen, (uint32_t)(i >> 2), p.og);
                     s = scale_u32(word(v, i & 3), (uint32_t)N);
+                }
+                const uint32_t cv = cn[c].step(s, valid, lane);
+                if (valid) {
+                    if (a.i32_out) a.i32_out[(o0 + slot) * N + i] = (int32_t)cv;
+                    else cm_out[(o0 + slot) * a.ldn + i] = (uint16_t)cv;
+                }
+                tile[(32 * sc + lane) * BS + slot] = (uint16_t)cv;
+            }
+        }
+        __syncthreads();
+        if (!a.i32_out) {
+            // gene-major rows: genes base..base+127, slots o0..o0+BS-1
+            for (int e = threadIdx.x; e < GCH * (BS / 2); e += BW * 32) {
+                const int g = e / (BS / 2), pr = e - g * (BS / 2);
+                const int i = base + g;
+                const int64_t o = o0 + 2 * pr;
+                if (i < N && o < a.P) {
+                    const uint32_t two = *reinterpret_cast<const uint32_t *>(&tile[g * BS + 2 * pr]);
+                    if (o + 1 < a.P) *reinterpret_cast<uint32_t *>(&gm_out[(int64_t)i * a.Pcap + o]) = two;
+                    else gm_out[(int64_t)i * a.Pcap + o] = (uint16_t)(two & 0xFFFF);
                 }
             }
         }
-        const uint32_t c = cn.step(s, valid, lane);
-        if (valid) {
-            if (a.i32_out) {
-                a.i32_out[o * N + i] = (int32_t)c;
-            } else {
-                cm_out[o * a.ldn + i] = (uint16_t)c;
-                gm_out[(int64_t)i * a.Pcap + o] = (uint16_t)c;
-            }
-        }
+        __syncthreads();
     }
 }
 
@@ -486,6 +550,8 @@ __global__ void k_import(const unsigned char *__restrict__ in, int G, int Em, in
 
 namespace pga {
 
+static size_t breed_smem(int N) { return ((size_t)GCH * BS + (size_t)BS * (N + 1)) * sizeof(uint16_t); }
+
 static int breed_warps(int N) {
     const size_t per = (size_t)(N + 1) * sizeof(uint16_t);
     int w = (int)((48 * 1024) / per);
@@ -507,6 +573,11 @@ int launch_init_raw(uint64_t seed, int N, int ldn, int64_t P, int64_t Pcap, int6
     k_init<<<(unsigned)((P + w - 1) / w), 32 * w, (size_t)w * (N + 1) * 2, s>>>(
         seed, N, ldn, P, Pcap, p_off, island, CM, GM, out32);
     PGA_LAUNCHED();
+    return PGA_OK;
+}
+
+int prepare_breed(int N) {
+    PGA_CUDA(cudaFuncSetAttribute(k_breed, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)breed_smem(N)));
     return PGA_OK;
 }
 
@@ -632,8 +703,7 @@ int launch_breed_hook(const int32_t *pop, const int32_t *top, const int32_t *ord
     a.island = (uint32_t)island;
     a.ldn = N;
     a.Pcap = P;
-    const int w = breed_warps(N);
-    k_breed<<<(unsigned)((P + w - 1) / w), 32 * w, (size_t)w * (N + 1) * 2, s>>>(a);
+    k_breed<<<(unsigned)((P + BS - 1) / BS), BW * 32, breed_smem(N), s>>>(a);
     PGA_LAUNCHED();
     return PGA_OK;
 }
@@ -673,8 +743,7 @@ int launch_select_breed(pga_ctx *c, cudaStream_t s) {
     a.ldn = c->ldn;
     a.done = done;
     a.gen_ptr = genp;
-    const int w = breed_warps(c->N);
-    k_breed<<<(unsigned)((c->P + w - 1) / w), 32 * w, (size_t)w * (c->N + 1) * 2, s>>>(a);
+    k_breed<<<(unsigned)((c->P + BS - 1) / BS), BW * 32, breed_smem(c->N), s>>>(a);
     PGA_LAUNCHED();
     k_advance<<<1, 1, 0, s>>>(c->st);
     PGA_LAUNCHED();
