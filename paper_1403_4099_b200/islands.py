@@ -73,8 +73,12 @@ class IslandRunner:
     def _allgather(self):
         if self.world == 1:
             self.recv.copy_(self.send)
-        else:
+        elif dist.get_backend(self.group) == "nccl":
             dist.all_gather_into_tensor(self.recv, self.send, group=self.group)
+        else:  # gloo (CPU tests): list form
+            parts = list(self.recv.chunk(self.world))
+            dist.all_gather(parts, self.send, group=self.group)
+            self.recv.copy_(torch.cat(parts))
         self.exchanges += 1
 
     def step(self):
@@ -108,9 +112,9 @@ class IslandRunner:
         if self.world > 1:
             dev = getattr(self.e, "device", torch.device("cpu"))
             r = rec.to(dev)
-            out = torch.zeros(self.world * (1 + N), dtype=torch.float64, device=dev)
-            dist.all_gather_into_tensor(out, r, group=self.group)
-            allr = out.cpu().view(self.world, 1 + N)
+            parts = [torch.zeros_like(r) for _ in range(self.world)]
+            dist.all_gather(parts, r, group=self.group)
+            allr = torch.stack(parts).cpu()
         else:
             allr = rec.view(1, 1 + N)
         k = int(torch.argmax(allr[:, 0]).item())   # first max = lowest island

@@ -1,0 +1,94 @@
+"""An oracle-backed island engine (TEST INFRASTRUCTURE) with the same
+interface as paper_1403_4099_b200.islands.GpuIsland, so the island driver and
+its collectives can be exercised on CPU (gloo, world_size 2).  The record
+layout it exports/imports is the one libpga.so uses (include/pga.h:
+{f64 L, u16 top, pad, u16 labels[N]} padded to 16 bytes)."""
+import numpy as np
+import torch
+
+import oracle as orc
+
+
+class OracleIsland:
+    def __init__(self, C, params, island, n_islands):
+        self.C = np.ascontiguousarray(C, np.float64)
+        self.N = self.C.shape[0]
+        self.p = params
+        self.island = island
+        self.G = n_islands
+        self.P = params.pop
+        self.rec = (16 + 2 * self.N + 15) // 16 * 16
+        self.device = torch.device("cpu")
+
+    def init(self, seed):
+        self.p.seed = seed
+        self.pop = orc.init_population(seed, self.N, self.P, p_off=self.island * self.P,
+                                       island=self.island)
+        self.gen = 0
+        self.best_ever = -1.0
+        self.best_labels = np.zeros(self.N, np.int32)
+        self.history = []
+
+    def _stats(self):
+        b = int(np.argmax(self.L))
+        self.history.append(float(self.L[b]))
+        if self.L[b] > self.best_ever:
+            self.best_ever = float(self.L[b])
+            self.best_labels = self.pop[b].copy()
+
+    def gen_evaluate(self):
+        self.L, self.top = orc.evaluate(self.C, self.pop)
+        mig = self.G > 1 and (self.gen + 1) % self.p.migrate_every == 0
+        if not mig:
+            self._stats()
+        return mig
+
+    def migrant_bytes(self):
+        return self.rec * self.p.migrants
+
+    def export_migrants(self, send):
+        order = orc.order(self.L)
+        buf = np.zeros(self.migrant_bytes(), np.uint8)
+        for r in range(self.p.migrants):
+            i = order[r]
+            rec = buf[r * self.rec:(r + 1) * self.rec]
+            rec[0:8] = np.frombuffer(np.float64(self.L[i]).tobytes(), np.uint8)
+            t = 0xFFFF if self.top[i] < 0 else int(self.top[i])
+            rec[8:10] = np.frombuffer(np.uint16(t).tobytes(), np.uint8)
+            rec[16:16 + 2 * self.N] = np.frombuffer(self.pop[i].astype(np.uint16).tobytes(), np.uint8)
+        send.copy_(torch.from_numpy(buf))
+
+    def import_migrants(self, recv, n_islands):
+        buf = recv.numpy()
+        Em = self.p.migrants
+        cands = []
+        for j in range(n_islands * Em):
+            rec = buf[j * self.rec:(j + 1) * self.rec]
+            L = float(np.frombuffer(rec[0:8].tobytes(), np.float64)[0])
+            t = int(np.frombuffer(rec[8:10].tobytes(), np.uint16)[0])
+            lab = np.frombuffer(rec[16:16 + 2 * self.N].tobytes(), np.uint16).astype(np.int32)
+            cands.append((L, -1 if t == 0xFFFF else t, lab))
+        used = [False] * len(cands)
+        chosen = []
+        for _ in range(Em):           # (L desc, island asc, rank asc): strict '>' scan
+            b = -1
+            for j, c in enumerate(cands):
+                if not used[j] and (b < 0 or c[0] > cands[b][0]):
+                    b = j
+            used[b] = True
+            chosen.append(cands[b])
+        order = orc.order(self.L)
+        for r, (L, t, lab) in enumerate(chosen):
+            w = order[self.P - 1 - r]
+            self.pop[w] = lab
+            self.L[w] = L
+            self.top[w] = t
+        self._stats()
+
+    def gen_breed(self):
+        self.pop = orc.step(self.p, self.pop, self.L, self.top, self.gen, island=self.island,
+                            p_off=self.island * self.P)
+        self.gen += 1
+
+    def state(self):
+        return dict(generation=self.gen, best_L=self.best_ever, best_labels=self.best_labels + 1)

@@ -429,3 +429,44 @@ def test_set_get_population_roundtrip(pga, orc):
     op = orc.default_params(pop=P, seed=4)
     nxt = orc.step(op, pop, Lo, to, gen=3)
     assert np.array_equal(got2 - 1, nxt)
+
+
+def test_gpu_islands_match_oracle(pga, orc):
+    """Two islands as two contexts on one device; the all-gather is emulated
+    by concatenating the send buffers (the migration kernels run unchanged).
+    Generation-by-generation global best L must equal the oracle's two-island
+    simulation (orc_run, n_islands = 2) while no last-bit rank flip occurs."""
+    import torch
+    C, _ = _corr(orc, workloads.CONFIGS["C1"])
+    N, P, G, gens = C.shape[0], 64, 2, 9
+    ctxs = [pga.pga_create(C, _par(pga, P, max_gens=gens, tol=-1.0, seed=31, n_islands=G,
+                                   island=g, migrate_every=4, migrants=5)) for g in range(G)]
+    try:
+        for c in ctxs:
+            pga.pga_init(c, 31)
+        nb = pga.pga_migrant_bytes(ctxs[0])
+        send = [torch.zeros(nb, dtype=torch.uint8, device="cuda") for _ in range(G)]
+        hist = []
+        for g in range(gens):
+            mig = [pga.pga_gen_evaluate(c) for c in ctxs]
+            assert all(m == ((g + 1) % 4 == 0) for m in mig)
+            if mig[0]:
+                for c, s in zip(ctxs, send):
+                    pga.pga_export_migrants(c, s)
+                torch.cuda.synchronize()
+                recv = torch.cat(send)
+                for c in ctxs:
+                    pga.pga_import_migrants(c, recv, G)
+            best = []
+            for c in ctxs:
+                lab, L = pga.pga_get_population(c, P, N)
+                best.append(L.max())
+            hist.append(max(best))
+            for c in ctxs:
+                pga.pga_gen_breed(c)
+    finally:
+        for c in ctxs:
+            pga.pga_destroy(c)
+    ref = orc.run(C, orc.default_params(pop=P, max_gens=gens, tol=-1.0, seed=31, n_islands=G,
+                                        migrate_every=4, migrants=5))
+    _assert_L(np.array(hist), ref["history"])
