@@ -163,12 +163,14 @@ __device__ __forceinline__ void pairs16(uint32_t caddr, uint32_t w, const uint32
 }
 
 // Fold (warp-wide) of NC chromosomes at once (independent chains -> ILP):
-// n_s by match_any/popc, c_s by deterministic pointer-jumping group sums
-// (fixed order of additions, no float atomics), then Eq. 8 (Q1-Q3).
+// n_s by match_any/popc; the group sum of V is gathered by the group's
+// leader (lowest lane) from a per-warp shared buffer in lane order, so the
+// order of additions is fixed (no float atomics -> deterministic); then
+// Eq. 8 (Q1-Q3) for labels up to the chromosome's largest.
 template <int NC>
 __device__ __forceinline__ void fold_multi(const uint16_t *const (&lab)[NC], const double *const (&v)[NC],
                                            int N, double *const (&cs)[NC], int32_t *const (&ns)[NC],
-                                           int lane, double *const (&L_out)[NC],
+                                           double *gbuf, int lane, double *const (&L_out)[NC],
                                            uint16_t *const (&top_out)[NC]) {
 #pragma unroll
     for (int q = 0; q < NC; ++q)
@@ -188,54 +190,44 @@ __device__ __forceinline__ void fold_multi(const uint16_t *const (&lab)[NC], con
         s_n2[q] = (i2 < N) ? (uint32_t)lab[q][i2] : (0x10000u + (uint32_t)lane);
         v_n2[q] = (i2 < N) ? __ldcg(v[q] + i2) : 0.0;
     }
+    uint32_t kmax = 0;
     for (int base = 0; base < N; base += 32) {
-        const int i = base + lane;
-        const bool valid = i < N;
+        const bool valid = base + lane < N;
         uint32_t s[NC];
-        double sum[NC];
         unsigned m[NC];
-        int nxt[NC];
 #pragma unroll
         for (int q = 0; q < NC; ++q) {
             s[q] = s_n1[q];
-            sum[q] = v_n1[q];
+            gbuf[q * 32 + lane] = v_n1[q];
             s_n1[q] = s_n2[q];
             v_n1[q] = v_n2[q];
             const int i3 = base + 64 + lane;
             s_n2[q] = (i3 < N) ? (uint32_t)lab[q][i3] : (0x10000u + (uint32_t)lane);
             v_n2[q] = (i3 < N) ? __ldcg(v[q] + i3) : 0.0;
+            if (valid) kmax = max(kmax, s[q]);
         }
 #pragma unroll
-        for (int q = 0; q < NC; ++q) {
-            m[q] = __match_any_sync(0xFFFFFFFFu, s[q]);
-            const unsigned after = (lane == 31) ? 0u : (m[q] & ~((2u << lane) - 1u));
-            nxt[q] = after ? (__ffs(after) - 1) : 32;
-        }
-#pragma unroll
-        for (int step = 0; step < 5; ++step) {
-#pragma unroll
-            for (int q = 0; q < NC; ++q) {
-                const double o = __shfl_sync(0xFFFFFFFFu, sum[q], nxt[q] & 31);
-                const int on = __shfl_sync(0xFFFFFFFFu, nxt[q], nxt[q] & 31);
-                if (nxt[q] < 32) {
-                    sum[q] += o;
-                    nxt[q] = on;
-                }
-            }
-        }
+        for (int q = 0; q < NC; ++q) m[q] = __match_any_sync(0xFFFFFFFFu, s[q]);
+        __syncwarp();
 #pragma unroll
         for (int q = 0; q < NC; ++q)
             if (valid && lane == __ffs(m[q]) - 1) {
-                cs[q][s[q]] += sum[q];
+                double sum = 0.0;
+                for (unsigned mm = m[q]; mm; mm &= mm - 1u) sum += gbuf[q * 32 + __ffs(mm) - 1];
+                cs[q][s[q]] += sum;
                 ns[q][s[q]] += __popc(m[q]);
             }
         __syncwarp();
     }
+    // largest label of the (up to NC) chromosomes, warp-uniform
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) kmax = max(kmax, __shfl_xor_sync(0xFFFFFFFFu, kmax, off));
+    const int K = (int)min(kmax + 1u, (uint32_t)N);
 #pragma unroll
     for (int q = 0; q < NC; ++q) {
         double fsum = 0.0, fbest = 0.0;
         int kbest = 0x7FFFFFFF;
-        for (int k = lane; k < N; k += 32) {
+        for (int k = lane; k < K; k += 32) {
             const int n = ns[q][k];
             if (n >= 2) {
                 const double f = cluster_term(n, cs[q][k]);
@@ -390,6 +382,7 @@ k_fitness(const __grid_constant__ CUtensorMap tmLab0, const __grid_constant__ CU
         double *csb = reinterpret_cast<double *>(smem) + (size_t)warp * NCF * N;
         int32_t *nsb = reinterpret_cast<int32_t *>(reinterpret_cast<double *>(smem) + (size_t)a.fold_warps * NCF * N) +
                        (size_t)warp * NCF * N;
+        double *gbuf = reinterpret_cast<double *>(nsb + (size_t)(a.fold_warps - warp) * NCF * N) + warp * NCF * 32;
         for (int q = NCF * warp; q < pga::CB; q += NCF * a.fold_warps) {
             const int64_t p = (int64_t)cb * pga::CB + q;
             if (p >= a.P) break;
@@ -409,7 +402,7 @@ k_fitness(const __grid_constant__ CUtensorMap tmLab0, const __grid_constant__ CU
                 Lo[c] = &a.L[pc];
                 to[c] = a.top ? &a.top[pc] : nullptr;
             }
-            fold_multi<NCF>(lab, vv, N, cs, ns, lane, Lo, to);
+            fold_multi<NCF>(lab, vv, N, cs, ns, gbuf, lane, Lo, to);
         }
     }
     if (tid == 0) a.counters[cb] = 0u;
@@ -468,14 +461,14 @@ int make_c_tmap(CUtensorMap *tm, const double *C, int N, int ldc) {
 }
 
 int fold_warps(int N) {
-    const size_t per = 2 * (size_t)N * (sizeof(double) + sizeof(int32_t));
+    const size_t per = 2 * (size_t)N * (sizeof(double) + sizeof(int32_t)) + 2 * 32 * sizeof(double);
     int w = (int)((size_t)(NSTAGE * STAGE_BYTES) / per);
     if (w < 1) w = 1;
     return w > CW + 1 ? CW + 1 : w;
 }
 
 size_t fitness_smem(int N) {
-    const size_t fold = (size_t)fold_warps(N) * 2 * N * (sizeof(double) + sizeof(int32_t));
+    const size_t fold = (size_t)fold_warps(N) * (2 * N * (sizeof(double) + sizeof(int32_t)) + 2 * 32 * sizeof(double)) + 16;
     const size_t pipe = (size_t)NSTAGE * STAGE_BYTES;
     return (fold > pipe ? fold : pipe) + 2 * NSTAGE * sizeof(uint64_t) + 128;
 }
