@@ -251,6 +251,7 @@ def main():
     launches = pga.pga_launch_count() - launches0
     ms = ev0.elapsed_time(ev1)
     prof = pga.pga_profile_read(eng.ctx)
+    phases, _ = pga.pga_profile_phases(eng.ctx)
     pga.pga_profile_enable(eng.ctx, False)
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
@@ -312,8 +313,9 @@ def main():
             "evals_per_s": P_TOTAL / (ms_step / 1000.0),
             "gens_per_s": 1000.0 / ms_step,
             "executed_pair_updates_per_s": executed_local * world / (ms_step / 1000.0),
-            "kernel_ms_per_generation": {"k_sweep": sweep_ms, "k_fold": fold_ms,
-                                         "generation": gen_ms},
+            "kernel_ms_per_generation": {"k_fitness": sweep_ms, "generation": gen_ms},
+            "phase_ms_per_generation": {k: round(v, 4) for k, v in phases.items()
+                                        if k != "fitness_fold_fused"},
             "roofline": {"bound": "alu", "kernel": "k_sweep", "achieved": achieved,
                          "peak": peak, "unit": "pair-updates/s", "frac": achieved / peak,
                          "traffic": traffic,

@@ -205,7 +205,7 @@ int pga_correlation_device(const double *X_dev, int32_t T, int32_t N, double *C_
 int pga_op_select(const double *L, int64_t P, const pga_params *p, int32_t gen,
                   int32_t island, int32_t *order_out, int32_t *sel_out);
 
-/* Mate pairing: sigma_out [M], the slot permutation (Philox keys, ties by slot). */
+/* Mate pairing (Q10): sigma_out [M], a keyed Feistel permutation of the slots. */
 int pga_op_mates(int64_t M, const pga_params *p, int32_t gen, int32_t island,
                  int32_t *sigma_out);
 
@@ -238,6 +238,12 @@ int64_t pga_launch_count(void);
 int pga_profile_enable(pga_ctx *ctx, int32_t on);
 int pga_profile_read(pga_ctx *ctx, double *sweep_ms, double *fold_ms, double *gen_ms,
                      int32_t *count);
+
+/* Per-phase AVERAGE milliseconds of the profiled generations, ms[PGA_PROF_PHASES]:
+ * 0 fitness sweep+fold kernel, 1 (fused, 0), 2 statistics/termination,
+ * 3 order sort, 4 scaling+selection, 5 mate pairing, 6 breed, 7 advance. */
+#define PGA_PROF_PHASES 8
+int pga_profile_phases(pga_ctx *ctx, double *ms, int32_t *count);
 
 #ifdef __cplusplus
 }

@@ -395,30 +395,36 @@ void orc_select(const double *L, const int32_t *order, int32_t P, int32_t E,
     }
 }
 
-typedef struct { uint32_t key; int32_t m; } mkey;
-
-static int cmp_mkey(const void *a, const void *b)
+/* Mate pairing (unspecified in the paper, Q10): sigma is a keyed pseudo-
+ * random permutation of the M offspring slots -- a 4-round Feistel network
+ * on h+h bits (2^(2h) >= M) with round function Philox(PERM; R, round)[0],
+ * cycle-walked back into [0, M); pair k = (sigma[2k], sigma[2k+1]). */
+static uint32_t feistel_perm(uint32_t m, uint32_t M, uint64_t seed, uint32_t gen, uint32_t island)
 {
-    const mkey *x = (const mkey *)a, *y = (const mkey *)b;
-    if (x->key != y->key) return (x->key < y->key) ? -1 : 1;
-    return (x->m < y->m) ? -1 : (x->m > y->m);
+    int32_t h = (ceil_log2(M) + 1) / 2;
+    uint32_t mask, x = m;
+    if (h < 1) h = 1;
+    mask = (1u << h) - 1u;
+    do {
+        uint32_t Lh = x >> h, R = x & mask;
+        int r;
+        for (r = 0; r < 4; r++) {
+            uint32_t f[4], t;
+            draw(seed, ORC_TAG_PERM, island, gen, R, (uint32_t)r, f);
+            t = R;
+            R = Lh ^ (f[0] & mask);
+            Lh = t;
+        }
+        x = (Lh << h) | R;
+    } while (x >= M);
+    return x;
 }
 
-/* Mate pairing (unspecified in the paper, Q10): slots sorted by a Philox
- * random key, ties by slot index; pair k = (sigma[2k], sigma[2k+1]). */
 void orc_mates(int32_t M, uint64_t seed, uint32_t gen, uint32_t island, int32_t *sigma)
 {
-    mkey *k = (mkey *)malloc(sizeof(mkey) * (size_t)M);
     int32_t m;
-    for (m = 0; m < M; m++) {
-        uint32_t x[4];
-        draw(seed, ORC_TAG_PERM, island, gen, (uint32_t)(m >> 2), 0u, x);
-        k[m].key = x[m & 3];
-        k[m].m = m;
-    }
-    qsort(k, (size_t)M, sizeof(mkey), cmp_mkey);
-    for (m = 0; m < M; m++) sigma[m] = k[m].m;
-    free(k);
+    for (m = 0; m < M; m++)
+        sigma[m] = (int32_t)feistel_perm((uint32_t)m, (uint32_t)M, seed, gen, island);
 }
 
 /* Crossover (Table 3; Q11, Q12), mutation

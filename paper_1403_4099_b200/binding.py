@@ -61,6 +61,7 @@ _SIGS = {
     "pga_profile_enable": (ct.c_int, [ct.c_void_p, ct.c_int32]),
     "pga_profile_read": (ct.c_int, [ct.c_void_p, ct.c_void_p, ct.c_void_p, ct.c_void_p,
                                     ct.c_void_p]),
+    "pga_profile_phases": (ct.c_int, [ct.c_void_p, ct.c_void_p, ct.c_void_p]),
     "pga_set_population": (ct.c_int, [ct.c_void_p, ct.c_void_p, ct.c_int32]),
     "pga_migrant_bytes": (ct.c_int, [ct.c_void_p, ct.c_void_p]),
     "pga_export_migrants": (ct.c_int, [ct.c_void_p, ct.c_void_p]),
@@ -210,6 +211,16 @@ def pga_get_population(ctx, P: int, N: int, with_top: bool = False):
 
 def pga_profile_enable(ctx, on: bool = True):
     _check(lib().pga_profile_enable(ctx, 1 if on else 0))
+
+
+PHASES = ["fitness", "fitness_fold_fused", "stats", "order_sort", "selection", "mates", "breed", "advance"]
+
+
+def pga_profile_phases(ctx):
+    ms = np.zeros(len(PHASES), np.float64)
+    n = ct.c_int32()
+    _check(lib().pga_profile_phases(ctx, _p(ms), ct.byref(n)))
+    return dict(zip(PHASES, ms.tolist())), n.value
 
 
 def pga_profile_read(ctx):

@@ -192,7 +192,7 @@ bool is_migration_gen(const pga_ctx *c, int32_t g) {
 
 cudaEvent_t *prof_slot(pga_ctx *c) {
     if (!c->prof) return nullptr;
-    while (c->prof_ev.size() < c->prof_used + 4) {
+    while (c->prof_ev.size() < c->prof_used + PROF_EV) {
         cudaEvent_t e;
         if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
         c->prof_ev.push_back(e);
@@ -200,9 +200,12 @@ cudaEvent_t *prof_slot(pga_ctx *c) {
     return &c->prof_ev[c->prof_used];
 }
 
+// Phase marks (profiling only): 0 start, 1 sweep end, 2 fitness end,
+// 3 statistics end, 4 order sort end, 5 selection end, 6 mating end,
+// 7 breed end, 8 generation end.
 int phase_a(pga_ctx *c, int32_t g, int32_t *is_mig) {
-    cudaEvent_t *ev = prof_slot(c);
-    TRY(launch_fitness(c, ga_bufs(c), c->P, c->L, c->top, c->stream, ev));
+    c->pev = prof_slot(c);
+    TRY(launch_fitness(c, ga_bufs(c), c->P, c->L, c->top, c->stream, c->pev));
     const bool mig = is_migration_gen(c, g);
     if (is_mig) *is_mig = mig ? 1 : 0;
     if (mig) {
@@ -211,15 +214,18 @@ int phase_a(pga_ctx *c, int32_t g, int32_t *is_mig) {
     } else {
         TRY(launch_stats(c, c->p.n_islands > 1 ? 1 : 0, c->stream));
     }
+    PGA_MARK(c, 3, c->stream);
     return PGA_OK;
 }
 
 int phase_b(pga_ctx *c) {
     TRY(launch_sort_order(c, c->stream));
+    PGA_MARK(c, 4, c->stream);
     TRY(launch_select_breed(c, c->stream));
-    if (c->prof && c->prof_ev.size() >= c->prof_used + 4) {
-        PGA_CUDA(cudaEventRecord(c->prof_ev[c->prof_used + 3], c->stream));
-        c->prof_used += 4;
+    if (c->pev) {
+        PGA_CUDA(cudaEventRecord(c->pev[8], c->stream));
+        c->prof_used += PROF_EV;
+        c->pev = nullptr;
     }
     return PGA_OK;
 }
@@ -585,24 +591,35 @@ int pga_profile_enable(pga_ctx *c, int32_t on) {
 }
 
 int pga_profile_read(pga_ctx *c, double *sweep_ms, double *fold_ms, double *gen_ms, int32_t *count) {
-    if (!c) return fail(PGA_EINVAL, "ctx is NULL");
+    double ph[PGA_PROF_PHASES];
+    int32_t n = 0;
+    TRY(pga_profile_phases(c, ph, &n));
+    if (sweep_ms) *sweep_ms = ph[0] * n;
+    if (fold_ms) *fold_ms = ph[1] * n;
+    if (gen_ms) {
+        double t = 0;
+        for (int k = 0; k < PGA_PROF_PHASES; ++k) t += ph[k];
+        *gen_ms = t * n;
+    }
+    if (count) *count = n;
+    return PGA_OK;
+}
+
+int pga_profile_phases(pga_ctx *c, double *ms, int32_t *count) {
+    if (!c || !ms) return fail(PGA_EINVAL, "NULL argument");
     PGA_CUDA(cudaSetDevice(c->device));
     PGA_CUDA(cudaStreamSynchronize(c->stream));
-    double s = 0, f = 0, g = 0;
+    double acc[PGA_PROF_PHASES] = {0};
     int32_t n = 0;
-    for (size_t k = 0; k + 4 <= c->prof_used; k += 4) {
-        float a = 0, b = 0, d = 0;
-        PGA_CUDA(cudaEventElapsedTime(&a, c->prof_ev[k], c->prof_ev[k + 1]));
-        PGA_CUDA(cudaEventElapsedTime(&b, c->prof_ev[k + 1], c->prof_ev[k + 2]));
-        PGA_CUDA(cudaEventElapsedTime(&d, c->prof_ev[k], c->prof_ev[k + 3]));
-        s += a;
-        f += b;
-        g += d;
+    for (size_t k = 0; k + PROF_EV <= c->prof_used; k += PROF_EV) {
+        for (int j = 0; j < PGA_PROF_PHASES; ++j) {
+            float t = 0;
+            PGA_CUDA(cudaEventElapsedTime(&t, c->prof_ev[k + j], c->prof_ev[k + j + 1]));
+            acc[j] += t;
+        }
         ++n;
     }
-    if (sweep_ms) *sweep_ms = s;
-    if (fold_ms) *fold_ms = f;
-    if (gen_ms) *gen_ms = g;
+    for (int j = 0; j < PGA_PROF_PHASES; ++j) ms[j] = n ? acc[j] / n : 0.0;
     if (count) *count = n;
     return PGA_OK;
 }

@@ -108,13 +108,16 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t *b) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
+// try_wait with a suspend-time hint: a waiting thread sleeps in hardware
+// until the phase completes (or the hint expires) instead of spinning and
+// stealing issue slots from the consumer warps on its SMSP.
 __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
         "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(b)),
-        "r"(parity)
+        "r"(parity), "r"(1000000u)
         : "memory");
 }
 __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *tm, int x, int y, uint64_t *bar) {
@@ -225,17 +228,38 @@ __device__ __forceinline__ void fold_multi(const uint16_t *const (&lab)[NC], con
     const int K = (int)min(kmax + 1u, (uint32_t)N);
 #pragma unroll
     for (int q = 0; q < NC; ++q) {
+        // compact the clusters with n_s >= 2 and c_s > n_s (the only ones with
+        // a non-zero Eq. 8 summand, Q2) to the front of cs/ns, in label order,
+        // so the logs below run on dense lanes; ns keeps n | label << 16.
+        int M = 0;
+        for (int k0 = 0; k0 < K; k0 += 32) {
+            const int k = k0 + lane;
+            int n = 0;
+            double c = 0.0;
+            if (k < K) {
+                n = ns[q][k];
+                c = cs[q][k];
+            }
+            const bool act = (n >= 2) && (c > (double)n);
+            const unsigned bal = __ballot_sync(0xFFFFFFFFu, act);
+            __syncwarp();
+            if (act) {
+                const int idx = M + __popc(bal & lanemask_lt());
+                cs[q][idx] = c;
+                ns[q][idx] = n | (k << 16);
+            }
+            M += __popc(bal);
+            __syncwarp();
+        }
         double fsum = 0.0, fbest = 0.0;
         int kbest = 0x7FFFFFFF;
-        for (int k = lane; k < K; k += 32) {
-            const int n = ns[q][k];
-            if (n >= 2) {
-                const double f = cluster_term(n, cs[q][k]);
-                fsum += f;
-                if (f > fbest) {
-                    fbest = f;
-                    kbest = k;
-                }
+        for (int j = lane; j < M; j += 32) {
+            const int nk = ns[q][j];
+            const double f = cluster_term(nk & 0xFFFF, cs[q][j]);
+            fsum += f;
+            if (f > fbest) {
+                fbest = f;
+                kbest = nk >> 16;
             }
         }
 #pragma unroll
@@ -505,7 +529,7 @@ int launch_fitness(pga_ctx *c, const FitBufs &b, int64_t P, double *L, uint16_t 
     k_fitness<<<(unsigned)(a.nRT * a.nCB), FIT_THREADS, fitness_smem(N), s>>>(*b.tm0, *b.tm1, c->tmC, a);
     PGA_LAUNCHED();
     if (ev) {
-        PGA_CUDA(cudaEventRecord(ev[1], s));
+        PGA_CUDA(cudaEventRecord(ev[1], s));   // sweep and fold are one fused kernel
         PGA_CUDA(cudaEventRecord(ev[2], s));
     }
     return PGA_OK;

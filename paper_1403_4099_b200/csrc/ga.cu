@@ -24,7 +24,10 @@ struct Canon {
     int next;
     __device__ __forceinline__ uint32_t step(uint32_t s, bool valid, int lane) {
         const uint32_t key = valid ? s : (0x10000u + (uint32_t)lane);
-        const unsigned m = __match_any_sync(0xFFFFFFFFu, key);
+        return assign(s, valid, lane, __match_any_sync(0xFFFFFFFFu, key));
+    }
+    // m = __match_any_sync of this step's keys (may be computed ahead).
+    __device__ __forceinline__ uint32_t assign(uint32_t s, bool valid, int lane, unsigned m) {
         const bool leader = (__ffs(m) - 1) == lane;
         const bool fresh = valid && leader && table[s] == 0xFFFF;
         const unsigned bal = __ballot_sync(0xFFFFFFFFu, fresh);
@@ -274,17 +277,31 @@ __global__ void k_tournament(const double *__restrict__ L, int64_t P, int64_t M,
     sel[m] = best;
 }
 
-__global__ void k_mate_keys(int64_t M, uint64_t seed, uint32_t gen, uint32_t island, uint32_t *keys,
-                            int32_t *idx, const int32_t *done, const int32_t *gen_ptr) {
+// Mate pairing (Q10): sigma = keyed Feistel permutation of the M slots
+// (4 rounds, round function Philox(PERM; R, round)[0], cycle-walking).
+__global__ void k_mates(int64_t M, uint64_t seed, uint32_t gen, uint32_t island, int32_t *sigma,
+                        const int32_t *done, const int32_t *gen_ptr) {
     if (done && *done) return;
     const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (m >= M) return;
     if (gen_ptr) gen = (uint32_t)*gen_ptr;
-    const U4 u = draw(seed, pga::TAG_PERM, island, gen, (uint32_t)(m >> 2), 0u);
-    keys[m] = word(u, (int)(m & 3));
-    idx[m] = (int32_t)m;
+    int h = (ceil_log2_d(M) + 1) / 2;
+    if (h < 1) h = 1;
+    const uint32_t mask = (1u << h) - 1u;
+    uint32_t x = (uint32_t)m;
+    do {
+        uint32_t Lh = x >> h, R = x & mask;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const U4 f = draw(seed, pga::TAG_PERM, island, gen, R, (uint32_t)r);
+            const uint32_t t = R;
+            R = Lh ^ (f.x & mask);
+            Lh = t;
+        }
+        x = (Lh << h) | R;
+    } while (x >= (uint32_t)M);
+    sigma[m] = (int32_t)x;
 }
-
 
 // ---------------------------------------------------------------------------
 // k_breed: warp per output slot o.  o < E: copy elite order[o];
@@ -326,6 +343,7 @@ __device__ __forceinline__ int parent_top(const BreedArgs &a, int64_t p) {
 // children's canonical genes go to CM directly (coalesced) and through a
 // shared-memory tile [128][BS] to the gene-major layout (BS*2-byte rows).
 constexpr int BW = 16, BC = 1, BS = BW * BC, GCH = 128;
+constexpr int TS = BS + 2;   // tile row stride (u16): 36 B, odd multiple of 4 B -> conflict-free
 
 struct ChildPlan {
     int64_t pa, pb;
@@ -365,6 +383,7 @@ __device__ __forceinline__ ChildPlan plan_child(const BreedArgs &a, int64_t o, u
     return c;
 }
 
+template <bool HOOK>
 __global__ void __launch_bounds__(BW * 32, 2) k_breed(BreedArgs a) {
     if (a.done && *a.done) return;
     extern __shared__ uint16_t sm16[];
@@ -375,8 +394,8 @@ __global__ void __launch_bounds__(BW * 32, 2) k_breed(BreedArgs a) {
     const uint16_t *cm_in = par ? a.cm_in1 : a.cm_in0;
     uint16_t *cm_out = par ? a.cm_out0 : a.cm_out1;
     uint16_t *gm_out = par ? a.gm_out0 : a.gm_out1;
-    uint16_t *tile = sm16;                               // [GCH][BS]
-    uint16_t *tables = sm16 + GCH * BS;                  // [BS][N+1]
+    uint16_t *tile = sm16;                               // 2 x [GCH][TS]
+    uint16_t *tables = sm16 + 2 * GCH * TS;              // [BS][N+1]
     const int64_t o0 = (int64_t)blockIdx.x * BS;
 
     ChildPlan cp[BC];
@@ -390,6 +409,7 @@ __global__ void __launch_bounds__(BW * 32, 2) k_breed(BreedArgs a) {
         table_reset(cn[c].table, N + 1, lane);
     }
     for (int base = 0; base < N; base += GCH) {
+        const int tb = ((base / GCH) & 1) * GCH * TS;     // double-buffered tile
 #pragma unroll
         for (int c = 0; c < BC; ++c) {
             const ChildPlan &p = cp[c];
@@ -400,8 +420,13 @@ __global__ void __launch_bounds__(BW * 32, 2) k_breed(BreedArgs a) {
             for (int sc = 0; sc < GCH / 32; ++sc) {
                 const int i = base + 32 * sc + lane;
                 const bool valid = p.valid && i < N;
-                ga[sc] = valid ? parent_gene(a, cm_in, p.pa, i) : 0u;
-                gb[sc] = (valid && p.mode != 0) ? parent_gene(a, cm_in, p.pb, i) : 0u;
+                if (HOOK) {
+                    ga[sc] = valid ? (uint32_t)a.i32_in[p.pa * N + i] : 0u;
+                    gb[sc] = (valid && p.mode != 0) ? (uint32_t)a.i32_in[p.pb * N + i] : 0u;
+                } else {
+                    ga[sc] = valid ? (uint32_t)cm_in[p.pa * a.ldn + i] : 0u;
+                    gb[sc] = (valid && p.mode != 0) ? (uint32_t)cm_in[p.pb * a.ldn + i] : 0u;
+                }
             }
             // mutation mask of genes base+4*lane .. base+4*lane+3
             uint32_t mbits = 0;
@@ -410,6 +435,8 @@ __global__ void __launch_bounds__(BW * 32, 2) k_breed(BreedArgs a) {
                 mbits = ((uint64_t)u.x < a.thr_m ? 1u : 0u) | ((uint64_t)u.y < a.thr_m ? 2u : 0u) |
                         ((uint64_t)u.z < a.thr_m ? 4u : 0u) | ((uint64_t)u.w < a.thr_m ? 8u : 0u);
             }
+            uint32_t sv[GCH / 32];
+            unsigned mm[GCH / 32];
 #pragma unroll
             for (int sc = 0; sc < GCH / 32; ++sc) {
                 const int i = base + 32 * sc + lane;
@@ -425,29 +452,40 @@ __global__ void __launch_bounds__(BW * 32, 2) k_breed(BreedArgs a) {
                     const U4 v = draw(a.seed, pga::TAG_MUTV, a.island, gen, (uint32_t)(i >> 2), p.og);
                     s = scale_u32(word(v, i & 3), (uint32_t)N);
                 }
-                const uint32_t cv = cn[c].step(s, valid, lane);
+                sv[sc] = s;
+            }
+            // the four group masks are independent: issue them back to back
+#pragma unroll
+            for (int sc = 0; sc < GCH / 32; ++sc) {
+                const bool valid = p.valid && base + 32 * sc + lane < N;
+                mm[sc] = __match_any_sync(0xFFFFFFFFu, valid ? sv[sc] : (0x10000u + (uint32_t)lane));
+            }
+#pragma unroll
+            for (int sc = 0; sc < GCH / 32; ++sc) {
+                const int i = base + 32 * sc + lane;
+                const bool valid = p.valid && i < N;
+                const uint32_t cv = cn[c].assign(sv[sc], valid, lane, mm[sc]);
                 if (valid) {
-                    if (a.i32_out) a.i32_out[(o0 + slot) * N + i] = (int32_t)cv;
+                    if (HOOK) a.i32_out[(o0 + slot) * N + i] = (int32_t)cv;
                     else cm_out[(o0 + slot) * a.ldn + i] = (uint16_t)cv;
                 }
-                tile[(32 * sc + lane) * BS + slot] = (uint16_t)cv;
+                if (!HOOK) tile[tb + (32 * sc + lane) * TS + slot] = (uint16_t)cv;
             }
         }
-        __syncthreads();
-        if (!a.i32_out) {
+        __syncthreads();     // tile[tb] complete; the other half is free again
+        if (!HOOK) {
             // gene-major rows: genes base..base+127, slots o0..o0+BS-1
             for (int e = threadIdx.x; e < GCH * (BS / 2); e += BW * 32) {
                 const int g = e / (BS / 2), pr = e - g * (BS / 2);
                 const int i = base + g;
                 const int64_t o = o0 + 2 * pr;
                 if (i < N && o < a.P) {
-                    const uint32_t two = *reinterpret_cast<const uint32_t *>(&tile[g * BS + 2 * pr]);
+                    const uint32_t two = *reinterpret_cast<const uint32_t *>(&tile[tb + g * TS + 2 * pr]);
                     if (o + 1 < a.P) *reinterpret_cast<uint32_t *>(&gm_out[(int64_t)i * a.Pcap + o]) = two;
                     else gm_out[(int64_t)i * a.Pcap + o] = (uint16_t)(two & 0xFFFF);
                 }
             }
         }
-        __syncthreads();
     }
 }
 
@@ -550,7 +588,7 @@ __global__ void k_import(const unsigned char *__restrict__ in, int G, int Em, in
 
 namespace pga {
 
-static size_t breed_smem(int N) { return ((size_t)GCH * BS + (size_t)BS * (N + 1)) * sizeof(uint16_t); }
+static size_t breed_smem(int N) { return ((size_t)2 * GCH * TS + (size_t)BS * (N + 1)) * sizeof(uint16_t); }
 
 static int breed_warps(int N) {
     const size_t per = (size_t)(N + 1) * sizeof(uint16_t);
@@ -577,7 +615,8 @@ int launch_init_raw(uint64_t seed, int N, int ldn, int64_t P, int64_t Pcap, int6
 }
 
 int prepare_breed(int N) {
-    PGA_CUDA(cudaFuncSetAttribute(k_breed, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)breed_smem(N)));
+    PGA_CUDA(cudaFuncSetAttribute(k_breed<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)breed_smem(N)));
+    PGA_CUDA(cudaFuncSetAttribute(k_breed<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)breed_smem(N)));
     return PGA_OK;
 }
 
@@ -660,13 +699,10 @@ int run_select_ops(const double *L, int64_t P, const pga_params &p, int32_t gen,
 int run_mates(int64_t M, const pga_params &p, int32_t gen, int32_t island, uint32_t *k_in,
               uint32_t *k_out, int32_t *m_in, int32_t *sigma, void *tmp, size_t tmp_bytes,
               const int32_t *done, cudaStream_t s, const int32_t *gen_ptr) {
-    k_mate_keys<<<(unsigned)((M + 255) / 256), 256, 0, s>>>(M, p.seed, (uint32_t)gen,
-                                                            (uint32_t)island, k_in, m_in, done,
-                                                            gen_ptr);
+    (void)k_in; (void)k_out; (void)m_in; (void)tmp; (void)tmp_bytes;
+    k_mates<<<(unsigned)((M + 255) / 256), 256, 0, s>>>(M, p.seed, (uint32_t)gen, (uint32_t)island, sigma,
+                                                        done, gen_ptr);
     PGA_LAUNCHED();
-    size_t tb = tmp_bytes;
-    PGA_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, k_in, k_out, m_in, sigma, (int)M, 0, 32, s));
-    count_launch();
     return PGA_OK;
 }
 
@@ -703,7 +739,7 @@ int launch_breed_hook(const int32_t *pop, const int32_t *top, const int32_t *ord
     a.island = (uint32_t)island;
     a.ldn = N;
     a.Pcap = P;
-    k_breed<<<(unsigned)((P + BS - 1) / BS), BW * 32, breed_smem(N), s>>>(a);
+    k_breed<true><<<(unsigned)((P + BS - 1) / BS), BW * 32, breed_smem(N), s>>>(a);
     PGA_LAUNCHED();
     return PGA_OK;
 }
@@ -722,10 +758,12 @@ int launch_select_breed(pga_ctx *c, cudaStream_t s) {
                             c->idx_in, c->q, c->prefix, c->cub_tmp, c->cub_tmp_bytes, done, s,
                             genp, true);
     if (rc) return rc;
+    PGA_MARK(c, 5, s);
     const int64_t M = 2 * ((c->P - p.elite + 1) / 2);
     rc = run_mates(M, p, 0, p.island, c->mkeys_in, c->mkeys_out, c->m_in, c->sigma, c->cub_tmp,
                    c->cub_tmp_bytes, done, s, genp);
     if (rc) return rc;
+    PGA_MARK(c, 6, s);
     BreedArgs a{};
     fill_breed(a, p, c->P, c->N);
     a.cm_in0 = c->pop[0];
@@ -743,8 +781,9 @@ int launch_select_breed(pga_ctx *c, cudaStream_t s) {
     a.ldn = c->ldn;
     a.done = done;
     a.gen_ptr = genp;
-    k_breed<<<(unsigned)((c->P + BS - 1) / BS), BW * 32, breed_smem(c->N), s>>>(a);
+    k_breed<false><<<(unsigned)((c->P + BS - 1) / BS), BW * 32, breed_smem(c->N), s>>>(a);
     PGA_LAUNCHED();
+    PGA_MARK(c, 7, s);
     k_advance<<<1, 1, 0, s>>>(c->st);
     PGA_LAUNCHED();
     return PGA_OK;

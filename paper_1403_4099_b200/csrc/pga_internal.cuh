@@ -26,6 +26,11 @@ void count_launch(int n = 1);
         if (_e != cudaSuccess) return ::pga::cuda_fail(_e, #call);         \
     } while (0)
 
+#define PGA_MARK(c, k, s)                                                  \
+    do {                                                                   \
+        if ((c)->pev) PGA_CUDA(cudaEventRecord((c)->pev[k], (s)));         \
+    } while (0)
+
 #define PGA_LAUNCHED()                                                     \
     do {                                                                   \
         ::pga::count_launch();                                             \
@@ -38,6 +43,7 @@ enum : uint32_t {
     TAG_INIT = 1, TAG_SUS = 2, TAG_PERM = 3, TAG_TOUR = 4, TAG_XO = 5, TAG_MUT = 6, TAG_MUTV = 7
 };
 
+constexpr int PROF_EV = 9;     // phase marks per profiled generation
 constexpr int CB = 32;         // chromosomes per fitness CTA tile (one per lane)
 
 // Device-resident GA state (one island).  Read/written only by kernels.
@@ -111,8 +117,9 @@ struct pga_ctx {
     pga::DevState *h_st = nullptr;
     // profiling (pga_profile_enable): per generation 4 events
     bool prof = false;
-    std::vector<cudaEvent_t> prof_ev;   // groups of 4: gen start, sweep end, fold end, gen end
+    std::vector<cudaEvent_t> prof_ev;   // groups of PROF_EV events per generation (see api.cu)
     size_t prof_used = 0;
+    cudaEvent_t *pev = nullptr;         // this generation's events while profiling, else null
 };
 
 namespace pga {
