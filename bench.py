@@ -30,14 +30,16 @@ sys.path.insert(0, ROOT)
 
 import workloads  # noqa: E402
 
-CONFIG = "C4"
+CONFIG = "C4"            # default workload (BASELINE configs[3]); --config selects another
 P_TOTAL = 65536
+# population per config (BASELINE.json configs) and mutation rate (Q13)
+CFG_POP = {"C1": 128, "C2": 1024, "C3": 4096, "C4": 65536, "C5": 262144}
 SEED = 2024
 SM_COUNT = 148
 FP64_LANES_PER_SM = 64           # DFMA lanes / clk / SM (B200: 37 TF fp64 = 148*64*2*1.965G)
 
 METRIC = ("GA generation throughput, nominal pair-updates/s (N^2 * P per generation; "
-          "fitness + all operators), BASELINE config 4")
+          "fitness + all operators)")
 
 
 def env_int(k, d):
@@ -120,7 +122,7 @@ def oracle_generation(orc, C, pop, params, gen):
     return orc.step(params, pop, L, top, gen)
 
 
-def oracle_rate(C, planted, target_s=10.0, max_P=16384):
+def oracle_rate(C, planted, target_s=15.0, max_P=65536):
     """Time the oracle's full generation (evaluate on all host cores + the
     single-threaded operators) on a bounded sample population; return
     (nominal pair-updates/s, sample size, seconds)."""
@@ -192,6 +194,7 @@ def run_reference(args):
 # GPU arm
 # ---------------------------------------------------------------------------
 def main():
+    global CONFIG, P_TOTAL
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=1000)
@@ -199,7 +202,11 @@ def main():
     ap.add_argument("--impl", default="pga", choices=["pga", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--config", default=CONFIG, choices=sorted(CFG_POP),
+                    help="workload (default C4, the config the metric is quoted on)")
     args = ap.parse_args()
+    CONFIG = args.config
+    P_TOTAL = CFG_POP[CONFIG]
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
         return run_reference(args)
@@ -219,8 +226,9 @@ def main():
     N = X.shape[1]
     C = pga.pga_correlation(X, device=local)        # Eq. 7 on the device
     P_local = P_TOTAL // world
+    pm = 0.1 if N <= 40 else 2.0 / N            # Table 3 for N <= 40, else 2/N (Q13)
     params = pga.pga_params_default(
-        pop_size=P_local, elite=10, p_mutation=2.0 / N, tol=-1.0, max_gens=W + K + 2,
+        pop_size=P_local, elite=10, p_mutation=pm, tol=-1.0, max_gens=W + K + 2,
         device=local, island=rank, n_islands=world, migrate_every=10, migrants=10, seed=SEED)
 
     eng = GpuIsland(C, params)
@@ -304,8 +312,8 @@ def main():
             "steps": K, "warmup": W, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (Noh-model returns T=2000, seed 50004; Pearson C on device)",
-            "config": {"workload": "C4: N=500, P=65536 total (%d per GPU), 1 step = 1 generation"
-                                   % P_local, "N": N, "population": P_TOTAL,
+            "config": {"workload": "%s: N=%d, P=%d total (%d per GPU), 1 step = 1 generation"
+                                   % (CONFIG, N, P_TOTAL, P_local), "N": N, "population": P_TOTAL,
                        "population_per_gpu": P_local, "parallelism": "islands x%d" % world,
                        "migration": "every 10 generations, 10 elites, NCCL all-gather",
                        "l2": "working set > L2 (two population layouts x2 buffers + 264 MB "

@@ -45,6 +45,8 @@ int launch_breed_hook(const int32_t *pop, const int32_t *top, const int32_t *ord
                       int32_t gen, int32_t island, int64_t p_off, int32_t *next, cudaStream_t s);
 int launch_set_pop(pga_ctx *c, const int32_t *lab32, int par, cudaStream_t s);
 int prepare_breed(int N);
+int prepare_select_small();
+bool small_select(const pga_ctx *c);
 
 static int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
@@ -219,7 +221,7 @@ int phase_a(pga_ctx *c, int32_t g, int32_t *is_mig) {
 }
 
 int phase_b(pga_ctx *c) {
-    TRY(launch_sort_order(c, c->stream));
+    if (!small_select(c)) TRY(launch_sort_order(c, c->stream));   // small P: fused in selection
     PGA_MARK(c, 4, c->stream);
     TRY(launch_select_breed(c, c->stream));
     if (c->pev) {
@@ -393,6 +395,7 @@ int pga_create(const double *C, int32_t N, const pga_params *p, pga_ctx **out) {
     }
     rc = prepare_fitness(N);
     if (!rc) rc = prepare_breed(N);
+    if (!rc) rc = prepare_select_small();
     if (!rc) rc = make_c_tmap(&c->tmC, c->C, N, c->ldc);
     if (!rc) rc = make_label_tmap(&c->tmLab[0], c->popT[0], N, c->Pcap);
     if (!rc) rc = make_label_tmap(&c->tmLab[1], c->popT[1], N, c->Pcap);
@@ -712,6 +715,7 @@ int pga_op_select(const double *L, int64_t P, const pga_params *p, int32_t gen, 
     if (P < 2 || p->elite < 0 || p->elite >= P) return fail(PGA_EINVAL, "need P >= 2 and 0 <= elite < P");
     if (p->tournament_k < 1 || p->tournament_k > 4) return fail(PGA_EINVAL, "tournament_k must be 1..4");
     TRY(ensure_device(p->device));
+    TRY(prepare_select_small());
     const int64_t M = 2 * ((P - p->elite + 1) / 2);
     HookBufs hb;
     double *dL;

@@ -277,14 +277,8 @@ __global__ void k_tournament(const double *__restrict__ L, int64_t P, int64_t M,
     sel[m] = best;
 }
 
-// Mate pairing (Q10): sigma = keyed Feistel permutation of the M slots
-// (4 rounds, round function Philox(PERM; R, round)[0], cycle-walking).
-__global__ void k_mates(int64_t M, uint64_t seed, uint32_t gen, uint32_t island, int32_t *sigma,
-                        const int32_t *done, const int32_t *gen_ptr) {
-    if (done && *done) return;
-    const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (m >= M) return;
-    if (gen_ptr) gen = (uint32_t)*gen_ptr;
+__device__ __forceinline__ int32_t feistel_slot(int64_t m, int64_t M, uint64_t seed, uint32_t gen,
+                                                uint32_t island) {
     int h = (ceil_log2_d(M) + 1) / 2;
     if (h < 1) h = 1;
     const uint32_t mask = (1u << h) - 1u;
@@ -300,8 +294,163 @@ __global__ void k_mates(int64_t M, uint64_t seed, uint32_t gen, uint32_t island,
         }
         x = (Lh << h) | R;
     } while (x >= (uint32_t)M);
-    sigma[m] = (int32_t)x;
+    return (int32_t)x;
 }
+
+// Mate pairing (Q10): sigma = keyed Feistel permutation of the M slots
+// (4 rounds, round function Philox(PERM; R, round)[0], cycle-walking).
+__global__ void k_mates(int64_t M, uint64_t seed, uint32_t gen, uint32_t island, int32_t *sigma,
+                        const int32_t *done, const int32_t *gen_ptr) {
+    if (done && *done) return;
+    const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= M) return;
+    if (gen_ptr) gen = (uint32_t)*gen_ptr;
+    sigma[m] = feistel_slot(m, M, seed, gen, island);
+}
+
+// ---------------------------------------------------------------------------
+// k_select_small: P <= SMALL_P in ONE CTA (what the multi-kernel path does
+// with ~8 launches): order by (L desc, idx asc) via a shared-memory bitonic
+// sort, rank scaling, exact u64 prefix, SUS or tournament, Feistel mates.
+// what: bit 0 = order, bit 1 = selection + mates.
+// ---------------------------------------------------------------------------
+constexpr int SMALL_P = 4096, SMALL_T = 1024;
+
+__device__ __forceinline__ bool kv_less(uint64_t ka, uint32_t va, uint64_t kb, uint32_t vb) {
+    return ka < kb || (ka == kb && va < vb);
+}
+
+__global__ void __launch_bounds__(SMALL_T)
+k_select_small(int what, const double *__restrict__ L, int P, int M, int selection, int tour_k, int scaling,
+               uint64_t seed, uint32_t gen, uint32_t island, const int32_t *gen_ptr, int32_t *order,
+               int32_t *sel, int32_t *sigma, const int32_t *done) {
+    if (done && *done) return;
+    extern __shared__ __align__(16) unsigned char ssm[];
+    uint64_t *sk = reinterpret_cast<uint64_t *>(ssm);               // [SMALL_P] keys, then prefix
+    double *sL = reinterpret_cast<double *>(sk + SMALL_P);          // [SMALL_P]
+    uint32_t *sv = reinterpret_cast<uint32_t *>(sL + SMALL_P);      // [SMALL_P]
+    int32_t *srank = reinterpret_cast<int32_t *>(sv + SMALL_P);     // [SMALL_P]
+    __shared__ uint64_t wsum[SMALL_T / 32];
+    __shared__ int32_t s_top;
+    const int tid = threadIdx.x;
+    if (gen_ptr) gen = (uint32_t)*gen_ptr;
+    int n2 = 2;
+    while (n2 < P) n2 <<= 1;
+    for (int t = tid; t < n2; t += SMALL_T) {
+        if (t < P) {
+            double x = L[t];
+            if (x == 0.0) x = 0.0;
+            sL[t] = x;
+            sk[t] = ~(uint64_t)__double_as_longlong(x);
+            sv[t] = (uint32_t)t;
+        } else {
+            sk[t] = ~0ull;
+            sv[t] = 0xFFFFFFFFu;
+        }
+    }
+    __syncthreads();
+    for (int size = 2; size <= n2; size <<= 1)
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int t = tid; t < n2 / 2; t += SMALL_T) {
+                const int i = 2 * t - (t & (stride - 1)), j = i + stride;
+                const bool up = (i & size) == 0;
+                const uint64_t ki = sk[i], kj = sk[j];
+                const uint32_t vi = sv[i], vj = sv[j];
+                if (kv_less(kj, vj, ki, vi) == up) {
+                    sk[i] = kj; sk[j] = ki;
+                    sv[i] = vj; sv[j] = vi;
+                }
+            }
+            __syncthreads();
+        }
+    for (int r = tid; r < P; r += SMALL_T) {
+        srank[sv[r]] = r + 1;
+        if (what & 1) order[r] = (int32_t)sv[r];
+    }
+    if (tid == 0) s_top = (int32_t)sv[0];
+    __syncthreads();
+    if (!(what & 2)) return;
+    if (selection == PGA_SEL_TOURNAMENT) {
+        for (int m = tid; m < M; m += SMALL_T) {
+            const U4 u = draw(seed, pga::TAG_TOUR, island, gen, (uint32_t)m, 0u);
+            int best = (int)scale_u32(u.x, (uint32_t)P);
+            for (int t = 1; t < tour_k; ++t) {
+                const int c = (int)scale_u32(word(u, t), (uint32_t)P);
+                if (sL[c] > sL[best] || (sL[c] == sL[best] && c < best)) best = c;
+            }
+            sel[m] = best;
+        }
+    } else {
+        const double wmax = (scaling == PGA_SCALE_RANK) ? 1.0 : sL[s_top];
+        if (!(wmax > 0.0)) {
+            for (int m = tid; m < M; m += SMALL_T) {
+                const U4 u = draw(seed, pga::TAG_SUS, island, gen, (uint32_t)m, 0u);
+                sel[m] = (int32_t)scale_u32(u.x, (uint32_t)P);
+            }
+        } else {
+            const int B = 62 - ceil_log2_d(P);
+            // q_i (index order) and an inclusive block scan: thread t owns
+            // items 4t .. 4t+3 (P <= 4 * SMALL_T)
+            uint64_t q[4], run = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int i = 4 * tid + k;
+                uint64_t qi = 0;
+                if (i < P) {
+                    const double w = (scaling == PGA_SCALE_RANK) ? 1.0 / sqrt((double)srank[i]) : sL[i];
+                    const double x = w / wmax;
+                    if (x > 0.0) qi = (uint64_t)floor(ldexp(x, B));
+                }
+                run += qi;
+                q[k] = run;
+            }
+            const int lane = tid & 31, wid = tid >> 5;
+            uint64_t incl = run;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint64_t o = __shfl_up_sync(0xFFFFFFFFu, incl, off);
+                if (lane >= off) incl += o;
+            }
+            if (lane == 31) wsum[wid] = incl;
+            __syncthreads();
+            if (wid == 0) {
+                uint64_t v = wsum[lane];
+#pragma unroll
+                for (int off = 1; off < 32; off <<= 1) {
+                    const uint64_t o = __shfl_up_sync(0xFFFFFFFFu, v, off);
+                    if (lane >= off) v += o;
+                }
+                wsum[lane] = v;
+            }
+            __syncthreads();
+            const uint64_t base = (incl - run) + (wid ? wsum[wid - 1] : 0ull);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int i = 4 * tid + k;
+                if (i < P) sk[i] = base + q[k];
+            }
+            __syncthreads();
+            const uint64_t Q = sk[P - 1];
+            const uint64_t step = Q / (uint64_t)M;
+            const U4 u = draw(seed, pga::TAG_SUS, island, gen, 0u, 0xFFFFFFFFu);
+            const uint64_t x = ((uint64_t)u.x << 32) | (uint64_t)u.y;
+            const uint64_t start = __umul64hi(x, step);
+            for (int m = tid; m < M; m += SMALL_T) {
+                const uint64_t ptr = start + (uint64_t)m * step;
+                int lo = 0, hi = P - 1;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (sk[mid] > ptr) hi = mid;
+                    else lo = mid + 1;
+                }
+                sel[m] = lo;
+            }
+        }
+    }
+    for (int m = tid; m < M; m += SMALL_T) sigma[m] = feistel_slot(m, M, seed, gen, island);
+}
+
+static size_t select_small_smem() { return (size_t)SMALL_P * (8 + 8 + 4 + 4); }
 
 // ---------------------------------------------------------------------------
 // k_breed: warp per output slot o.  o < E: copy elite order[o];
@@ -325,10 +474,6 @@ struct BreedArgs {
     const int32_t *done, *gen_ptr;
 };
 
-__device__ __forceinline__ uint32_t parent_gene(const BreedArgs &a, const uint16_t *cm, int64_t p,
-                                                int i) {
-    return a.i32_in ? (uint32_t)a.i32_in[p * a.N + i] : (uint32_t)cm[p * a.ldn + i];
-}
 
 __device__ __forceinline__ int parent_top(const BreedArgs &a, int64_t p) {
     if (a.top32) return a.top32[p];
@@ -666,12 +811,33 @@ static int sort_order(const double *L, int64_t P, int32_t *order, uint64_t *keys
     return PGA_OK;
 }
 
+int prepare_select_small() {
+    PGA_CUDA(cudaFuncSetAttribute(k_select_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)select_small_smem()));
+    return PGA_OK;
+}
+
+// order (what & 1) and/or selection + mates (what & 2) for P <= SMALL_P
+int launch_select_small(int what, const double *L, int64_t P, const pga_params &p, int32_t gen,
+                        int32_t island, const int32_t *gen_ptr, int32_t *order, int32_t *sel,
+                        int32_t *sigma, const int32_t *done, cudaStream_t s) {
+    const int64_t M = 2 * ((P - p.elite + 1) / 2);
+    k_select_small<<<1, SMALL_T, select_small_smem(), s>>>(what, L, (int)P, (int)M, p.selection, p.tournament_k,
+                                                             p.scaling, p.seed, (uint32_t)gen, (uint32_t)island,
+                                                             gen_ptr, order, sel, sigma, done);
+    PGA_LAUNCHED();
+    return PGA_OK;
+}
+
 int run_select_ops(const double *L, int64_t P, const pga_params &p, int32_t gen, int32_t island,
                    int32_t *order, int32_t *sel, uint64_t *keys_in, uint64_t *keys_out,
                    int32_t *idx_in, uint64_t *q, uint64_t *prefix, void *tmp, size_t tmp_bytes,
                    const int32_t *done, cudaStream_t s, const int32_t *gen_ptr, bool sorted) {
     const int64_t M = 2 * ((P - p.elite + 1) / 2);
     const unsigned nb = (unsigned)((P + 255) / 256);
+    if (!sorted && P <= SMALL_P)   // one CTA; mates go to scratch (q)
+        return launch_select_small(3, L, P, p, gen, island, gen_ptr, order, sel,
+                                   reinterpret_cast<int32_t *>(q), done, s);
     int rc;
     if (!sorted) {
         rc = sort_order(L, P, order, keys_in, keys_out, idx_in, tmp, tmp_bytes, done, s);
@@ -744,7 +910,12 @@ int launch_breed_hook(const int32_t *pop, const int32_t *top, const int32_t *ord
     return PGA_OK;
 }
 
+bool small_select(const pga_ctx *c) { return c->P <= SMALL_P; }
+
 int launch_sort_order(pga_ctx *c, cudaStream_t s) {
+    if (small_select(c))
+        return launch_select_small(1, c->L, c->P, c->p, 0, c->p.island, &c->st->gen, c->order, c->sel,
+                                   c->sigma, &c->st->done, s);
     return sort_order(c->L, c->P, c->order, c->keys_in, c->keys_out, c->idx_in, c->cub_tmp,
                       c->cub_tmp_bytes, &c->st->done, s);
 }
@@ -754,16 +925,25 @@ int launch_select_breed(pga_ctx *c, cudaStream_t s) {
     const pga_params &p = c->p;
     const int32_t *done = &c->st->done;
     const int32_t *genp = &c->st->gen;
-    int rc = run_select_ops(c->L, c->P, p, 0, p.island, c->order, c->sel, c->keys_in, c->keys_out,
+    int rc;
+    if (small_select(c)) {
+        // one CTA: order + scaling + selection + mates
+        rc = launch_select_small(3, c->L, c->P, p, 0, p.island, genp, c->order, c->sel, c->sigma, done, s);
+        if (rc) return rc;
+        PGA_MARK(c, 5, s);
+        PGA_MARK(c, 6, s);
+    } else {
+        rc = run_select_ops(c->L, c->P, p, 0, p.island, c->order, c->sel, c->keys_in, c->keys_out,
                             c->idx_in, c->q, c->prefix, c->cub_tmp, c->cub_tmp_bytes, done, s,
                             genp, true);
-    if (rc) return rc;
-    PGA_MARK(c, 5, s);
-    const int64_t M = 2 * ((c->P - p.elite + 1) / 2);
-    rc = run_mates(M, p, 0, p.island, c->mkeys_in, c->mkeys_out, c->m_in, c->sigma, c->cub_tmp,
-                   c->cub_tmp_bytes, done, s, genp);
-    if (rc) return rc;
-    PGA_MARK(c, 6, s);
+        if (rc) return rc;
+        PGA_MARK(c, 5, s);
+        const int64_t M = 2 * ((c->P - p.elite + 1) / 2);
+        rc = run_mates(M, p, 0, p.island, c->mkeys_in, c->mkeys_out, c->m_in, c->sigma, c->cub_tmp,
+                       c->cub_tmp_bytes, done, s, genp);
+        if (rc) return rc;
+        PGA_MARK(c, 6, s);
+    }
     BreedArgs a{};
     fill_breed(a, p, c->P, c->N);
     a.cm_in0 = c->pop[0];
