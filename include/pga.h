@@ -230,16 +230,18 @@ int pga_op_init(uint64_t seed, int32_t N, int64_t P, int64_t p_off, int32_t isla
 int64_t pga_launch_count(void);
 
 /* Kernel timing with CUDA events on the ctx's stream (measurement only).
- * pga_profile_enable(ctx, 1) starts recording, for every generation launched
- * through pga_gen_evaluate / pga_gen_breed, the duration of the pair-sweep
- * kernel, of the fold kernel and of the whole generation; 0 stops and clears.
- * pga_profile_read synchronises and returns the SUMS in milliseconds and the
- * number of generations recorded. */
+ * pga_profile_enable(ctx, level): level 1 records, for every generation
+ * launched through pga_gen_evaluate / pga_gen_breed, 3 events (fitness
+ * kernel start/end, generation end); level 2 records every phase boundary
+ * (9 events, ~3 us of overhead per generation); 0 stops and clears.
+ * pga_profile_read synchronises and returns the SUMS in milliseconds of the
+ * fitness kernel (sweep_ms; fold_ms = 0, the fold is fused) and of whole
+ * generations, and the number of generations recorded. */
 int pga_profile_enable(pga_ctx *ctx, int32_t on);
 int pga_profile_read(pga_ctx *ctx, double *sweep_ms, double *fold_ms, double *gen_ms,
                      int32_t *count);
 
-/* Per-phase AVERAGE milliseconds of the profiled generations, ms[PGA_PROF_PHASES]:
+/* Level-2 profiling: per-phase AVERAGE milliseconds, ms[PGA_PROF_PHASES]:
  * 0 fitness sweep+fold kernel, 1 (fused, 0), 2 statistics/termination,
  * 3 order sort, 4 scaling+selection, 5 mate pairing, 6 breed, 7 advance. */
 #define PGA_PROF_PHASES 8

@@ -209,8 +209,9 @@ def pga_get_population(ctx, P: int, N: int, with_top: bool = False):
     return (lab, L, top) if with_top else (lab, L)
 
 
-def pga_profile_enable(ctx, on: bool = True):
-    _check(lib().pga_profile_enable(ctx, 1 if on else 0))
+def pga_profile_enable(ctx, on=True):
+    """on: False/0 off, True/1 fitness + generation events, 2 every phase."""
+    _check(lib().pga_profile_enable(ctx, int(on)))
 
 
 PHASES = ["fitness", "fitness_fold_fused", "stats", "order_sort", "selection", "mates", "breed", "advance"]

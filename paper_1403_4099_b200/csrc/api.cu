@@ -589,35 +589,45 @@ int pga_get_population(pga_ctx *c, int32_t *labels, double *L, int32_t *top) {
 int pga_profile_enable(pga_ctx *c, int32_t on) {
     if (!c) return fail(PGA_EINVAL, "ctx is NULL");
     c->prof = on != 0;
+    c->prof_level = on;
     c->prof_used = 0;
     return PGA_OK;
 }
 
 int pga_profile_read(pga_ctx *c, double *sweep_ms, double *fold_ms, double *gen_ms, int32_t *count) {
-    double ph[PGA_PROF_PHASES];
+    if (!c) return fail(PGA_EINVAL, "ctx is NULL");
+    PGA_CUDA(cudaSetDevice(c->device));
+    PGA_CUDA(cudaStreamSynchronize(c->stream));
+    double s = 0, g = 0;
     int32_t n = 0;
-    TRY(pga_profile_phases(c, ph, &n));
-    if (sweep_ms) *sweep_ms = ph[0] * n;
-    if (fold_ms) *fold_ms = ph[1] * n;
-    if (gen_ms) {
-        double t = 0;
-        for (int k = 0; k < PGA_PROF_PHASES; ++k) t += ph[k];
-        *gen_ms = t * n;
+    for (size_t k = 0; k + PROF_EV <= c->prof_used; k += PROF_EV) {
+        float a = 0, d = 0;
+        PGA_CUDA(cudaEventElapsedTime(&a, c->prof_ev[k], c->prof_ev[k + 2]));
+        PGA_CUDA(cudaEventElapsedTime(&d, c->prof_ev[k], c->prof_ev[k + 8]));
+        s += a;
+        g += d;
+        ++n;
     }
+    if (sweep_ms) *sweep_ms = s;
+    if (fold_ms) *fold_ms = 0.0;   // the fold is fused into the fitness kernel
+    if (gen_ms) *gen_ms = g;
     if (count) *count = n;
     return PGA_OK;
 }
 
 int pga_profile_phases(pga_ctx *c, double *ms, int32_t *count) {
     if (!c || !ms) return fail(PGA_EINVAL, "NULL argument");
+    if (c->prof_level < 2) return fail(PGA_ESTATE, "pga_profile_phases needs pga_profile_enable(ctx, 2)");
     PGA_CUDA(cudaSetDevice(c->device));
     PGA_CUDA(cudaStreamSynchronize(c->stream));
     double acc[PGA_PROF_PHASES] = {0};
     int32_t n = 0;
     for (size_t k = 0; k + PROF_EV <= c->prof_used; k += PROF_EV) {
         for (int j = 0; j < PGA_PROF_PHASES; ++j) {
+            if (j == 1) continue;                       // fused: no separate fold mark
             float t = 0;
-            PGA_CUDA(cudaEventElapsedTime(&t, c->prof_ev[k + j], c->prof_ev[k + j + 1]));
+            const int a0 = (j == 0) ? 0 : j, a1 = (j == 0) ? 2 : j + 1;
+            PGA_CUDA(cudaEventElapsedTime(&t, c->prof_ev[k + a0], c->prof_ev[k + a1]));
             acc[j] += t;
         }
         ++n;

@@ -528,10 +528,7 @@ int launch_fitness(pga_ctx *c, const FitBufs &b, int64_t P, double *L, uint16_t 
     if (ev) PGA_CUDA(cudaEventRecord(ev[0], s));
     k_fitness<<<(unsigned)(a.nRT * a.nCB), FIT_THREADS, fitness_smem(N), s>>>(*b.tm0, *b.tm1, c->tmC, a);
     PGA_LAUNCHED();
-    if (ev) {
-        PGA_CUDA(cudaEventRecord(ev[1], s));   // sweep and fold are one fused kernel
-        PGA_CUDA(cudaEventRecord(ev[2], s));
-    }
+    if (ev) PGA_CUDA(cudaEventRecord(ev[2], s));   // sweep and fold are one fused kernel
     return PGA_OK;
 }
 

@@ -326,43 +326,80 @@ k_select_small(int what, const double *__restrict__ L, int P, int M, int selecti
                int32_t *sel, int32_t *sigma, const int32_t *done) {
     if (done && *done) return;
     extern __shared__ __align__(16) unsigned char ssm[];
-    uint64_t *sk = reinterpret_cast<uint64_t *>(ssm);               // [SMALL_P] keys, then prefix
-    double *sL = reinterpret_cast<double *>(sk + SMALL_P);          // [SMALL_P]
+    using BRS0 = cub::BlockRadixSort<uint64_t, SMALL_T, SMALL_P / SMALL_T, uint32_t>;
+    constexpr size_t SK_BYTES = (size_t)SMALL_P * 8 > sizeof(typename BRS0::TempStorage)
+                                    ? (size_t)SMALL_P * 8 : sizeof(typename BRS0::TempStorage);
+    uint64_t *sk = reinterpret_cast<uint64_t *>(ssm);               // sort temp storage, then prefix
+    double *sL = reinterpret_cast<double *>(ssm + SK_BYTES);        // [SMALL_P]
     uint32_t *sv = reinterpret_cast<uint32_t *>(sL + SMALL_P);      // [SMALL_P]
     int32_t *srank = reinterpret_cast<int32_t *>(sv + SMALL_P);     // [SMALL_P]
     __shared__ uint64_t wsum[SMALL_T / 32];
     __shared__ int32_t s_top;
     const int tid = threadIdx.x;
     if (gen_ptr) gen = (uint32_t)*gen_ptr;
-    int n2 = 2;
-    while (n2 < P) n2 <<= 1;
-    for (int t = tid; t < n2; t += SMALL_T) {
-        if (t < P) {
-            double x = L[t];
-            if (x == 0.0) x = 0.0;
-            sL[t] = x;
-            sk[t] = ~(uint64_t)__double_as_longlong(x);
-            sv[t] = (uint32_t)t;
-        } else {
-            sk[t] = ~0ull;
-            sv[t] = 0xFFFFFFFFu;
-        }
-    }
-    __syncthreads();
-    for (int size = 2; size <= n2; size <<= 1)
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-            for (int t = tid; t < n2 / 2; t += SMALL_T) {
-                const int i = 2 * t - (t & (stride - 1)), j = i + stride;
-                const bool up = (i & size) == 0;
-                const uint64_t ki = sk[i], kj = sk[j];
-                const uint32_t vi = sv[i], vj = sv[j];
-                if (kv_less(kj, vj, ki, vi) == up) {
-                    sk[i] = kj; sk[j] = ki;
-                    sv[i] = vj; sv[j] = vi;
-                }
+    if (P <= SMALL_T) {
+        // small: bitonic network on n2 <= 1024 items (one pair per thread per stage)
+        int n2 = 2;
+        while (n2 < P) n2 <<= 1;
+        uint32_t *svv = sv;
+        uint64_t *skk = reinterpret_cast<uint64_t *>(srank + SMALL_P);   // scratch after srank
+        for (int t = tid; t < n2; t += SMALL_T) {
+            if (t < P) {
+                double x = L[t];
+                if (x == 0.0) x = 0.0;
+                sL[t] = x;
+                skk[t] = ~(uint64_t)__double_as_longlong(x);
+                svv[t] = (uint32_t)t;
+            } else {
+                skk[t] = ~0ull;
+                svv[t] = 0xFFFFFFFFu;
             }
-            __syncthreads();
         }
+        __syncthreads();
+        for (int size = 2; size <= n2; size <<= 1)
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                const int t = tid;
+                if (t < n2 / 2) {
+                    const int i = 2 * t - (t & (stride - 1)), j = i + stride;
+                    const bool up = (i & size) == 0;
+                    const uint64_t ki = skk[i], kj = skk[j];
+                    const uint32_t vi = svv[i], vj = svv[j];
+                    if (kv_less(kj, vj, ki, vi) == up) {
+                        skk[i] = kj; skk[j] = ki;
+                        svv[i] = vj; svv[j] = vi;
+                    }
+                }
+                __syncthreads();
+            }
+    } else {
+        // stable in-CTA radix sort of (key = ~bits(L), value = index); items
+        // are loaded in index order (blocked), so equal keys stay in index order
+        using BRS = cub::BlockRadixSort<uint64_t, SMALL_T, SMALL_P / SMALL_T, uint32_t>;
+        uint64_t kk[SMALL_P / SMALL_T];
+        uint32_t vv[SMALL_P / SMALL_T];
+#pragma unroll
+        for (int k = 0; k < SMALL_P / SMALL_T; ++k) {
+            const int t = tid * (SMALL_P / SMALL_T) + k;
+            if (t < P) {
+                double x = L[t];
+                if (x == 0.0) x = 0.0;
+                sL[t] = x;
+                kk[k] = ~(uint64_t)__double_as_longlong(x);
+                vv[k] = (uint32_t)t;
+            } else {
+                kk[k] = ~0ull;
+                vv[k] = 0xFFFFFFFFu;
+            }
+        }
+        {
+            typename BRS::TempStorage &ts = *reinterpret_cast<typename BRS::TempStorage *>(sk);
+            BRS(ts).Sort(kk, vv);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < SMALL_P / SMALL_T; ++k) sv[tid * (SMALL_P / SMALL_T) + k] = vv[k];
+        __syncthreads();
+    }
     for (int r = tid; r < P; r += SMALL_T) {
         srank[sv[r]] = r + 1;
         if (what & 1) order[r] = (int32_t)sv[r];
@@ -450,7 +487,12 @@ k_select_small(int what, const double *__restrict__ L, int P, int M, int selecti
     for (int m = tid; m < M; m += SMALL_T) sigma[m] = feistel_slot(m, M, seed, gen, island);
 }
 
-static size_t select_small_smem() { return (size_t)SMALL_P * (8 + 8 + 4 + 4); }
+static size_t select_small_smem() {
+    using BRS = cub::BlockRadixSort<uint64_t, SMALL_T, SMALL_P / SMALL_T, uint32_t>;
+    const size_t a = (size_t)SMALL_P * 8 > sizeof(typename BRS::TempStorage) ? (size_t)SMALL_P * 8
+                                                                             : sizeof(typename BRS::TempStorage);
+    return a + (size_t)SMALL_P * (8 + 4 + 4) + (size_t)SMALL_T * 8;   // + bitonic key scratch
+}
 
 // ---------------------------------------------------------------------------
 // k_breed: warp per output slot o.  o < E: copy elite order[o];

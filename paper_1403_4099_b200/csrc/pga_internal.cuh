@@ -28,7 +28,7 @@ void count_launch(int n = 1);
 
 #define PGA_MARK(c, k, s)                                                  \
     do {                                                                   \
-        if ((c)->pev) PGA_CUDA(cudaEventRecord((c)->pev[k], (s)));         \
+        if ((c)->pev && (c)->prof_level >= 2) PGA_CUDA(cudaEventRecord((c)->pev[k], (s))); \
     } while (0)
 
 #define PGA_LAUNCHED()                                                     \
@@ -117,6 +117,7 @@ struct pga_ctx {
     pga::DevState *h_st = nullptr;
     // profiling (pga_profile_enable): per generation 4 events
     bool prof = false;
+    int prof_level = 0;                 // 1: fitness + generation only, 2: every phase
     std::vector<cudaEvent_t> prof_ev;   // groups of PROF_EV events per generation (see api.cu)
     size_t prof_used = 0;
     cudaEvent_t *pev = nullptr;         // this generation's events while profiling, else null
