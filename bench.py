@@ -37,6 +37,10 @@ CFG_POP = {"C1": 128, "C2": 1024, "C3": 4096, "C4": 65536, "C5": 262144}
 SEED = 2024
 SM_COUNT = 148
 FP64_LANES_PER_SM = 64           # DFMA lanes / clk / SM (B200: 37 TF fp64 = 148*64*2*1.965G)
+# Measured ceiling of the exact fp64 masked-accumulate inner loop on this pool
+# (tools/mb_pairloop.cu, shared-memory resident, no pipeline/fold): 26.8
+# executed pair-updates per SM-clock, register-file-read bound.
+LOOP_PAIRS_PER_CLK = 26.8
 
 METRIC = ("GA generation throughput, nominal pair-updates/s (N^2 * P per generation; "
           "fitness + all operators)")
@@ -339,7 +343,11 @@ def main():
                                        "x %.0f MHz (sm_max_mhz)" % sm_max,
                          "frac_at_measured_clock": (achieved / (FP64_LANES_PER_SM * SM_COUNT *
                                                     clk["sm_mhz"] * 1e6))
-                         if clk and clk.get("sm_mhz") else None},
+                         if clk and clk.get("sm_mhz") else None,
+                         "loop_ceiling": LOOP_PAIRS_PER_CLK * SM_COUNT * sm_max * 1e6,
+                         "frac_of_loop_ceiling": achieved / (LOOP_PAIRS_PER_CLK * SM_COUNT * sm_max * 1e6),
+                         "loop_ceiling_basis": "measured bare inner loop (tools/mb_pairloop.cu): "
+                                               "26.8 pairs/clk/SM, register-file-read bound"},
             "gpu_launches": int(launches),
             "clocks": clk,
             "best_L": st["best_L"],

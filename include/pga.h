@@ -225,6 +225,58 @@ int pga_op_canonicalize(int32_t *labels, int64_t P, int32_t N, int32_t device);
 int pga_op_init(uint64_t seed, int32_t N, int64_t P, int64_t p_off, int32_t island,
                 int32_t device, int32_t *out);
 
+/* ---------------------------------------------------------------------
+ * Batched GA: many small, independent clustering
+ * problems in ONE kernel launch.  This is the paper's own test workload
+ * (1760 correlation matrices of 18 JSE stocks, each clustered by its
+ * own PGA run with the Table 3 configuration; timed per matrix in Table 4,
+ * P:356-375).  One CTA per matrix keeps C, both populations, L, and the
+ * selection state in shared memory for the whole run.
+ *
+ * Matrix b runs exactly the single-population GA of pga_run (Alg. 1
+ * P:208-234 with DESIGN.md §3's operators, one island, island id 0, global
+ * index offset 0) under the seed params->seed + b.  The oracle equivalent is
+ * orc_run(C_b, seed + b, n_islands = 1).
+ *
+ * C            fp64 [B][N][N], each exactly symmetric with unit diagonal
+ *              (checked for host input; device input is trusted).
+ * B            number of matrices, 1 <= B <= 2^20.
+ * N            2 <= N <= 32 (one gene per lane).
+ * params       pop_size 2..2048; the shared-memory footprint
+ *              (pga_batch_smem_bytes) must fit one CTA; n_islands must be 1;
+ *              device selects the GPU.
+ * on_device    0: every array is host memory and the call is synchronous.
+ *              1: every array is device memory on params->device and the call
+ *              is stream-ordered on `stream` (NULL = legacy default stream).
+ * best_labels  int32 [B][N], 1-based canonical best labelling per matrix.
+ * best_L       fp64 [B], its Eq. 8 likelihood.
+ * gens         int32 [B], generations evaluated.
+ * reason       int32 [B], PGA_REASON_*.
+ * history      fp64 [B][max_gens] per-generation best L, or NULL.  Entries
+ *              past gens[b] are 0 (host) / untouched (device).
+ * Any of best_labels .. history may be NULL except best_L.
+ * ------------------------------------------------------------------- */
+int pga_batch_run(const double *C, int32_t B, int32_t N, const pga_params *params,
+                  int32_t on_device, int32_t *best_labels, double *best_L, int32_t *gens,
+                  int32_t *reason, double *history, void *stream);
+
+/* Shared memory one CTA of pga_batch_run needs for (N, pop_size, elite);
+ * PGA_EINVAL if it exceeds the device's per-block opt-in limit. */
+int pga_batch_smem_bytes(int32_t N, int32_t pop_size, int32_t elite, int32_t device,
+                         int64_t *bytes);
+
+/* Test hooks of the batched kernel (host memory, 0-based labels):
+ * pga_batch_op_evaluate: Eq. 8 for labels [B][P][N] (values 0..2N) against
+ *   C [B][N][N] -> L [B][P], top [B][P] (-1 = none), as pga_evaluate.
+ * pga_batch_op_step: one generation's operators (order, scaling, selection,
+ *   mates, crossover, mutation, canonicalisation, elitism) of every matrix,
+ *   given its canonical population pop [B][P][N], L [B][P] and top [B][P],
+ *   at generation `gen` -> next [B][P][N]; matrix b uses seed + b. */
+int pga_batch_op_evaluate(const double *C, int32_t B, int32_t N, const int32_t *labels,
+                          int32_t P, int32_t device, double *L, int32_t *top);
+int pga_batch_op_step(int32_t B, int32_t N, const pga_params *params, const int32_t *pop,
+                      const double *L, const int32_t *top, int32_t gen, int32_t *next);
+
 /* Number of this library's kernel launches issued so far in this process
  * (for the bench's gpu_launches claim). */
 int64_t pga_launch_count(void);

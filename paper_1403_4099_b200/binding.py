@@ -80,6 +80,14 @@ _SIGS = {
     "pga_op_init": (ct.c_int, [ct.c_uint64, ct.c_int32, ct.c_int64, ct.c_int64, ct.c_int32,
                                ct.c_int32, ct.c_void_p]),
     "pga_launch_count": (ct.c_int64, []),
+    "pga_batch_run": (ct.c_int, [ct.c_void_p, ct.c_int32, ct.c_int32, ct.c_void_p, ct.c_int32,
+                                 ct.c_void_p, ct.c_void_p, ct.c_void_p, ct.c_void_p, ct.c_void_p,
+                                 ct.c_void_p]),
+    "pga_batch_smem_bytes": (ct.c_int, [ct.c_int32, ct.c_int32, ct.c_int32, ct.c_int32, ct.c_void_p]),
+    "pga_batch_op_evaluate": (ct.c_int, [ct.c_void_p, ct.c_int32, ct.c_int32, ct.c_void_p, ct.c_int32,
+                                         ct.c_int32, ct.c_void_p, ct.c_void_p]),
+    "pga_batch_op_step": (ct.c_int, [ct.c_int32, ct.c_int32, ct.c_void_p, ct.c_void_p, ct.c_void_p,
+                                     ct.c_void_p, ct.c_int32, ct.c_void_p]),
 }
 
 
@@ -309,6 +317,56 @@ def pga_op_init(seed: int, N: int, P: int, p_off: int = 0, island: int = 0, devi
     out = np.zeros((P, N), np.int32)
     _check(lib().pga_op_init(seed, N, P, p_off, island, device, _p(out)))
     return out
+
+
+def pga_batch_run(C, params: pga_params, history: bool = False):
+    """Batched GA over host matrices C [B][N][N] (include/pga.h pga_batch_run).
+    Returns dict(best_labels [B][N] 1-based, best_L [B], gens [B], reason [B],
+    history [B][max_gens] or None)."""
+    C = _c(C, np.float64)
+    B, N = C.shape[0], C.shape[1]
+    out = dict(best_labels=np.zeros((B, N), np.int32), best_L=np.zeros(B),
+               gens=np.zeros(B, np.int32), reason=np.zeros(B, np.int32),
+               history=np.zeros((B, params.max_gens)) if history else None)
+    _check(lib().pga_batch_run(_p(C), B, N, ct.byref(params), 0, _p(out["best_labels"]),
+                               _p(out["best_L"]), _p(out["gens"]), _p(out["reason"]),
+                               _p(out["history"]), None))
+    return out
+
+
+def pga_batch_run_device(C_dev, params: pga_params, best_labels_dev, best_L_dev, gens_dev=None,
+                         reason_dev=None, history_dev=None, stream=None):
+    """Device variant (torch tensors / raw pointers), stream-ordered."""
+    B, N = C_dev.shape[0], C_dev.shape[1]
+    _check(lib().pga_batch_run(_p(C_dev), B, N, ct.byref(params), 1, _p(best_labels_dev),
+                               _p(best_L_dev), _p(gens_dev), _p(reason_dev), _p(history_dev),
+                               None if stream is None else ct.c_void_p(stream)))
+
+
+def pga_batch_smem_bytes(N: int, pop_size: int, elite: int, device: int = 0) -> int:
+    v = ct.c_int64()
+    _check(lib().pga_batch_smem_bytes(N, pop_size, elite, device, ct.byref(v)))
+    return v.value
+
+
+def pga_batch_op_evaluate(C, labels, device: int = 0):
+    C = _c(C, np.float64)
+    labels = _c(labels, np.int32)
+    B, P, N = labels.shape
+    L = np.zeros((B, P))
+    top = np.zeros((B, P), np.int32)
+    _check(lib().pga_batch_op_evaluate(_p(C), B, N, _p(labels), P, device, _p(L), _p(top)))
+    return L, top
+
+
+def pga_batch_op_step(params: pga_params, pop, L, top, gen: int):
+    pop = _c(pop, np.int32)
+    B, P, N = pop.shape
+    L = _c(L, np.float64)
+    top = _c(top, np.int32)
+    nxt = np.zeros_like(pop)
+    _check(lib().pga_batch_op_step(B, N, ct.byref(params), _p(pop), _p(L), _p(top), gen, _p(nxt)))
+    return nxt
 
 
 def pga_launch_count() -> int:

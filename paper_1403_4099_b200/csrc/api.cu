@@ -50,7 +50,7 @@ bool small_select(const pga_ctx *c);
 
 static int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
-static int check_params(const pga_params *p) {
+int check_params(const pga_params *p) {
     if (!p) return fail(PGA_EINVAL, "params is NULL");
     if (p->pop_size < 2) return fail(PGA_EINVAL, "pop_size must be >= 2 (S:113)");
     if (p->pop_size > (1 << 26)) return fail(PGA_EINVAL, "pop_size too large");
@@ -78,7 +78,7 @@ static int check_params(const pga_params *p) {
     return PGA_OK;
 }
 
-static int check_corr(const double *C, int32_t N) {
+int check_corr(const double *C, int32_t N) {
     if (!C) return fail(PGA_EINVAL, "C is NULL");
     if (N < 2 || N > 16384) return fail(PGA_EINVAL, "N must be in [2, 16384]");
     for (int64_t i = 0; i < N; ++i) {
@@ -93,6 +93,15 @@ static int check_corr(const double *C, int32_t N) {
             }
         }
     }
+    return PGA_OK;
+}
+
+int ensure_device(int dev) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) return fail(PGA_EDEVICE, "no CUDA device available (libpga has no CPU fallback)");
+    if (dev >= n) return fail(PGA_EINVAL, "device ordinal out of range");
+    PGA_CUDA(cudaSetDevice(dev));
     return PGA_OK;
 }
 
@@ -119,15 +128,6 @@ void free_ctx(pga_ctx *c) {
     if (c->h_st) cudaFreeHost(c->h_st);
     for (cudaEvent_t e : c->prof_ev) cudaEventDestroy(e);
     if (c->stream) cudaStreamDestroy(c->stream);
-}
-
-int ensure_device(int dev) {
-    int n = 0;
-    cudaError_t e = cudaGetDeviceCount(&n);
-    if (e != cudaSuccess || n == 0) return fail(PGA_EDEVICE, "no CUDA device available (libpga has no CPU fallback)");
-    if (dev >= n) return fail(PGA_EINVAL, "device ordinal out of range");
-    PGA_CUDA(cudaSetDevice(dev));
-    return PGA_OK;
 }
 
 template <typename T>

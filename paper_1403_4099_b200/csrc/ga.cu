@@ -201,12 +201,6 @@ __global__ void k_sort_keys(const double *__restrict__ L, int64_t P, uint64_t *k
     idx[i] = (int32_t)i;
 }
 
-__device__ __forceinline__ int ceil_log2_d(int64_t x) {
-    int b = 0;
-    while (((int64_t)1 << b) < x) ++b;
-    return b;
-}
-
 // q_i = floor(2^B * w_i / w_max), w = 1/sqrt(rank) (RANK) or L (NONE)
 __global__ void k_weights(const double *__restrict__ L, const int32_t *__restrict__ order, int64_t P,
                           int scaling, uint64_t *q, const int32_t *done) {
@@ -275,26 +269,6 @@ __global__ void k_tournament(const double *__restrict__ L, int64_t P, int64_t M,
         if (L[c] > L[best] || (L[c] == L[best] && c < best)) best = c;
     }
     sel[m] = best;
-}
-
-__device__ __forceinline__ int32_t feistel_slot(int64_t m, int64_t M, uint64_t seed, uint32_t gen,
-                                                uint32_t island) {
-    int h = (ceil_log2_d(M) + 1) / 2;
-    if (h < 1) h = 1;
-    const uint32_t mask = (1u << h) - 1u;
-    uint32_t x = (uint32_t)m;
-    do {
-        uint32_t Lh = x >> h, R = x & mask;
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            const U4 f = draw(seed, pga::TAG_PERM, island, gen, R, (uint32_t)r);
-            const uint32_t t = R;
-            R = Lh ^ (f.x & mask);
-            Lh = t;
-        }
-        x = (Lh << h) | R;
-    } while (x >= (uint32_t)M);
-    return (int32_t)x;
 }
 
 // Mate pairing (Q10): sigma = keyed Feistel permutation of the M slots
@@ -924,7 +898,7 @@ static void fill_breed(BreedArgs &a, const pga_params &p, int64_t P, int N) {
     auto thr = [](double x) -> uint64_t {
         if (x >= 1.0) return (uint64_t)1 << 32;
         if (x <= 0.0) return 0;
-        return (uint64_t)llrint(x * 4294967296.0);
+        return (uint64_t)llround(x * 4294967296.0);   // Q13: llround(p * 2^32)
     };
     a.thr_c = thr(p.p_crossover);
     a.thr_m = thr(p.p_mutation);

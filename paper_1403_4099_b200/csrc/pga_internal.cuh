@@ -19,6 +19,9 @@ void set_error(const std::string &msg);
 int fail(int code, const std::string &msg);
 int cuda_fail(cudaError_t e, const char *what);
 void count_launch(int n = 1);
+int check_params(const pga_params *p);       // api.cu: pga_params validation
+int check_corr(const double *C, int32_t N);  // api.cu: C finite, unit diagonal, symmetric
+int ensure_device(int dev);                  // api.cu: device present, made current
 
 #define PGA_CUDA(call)                                                     \
     do {                                                                   \
@@ -215,6 +218,36 @@ __device__ __forceinline__ double cluster_term(int n_s, double c_s) {
     const double n2 = n * n;
     const double ch = fmin(c_s, n2 - 1e-9);
     return log(n / ch) + (n - 1.0) * log((n2 - n) / (n2 - ch));
+}
+
+
+__device__ __forceinline__ int ceil_log2_d(int64_t x) {
+    int b = 0;
+    while (((int64_t)1 << b) < x) ++b;
+    return b;
+}
+
+// Mate slot m of M (Q10): keyed 4-round Feistel permutation on h+h bits
+// (2^(2h) >= M), round function Philox(PERM; R, round)[0], cycle-walked
+// back into [0, M).
+__device__ __forceinline__ int32_t feistel_slot(int64_t m, int64_t M, uint64_t seed, uint32_t gen,
+                                                uint32_t island) {
+    int h = (ceil_log2_d(M) + 1) / 2;
+    if (h < 1) h = 1;
+    const uint32_t mask = (1u << h) - 1u;
+    uint32_t x = (uint32_t)m;
+    do {
+        uint32_t Lh = x >> h, R = x & mask;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const U4 f = draw(seed, pga::TAG_PERM, island, gen, R, (uint32_t)r);
+            const uint32_t t = R;
+            R = Lh ^ (f.x & mask);
+            Lh = t;
+        }
+        x = (Lh << h) | R;
+    } while (x >= (uint32_t)M);
+    return (int32_t)x;
 }
 
 }  // namespace pgad

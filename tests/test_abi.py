@@ -91,3 +91,21 @@ def test_no_cpu_fallback(pga):
     with pytest.raises(pga.PgaError) as e:
         pga.pga_correlation(np.random.default_rng(0).standard_normal((10, 3)))
     assert e.value.code == pga.binding.PGA_EDEVICE
+
+
+@pytest.mark.parametrize("N,kw,msg", [
+    (33, {}, "2 <= N <= 32"),
+    (8, dict(pop_size=4096), "pop_size <= 2048"),
+    (8, dict(n_islands=2), "one island per matrix"),
+    (8, dict(elite=100), "elite"),
+])
+def test_batch_validation(pga, N, kw, msg):
+    """pga_batch_run validates before touching a device."""
+    kw.setdefault("pop_size", 100)
+    with pytest.raises(pga.PgaError) as e:
+        pga.pga_batch_run(np.stack([np.eye(N)] * 2), pga.pga_params_default(**kw))
+    assert e.value.code == pga.binding.PGA_EINVAL and msg in str(e.value)
+    bad = np.stack([np.eye(4), np.eye(4)])
+    bad[1, 0, 1] = 0.5        # matrix 1 not symmetric
+    with pytest.raises(pga.PgaError, match="matrix 1"):
+        pga.pga_batch_run(bad, pga.pga_params_default(pop_size=10, elite=2))

@@ -121,3 +121,36 @@ def adversarial_population(N):
         pair[1] = 0
     rows.append(pair)
     return np.asarray(rows, np.int32)
+
+
+# ---------------------------------------------------------------------------
+# F1: the paper's test-set shape -- many windows of
+# 18 stocks, each clustered by its own GA (1760 matrices from 3-minute
+# bars; Table 3 GA configuration).  Reading Q29: the
+# paper does not give the window length; a trading day of 3-minute bars
+# (8 h -> T = 160) is used.  Per window: 2..4 planted clusters of 2..7 stocks,
+# loadings g ~ U(0.55, 0.85), the remaining stocks independent.
+# ---------------------------------------------------------------------------
+F1 = dict(B=1760, N=18, T=160, seed0=1_760_000, pop=1000, gens=400)
+
+
+def window_spec(b: int, N: int = 18, T: int = 160, seed0: int = 1_760_000) -> PlantedSpec:
+    rng = np.random.Generator(np.random.PCG64(seed0 + b))
+    k = int(rng.integers(2, 5))
+    sizes = []
+    for _ in range(k):
+        n = int(rng.integers(2, 8))
+        if sum(sizes) + n > N:
+            break
+        sizes.append(n)
+    g = tuple(float(x) for x in rng.uniform(0.55, 0.85, len(sizes)))
+    return PlantedSpec(tuple(sizes), g, T, seed0 + b, singletons=N - sum(sizes))
+
+
+def window_returns(B: int, N: int = 18, T: int = 160, seed0: int = 1_760_000):
+    """Returns X [B][T][N] and planted labels [B][N] (0-based canonical)."""
+    X = np.empty((B, T, N))
+    planted = np.empty((B, N), np.int32)
+    for b in range(B):
+        X[b], planted[b] = noh_returns(window_spec(b, N, T, seed0))
+    return X, planted
