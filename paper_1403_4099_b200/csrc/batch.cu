@@ -36,8 +36,47 @@ using namespace pgad;
 constexpr int BT = 256, BNW = BT / 32;   // threads per CTA (one CTA per matrix)
 constexpr int BMAX_N = 32, BMAX_P = 2048;
 constexpr int TAB = 36;                  // per-thread canonicalisation table (labels 0..N)
+constexpr int EB = 8;                    // chromosomes per warp per evaluation batch
 
 enum { MODE_RUN = 0, MODE_EVAL = 1, MODE_STEP = 2 };
+
+// Shared-memory layout of one CTA.  The L array doubles as the SUS prefix
+// (u64) once the weights are formed and as the per-thread canonicalisation
+// tables during init and breed (L is dead then).
+struct BLayout {
+    int ldb, n2, qcap;
+    size_t oL, oC, oVal, oRank, oSel, oSig, oTop, oPop0, oPop1, oV, oQf, oQn, oQl, oQs, oLg, total;
+};
+
+__host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+__host__ __device__ inline BLayout b_layout(int N, int P, int M) {
+    BLayout l;
+    l.ldb = (N + 3) & ~3;
+    int n2 = 2;
+    while (n2 < P) n2 <<= 1;
+    l.n2 = n2;
+    l.qcap = EB * (N / 2 > 0 ? N / 2 : 1);   // clusters with n_s >= 2 per chromosome <= N/2
+    l.oL = 0;
+    size_t o = al16((size_t)8 * P);
+    if (o < (size_t)BT * TAB) o = al16((size_t)BT * TAB);
+    l.oC = o;     o += al16((size_t)8 * N * N);
+    l.oVal = o;   o += al16((size_t)4 * n2);
+    l.oRank = o;  o += al16((size_t)2 * P);
+    l.oSel = o;   o += al16((size_t)2 * M);
+    l.oSig = o;   o += al16((size_t)2 * M);
+    l.oTop = o;   o += al16((size_t)P);
+    l.oPop0 = o;  o += al16((size_t)P * l.ldb);
+    l.oPop1 = o;  o += al16((size_t)P * l.ldb);
+    l.oV = o;     o += (size_t)8 * 32 * BNW;
+    l.oQf = o;    o += al16((size_t)8 * l.qcap * BNW);
+    l.oQn = o;    o += al16((size_t)l.qcap * BNW);
+    l.oQl = o;    o += al16((size_t)l.qcap * BNW);
+    l.oQs = o;    o += al16((size_t)2 * (EB + 1) * BNW);
+    l.oLg = o;    o += (size_t)8 * 2 * (BMAX_N + 1);
+    l.total = o;
+    return l;
+}
 
 struct BArgs {
     const double *C;                     // [B][N][N]
@@ -60,53 +99,23 @@ struct BArgs {
     int32_t *out_pop;                    // [B][P][N]
     double *out_L;                       // [B][P]
     int32_t *out_top;                    // [B][P]
+    BLayout ly;                          // shared-memory layout (host-computed)
 };
-
-// Shared-memory layout of one CTA.  [L | key] doubles as the per-thread
-// canonicalisation tables during init and breed (L and the keys are dead
-// then).
-struct BLayout {
-    int ldb, n2;
-    size_t oL, oKey, oC, oVal, oRank, oSel, oSig, oTop, oPop0, oPop1, oV, total;
-};
-
-__host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~(size_t)15; }
-
-__host__ __device__ inline BLayout b_layout(int N, int P, int M) {
-    BLayout l;
-    l.ldb = (N + 3) & ~3;
-    int n2 = 2;
-    while (n2 < P) n2 <<= 1;
-    l.n2 = n2;
-    l.oL = 0;
-    l.oKey = al16((size_t)8 * P);
-    size_t o = l.oKey + al16((size_t)8 * n2);
-    if (o < (size_t)BT * TAB) o = al16((size_t)BT * TAB);
-    l.oC = o;     o += al16((size_t)8 * N * N);
-    l.oVal = o;   o += al16((size_t)4 * n2);
-    l.oRank = o;  o += al16((size_t)2 * P);
-    l.oSel = o;   o += al16((size_t)2 * M);
-    l.oSig = o;   o += al16((size_t)2 * M);
-    l.oTop = o;   o += al16((size_t)P);
-    l.oPop0 = o;  o += al16((size_t)P * l.ldb);
-    l.oPop1 = o;  o += al16((size_t)P * l.ldb);
-    l.oV = o;     o += (size_t)8 * 32 * BNW;
-    l.total = o;
-    return l;
-}
 
 struct BSmem {
-    double *L, *C, *V;
-    uint64_t *key;
+    double *L, *C, *V, *qf, *lgn, *lgnn;
+    uint64_t *prefix;
     uint32_t *val;
     int16_t *rank, *sel, *sig;
-    uint8_t *top, *pop[2], *tabs;
+    uint16_t *qs;
+    uint8_t *top, *pop[2], *tabs, *qn, *ql;
+    int qcap;
 };
 
 __device__ __forceinline__ BSmem b_smem(unsigned char *sm, const BLayout &ly) {
     BSmem s;
     s.L = reinterpret_cast<double *>(sm + ly.oL);
-    s.key = reinterpret_cast<uint64_t *>(sm + ly.oKey);
+    s.prefix = reinterpret_cast<uint64_t *>(sm + ly.oL);
     s.C = reinterpret_cast<double *>(sm + ly.oC);
     s.val = reinterpret_cast<uint32_t *>(sm + ly.oVal);
     s.rank = reinterpret_cast<int16_t *>(sm + ly.oRank);
@@ -117,6 +126,13 @@ __device__ __forceinline__ BSmem b_smem(unsigned char *sm, const BLayout &ly) {
     s.pop[1] = sm + ly.oPop1;
     s.V = reinterpret_cast<double *>(sm + ly.oV);
     s.tabs = sm + ly.oL;
+    s.qf = reinterpret_cast<double *>(sm + ly.oQf);
+    s.qn = sm + ly.oQn;
+    s.ql = sm + ly.oQl;
+    s.qs = reinterpret_cast<uint16_t *>(sm + ly.oQs);
+    s.qcap = ly.qcap;
+    s.lgn = reinterpret_cast<double *>(sm + ly.oLg);
+    s.lgnn = s.lgn + (BMAX_N + 1);
     return s;
 }
 
@@ -154,74 +170,101 @@ __device__ __forceinline__ void b_init(const BArgs &a, const BSmem &s, int ldb, 
     }
 }
 
-// Eq. 5/6/8 for every chromosome of `pop`: warp per chromosome, lane = gene.
+// Eq. 5/6/8 for every chromosome of `pop`: warp per chromosome, lane = gene,
+// EB chromosomes per batch.  n_s by __match_any_sync/popc; V_i = sum of C_ji
+// over i's group (set bits, ascending j); each group leader sums V over its
+// group (c_s, Eq. 6).  Clusters with n_s >= 2 and c_s > n_s (the only
+// non-zero summands, Q2) are queued; the Eq. 8 summands of the whole batch
+// are then taken lane-parallel, and lane e adds chromosome e's summands in
+// queue (= label, for canonical labels) order.
 __device__ __forceinline__ void b_evaluate(const BSmem &s, const uint8_t *pop, int N, int P, int ldb) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double *Vw = s.V + warp * 32;
+    double *qf = s.qf + warp * s.qcap;
+    uint8_t *qn = s.qn + warp * s.qcap, *ql = s.ql + warp * s.qcap;
+    uint16_t *qs = s.qs + warp * (EB + 1);
     const bool valid = lane < N;
-    for (int p = warp; p < P; p += BNW) {
-        const uint32_t lab = valid ? (uint32_t)pop[(size_t)p * ldb + lane] : 0x100u + (uint32_t)lane;
-        const unsigned m = __match_any_sync(0xFFFFFFFFu, lab);
-        double V = 0.0;                         // V_i = sum_{j in s_i} C_ji (ascending j)
-        if (valid)
-            for (unsigned mm = m; mm; mm &= mm - 1) V += s.C[(__ffs(mm) - 1) * N + lane];
-        Vw[lane] = V;
-        __syncwarp();
-        double f = 0.0;
-        if (valid && (__ffs(m) - 1) == lane) {  // group leader: c_s (Eq. 6), summand (Eq. 8)
+    for (int p0 = warp * EB; p0 < P; p0 += BNW * EB) {
+        const int ne = min(EB, P - p0);
+        int cnt = 0;
+        for (int e = 0; e < ne; ++e) {
+            const uint32_t lab = valid ? (uint32_t)pop[(size_t)(p0 + e) * ldb + lane] : 0x100u + (uint32_t)lane;
+            const unsigned m = __match_any_sync(0xFFFFFFFFu, lab);
+            double V = 0.0;                         // V_i = sum_{j in s_i} C_ji (ascending j)
+            if (valid)
+                for (unsigned mm = m; mm; mm &= mm - 1) V += s.C[(__ffs(mm) - 1) * N + lane];
+            Vw[lane] = V;
+            __syncwarp();
+            const int n = __popc(m);
             double c = 0.0;
-            for (unsigned mm = m; mm; mm &= mm - 1) c += Vw[__ffs(mm) - 1];
-            f = cluster_term(__popc(m), c);
-        }
-        double sum = f, bf = f;
-        uint32_t bs = f > 0.0 ? lab : 0xFFFFFFFFu;
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            sum += __shfl_xor_sync(0xFFFFFFFFu, sum, off);
-            const double of = __shfl_xor_sync(0xFFFFFFFFu, bf, off);
-            const uint32_t os = __shfl_xor_sync(0xFFFFFFFFu, bs, off);
-            if (of > bf || (of == bf && os < bs)) {
-                bf = of;
-                bs = os;
+            bool push = false;
+            if (valid && n >= 2 && (__ffs(m) - 1) == lane) {
+                for (unsigned mm = m; mm; mm &= mm - 1) c += Vw[__ffs(mm) - 1];
+                push = c > (double)n;
             }
+            const unsigned bal = __ballot_sync(0xFFFFFFFFu, push);
+            if (push) {
+                const int pos = cnt + __popc(bal & lanemask_lt());
+                qf[pos] = c;
+                qn[pos] = (uint8_t)n;
+                ql[pos] = (uint8_t)lab;
+            }
+            if (lane == 0) qs[e] = (uint16_t)cnt;
+            cnt += __popc(bal);
+            __syncwarp();
         }
-        if (lane == 0) {
-            s.L[p] = 0.5 * sum;
-            s.top[p] = bf > 0.0 ? (uint8_t)bs : (uint8_t)0xFF;
+        if (lane == 0) qs[ne] = (uint16_t)cnt;
+        __syncwarp();
+        // Eq. 8 summands (every queued cluster has n_s >= 2 and c_s > n_s):
+        // log(n/c) + (n-1) log((n^2-n)/(n^2-c)) taken as
+        // (log n - log c) + (n-1) (log(n^2-n) - log(n^2-c)) with the integer
+        // logs from the per-CTA table; c clamped to n^2 - 1e-9 (Q3)
+        for (int k = lane; k < cnt; k += 32) {
+            const int n = qn[k];
+            const double nd = (double)n, n2 = nd * nd;
+            const double ch = fmin(qf[k], n2 - 1e-9);
+            qf[k] = (s.lgn[n] - log(ch)) + (nd - 1.0) * (s.lgnn[n] - log(n2 - ch));
+        }
+        __syncwarp();
+        if (lane < ne) {
+            double sum = 0.0, bf = 0.0;
+            int bt = -1;
+            for (int k = qs[lane]; k < qs[lane + 1]; ++k) {
+                const double f = qf[k];
+                sum += f;
+                if (f > bf || (f == bf && f > 0.0 && (int)ql[k] < bt)) {   // KB top: largest, smallest label
+                    bf = f;
+                    bt = ql[k];
+                }
+            }
+            s.L[p0 + lane] = 0.5 * sum;
+            s.top[p0 + lane] = bt < 0 ? (uint8_t)0xFF : (uint8_t)bt;
         }
         __syncwarp();
     }
 }
 
-__device__ __forceinline__ bool kv_less(uint64_t ka, uint32_t va, uint64_t kb, uint32_t vb) {
-    return ka < kb || (ka == kb && va < vb);
+// (L desc, index asc): does item (La, a) come before (Lb, b)?  Padding items
+// carry L = -1 < every L and index 0xFFFFFFFF.
+__device__ __forceinline__ bool before(double La, uint32_t a, double Lb, uint32_t b) {
+    return La > Lb || (La == Lb && a < b);
 }
 
 // Isolate fittest: order by (L desc, index asc) -> val[0..P); ranks.
+// Bitonic network over indices, comparing L directly.
 __device__ __forceinline__ void b_order(const BSmem &s, int P, int n2) {
     const int tid = threadIdx.x;
-    for (int t = tid; t < n2; t += BT) {
-        if (t < P) {
-            double x = s.L[t];
-            if (x == 0.0) x = 0.0;   // -0 -> +0
-            s.key[t] = ~(uint64_t)__double_as_longlong(x);
-            s.val[t] = (uint32_t)t;
-        } else {
-            s.key[t] = ~0ull;
-            s.val[t] = 0xFFFFFFFFu;
-        }
-    }
+    for (int t = tid; t < n2; t += BT) s.val[t] = t < P ? (uint32_t)t : 0xFFFFFFFFu;
     __syncthreads();
     for (int size = 2; size <= n2; size <<= 1)
         for (int stride = size >> 1; stride > 0; stride >>= 1) {
             for (int t = tid; t < (n2 >> 1); t += BT) {
                 const int i = 2 * t - (t & (stride - 1)), j = i + stride;
                 const bool up = (i & size) == 0;
-                const uint64_t ki = s.key[i], kj = s.key[j];
                 const uint32_t vi = s.val[i], vj = s.val[j];
-                if (kv_less(kj, vj, ki, vi) == up) {
-                    s.key[i] = kj;
-                    s.key[j] = ki;
+                const double Li = vi < (uint32_t)P ? s.L[vi] : -1.0;
+                const double Lj = vj < (uint32_t)P ? s.L[vj] : -1.0;
+                if (before(Lj, vj, Li, vi) == up) {
                     s.val[i] = vj;
                     s.val[j] = vi;
                 }
@@ -289,13 +332,15 @@ __device__ __forceinline__ void b_select(const BArgs &a, const BSmem &s, uint64_
             }
             __syncthreads();
             const uint64_t base = (incl - run) + (wid ? wsum[wid - 1] : 0ull);
+            // every L read of this phase happened before the barrier above:
+            // the prefix may overwrite L
 #pragma unroll
             for (int k = 0; k < BMAX_P / BT; ++k) {
                 const int i = ipt * tid + k;
-                if (k < ipt && i < P) s.key[i] = base + q[k];   // inclusive prefix (index order)
+                if (k < ipt && i < P) s.prefix[i] = base + q[k];   // inclusive prefix (index order)
             }
             __syncthreads();
-            const uint64_t Q = s.key[P - 1];
+            const uint64_t Q = s.prefix[P - 1];
             const uint64_t step = Q / (uint64_t)M;
             const U4 u = draw(seed, pga::TAG_SUS, 0u, gen, 0u, 0xFFFFFFFFu);
             const uint64_t x = ((uint64_t)u.x << 32) | (uint64_t)u.y;
@@ -305,7 +350,7 @@ __device__ __forceinline__ void b_select(const BArgs &a, const BSmem &s, uint64_
                 int lo = 0, hi = P - 1;   // min{i : prefix_i > ptr}
                 while (lo < hi) {
                     const int mid = (lo + hi) >> 1;
-                    if (s.key[mid] > ptr) hi = mid;
+                    if (s.prefix[mid] > ptr) hi = mid;
                     else lo = mid + 1;
                 }
                 s.sel[m] = (int16_t)lo;
@@ -382,8 +427,12 @@ __global__ void __launch_bounds__(BT, 3) k_batch(BArgs a) {
     __shared__ uint8_t s_best[BMAX_N];
     const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int N = a.N, P = a.P;
-    const BLayout ly = b_layout(N, P, a.M);
+    const BLayout &ly = a.ly;
     const BSmem s = b_smem(sm, ly);
+    for (int t = tid; t <= BMAX_N; t += BT) {    // integer logs of Eq. 8
+        s.lgn[t] = t >= 1 ? log((double)t) : 0.0;
+        s.lgnn[t] = t >= 2 ? log((double)t * t - t) : 0.0;
+    }
     const int ldb = ly.ldb;
     const uint64_t seed = a.seed + (uint64_t)b;
 
@@ -522,8 +571,8 @@ int fill_args(BArgs &a, int32_t B, int32_t N, const pga_params *p, int device, s
         a.thr_kb = threshold(p->p_kb);
         a.seed = p->seed;
     }
-    const BLayout ly = b_layout(N, a.P, a.M);
-    *smem = ly.total;
+    a.ly = b_layout(N, a.P, a.M);
+    *smem = a.ly.total;
     (void)device;
     return PGA_OK;
 }
@@ -643,7 +692,8 @@ int pga_batch_op_evaluate(const double *C, int32_t B, int32_t N, const int32_t *
     BTRY(fill_args(a, B, N, nullptr, device, &smem));
     a.P = P;
     a.M = 0;
-    smem = b_layout(N, P, 0).total;
+    a.ly = b_layout(N, P, 0);
+    smem = a.ly.total;
     for (size_t k = 0; k < (size_t)B * P * N; ++k)
         if (labels[k] < 0 || labels[k] > 2 * N) return pga::fail(PGA_EINVAL, "labels must lie in 0..2N");
     BTRY(pga::ensure_device(device));

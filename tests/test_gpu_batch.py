@@ -192,8 +192,8 @@ def test_batch_recovers_planted_windows(pga, orc):
     ari = np.array([_ari(best[b], planted[b]) for b in range(B)])
     print("best>=planted %.3f local-opt %.3f mean ARI %.3f" % (ge.mean(), local.mean(), ari.mean()))
     assert ge.mean() >= 0.95, ge.mean()
-    assert local.mean() >= 0.9, local.mean()
-    assert ari.mean() >= 0.5, ari.mean()
+    assert local.mean() >= 0.95, local.mean()
+    assert ari.mean() >= 0.8, ari.mean()     # oracle GA on the same windows: 0.894
 
 
 def test_batch_validation(pga):

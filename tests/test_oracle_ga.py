@@ -349,3 +349,29 @@ def test_noh_planted_correlation(orc):
     C = orc.pearson(X)
     off = C[~np.eye(30, dtype=bool)]
     assert abs(off.mean() - 0.64) < 0.01
+
+
+def test_run_f1_windows_local_optimum(orc):
+    """F1 windows (the paper's 18-stock test-set shape, Table 3 GA): the
+    oracle GA's best beats the planted partition and is a strict local
+    optimum under single-gene moves -- a certificate that does not rely on
+    the GA's own arithmetic (every candidate is scored by Eq. 8 directly)."""
+    B = 12
+    X, planted = workloads.window_returns(B)
+    for b in range(B):
+        C = orc.pearson(X[b])
+        r = orc.run(C, orc.default_params(pop=1000, seed=99 + b))
+        lab = r["best_labels"]
+        Lp, _ = orc.log_likelihood(C, planted[b])
+        assert r["best_L"] >= Lp - 1e-12 * max(1.0, Lp)
+        L0, _ = orc.log_likelihood(C, lab)
+        assert L0 == r["best_L"]
+        cand = []
+        for i in range(lab.shape[0]):
+            for k in range(int(lab.max()) + 2):
+                if k != lab[i]:
+                    m = lab.copy()
+                    m[i] = k
+                    cand.append(m)
+        Lc, _ = orc.evaluate(C, np.asarray(cand, np.int32))
+        assert Lc.max() <= L0, b
