@@ -36,11 +36,24 @@ open(os.path.join(out_dir, "%s_launches.md" % tag), "w").write("\n".join(lines) 
 import shutil
 shutil.copy(os.path.join(gdir, "launches.csv"), os.path.join(out_dir, "%s_launches.csv" % tag))
 
+# 1b. F1 launch list (k_batch only)
+f1csv = os.path.join(gdir, "launches_f1.csv")
+if os.path.exists(f1csv):
+    shutil.copy(f1csv, os.path.join(out_dir, "%s_launches_f1.csv" % tag))
+
 # 2. full-set metrics of the captured kernels
-rep = os.path.join(gdir, "prof_full.ncu-rep")
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-rows = list(csv.reader(raw.splitlines()))
-hdr, units, kern = rows[0], rows[1], rows[2:]
+kern_rows = []
+hdr = units = None
+for repname in ("prof_full.ncu-rep", "prof_f1.ncu-rep"):
+    rep = os.path.join(gdir, repname)
+    if not os.path.exists(rep):
+        continue
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(raw.splitlines()))
+    h = rows[0]
+    for r in rows[2:]:
+        kern_rows.append((h, rows[1], r))
 keys = ["gpu__time_duration.sum", "launch__registers_per_thread", "launch__grid_size",
         "sm__warps_active.avg.per_cycle_active", "smsp__issue_active.avg.pct_of_peak_sustained_active",
         "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
@@ -52,7 +65,7 @@ keys = ["gpu__time_duration.sum", "launch__registers_per_thread", "launch__grid_
         "sm__cycles_elapsed.avg.per_second"]
 traffic = {}
 md = ["# ncu --set full (%s)" % tag, ""]
-for d in kern:
+for hdr, units, d in kern_rows:
     name = d[hdr.index("Kernel Name")].split("(")[0].replace("<unnamed>::", "")
     md += ["## %s" % name, "", "| metric | value | unit |", "|---|---|---|"]
     vals = {}
