@@ -43,6 +43,17 @@ __device__ __forceinline__ void table_reset(uint16_t *table, int n, int lane) {
     __syncwarp();
 }
 
+// Same for a 16-byte-aligned table whose capacity is a multiple of 8 entries.
+__device__ __forceinline__ void table_reset16(uint16_t *table, int n, int lane) {
+    uint4 *t = reinterpret_cast<uint4 *>(table);
+    const uint4 ones = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+    for (int k = lane; k < (n + 7) / 8; k += 32) t[k] = ones;
+    __syncwarp();
+}
+
+// per-child table stride in the breed kernel: N + 1 entries rounded to 8 (16 B)
+__host__ __device__ __forceinline__ int breed_tab(int N) { return (N + 1 + 7) & ~7; }
+
 // ---------------------------------------------------------------------------
 // k_init: warp per chromosome.  gene i of chromosome p_global:
 // scale(Philox(INIT; i>>2, p_global)[i&3], N), generation field 0xFFFFFFFF.
@@ -545,7 +556,7 @@ __device__ __forceinline__ ChildPlan plan_child(const BreedArgs &a, int64_t o, u
 }
 
 template <bool HOOK>
-__global__ void __launch_bounds__(BW * 32, 2) k_breed(BreedArgs a) {
+__global__ void __launch_bounds__(BW * 32, 3) k_breed(BreedArgs a) {
     if (a.done && *a.done) return;
     extern __shared__ uint16_t sm16[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -565,9 +576,9 @@ __global__ void __launch_bounds__(BW * 32, 2) k_breed(BreedArgs a) {
     for (int c = 0; c < BC; ++c) {
         const int slot = warp * BC + c;
         cp[c] = plan_child(a, o0 + slot, gen);
-        cn[c].table = tables + (size_t)slot * (N + 1);
+        cn[c].table = tables + (size_t)slot * breed_tab(N);
         cn[c].next = 0;
-        table_reset(cn[c].table, N + 1, lane);
+        table_reset16(cn[c].table, N + 1, lane);
     }
     for (int base = 0; base < N; base += GCH) {
         const int tb = ((base / GCH) & 1) * GCH * TS;     // double-buffered tile
@@ -749,7 +760,7 @@ __global__ void k_import(const unsigned char *__restrict__ in, int G, int Em, in
 
 namespace pga {
 
-static size_t breed_smem(int N) { return ((size_t)2 * GCH * TS + (size_t)BS * (N + 1)) * sizeof(uint16_t); }
+static size_t breed_smem(int N) { return ((size_t)2 * GCH * TS + (size_t)BS * breed_tab(N)) * sizeof(uint16_t); }
 
 static int breed_warps(int N) {
     const size_t per = (size_t)(N + 1) * sizeof(uint16_t);
