@@ -206,6 +206,10 @@ def main():
     ap.add_argument("--impl", default="pga", choices=["pga", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--mode", default="islands", choices=["islands", "replicated"],
+                    help="multi-GPU model: islands (population sharded, elite migration; default) or "
+                         "replicated master-slave (one population, fitness sharded, L all-gathered; "
+                         "SURVEY §8(f) f3)")
     ap.add_argument("--config", default=CONFIG, choices=sorted(CFG_POP) + ["F1"],
                     help="workload (default C4, the config the metric is quoted on; F1 = the "
                          "batched GA over 1760 windows x 18 stocks, SURVEY §8(f))")
@@ -222,6 +226,8 @@ def main():
     import torch.distributed as dist
     import paper_1403_4099_b200 as pga
     from paper_1403_4099_b200.islands import GpuIsland, IslandRunner
+    from paper_1403_4099_b200.replicated import GpuReplica, ReplicatedRunner
+    replicated = args.mode == "replicated"
 
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
     torch.cuda.set_device(local)
@@ -232,14 +238,19 @@ def main():
     X, planted = workloads.noh_returns(workloads.CONFIGS[CONFIG])
     N = X.shape[1]
     C = pga.pga_correlation(X, device=local)        # Eq. 7 on the device
-    P_local = P_TOTAL // world
+    P_local = P_TOTAL if replicated else P_TOTAL // world
     pm = 0.1 if N <= 40 else 2.0 / N            # Table 3 for N <= 40, else 2/N (Q13)
     params = pga.pga_params_default(
         pop_size=P_local, elite=10, p_mutation=pm, tol=-1.0, max_gens=W + K + 40,
-        device=local, island=rank, n_islands=world, migrate_every=10, migrants=10, seed=SEED)
+        device=local, island=0 if replicated else rank, n_islands=1 if replicated else world,
+        migrate_every=10, migrants=10, seed=SEED)
 
-    eng = GpuIsland(C, params)
-    runner = IslandRunner(eng)
+    if replicated:
+        eng = GpuReplica(C, params)
+        runner = ReplicatedRunner(eng)
+    else:
+        eng = GpuIsland(C, params)
+        runner = IslandRunner(eng)
     eng.init(SEED)
     stream = eng.stream
     for _ in range(W):
@@ -283,7 +294,8 @@ def main():
 
     ms_step = ms / K
     nominal = float(N) * N * P_TOTAL
-    executed_local = N * (N - 1) / 2.0 * P_local
+    P_eval = (runner.end - runner.begin) if replicated else P_local   # chromosomes evaluated here
+    executed_local = N * (N - 1) / 2.0 * P_eval
     value = nominal / (ms_step / 1000.0)
 
     # roofline of the dominant kernel (k_sweep), from live CUDA events
@@ -303,7 +315,7 @@ def main():
 
     # end-to-end through the public API from host memory (rank-local), see DESIGN.md §7
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not replicated:
         eng.close()
         e2e = e2e_run(pga, torch, dist, C, params, world, min(K, 200), planted)
 
@@ -326,8 +338,11 @@ def main():
             "data": "synthetic (Noh-model returns T=2000, seed 50004; Pearson C on device)",
             "config": {"workload": "%s: N=%d, P=%d total (%d per GPU), 1 step = 1 generation"
                                    % (CONFIG, N, P_TOTAL, P_local), "N": N, "population": P_TOTAL,
-                       "population_per_gpu": P_local, "parallelism": "islands x%d" % world,
-                       "migration": "every 10 generations, 10 elites, NCCL all-gather",
+                       "population_per_gpu": P_local,
+                       "parallelism": ("replicated master-slave x%d (fitness shard %d per GPU)"
+                                       % (world, P_eval)) if replicated else "islands x%d" % world,
+                       "migration": "none: L and top all-gathered every generation (NCCL)"
+                                    if replicated else "every 10 generations, 10 elites, NCCL all-gather",
                        "l2": "working set > L2 (two population layouts x2 buffers + 264 MB "
                              "fold scratch per GPU); no flush"},
             "evals_per_s": P_TOTAL / (ms_step / 1000.0),

@@ -226,6 +226,34 @@ int pga_op_init(uint64_t seed, int32_t N, int64_t P, int64_t p_off, int32_t isla
                 int32_t device, int32_t *out);
 
 /* ---------------------------------------------------------------------
+ * Replicated master-slave across GPUs.  The paper's
+ * own parallel model (§3.2): ONE population, fitness evaluated
+ * by the slaves, operators on the master.  Here every GPU holds a replica
+ * of the population and runs the same deterministic operators, and the
+ * fitness evaluation is sharded over the GPUs.  Every rank creates its ctx
+ * with the same C and params (n_islands = 1) and calls pga_init with the
+ * same seed.  Per generation:
+ *   pga_rep_evaluate(this rank's shard) -> all-gather L and top over the
+ *   ranks (the caller, e.g. NCCL) -> pga_rep_commit(full vectors) ->
+ *   pga_gen_breed.
+ * The replicas stay bit-identical and the run equals pga_run on one GPU:
+ * a chromosome's fitness does not depend on which launch evaluated it.
+ * ------------------------------------------------------------------- */
+
+/* Fitness (Eq. 5/6/8) of chromosomes [begin, end) of the current
+ * population.  begin must be a multiple of 32 and end <= pop_size.  L_dev
+ * (fp64 [end - begin]) and top_dev (uint16 [end - begin]: 0-based label of
+ * the largest Eq. 8 summand, 0xFFFF = none) are device buffers.
+ * Stream-ordered on the ctx's stream (pga_get_stream). */
+int pga_rep_evaluate(pga_ctx *ctx, int64_t begin, int64_t end, double *L_dev, uint16_t *top_dev);
+
+/* Install the gathered fitness of the whole population (device fp64
+ * [pop_size] and uint16 [pop_size], in chromosome order) and run the
+ * statistics / termination step of Alg. 1 (Q16, Q17) -- the part
+ * of pga_gen_evaluate after the fitness kernel.  Stream-ordered. */
+int pga_rep_commit(pga_ctx *ctx, const double *L_dev, const uint16_t *top_dev);
+
+/* ---------------------------------------------------------------------
  * Batched GA: many small, independent clustering
  * problems in ONE kernel launch.  This is the paper's own test workload
  * (1760 correlation matrices of 18 JSE stocks, each clustered by its

@@ -80,6 +80,8 @@ _SIGS = {
     "pga_op_init": (ct.c_int, [ct.c_uint64, ct.c_int32, ct.c_int64, ct.c_int64, ct.c_int32,
                                ct.c_int32, ct.c_void_p]),
     "pga_launch_count": (ct.c_int64, []),
+    "pga_rep_evaluate": (ct.c_int, [ct.c_void_p, ct.c_int64, ct.c_int64, ct.c_void_p, ct.c_void_p]),
+    "pga_rep_commit": (ct.c_int, [ct.c_void_p, ct.c_void_p, ct.c_void_p]),
     "pga_batch_run": (ct.c_int, [ct.c_void_p, ct.c_int32, ct.c_int32, ct.c_void_p, ct.c_int32,
                                  ct.c_void_p, ct.c_void_p, ct.c_void_p, ct.c_void_p, ct.c_void_p,
                                  ct.c_void_p]),
@@ -317,6 +319,16 @@ def pga_op_init(seed: int, N: int, P: int, p_off: int = 0, island: int = 0, devi
     out = np.zeros((P, N), np.int32)
     _check(lib().pga_op_init(seed, N, P, p_off, island, device, _p(out)))
     return out
+
+
+def pga_rep_evaluate(ctx, begin: int, end: int, L_dev, top_dev):
+    """Fitness of chromosomes [begin, end) into device buffers (torch tensors:
+    float64 [end-begin], int16/uint16 [end-begin])."""
+    _check(lib().pga_rep_evaluate(ctx, begin, end, _p(L_dev), _p(top_dev)))
+
+
+def pga_rep_commit(ctx, L_dev, top_dev):
+    _check(lib().pga_rep_commit(ctx, _p(L_dev), _p(top_dev)))
 
 
 def pga_batch_run(C, params: pga_params, history: bool = False):

@@ -482,6 +482,30 @@ int pga_gen_evaluate(pga_ctx *c, int32_t *is_migration) {
     return phase_a(c, c->host_gen, is_migration);
 }
 
+int pga_rep_evaluate(pga_ctx *c, int64_t begin, int64_t end, double *L_dev, uint16_t *top_dev) {
+    if (!c || !L_dev || !top_dev) return fail(PGA_EINVAL, "NULL argument");
+    if (c->p.n_islands != 1) return fail(PGA_ESTATE, "replicated mode needs n_islands = 1 (one population)");
+    if (!c->has_pop) return fail(PGA_ESTATE, "no population: call pga_init first");
+    if (begin < 0 || end > c->P || begin >= end || begin % CB)
+        return fail(PGA_EINVAL, "need 0 <= begin < end <= pop_size and begin a multiple of 32");
+    PGA_CUDA(cudaSetDevice(c->device));
+    c->pev = prof_slot(c);
+    return launch_fitness_range(c, ga_bufs(c), begin, end, L_dev - begin, top_dev - begin, c->stream,
+                                c->pev);
+}
+
+int pga_rep_commit(pga_ctx *c, const double *L_dev, const uint16_t *top_dev) {
+    if (!c || !L_dev || !top_dev) return fail(PGA_EINVAL, "NULL argument");
+    if (c->p.n_islands != 1) return fail(PGA_ESTATE, "replicated mode needs n_islands = 1 (one population)");
+    if (!c->has_pop) return fail(PGA_ESTATE, "no population: call pga_init first");
+    PGA_CUDA(cudaSetDevice(c->device));
+    PGA_CUDA(cudaMemcpyAsync(c->L, L_dev, sizeof(double) * c->P, cudaMemcpyDeviceToDevice, c->stream));
+    PGA_CUDA(cudaMemcpyAsync(c->top, top_dev, sizeof(uint16_t) * c->P, cudaMemcpyDeviceToDevice, c->stream));
+    TRY(launch_stats(c, 0, c->stream));
+    PGA_MARK(c, 3, c->stream);
+    return PGA_OK;
+}
+
 int pga_gen_breed(pga_ctx *c) {
     if (!c) return fail(PGA_EINVAL, "ctx is NULL");
     if (!c->has_pop) return fail(PGA_ESTATE, "no population: call pga_init first");

@@ -130,6 +130,7 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *tm, in
 
 struct FitArgs {
     int N, ldn, nRT, nCB, fold_warps;
+    int cb0;                        // first chromosome block (shard offset / 32)
     int64_t P, Pcap;
     const double *diag;
     double *V;                      // [Pcap][ldn]: V[p][i] = C_ii + 2 r'_i
@@ -294,7 +295,7 @@ k_fitness(const __grid_constant__ CUtensorMap tmLab0, const __grid_constant__ CU
     __shared__ int s_last;
 
     const int N = a.N;
-    const int cb = blockIdx.x / a.nRT, rt = blockIdx.x - (blockIdx.x / a.nRT) * a.nRT;
+    const int cb = a.cb0 + (int)(blockIdx.x / a.nRT), rt = blockIdx.x - (blockIdx.x / a.nRT) * a.nRT;
     const int i0 = rt * RT;
     const int nchunks = (N - i0 + KC - 1) / KC;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -505,12 +506,21 @@ int prepare_fitness(int N) {
 
 int launch_fitness(pga_ctx *c, const FitBufs &b, int64_t P, double *L, uint16_t *top,
                    cudaStream_t s, cudaEvent_t *ev) {
+    return launch_fitness_range(c, b, 0, P, L, top, s, ev);
+}
+
+// chromosomes [begin, end) (begin a multiple of CB); L[p], top[p] are written
+// at the GLOBAL index p.
+int launch_fitness_range(pga_ctx *c, const FitBufs &b, int64_t begin, int64_t end, double *L,
+                         uint16_t *top, cudaStream_t s, cudaEvent_t *ev) {
     const int N = c->N;
+    const int64_t P = end;
     FitArgs a;
     a.N = N;
     a.ldn = c->ldn;
     a.nRT = (N + RT - 1) / RT;
-    a.nCB = (int)((P + CB - 1) / CB);
+    a.cb0 = (int)(begin / CB);
+    a.nCB = (int)((end - begin + CB - 1) / CB);
     a.fold_warps = fold_warps(N);
     a.P = P;
     a.Pcap = c->Pcap;

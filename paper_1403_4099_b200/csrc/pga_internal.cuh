@@ -147,6 +147,8 @@ int prepare_fitness(int N);
 // fold, and after the fold.
 int launch_fitness(pga_ctx *c, const FitBufs &b, int64_t P, double *L, uint16_t *top,
                    cudaStream_t s, cudaEvent_t *ev = nullptr);
+int launch_fitness_range(pga_ctx *c, const FitBufs &b, int64_t begin, int64_t end, double *L,
+                         uint16_t *top, cudaStream_t s, cudaEvent_t *ev = nullptr);
 int launch_init(pga_ctx *c, uint64_t seed, cudaStream_t s);
 int launch_stats(pga_ctx *c, int is_migration_check, cudaStream_t s);
 int launch_sort_order(pga_ctx *c, cudaStream_t s);

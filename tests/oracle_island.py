@@ -92,3 +92,47 @@ class OracleIsland:
 
     def state(self):
         return dict(generation=self.gen, best_L=self.best_ever, best_labels=self.best_labels + 1)
+
+
+class OracleReplica:
+    """Oracle-backed replica (TEST INFRASTRUCTURE) with the interface of
+    paper_1403_4099_b200.replicated.GpuReplica: holds the whole population,
+    evaluates only the requested shard, installs gathered fitness, breeds
+    with orc_step.  Labels, L and top travel exactly as libpga.so exchanges
+    them (fp64 L, 16-bit top with 0xFFFF = none)."""
+
+    def __init__(self, C, params):
+        self.C = np.ascontiguousarray(C, np.float64)
+        self.N = self.C.shape[0]
+        self.p = params
+        self.P = params.pop
+        self.device = torch.device("cpu")
+
+    def init(self, seed):
+        self.p.seed = seed
+        self.pop = orc.init_population(seed, self.N, self.P)
+        self.gen = 0
+        self.best_ever = -1.0
+        self.best_labels = np.zeros(self.N, np.int32)
+        self.history = []
+        self.evaluated = 0
+
+    def rep_evaluate(self, begin, end, L_out, top_out):
+        L, top = orc.evaluate(self.C, self.pop[begin:end])
+        self.evaluated += end - begin
+        L_out.copy_(torch.from_numpy(L))
+        top_out.copy_(torch.from_numpy(np.where(top < 0, -1, top).astype(np.int16)))
+
+    def rep_commit(self, L, top):
+        self.L = L.numpy().copy()
+        t = top.numpy().astype(np.int32)
+        self.top = np.where(t == -1, -1, t & 0xFFFF)
+        b = int(np.argmax(self.L))
+        self.history.append(float(self.L[b]))
+        if self.L[b] > self.best_ever:
+            self.best_ever = float(self.L[b])
+            self.best_labels = self.pop[b].copy()
+
+    def gen_breed(self):
+        self.pop = orc.step(self.p, self.pop, self.L, self.top, self.gen)
+        self.gen += 1
