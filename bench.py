@@ -210,6 +210,9 @@ def main():
                     help="multi-GPU model: islands (population sharded, elite migration; default) or "
                          "replicated master-slave (one population, fitness sharded, L all-gathered; "
                          "SURVEY §8(f) f3)")
+    ap.add_argument("--stream", action="store_true",
+                    help="F1 only: each step also computes the 1760 windows on the device from one "
+                         "return stream (EWMA lambda=0.98 + RMT cleaning, SURVEY §8(f) f4)")
     ap.add_argument("--config", default=CONFIG, choices=sorted(CFG_POP) + ["F1"],
                     help="workload (default C4, the config the metric is quoted on; F1 = the "
                          "batched GA over 1760 windows x 18 stocks, SURVEY §8(f))")
@@ -435,14 +438,27 @@ def bench_f1(args):
     K, W = args.steps, args.warmup
     f1 = workloads.F1
     B, N, T = f1["B"], f1["N"], f1["T"]
-    X, planted = workloads.window_returns(B, N, T, f1["seed0"] + rank * B)
-    dX = torch.from_numpy(X).cuda()
-    dC = torch.empty((B, N, N), dtype=torch.float64, device="cuda")
-    status = torch.zeros(B, dtype=torch.int32, device="cuda")
-    for b in range(B):                              # Eq. 7 on the device
-        pga.pga_correlation_device(dX[b], dC[b], status[b:b + 1])
-    torch.cuda.synchronize()
-    assert int(status.sum()) == 0
+    stride = 10
+    if args.stream:
+        # one return stream; window b = EWMA state after observation T-1 + b*stride, RMT-cleaned
+        Ts = T + (B - 1) * stride
+        Xs, planted1 = workloads.stream_returns(Ts, N, seed=f1["seed0"] + rank)
+        planted = np.tile(planted1, (B, 1))
+        dXs = torch.from_numpy(Xs).cuda()
+        dC = torch.empty((B, N, N), dtype=torch.float64, device="cuda")
+        status = torch.zeros(1, dtype=torch.int32, device="cuda")
+        pga.pga_corr_stream_device(dXs, dC, status, lam=0.98, warm=T, stride=stride, q=0.0,
+                                   device=local, stream=torch.cuda.current_stream().cuda_stream)
+        assert int(status.item()) == 0
+    else:
+        X, planted = workloads.window_returns(B, N, T, f1["seed0"] + rank * B)
+        dX = torch.from_numpy(X).cuda()
+        dC = torch.empty((B, N, N), dtype=torch.float64, device="cuda")
+        status = torch.zeros(B, dtype=torch.int32, device="cuda")
+        for b in range(B):                              # Eq. 7 on the device
+            pga.pga_correlation_device(dX[b], dC[b], status[b:b + 1])
+        torch.cuda.synchronize()
+        assert int(status.sum()) == 0
     params = pga.pga_params_default(pop_size=f1["pop"], max_gens=f1["gens"], seed=SEED + rank * B,
                                     device=local)
     lab = torch.zeros((B, N), dtype=torch.int32, device="cuda")
@@ -452,6 +468,9 @@ def bench_f1(args):
     stream = torch.cuda.current_stream()
 
     def step():
+        if args.stream:
+            pga.pga_corr_stream_device(dXs, dC, status, lam=0.98, warm=T, stride=stride, q=0.0,
+                                       device=local, stream=stream.cuda_stream)
         pga.pga_batch_run_device(dC, params, lab, bL, gens, reason, stream=stream.cuda_stream)
 
     for _ in range(W):
@@ -496,19 +515,27 @@ def bench_f1(args):
     e2e = None
     if not args.no_e2e:
         Cp = torch.from_numpy(dC.cpu().numpy()).pin_memory()
+        if args.stream:
+            Xp = torch.from_numpy(Xs).pin_memory()
         ke = max(1, min(K, 3))
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(ke):
-            res = pga.pga_batch_run(Cp.numpy(), params)
+            Cin = pga.pga_corr_stream(Xp.numpy(), lam=0.98, warm=T, stride=stride, q=0.0,
+                                      device=local) if args.stream else Cp.numpy()
+            res = pga.pga_batch_run(Cin, params)
         dt = (time.perf_counter() - t0) / ke
         if world > 1:
             t = torch.tensor([dt], dtype=torch.float64, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = float(t.item())
-        e2e = {"value": B * world / dt, "unit": "matrices/s", "h2d_bytes_per_step": B * N * N * 8,
-               "d2h_bytes_per_step": B * (N * 4 + 8 + 4 + 4), "steps": ke, "seconds_per_step": dt,
-               "includes": "pga_batch_run with host buffers: C upload, run, results download"}
+        h2d = (Xs.size * 8 + B * N * N * 8) if args.stream else B * N * N * 8
+        e2e = {"value": B * world / dt, "unit": "matrices/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": B * (N * 4 + 8 + 4 + 4) + (B * N * N * 8 if args.stream else 0),
+               "steps": ke, "seconds_per_step": dt,
+               "includes": ("pga_corr_stream with host returns (upload, EWMA/RMT, download) + "
+                            if args.stream else "") +
+                           "pga_batch_run with host buffers: C upload, run, results download"}
         assert np.array_equal(res["best_labels"], lab.cpu().numpy())
 
     cpu = None
@@ -534,11 +561,14 @@ def bench_f1(args):
             "value": value, "unit": "matrices/s", "n_gpus": world, "steps": K, "warmup": W,
             "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (Noh-model windows, T=160, seeds %d+b; Pearson C on device)"
-                    % f1["seed0"],
-            "config": {"workload": "F1: B=%d windows per GPU x N=%d stocks, population %d, <= %d "
+            "data": ("synthetic (one Noh-model return stream of %d observations, seed %d; windows = "
+                     "EWMA/RMT states every %d observations, computed on device)"
+                     % (T + (B - 1) * stride, f1["seed0"] + rank, stride)) if args.stream else
+                    "synthetic (Noh-model windows, T=160, seeds %d+b; Pearson C on device)" % f1["seed0"],
+            "config": {"workload": "F1%s: B=%d windows per GPU x N=%d stocks, population %d, <= %d "
                                    "generations, stall 50 / tol 1e-5; 1 step = all windows"
-                                   % (B, N, f1["pop"], f1["gens"]),
+                                   % (" + stream (returns -> EWMA/RMT windows on device)" if args.stream
+                                      else "", B, N, f1["pop"], f1["gens"]),
                        "B_per_gpu": B, "N": N, "population": f1["pop"],
                        "parallelism": "windows sharded x%d" % world,
                        "l2": "C (4.6 MB) read once per step; state lives in shared memory"},

@@ -305,6 +305,39 @@ int pga_batch_op_evaluate(const double *C, int32_t B, int32_t N, const int32_t *
 int pga_batch_op_step(int32_t B, int32_t N, const pga_params *params, const int32_t *pop,
                       const double *L, const int32_t *top, int32_t gen, int32_t *next);
 
+/* ---------------------------------------------------------------------
+ * Correlation stream: the paper's pre-processing
+ * (§4.2.5; operations as SPEC S:279-301, readings Q31-Q33) on the
+ * device, producing the windows the batched GA clusters ("fast online
+ * intraday correlation matrix estimation").
+ *   EWMA:   d = x_t - m; cov <- lambda cov + (1-lambda) d d^T;
+ *           m <- lambda m + (1-lambda) x_t; zero initial state.
+ *   After observation t = warm-1 + b*stride (b = 0 .. B-1) the state is
+ *   emitted as a correlation matrix C_ij = cov_ij / sqrt(cov_ii cov_jj)
+ *   and, if q >= 0, cleaned: eigenvalues inside the Marchenko-Pastur band
+ *   [(1-sqrt q)^2, (1+sqrt q)^2] are replaced by their mean (trace
+ *   preserving), C' = V diag(w') V^T, renormalised to a unit diagonal
+ *   from its upper triangle (exactly symmetric).  q == 0 selects the
+ *   SPEC's q = N (1 - lambda) (effective sample 1/(1-lambda)); q < 0
+ *   disables cleaning.
+ * X       fp64 [T][N] returns, row-major.   1 <= N <= 64, 0 < lambda < 1,
+ *         warm >= 1, stride >= 1, T >= warm.
+ * C_out   fp64 [B][N][N], B = pga_stream_count(T, warm, stride).
+ * on_device 0: X, C_out host, synchronous; a non-positive variance at an
+ *         emission -> PGA_ENUMERIC (and *status = 1 if status != NULL).
+ *         1: X, C_out, status device memory on `device`; work is ordered on
+ *         `stream` and the call returns after it completes (its scratch is
+ *         freed); *status (caller-zeroed) is set to 1 on a non-positive
+ *         variance.
+ * The EWMA recurrences and the uncleaned correlation are computed without
+ * FMA contraction in the SPEC's operation order (bit-identical to a plain
+ * fp64 evaluation); the cleaning uses a two-sided Jacobi eigensolver.
+ * ------------------------------------------------------------------- */
+int pga_stream_count(int32_t T, int32_t warm, int32_t stride);
+int pga_corr_stream(const double *X, int32_t T, int32_t N, double lambda, int32_t warm,
+                    int32_t stride, double q, int32_t on_device, double *C_out, int32_t *status,
+                    int32_t device, void *stream);
+
 /* Number of this library's kernel launches issued so far in this process
  * (for the bench's gpu_launches claim). */
 int64_t pga_launch_count(void);

@@ -82,6 +82,10 @@ _SIGS = {
     "pga_launch_count": (ct.c_int64, []),
     "pga_rep_evaluate": (ct.c_int, [ct.c_void_p, ct.c_int64, ct.c_int64, ct.c_void_p, ct.c_void_p]),
     "pga_rep_commit": (ct.c_int, [ct.c_void_p, ct.c_void_p, ct.c_void_p]),
+    "pga_stream_count": (ct.c_int, [ct.c_int32, ct.c_int32, ct.c_int32]),
+    "pga_corr_stream": (ct.c_int, [ct.c_void_p, ct.c_int32, ct.c_int32, ct.c_double, ct.c_int32,
+                                   ct.c_int32, ct.c_double, ct.c_int32, ct.c_void_p, ct.c_void_p,
+                                   ct.c_int32, ct.c_void_p]),
     "pga_batch_run": (ct.c_int, [ct.c_void_p, ct.c_int32, ct.c_int32, ct.c_void_p, ct.c_int32,
                                  ct.c_void_p, ct.c_void_p, ct.c_void_p, ct.c_void_p, ct.c_void_p,
                                  ct.c_void_p]),
@@ -121,6 +125,8 @@ def _p(a):
     if isinstance(a, np.ndarray):
         return a.ctypes.data_as(ct.c_void_p)
     if hasattr(a, "data_ptr"):  # torch tensor (device pointer)
+        if not a.is_contiguous():
+            raise ValueError("tensors passed to libpga must be contiguous (row-major)")
         return ct.c_void_p(a.data_ptr())
     return a
 
@@ -329,6 +335,34 @@ def pga_rep_evaluate(ctx, begin: int, end: int, L_dev, top_dev):
 
 def pga_rep_commit(ctx, L_dev, top_dev):
     _check(lib().pga_rep_commit(ctx, _p(L_dev), _p(top_dev)))
+
+
+def pga_stream_count(T: int, warm: int, stride: int) -> int:
+    rc = lib().pga_stream_count(T, warm, stride)
+    if rc < 0:
+        _check(rc)
+    return rc
+
+
+def pga_corr_stream(X, lam: float = 0.98, warm: int = 160, stride: int = 10, q: float = 0.0,
+                    device: int = 0):
+    """Host returns X [T][N] -> cleaned correlation windows [B][N][N]
+    (include/pga.h pga_corr_stream; q = 0: N (1 - lam), q < 0: no cleaning)."""
+    X = _c(X, np.float64)
+    T, N = X.shape
+    B = pga_stream_count(T, warm, stride)
+    out = np.zeros((B, N, N))
+    st = ct.c_int32(0)
+    _check(lib().pga_corr_stream(_p(X), T, N, lam, warm, stride, q, 0, _p(out), ct.byref(st),
+                                 device, None))
+    return out
+
+
+def pga_corr_stream_device(X_dev, C_dev, status_dev, lam: float = 0.98, warm: int = 160,
+                           stride: int = 10, q: float = 0.0, device: int = 0, stream=None):
+    T, N = X_dev.shape
+    _check(lib().pga_corr_stream(_p(X_dev), T, N, lam, warm, stride, q, 1, _p(C_dev), _p(status_dev),
+                                 device, None if stream is None else ct.c_void_p(stream)))
 
 
 def pga_batch_run(C, params: pga_params, history: bool = False):

@@ -11,7 +11,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpga.so")
-SOURCES = ["api.cu", "fitness.cu", "ga.cu", "corr.cu", "batch.cu"]
+SOURCES = ["api.cu", "fitness.cu", "ga.cu", "corr.cu", "batch.cu", "stream.cu"]
 HEADERS = ["pga_internal.cuh", os.path.join("..", "..", "include", "pga.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

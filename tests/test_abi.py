@@ -109,3 +109,15 @@ def test_batch_validation(pga, N, kw, msg):
     bad[1, 0, 1] = 0.5        # matrix 1 not symmetric
     with pytest.raises(pga.PgaError, match="matrix 1"):
         pga.pga_batch_run(bad, pga.pga_params_default(pop_size=10, elite=2))
+
+
+def test_corr_stream_validation(pga):
+    X = np.random.default_rng(0).standard_normal((50, 4))
+    for kw, msg in [(dict(lam=1.0), "lambda"), (dict(warm=0), "warm"), (dict(warm=60), "T >= warm"),
+                    (dict(stride=0), "stride")]:
+        with pytest.raises(pga.PgaError) as e:
+            pga.pga_corr_stream(X, **{**dict(warm=10, stride=5), **kw})
+        assert e.value.code == pga.binding.PGA_EINVAL
+    with pytest.raises(pga.PgaError, match="1 <= N <= 64"):
+        pga.pga_corr_stream(np.zeros((20, 65)), warm=5, stride=5)
+    assert pga.pga_stream_count(57, 20, 9) == 5

@@ -73,7 +73,7 @@ def noh_returns(spec: PlantedSpec):
     eta = rng.standard_normal((T, k + spec.singletons))
     eps = rng.standard_normal((T, N))
     g = gs[cluster]
-    X = g[None, :] * eta[:, cluster] + np.sqrt(1.0 - g * g)[None, :] * eps
+    X = np.ascontiguousarray(g[None, :] * eta[:, cluster] + np.sqrt(1.0 - g * g)[None, :] * eps)
     # first-occurrence relabelling of the planted partition (pure bookkeeping)
     first = {}
     planted = np.empty(N, np.int32)
@@ -154,3 +154,11 @@ def window_returns(B: int, N: int = 18, T: int = 160, seed0: int = 1_760_000):
     for b in range(B):
         X[b], planted[b] = noh_returns(window_spec(b, N, T, seed0))
     return X, planted
+
+
+def stream_returns(T: int, N: int = 18, seed: int = 1_800_000):
+    """A continuous return stream for the correlation stream (f4): the Noh
+    model (Eq. 2) with one fixed planted structure drawn like an F1 window
+    (window_spec), T observations.  Returns (X [T][N], planted [N])."""
+    spec = window_spec(0, N, T, seed)
+    return noh_returns(spec)
