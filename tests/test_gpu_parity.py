@@ -383,6 +383,27 @@ def test_run_recovers_planted_C3_device_pearson(pga, orc):
         _assert_L(L[idx], orc.evaluate(C, pop[idx])[0])
 
 
+def test_run_recovers_planted_C4(pga, orc):
+    """C4 (BASELINE configs[3]): N=500, P=65536, p_m = 2/N, C on the device.
+    The planted 9-cluster partition is recovered exactly (by generation
+    ~5000 with seed 5; 6000 are run, ~11 s), and its L equals the oracle's
+    Eq. 8 value of the planted labels."""
+    X, planted = workloads.noh_returns(workloads.CONFIGS["C4"])
+    C = pga.pga_correlation(X)
+    Lp, _ = orc.log_likelihood(C, planted)
+    params = _par(pga, 65536, max_gens=6000, tol=-1.0, p_mutation=2.0 / 500, seed=5)
+    ctx = pga.pga_create(C, params)
+    try:
+        r = pga.pga_run(ctx, 6000, 5, 500)
+        hist = pga.pga_get_history(ctx, 6000)
+    finally:
+        pga.pga_destroy(ctx)
+    assert np.array_equal(r["best_labels"] - 1, planted)
+    assert abs(r["best_L"] - Lp) <= TOL * max(1, Lp)
+    assert np.all(np.diff(hist) >= 0.0)       # elitism: the generation best never drops (S:188)
+    assert hist[999] >= 0.75 * Lp
+
+
 def test_run_C2_matches_brute_force(pga, orc):
     X, planted = workloads.noh_returns(workloads.CONFIGS["C2"])
     C = orc.pearson(X)
