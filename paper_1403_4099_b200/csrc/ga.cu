@@ -200,17 +200,6 @@ k_stats(const double *__restrict__ L, int64_t P, const uint16_t *CM0, const uint
 // ---------------------------------------------------------------------------
 // selection
 // ---------------------------------------------------------------------------
-__global__ void k_sort_keys(const double *__restrict__ L, int64_t P, uint64_t *keys, int32_t *idx,
-                            const int32_t *done) {
-    if (done && *done) return;
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= P) return;
-    double v = L[i];
-    if (v == 0.0) v = 0.0;  // -0 -> +0
-    // ascending key order == (L desc); L >= 0 so the raw bits are monotone.
-    keys[i] = ~(uint64_t)__double_as_longlong(v);
-    idx[i] = (int32_t)i;
-}
 
 // q_i = floor(2^B * w_i / w_max), w = 1/sqrt(rank) (RANK) or L (NONE)
 __global__ void k_weights(const double *__restrict__ L, const int32_t *__restrict__ order, int64_t P,
@@ -470,6 +459,86 @@ k_select_small(int what, const double *__restrict__ L, int P, int M, int selecti
         }
     }
     for (int m = tid; m < M; m += SMALL_T) sigma[m] = feistel_slot(m, M, seed, gen, island);
+}
+
+// ---------------------------------------------------------------------------
+// Order (isolate fittest) for P > 4096: (1) runs of RUN items, each
+// sorted in one CTA by a shared-memory bitonic network on (key = ~bits(L),
+// index) -- a total order, indices being unique; (2) a merge tree: at width
+// w every item moves to (start of its 2w block) + (its offset in its run) +
+// (number of items of the sibling run before it), found by binary search.
+// The last level writes the indices to order.  1 + ceil(log2(P / RUN))
+// launches, each spread over the whole GPU.
+// ---------------------------------------------------------------------------
+constexpr int RUN = 1024, RUN_T = 512;
+
+__global__ void __launch_bounds__(RUN_T)
+k_sort_runs(const double *__restrict__ L, int64_t P, uint64_t *keys, int32_t *idx, const int32_t *done) {
+    if (done && *done) return;
+    __shared__ uint64_t sk[RUN];
+    __shared__ uint32_t sv[RUN];
+    const int tid = threadIdx.x;
+    const int64_t base = (int64_t)blockIdx.x * RUN;
+    for (int t = tid; t < RUN; t += RUN_T) {
+        const int64_t i = base + t;
+        if (i < P) {
+            double x = L[i];
+            if (x == 0.0) x = 0.0;
+            sk[t] = ~(uint64_t)__double_as_longlong(x);
+            sv[t] = (uint32_t)i;
+        } else {
+            sk[t] = ~0ull;
+            sv[t] = 0xFFFFFFFFu;
+        }
+    }
+    __syncthreads();
+    for (int size = 2; size <= RUN; size <<= 1)
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            const int t = tid;
+            const int i = 2 * t - (t & (stride - 1)), j = i + stride;
+            const bool up = (i & size) == 0;
+            const uint64_t ki = sk[i], kj = sk[j];
+            const uint32_t vi = sv[i], vj = sv[j];
+            if (kv_less(kj, vj, ki, vi) == up) {
+                sk[i] = kj;
+                sk[j] = ki;
+                sv[i] = vj;
+                sv[j] = vi;
+            }
+            __syncthreads();
+        }
+    for (int t = tid; t < RUN; t += RUN_T) {
+        const int64_t o = base + t;
+        if (o < P) {
+            keys[o] = sk[t];
+            idx[o] = (int32_t)sv[t];
+        }
+    }
+}
+
+// one merge level at run width w: (ks, is) -> (kd, id); kd may be null (last level)
+__global__ void k_merge_level(const uint64_t *__restrict__ ks, const int32_t *__restrict__ is, int64_t P,
+                              int64_t w, uint64_t *kd, int32_t *id, const int32_t *done) {
+    if (done && *done) return;
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= P) return;
+    const int64_t blk = g / (2 * w) * (2 * w);
+    const bool left = g - blk < w;
+    const int64_t sib = left ? blk + w : blk;
+    const int64_t off = left ? g - blk : g - blk - w;
+    const int64_t slen = max((int64_t)0, min(w, P - sib));
+    const uint64_t ke = ks[g];
+    const uint32_t ie = (uint32_t)is[g];
+    int64_t lo = 0, hi = slen;
+    while (lo < hi) {            // sibling items before (ke, ie)
+        const int64_t mid = (lo + hi) >> 1;
+        const uint64_t km = __ldg(ks + sib + mid);
+        if (km < ke || (km == ke && (uint32_t)__ldg(is + sib + mid) < ie)) lo = mid + 1;
+        else hi = mid;
+    }
+    const int64_t pos = blk + off + lo;
+    if (kd) kd[pos] = ke;
+    id[pos] = (int32_t)ie;
 }
 
 static size_t select_small_smem() {
@@ -826,15 +895,30 @@ size_t cub_tmp_needed(int64_t P) {
 
 // order = indices by (L desc, idx asc)
 static int sort_order(const double *L, int64_t P, int32_t *order, uint64_t *keys_in,
-                      uint64_t *keys_out, int32_t *idx_in, void *tmp, size_t tmp_bytes,
-                      const int32_t *done, cudaStream_t s) {
-    const unsigned nb = (unsigned)((P + 255) / 256);
-    k_sort_keys<<<nb, 256, 0, s>>>(L, P, keys_in, idx_in, done);
+                      uint64_t *keys_out, int32_t *idx_in, int32_t *idx_tmp, const int32_t *done,
+                      cudaStream_t s) {
+    const int nruns = (int)((P + RUN - 1) / RUN);
+    uint64_t *kA = keys_out, *kB = keys_in;
+    int32_t *iA = idx_in, *iB = idx_tmp;
+    k_sort_runs<<<nruns, RUN_T, 0, s>>>(L, P, kA, iA, done);
     PGA_LAUNCHED();
-    size_t tb = tmp_bytes;
-    PGA_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, keys_in, keys_out, idx_in, order, (int)P, 0,
-                                             64, s));
-    count_launch();
+    const unsigned nb = (unsigned)((P + 255) / 256);
+    if (nruns == 1) {   // one run: copy its indices out through a width-P "merge"
+        k_merge_level<<<nb, 256, 0, s>>>(kA, iA, P, P, nullptr, order, done);
+        PGA_LAUNCHED();
+        return PGA_OK;
+    }
+    for (int64_t w = RUN; w < P; w *= 2) {
+        const bool last = 2 * w >= P;
+        k_merge_level<<<nb, 256, 0, s>>>(kA, iA, P, w, last ? nullptr : kB, last ? order : iB, done);
+        PGA_LAUNCHED();
+        uint64_t *tk = kA;
+        kA = kB;
+        kB = tk;
+        int32_t *ti = iA;
+        iA = iB;
+        iB = ti;
+    }
     return PGA_OK;
 }
 
@@ -867,7 +951,7 @@ int run_select_ops(const double *L, int64_t P, const pga_params &p, int32_t gen,
                                    reinterpret_cast<int32_t *>(q), done, s);
     int rc;
     if (!sorted) {
-        rc = sort_order(L, P, order, keys_in, keys_out, idx_in, tmp, tmp_bytes, done, s);
+        rc = sort_order(L, P, order, keys_in, keys_out, idx_in, reinterpret_cast<int32_t *>(q), done, s);
         if (rc) return rc;
     }
     if (p.selection == PGA_SEL_TOURNAMENT) {
@@ -943,8 +1027,8 @@ int launch_sort_order(pga_ctx *c, cudaStream_t s) {
     if (small_select(c))
         return launch_select_small(1, c->L, c->P, c->p, 0, c->p.island, &c->st->gen, c->order, c->sel,
                                    c->sigma, &c->st->done, s);
-    return sort_order(c->L, c->P, c->order, c->keys_in, c->keys_out, c->idx_in, c->cub_tmp,
-                      c->cub_tmp_bytes, &c->st->done, s);
+    return sort_order(c->L, c->P, c->order, c->keys_in, c->keys_out, c->idx_in,
+                      reinterpret_cast<int32_t *>(c->q), &c->st->done, s);
 }
 
 // Phase B of a generation, after launch_sort_order.
