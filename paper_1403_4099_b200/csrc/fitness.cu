@@ -428,6 +428,15 @@ k_fitness(const __grid_constant__ CUtensorMap tmLab0, const __grid_constant__ CU
                 to[c] = a.top ? &a.top[pc] : nullptr;
             }
             fold_multi<NCF>(lab, vv, N, cs, ns, gbuf, lane, Lo, to);
+            // V of these chromosomes is dead: drop its L2 lines without a
+            // DRAM write-back (rows are 128-byte aligned, ldn % 16 == 0)
+#pragma unroll
+            for (int c = 0; c < NCF; ++c) {
+                if (p + c >= a.P) break;
+                const char *row = reinterpret_cast<const char *>(a.V + (p + c) * a.ldn);
+                for (int l = lane; l < a.ldn / 16; l += 32)
+                    asm volatile("discard.global.L2 [%0], 128;" ::"l"(row + 128 * l) : "memory");
+            }
         }
     }
     if (tid == 0) a.counters[cb] = 0u;

@@ -730,6 +730,142 @@ __global__ void __launch_bounds__(BW * 32, 3) k_breed(BreedArgs a) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// k_breed2 (N <= BREED2_MAXN): the same operators and outputs as k_breed with
+// a canonicalisation that has no dependency chain across gene chunks.
+// Phase 1 writes every child's pre-canonical genes to a shared tile [N][BS].
+// Phase 2 (warp per child): (a) first-occurrence positions fp[v] -- chunks
+// visited last to first, each chunk's match_any leader (its first lane with
+// that value) stores its position, so the first occurrence is stored last;
+// (b) one ballot per chunk marks the genes i with fp[s_i] == i, and a running
+// count gives each chunk's base; (c) canonical(s_i) = rank of fp[s_i] among
+// the first occurrences = base[chunk] + popc(ballot[chunk] below fp's lane).
+// Phase 3 writes the gene-major rows of the CTA's 16 children from the tile.
+// ---------------------------------------------------------------------------
+constexpr int BREED2_MAXN = 1024;
+
+__host__ __device__ __forceinline__ int breed2_nch(int N) { return (N + 31) / 32; }
+
+static size_t breed2_smem(int N) {
+    const size_t tile = (size_t)N * TS * sizeof(uint16_t);
+    const size_t fp = (size_t)BS * ((N + 1 + 7) & ~7) * sizeof(uint16_t);
+    const size_t bal = (size_t)BS * breed2_nch(N) * (sizeof(uint32_t) + sizeof(uint16_t));
+    return ((tile + 15) & ~(size_t)15) + ((fp + 15) & ~(size_t)15) + bal + 16;
+}
+
+template <bool HOOK>
+__global__ void __launch_bounds__(BW * 32, 3) k_breed2(BreedArgs a) {
+    if (a.done && *a.done) return;
+    extern __shared__ __align__(16) unsigned char sm2[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int N = a.N, nch = breed2_nch(N);
+    const uint32_t gen = a.gen_ptr ? (uint32_t)*a.gen_ptr : a.gen;
+    const int par = a.gen_ptr ? (int)(gen & 1u) : 0;
+    const uint16_t *cm_in = par ? a.cm_in1 : a.cm_in0;
+    uint16_t *cm_out = par ? a.cm_out0 : a.cm_out1;
+    uint16_t *gm_out = par ? a.gm_out0 : a.gm_out1;
+    uint16_t *tile = reinterpret_cast<uint16_t *>(sm2);                               // [N][TS]
+    const size_t tile_b = ((size_t)N * TS * sizeof(uint16_t) + 15) & ~(size_t)15;
+    const int fpn = (N + 1 + 7) & ~7;
+    uint16_t *fp = reinterpret_cast<uint16_t *>(sm2 + tile_b) + (size_t)warp * fpn;    // [BS][fpn]
+    const size_t fp_b = ((size_t)BS * fpn * sizeof(uint16_t) + 15) & ~(size_t)15;
+    uint32_t *balv = reinterpret_cast<uint32_t *>(sm2 + tile_b + fp_b) + (size_t)warp * nch;
+    uint16_t *base = reinterpret_cast<uint16_t *>(sm2 + tile_b + fp_b + (size_t)BS * nch * sizeof(uint32_t)) +
+                     (size_t)warp * nch;
+    const int64_t o0 = (int64_t)blockIdx.x * BS;
+    const int slot = warp;
+    const int64_t o = o0 + slot;
+    const ChildPlan p = plan_child(a, o, gen);
+
+    // ---- phase 1: crossover + mutation -> pre-canonical genes in the tile
+    for (int b0 = 0; b0 < N; b0 += GCH) {
+        uint32_t ga[GCH / 32], gb[GCH / 32];
+#pragma unroll
+        for (int sc = 0; sc < GCH / 32; ++sc) {
+            const int i = b0 + 32 * sc + lane;
+            const bool valid = p.valid && i < N;
+            if (HOOK) {
+                ga[sc] = valid ? (uint32_t)a.i32_in[p.pa * N + i] : 0u;
+                gb[sc] = (valid && p.mode != 0) ? (uint32_t)a.i32_in[p.pb * N + i] : 0u;
+            } else {
+                ga[sc] = valid ? (uint32_t)cm_in[p.pa * a.ldn + i] : 0u;
+                gb[sc] = (valid && p.mode != 0) ? (uint32_t)cm_in[p.pb * a.ldn + i] : 0u;
+            }
+        }
+        uint32_t mbits = 0;
+        if (p.valid && p.mutate && b0 + 4 * lane < N) {
+            const U4 u = draw(a.seed, pga::TAG_MUT, a.island, gen, (uint32_t)((b0 >> 2) + lane), p.og);
+            mbits = ((uint64_t)u.x < a.thr_m ? 1u : 0u) | ((uint64_t)u.y < a.thr_m ? 2u : 0u) |
+                    ((uint64_t)u.z < a.thr_m ? 4u : 0u) | ((uint64_t)u.w < a.thr_m ? 8u : 0u);
+        }
+#pragma unroll
+        for (int sc = 0; sc < GCH / 32; ++sc) {
+            const int i = b0 + 32 * sc + lane;
+            const bool valid = p.valid && i < N;
+            const uint32_t mb = __shfl_sync(0xFFFFFFFFu, mbits, 8 * sc + (lane >> 2));
+            uint32_t s = ga[sc];
+            if (p.mode == 1) {
+                if (p.kb_top >= 0 && (int)gb[sc] == p.kb_top) s = (uint32_t)N;
+            } else if (p.mode == 2) {
+                if (i >= p.cut) s = gb[sc];
+            }
+            if (valid && ((mb >> (lane & 3)) & 1u)) {
+                const U4 v = draw(a.seed, pga::TAG_MUTV, a.island, gen, (uint32_t)(i >> 2), p.og);
+                s = scale_u32(word(v, i & 3), (uint32_t)N);
+            }
+            if (i < N) tile[i * TS + slot] = (uint16_t)s;
+        }
+    }
+    __syncwarp();
+
+    // ---- phase 2: canonical form (Q7), no chain across chunks
+    if (p.valid) {
+        for (int c = nch - 1; c >= 0; --c) {          // (a) first occurrences
+            const int i = 32 * c + lane;
+            const bool valid = i < N;
+            const uint32_t s = valid ? (uint32_t)tile[i * TS + slot] : 0x10000u + (uint32_t)lane;
+            const unsigned m = __match_any_sync(0xFFFFFFFFu, s);
+            if (valid && lane == __ffs(m) - 1) fp[s] = (uint16_t)i;
+            __syncwarp();
+        }
+        int run = 0;
+        for (int c = 0; c < nch; ++c) {               // (b) first-occurrence ballots, chunk bases
+            const int i = 32 * c + lane;
+            const bool first = i < N && fp[tile[i * TS + slot]] == (uint16_t)i;
+            const unsigned bal = __ballot_sync(0xFFFFFFFFu, first);
+            if (lane == 0) {
+                balv[c] = bal;
+                base[c] = (uint16_t)run;
+            }
+            run += __popc(bal);
+        }
+        __syncwarp();
+        for (int c = 0; c < nch; ++c) {               // (c) canonical labels
+            const int i = 32 * c + lane;
+            if (i < N) {
+                const int f = fp[tile[i * TS + slot]];
+                const uint32_t cv = (uint32_t)base[f >> 5] + __popc(balv[f >> 5] & ((1u << (f & 31)) - 1u));
+                tile[i * TS + slot] = (uint16_t)cv;
+                if (HOOK) a.i32_out[o * N + i] = (int32_t)cv;
+                else cm_out[o * a.ldn + i] = (uint16_t)cv;
+            }
+        }
+    }
+    if (HOOK) return;
+    __syncthreads();
+
+    // ---- phase 3: gene-major rows (BS children = 32 B per gene)
+    for (int e = threadIdx.x; e < N * (BS / 2); e += BW * 32) {
+        const int i = e / (BS / 2), pr = e - i * (BS / 2);
+        const int64_t oo = o0 + 2 * pr;
+        if (oo < a.P) {
+            const uint32_t two = *reinterpret_cast<const uint32_t *>(&tile[i * TS + 2 * pr]);
+            if (oo + 1 < a.P) *reinterpret_cast<uint32_t *>(&gm_out[(int64_t)i * a.Pcap + oo]) = two;
+            else gm_out[(int64_t)i * a.Pcap + oo] = (uint16_t)(two & 0xFFFF);
+        }
+    }
+}
+
 // k_set_pop: int32 1-based labels (validated on the host) -> canonical
 // u16 in both layouts of buffer `par`.
 __global__ void k_set_pop(const int32_t *__restrict__ lab, int64_t P, int N, int ldn, int64_t Pcap,
@@ -858,6 +994,12 @@ int launch_init_raw(uint64_t seed, int N, int ldn, int64_t P, int64_t Pcap, int6
 int prepare_breed(int N) {
     PGA_CUDA(cudaFuncSetAttribute(k_breed<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)breed_smem(N)));
     PGA_CUDA(cudaFuncSetAttribute(k_breed<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)breed_smem(N)));
+    if (N <= BREED2_MAXN) {
+        PGA_CUDA(cudaFuncSetAttribute(k_breed2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)breed2_smem(N)));
+        PGA_CUDA(cudaFuncSetAttribute(k_breed2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)breed2_smem(N)));
+    }
     return PGA_OK;
 }
 
@@ -1016,7 +1158,8 @@ int launch_breed_hook(const int32_t *pop, const int32_t *top, const int32_t *ord
     a.island = (uint32_t)island;
     a.ldn = N;
     a.Pcap = P;
-    k_breed<true><<<(unsigned)((P + BS - 1) / BS), BW * 32, breed_smem(N), s>>>(a);
+    if (N <= BREED2_MAXN) k_breed2<true><<<(unsigned)((P + BS - 1) / BS), BW * 32, breed2_smem(N), s>>>(a);
+    else k_breed<true><<<(unsigned)((P + BS - 1) / BS), BW * 32, breed_smem(N), s>>>(a);
     PGA_LAUNCHED();
     return PGA_OK;
 }
@@ -1072,7 +1215,10 @@ int launch_select_breed(pga_ctx *c, cudaStream_t s) {
     a.ldn = c->ldn;
     a.done = done;
     a.gen_ptr = genp;
-    k_breed<false><<<(unsigned)((c->P + BS - 1) / BS), BW * 32, breed_smem(c->N), s>>>(a);
+    if (c->N <= BREED2_MAXN)
+        k_breed2<false><<<(unsigned)((c->P + BS - 1) / BS), BW * 32, breed2_smem(c->N), s>>>(a);
+    else
+        k_breed<false><<<(unsigned)((c->P + BS - 1) / BS), BW * 32, breed_smem(c->N), s>>>(a);
     PGA_LAUNCHED();
     PGA_MARK(c, 7, s);
     k_advance<<<1, 1, 0, s>>>(c->st);
