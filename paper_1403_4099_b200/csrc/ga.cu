@@ -734,9 +734,9 @@ __global__ void __launch_bounds__(BW * 32, 3) k_breed(BreedArgs a) {
 // k_breed2 (N <= BREED2_MAXN): the same operators and outputs as k_breed with
 // a canonicalisation that has no dependency chain across gene chunks.
 // Phase 1 writes every child's pre-canonical genes to a shared tile [N][BS].
-// Phase 2 (warp per child): (a) first-occurrence positions fp[v] -- chunks
-// visited last to first, each chunk's match_any leader (its first lane with
-// that value) stores its position, so the first occurrence is stored last;
+// Phase 2 (warp per child): (a) first-occurrence positions fp[v] = min i --
+// each chunk's match_any leader (its first lane with that value) does a
+// shared atomicMin, so the chunks do not wait on one another;
 // (b) one ballot per chunk marks the genes i with fp[s_i] == i, and a running
 // count gives each chunk's base; (c) canonical(s_i) = rank of fp[s_i] among
 // the first occurrences = base[chunk] + popc(ballot[chunk] below fp's lane).
@@ -748,7 +748,7 @@ __host__ __device__ __forceinline__ int breed2_nch(int N) { return (N + 31) / 32
 
 static size_t breed2_smem(int N) {
     const size_t tile = (size_t)N * TS * sizeof(uint16_t);
-    const size_t fp = (size_t)BS * ((N + 1 + 7) & ~7) * sizeof(uint16_t);
+    const size_t fp = (size_t)BS * ((N + 1 + 3) & ~3) * sizeof(uint32_t);
     const size_t bal = (size_t)BS * breed2_nch(N) * (sizeof(uint32_t) + sizeof(uint16_t));
     return ((tile + 15) & ~(size_t)15) + ((fp + 15) & ~(size_t)15) + bal + 16;
 }
@@ -766,9 +766,9 @@ __global__ void __launch_bounds__(BW * 32, 3) k_breed2(BreedArgs a) {
     uint16_t *gm_out = par ? a.gm_out0 : a.gm_out1;
     uint16_t *tile = reinterpret_cast<uint16_t *>(sm2);                               // [N][TS]
     const size_t tile_b = ((size_t)N * TS * sizeof(uint16_t) + 15) & ~(size_t)15;
-    const int fpn = (N + 1 + 7) & ~7;
-    uint16_t *fp = reinterpret_cast<uint16_t *>(sm2 + tile_b) + (size_t)warp * fpn;    // [BS][fpn]
-    const size_t fp_b = ((size_t)BS * fpn * sizeof(uint16_t) + 15) & ~(size_t)15;
+    const int fpn = (N + 1 + 3) & ~3;
+    uint32_t *fp = reinterpret_cast<uint32_t *>(sm2 + tile_b) + (size_t)warp * fpn;    // [BS][fpn]
+    const size_t fp_b = ((size_t)BS * fpn * sizeof(uint32_t) + 15) & ~(size_t)15;
     uint32_t *balv = reinterpret_cast<uint32_t *>(sm2 + tile_b + fp_b) + (size_t)warp * nch;
     uint16_t *base = reinterpret_cast<uint16_t *>(sm2 + tile_b + fp_b + (size_t)BS * nch * sizeof(uint32_t)) +
                      (size_t)warp * nch;
@@ -820,18 +820,24 @@ __global__ void __launch_bounds__(BW * 32, 3) k_breed2(BreedArgs a) {
 
     // ---- phase 2: canonical form (Q7), no chain across chunks
     if (p.valid) {
-        for (int c = nch - 1; c >= 0; --c) {          // (a) first occurrences
-            const int i = 32 * c + lane;
-            const bool valid = i < N;
-            const uint32_t s = valid ? (uint32_t)tile[i * TS + slot] : 0x10000u + (uint32_t)lane;
-            const unsigned m = __match_any_sync(0xFFFFFFFFu, s);
-            if (valid && lane == __ffs(m) - 1) fp[s] = (uint16_t)i;
+        {                                             // (a) first occurrences: fp[v] = min i
+            uint4 *f4 = reinterpret_cast<uint4 *>(fp);
+            const uint4 inf = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+            for (int k = lane; k < fpn / 4; k += 32) f4[k] = inf;
+            __syncwarp();
+            for (int c = 0; c < nch; ++c) {           // independent chunks: atomics return nothing
+                const int i = 32 * c + lane;
+                const bool valid = i < N;
+                const uint32_t s = valid ? (uint32_t)tile[i * TS + slot] : 0x10000u + (uint32_t)lane;
+                const unsigned m = __match_any_sync(0xFFFFFFFFu, s);
+                if (valid && lane == __ffs(m) - 1) atomicMin(&fp[s], (uint32_t)i);
+            }
             __syncwarp();
         }
         int run = 0;
         for (int c = 0; c < nch; ++c) {               // (b) first-occurrence ballots, chunk bases
             const int i = 32 * c + lane;
-            const bool first = i < N && fp[tile[i * TS + slot]] == (uint16_t)i;
+            const bool first = i < N && fp[tile[i * TS + slot]] == (uint32_t)i;
             const unsigned bal = __ballot_sync(0xFFFFFFFFu, first);
             if (lane == 0) {
                 balv[c] = bal;
@@ -843,7 +849,7 @@ __global__ void __launch_bounds__(BW * 32, 3) k_breed2(BreedArgs a) {
         for (int c = 0; c < nch; ++c) {               // (c) canonical labels
             const int i = 32 * c + lane;
             if (i < N) {
-                const int f = fp[tile[i * TS + slot]];
+                const int f = (int)fp[tile[i * TS + slot]];
                 const uint32_t cv = (uint32_t)base[f >> 5] + __popc(balv[f >> 5] & ((1u << (f & 31)) - 1u));
                 tile[i * TS + slot] = (uint16_t)cv;
                 if (HOOK) a.i32_out[o * N + i] = (int32_t)cv;
