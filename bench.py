@@ -358,6 +358,10 @@ def main():
             "roofline": {"bound": "alu", "kernel": "k_sweep", "achieved": achieved,
                          "peak": peak, "unit": "pair-updates/s", "frac": achieved / peak,
                          "traffic": traffic,
+                         "algorithmic_bytes": P_eval * (N * 2 + 8 + 2),
+                         "traffic_note": "ncu dram bytes of one launch: labels are read twice (gene-major "
+                                         "by the sweep's TMA, chromosome-major by the fused fold); the "
+                                         "fold scratch V is discarded from L2 after use (no write-back)",
                          "work_per_launch": "%d chromosomes x N(N-1)/2 = %.4g executed pair-updates"
                                             % (P_local, executed_local),
                          "peak_basis": "1 DFMA per executed pair; 64 FP64 lanes/clk/SM x 148 SMs "
@@ -510,6 +514,12 @@ def bench_f1(args):
     achieved = executed / (ms_step / 1000.0)
     best = lab.cpu().numpy() - 1
     same = float(np.mean([np.array_equal(best[b], planted[b]) for b in range(B)]))
+    f1_traffic = None
+    try:
+        tj = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        f1_traffic = tj.get("k_batch", {}).get("dram_bytes_per_launch")
+    except Exception:
+        pass
 
     # e2e: the host-memory call (C from pinned host, results back to host)
     e2e = None
@@ -578,7 +588,8 @@ def bench_f1(args):
             "evals_per_s": evals * world / (ms_step / 1000.0),
             "planted_equals_best": same,
             "roofline": {"bound": "alu", "kernel": "k_batch", "achieved": achieved, "peak": peak,
-                         "unit": "pair-updates/s", "frac": achieved / peak, "traffic": None,
+                         "unit": "pair-updates/s", "frac": achieved / peak, "traffic": f1_traffic,
+                         "algorithmic_bytes": B * N * N * 8 + B * (N * 4 + 16),
                          "work_per_launch": "sum over windows of gens x %d chromosomes x N(N-1)/2"
                                             % f1["pop"],
                          "note": "the GA operators (sort, selection, Philox, breed) take most of "
