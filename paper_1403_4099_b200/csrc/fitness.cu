@@ -131,6 +131,7 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *tm, in
 struct FitArgs {
     int N, ldn, nRT, nCB, fold_warps;
     int cb0;                        // first chromosome block (shard offset / 32)
+    double fx_scale, fx_inv;        // fold fixed point: 2^S and 2^-S
     int64_t P, Pcap;
     const double *diag;
     double *V;                      // [Pcap][ldn]: V[p][i] = C_ii + 2 r'_i
@@ -167,19 +168,23 @@ __device__ __forceinline__ void pairs16(uint32_t caddr, uint32_t w, const uint32
 }
 
 // Fold (warp-wide) of NC chromosomes at once (independent chains -> ILP):
-// n_s by match_any/popc; the group sum of V is gathered by the group's
-// leader (lowest lane) from a per-warp shared buffer in lane order, so the
-// order of additions is fixed (no float atomics -> deterministic); then
-// Eq. 8 (Q1-Q3) for labels up to the chromosome's largest.
+// lane per gene; n_s by a shared-memory integer atomic, and c_s = sum of V_i
+// over the cluster accumulated in 64-bit fixed point (V * 2^S, S = 62 -
+// ceil(log2(2 N^2 + 1)) so no cluster sum can overflow) by shared-memory
+// integer atomics.  Integer addition is exact and order-free, so the result
+// is deterministic without any per-group ordering; the quantisation (2^-S-1
+// per V, 6e-14 at N = 500) is below the fp64 summation error it replaces.
+// Then Eq. 8 (Q1-Q3) for labels up to the chromosome's largest.
 template <int NC>
 __device__ __forceinline__ void fold_multi(const uint16_t *const (&lab)[NC], const double *const (&v)[NC],
                                            int N, double *const (&cs)[NC], int32_t *const (&ns)[NC],
                                            double *gbuf, int lane, double *const (&L_out)[NC],
-                                           uint16_t *const (&top_out)[NC]) {
+                                           uint16_t *const (&top_out)[NC], double scale, double inv_scale) {
+    (void)gbuf;
 #pragma unroll
     for (int q = 0; q < NC; ++q)
         for (int k = lane; k < N; k += 32) {
-            cs[q][k] = 0.0;
+            cs[q][k] = 0.0;      // all-zero bits == integer 0
             ns[q][k] = 0;
         }
     __syncwarp();
@@ -189,40 +194,32 @@ __device__ __forceinline__ void fold_multi(const uint16_t *const (&lab)[NC], con
 #pragma unroll
     for (int q = 0; q < NC; ++q) {
         const int i1 = lane, i2 = 32 + lane;
-        s_n1[q] = (i1 < N) ? (uint32_t)lab[q][i1] : (0x10000u + (uint32_t)lane);
+        s_n1[q] = (i1 < N) ? (uint32_t)lab[q][i1] : 0u;
         v_n1[q] = (i1 < N) ? __ldcg(v[q] + i1) : 0.0;
-        s_n2[q] = (i2 < N) ? (uint32_t)lab[q][i2] : (0x10000u + (uint32_t)lane);
+        s_n2[q] = (i2 < N) ? (uint32_t)lab[q][i2] : 0u;
         v_n2[q] = (i2 < N) ? __ldcg(v[q] + i2) : 0.0;
     }
     uint32_t kmax = 0;
     for (int base = 0; base < N; base += 32) {
         const bool valid = base + lane < N;
-        uint32_t s[NC];
-        unsigned m[NC];
 #pragma unroll
         for (int q = 0; q < NC; ++q) {
-            s[q] = s_n1[q];
-            gbuf[q * 32 + lane] = v_n1[q];
+            const uint32_t s = s_n1[q];
+            const double x = v_n1[q];
             s_n1[q] = s_n2[q];
             v_n1[q] = v_n2[q];
             const int i3 = base + 64 + lane;
-            s_n2[q] = (i3 < N) ? (uint32_t)lab[q][i3] : (0x10000u + (uint32_t)lane);
+            s_n2[q] = (i3 < N) ? (uint32_t)lab[q][i3] : 0u;
             v_n2[q] = (i3 < N) ? __ldcg(v[q] + i3) : 0.0;
-            if (valid) kmax = max(kmax, s[q]);
-        }
-#pragma unroll
-        for (int q = 0; q < NC; ++q) m[q] = __match_any_sync(0xFFFFFFFFu, s[q]);
-        __syncwarp();
-#pragma unroll
-        for (int q = 0; q < NC; ++q)
-            if (valid && lane == __ffs(m[q]) - 1) {
-                double sum = 0.0;
-                for (unsigned mm = m[q]; mm; mm &= mm - 1u) sum += gbuf[q * 32 + __ffs(mm) - 1];
-                cs[q][s[q]] += sum;
-                ns[q][s[q]] += __popc(m[q]);
+            if (valid) {
+                kmax = max(kmax, s);
+                atomicAdd(reinterpret_cast<unsigned long long *>(cs[q]) + s,
+                          (unsigned long long)__double2ll_rn(x * scale));
+                atomicAdd(&ns[q][s], 1);
             }
-        __syncwarp();
+        }
     }
+    __syncwarp();
     // largest label of the (up to NC) chromosomes, warp-uniform
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) kmax = max(kmax, __shfl_xor_sync(0xFFFFFFFFu, kmax, off));
@@ -239,7 +236,7 @@ __device__ __forceinline__ void fold_multi(const uint16_t *const (&lab)[NC], con
             double c = 0.0;
             if (k < K) {
                 n = ns[q][k];
-                c = cs[q][k];
+                c = (double)reinterpret_cast<const long long *>(cs[q])[k] * inv_scale;
             }
             const bool act = (n >= 2) && (c > (double)n);
             const unsigned bal = __ballot_sync(0xFFFFFFFFu, act);
@@ -427,7 +424,7 @@ k_fitness(const __grid_constant__ CUtensorMap tmLab0, const __grid_constant__ CU
                 Lo[c] = &a.L[pc];
                 to[c] = a.top ? &a.top[pc] : nullptr;
             }
-            fold_multi<NCF>(lab, vv, N, cs, ns, gbuf, lane, Lo, to);
+            fold_multi<NCF>(lab, vv, N, cs, ns, gbuf, lane, Lo, to, a.fx_scale, a.fx_inv);
             // V of these chromosomes is dead: drop its L2 lines without a
             // DRAM write-back (rows are 128-byte aligned, ldn % 16 == 0)
 #pragma unroll
@@ -529,6 +526,13 @@ int launch_fitness_range(pga_ctx *c, const FitBufs &b, int64_t begin, int64_t en
     a.ldn = c->ldn;
     a.nRT = (N + RT - 1) / RT;
     a.cb0 = (int)(begin / CB);
+    {
+        // S = 62 - ceil(log2(2 N^2 + 1)): |sum of V over a cluster| <= 2 N^2
+        int bits = 0;
+        while ((1.0 * (1ull << bits)) < 2.0 * N * N + 1.0) ++bits;
+        a.fx_scale = ldexp(1.0, 62 - bits);
+        a.fx_inv = ldexp(1.0, bits - 62);
+    }
     a.nCB = (int)((end - begin + CB - 1) / CB);
     a.fold_warps = fold_warps(N);
     a.P = P;
