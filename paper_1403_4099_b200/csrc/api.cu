@@ -118,7 +118,7 @@ struct Graphs {
 void free_ctx(pga_ctx *c) {
     if (!c) return;
     cudaSetDevice(c->device);
-    void *ptrs[] = {c->C, c->diag, c->pop[0], c->pop[1], c->popT[0], c->popT[1], c->V, c->L,
+    void *ptrs[] = {c->C, c->diag, c->lgtab, c->pop[0], c->pop[1], c->popT[0], c->popT[1], c->V, c->L,
                     c->top, c->keys_in, c->keys_out, c->idx_in, c->order, c->q, c->prefix,
                     c->sel, c->mkeys_in, c->mkeys_out, c->m_in, c->sigma, c->cub_tmp, c->st,
                     c->best_labels, c->history, c->stage_i32, c->evCM, c->evGM, c->evL,
@@ -345,6 +345,7 @@ int pga_create(const double *C, int32_t N, const pga_params *p, pga_ctx **out) {
     int rc = 0;
     rc = rc ? rc : dalloc(&c->C, (size_t)N * c->ldc);
     rc = rc ? rc : dalloc(&c->diag, (size_t)N);
+    rc = rc ? rc : dalloc(&c->lgtab, (size_t)2 * (N + 1));
     for (int b = 0; b < 2 && !rc; ++b) {
         rc = rc ? rc : dalloc(&c->pop[b], cm);
         rc = rc ? rc : dalloc(&c->popT[b], gm);
@@ -394,6 +395,8 @@ int pga_create(const double *C, int32_t N, const pga_params *p, pga_ctx **out) {
         if (e != cudaSuccess) return bail(cuda_fail(e, "copy C"));
     }
     rc = prepare_fitness(N);
+    if (!rc) rc = launch_logtab(c, c->stream);
+    if (!rc && cudaStreamSynchronize(c->stream) != cudaSuccess) rc = cuda_fail(cudaGetLastError(), "log table");
     if (!rc) rc = prepare_breed(N);
     if (!rc) rc = prepare_select_small();
     if (!rc) rc = make_c_tmap(&c->tmC, c->C, N, c->ldc);

@@ -132,6 +132,7 @@ struct FitArgs {
     int N, ldn, nRT, nCB, fold_warps;
     int cb0;                        // first chromosome block (shard offset / 32)
     double fx_scale, fx_inv;        // fold fixed point: 2^S and 2^-S
+    const double *lgn, *lgnn;       // log n, log(n^2 - n), n = 0..N (Q30)
     int64_t P, Pcap;
     const double *diag;
     double *V;                      // [Pcap][ldn]: V[p][i] = C_ii + 2 r'_i
@@ -179,15 +180,9 @@ template <int NC>
 __device__ __forceinline__ void fold_multi(const uint16_t *const (&lab)[NC], const double *const (&v)[NC],
                                            int N, double *const (&cs)[NC], int32_t *const (&ns)[NC],
                                            double *gbuf, int lane, double *const (&L_out)[NC],
-                                           uint16_t *const (&top_out)[NC], double scale, double inv_scale) {
-    (void)gbuf;
-#pragma unroll
-    for (int q = 0; q < NC; ++q)
-        for (int k = lane; k < N; k += 32) {
-            cs[q][k] = 0.0;      // all-zero bits == integer 0
-            ns[q][k] = 0;
-        }
-    __syncwarp();
+                                           uint16_t *const (&top_out)[NC], double scale, double inv_scale,
+                                           const double *__restrict__ lgn, const double *__restrict__ lgnn) {
+    (void)gbuf;   // cs / ns were zeroed by the caller (all-zero bits == integer 0)
     // software pipeline: loads of chunk c+2 are issued while chunk c folds
     uint32_t s_n1[NC], s_n2[NC];
     double v_n1[NC], v_n2[NC];
@@ -220,6 +215,11 @@ __device__ __forceinline__ void fold_multi(const uint16_t *const (&lab)[NC], con
         }
     }
     __syncwarp();
+#ifdef PGA_DIAG_NO_LOG   // measurement builds only (tools/): accumulation without compaction / Eq. 8
+    if (lane == 0)
+        for (int q = 0; q < NC; ++q) *L_out[q] = (double)kmax;
+    return;
+#endif
     // largest label of the (up to NC) chromosomes, warp-uniform
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) kmax = max(kmax, __shfl_xor_sync(0xFFFFFFFFu, kmax, off));
@@ -239,21 +239,25 @@ __device__ __forceinline__ void fold_multi(const uint16_t *const (&lab)[NC], con
                 c = (double)reinterpret_cast<const long long *>(cs[q])[k] * inv_scale;
             }
             const bool act = (n >= 2) && (c > (double)n);
-            const unsigned bal = __ballot_sync(0xFFFFFFFFu, act);
-            __syncwarp();
+            const unsigned bal = __ballot_sync(0xFFFFFFFFu, act);   // orders this chunk's reads before its writes
             if (act) {
                 const int idx = M + __popc(bal & lanemask_lt());
                 cs[q][idx] = c;
                 ns[q][idx] = n | (k << 16);
             }
             M += __popc(bal);
-            __syncwarp();
         }
         double fsum = 0.0, fbest = 0.0;
         int kbest = 0x7FFFFFFF;
         for (int j = lane; j < M; j += 32) {
+            // Eq. 8 summand of a compacted cluster (n >= 2, c > n; Q2, Q3),
+            // (log n - log c) + (n-1)(log(n^2-n) - log(n^2-c)) with the integer
+            // logs from the table (Q30: no divisions)
             const int nk = ns[q][j];
-            const double f = cluster_term(nk & 0xFFFF, cs[q][j]);
+            const int n = nk & 0xFFFF;
+            const double nd = (double)n, n2 = nd * nd;
+            const double ch = fmin(cs[q][j], n2 - 1e-9);
+            const double f = (__ldg(lgn + n) - log(ch)) + (nd - 1.0) * (__ldg(lgnn + n) - log(n2 - ch));
             fsum += f;
             if (f > fbest) {
                 fbest = f;
@@ -396,6 +400,10 @@ k_fitness(const __grid_constant__ CUtensorMap tmLab0, const __grid_constant__ CU
     }
     __syncthreads();
     if (!s_last) return;
+#ifdef PGA_DIAG_NO_FOLD   // measurement builds only (tools/): sweep without the fold
+    if (tid == 0) a.counters[cb] = 0u;
+    return;
+#endif
     __threadfence();
     if (warp < a.fold_warps) {
         // NCF chromosomes per warp per pass (independent chains -> ILP)
@@ -424,7 +432,14 @@ k_fitness(const __grid_constant__ CUtensorMap tmLab0, const __grid_constant__ CU
                 Lo[c] = &a.L[pc];
                 to[c] = a.top ? &a.top[pc] : nullptr;
             }
-            fold_multi<NCF>(lab, vv, N, cs, ns, gbuf, lane, Lo, to, a.fx_scale, a.fx_inv);
+            {   // zero this warp's NCF x N accumulators and counters (vector stores)
+                uint4 *c4 = reinterpret_cast<uint4 *>(csb);              // 16 N bytes, 16-byte aligned
+                for (int k = lane; k < N * NCF / 2; k += 32) c4[k] = make_uint4(0u, 0u, 0u, 0u);
+                uint2 *n2 = reinterpret_cast<uint2 *>(nsb);              // 8 N bytes, 8-byte aligned
+                for (int k = lane; k < N * NCF / 2; k += 32) n2[k] = make_uint2(0u, 0u);
+                __syncwarp();
+            }
+            fold_multi<NCF>(lab, vv, N, cs, ns, gbuf, lane, Lo, to, a.fx_scale, a.fx_inv, a.lgn, a.lgnn);
             // V of these chromosomes is dead: drop its L2 lines without a
             // DRAM write-back (rows are 128-byte aligned, ldn % 16 == 0)
 #pragma unroll
@@ -491,6 +506,19 @@ int make_c_tmap(CUtensorMap *tm, const double *C, int N, int ldc) {
     return PGA_OK;
 }
 
+__global__ void k_logtab(int N, double *t) {
+    const int n = blockIdx.x * blockDim.x + threadIdx.x;
+    if (n > N) return;
+    t[n] = n >= 1 ? log((double)n) : 0.0;
+    t[N + 1 + n] = n >= 2 ? log((double)n * n - n) : 0.0;
+}
+
+int launch_logtab(pga_ctx *c, cudaStream_t s) {
+    k_logtab<<<(c->N + 1 + 255) / 256, 256, 0, s>>>(c->N, c->lgtab);
+    PGA_LAUNCHED();
+    return PGA_OK;
+}
+
 int fold_warps(int N) {
     const size_t per = 2 * (size_t)N * (sizeof(double) + sizeof(int32_t)) + 2 * 32 * sizeof(double);
     int w = (int)((size_t)(NSTAGE * STAGE_BYTES) / per);
@@ -526,6 +554,8 @@ int launch_fitness_range(pga_ctx *c, const FitBufs &b, int64_t begin, int64_t en
     a.ldn = c->ldn;
     a.nRT = (N + RT - 1) / RT;
     a.cb0 = (int)(begin / CB);
+    a.lgn = c->lgtab;
+    a.lgnn = c->lgtab + (N + 1);
     {
         // S = 62 - ceil(log2(2 N^2 + 1)): |sum of V over a cluster| <= 2 N^2
         int bits = 0;

@@ -82,6 +82,7 @@ struct pga_ctx {
     // correlation matrix
     double *C = nullptr;
     double *diag = nullptr;
+    double *lgtab = nullptr;  // [2 (N+1)]: log n, log(n^2 - n) for the Eq. 8 fold (Q30)
     // population: chromosome-major [Pcap][ldn] and gene-major [N][Pcap], double buffered
     uint16_t *pop[2] = {nullptr, nullptr};
     uint16_t *popT[2] = {nullptr, nullptr};
@@ -143,6 +144,7 @@ int make_c_tmap(CUtensorMap *tm, const double *C, int N, int ldc);
 int launch_pack(pga_ctx *c, const uint16_t *lab16, const int32_t *lab32, int64_t P, int ld_in,
                 uint16_t *CM, uint16_t *GM, cudaStream_t s);
 int prepare_fitness(int N);
+int launch_logtab(pga_ctx *c, cudaStream_t s);
 // ev (optional): 3 events recorded before the sweep, between sweep and
 // fold, and after the fold.
 int launch_fitness(pga_ctx *c, const FitBufs &b, int64_t P, double *L, uint16_t *top,
