@@ -225,6 +225,18 @@ int pga_op_canonicalize(int32_t *labels, int64_t P, int32_t N, int32_t device);
 int pga_op_init(uint64_t seed, int32_t N, int64_t P, int64_t p_off, int32_t island,
                 int32_t device, int32_t *out);
 
+/* Label-sparse fitness.  Before the dense sweep, each
+ * block of 32 chromosomes is checked: if every chromosome in it needs at
+ * most theta * N(N-1)/2 pair updates (sum over clusters of n_s(n_s-1)/2),
+ * the block is evaluated from its clusters directly (counting sort by
+ * label, L2 gathers of C for the pairs inside each cluster) and skipped by
+ * the dense sweep.  The result is the same Eq. 5/6/8 value (within the
+ * parity tolerance; deterministic).  theta in [0, 1]; 0 = always dense,
+ * 1 = sparse whenever N <= 640.  Default 0.02.  During a GA run the check
+ * stops once a generation had no sparse block (the population only gets
+ * denser); pga_init / pga_set_population re-arm it.  Host only. */
+int pga_set_sparse_threshold(pga_ctx *ctx, double theta);
+
 /* ---------------------------------------------------------------------
  * Replicated master-slave across GPUs.  The paper's
  * own parallel model (§3.2): ONE population, fitness evaluated
@@ -348,14 +360,18 @@ int64_t pga_launch_count(void);
  * kernel start/end, generation end); level 2 records every phase boundary
  * (9 events, ~3 us of overhead per generation); 0 stops and clears.
  * pga_profile_read synchronises and returns the SUMS in milliseconds of the
- * fitness kernel (sweep_ms; fold_ms = 0, the fold is fused) and of whole
- * generations, and the number of generations recorded. */
+ * dense fitness kernel (sweep_ms: sweep + fused fold), of the label-sparse
+ * pre-pass (fold_ms; pga_set_sparse_threshold) and of whole generations, and
+ * the number of generations recorded.  pga_profile_sparse_blocks returns how
+ * many 32-chromosome blocks the pre-pass evaluated since profiling was
+ * enabled (the dense kernel skipped those). */
 int pga_profile_enable(pga_ctx *ctx, int32_t on);
 int pga_profile_read(pga_ctx *ctx, double *sweep_ms, double *fold_ms, double *gen_ms,
                      int32_t *count);
+int pga_profile_sparse_blocks(pga_ctx *ctx, int64_t *sparse_blocks);
 
 /* Level-2 profiling: per-phase AVERAGE milliseconds, ms[PGA_PROF_PHASES]:
- * 0 fitness sweep+fold kernel, 1 (fused, 0), 2 statistics/termination,
+ * 0 dense fitness kernel (sweep + fused fold), 1 label-sparse pre-pass, 2 statistics/termination,
  * 3 order sort, 4 scaling+selection, 5 mate pairing, 6 breed, 7 advance. */
 #define PGA_PROF_PHASES 8
 int pga_profile_phases(pga_ctx *ctx, double *ms, int32_t *count);

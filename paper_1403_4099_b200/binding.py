@@ -80,6 +80,8 @@ _SIGS = {
     "pga_op_init": (ct.c_int, [ct.c_uint64, ct.c_int32, ct.c_int64, ct.c_int64, ct.c_int32,
                                ct.c_int32, ct.c_void_p]),
     "pga_launch_count": (ct.c_int64, []),
+    "pga_set_sparse_threshold": (ct.c_int, [ct.c_void_p, ct.c_double]),
+    "pga_profile_sparse_blocks": (ct.c_int, [ct.c_void_p, ct.c_void_p]),
     "pga_rep_evaluate": (ct.c_int, [ct.c_void_p, ct.c_int64, ct.c_int64, ct.c_void_p, ct.c_void_p]),
     "pga_rep_commit": (ct.c_int, [ct.c_void_p, ct.c_void_p, ct.c_void_p]),
     "pga_stream_count": (ct.c_int, [ct.c_int32, ct.c_int32, ct.c_int32]),
@@ -230,7 +232,7 @@ def pga_profile_enable(ctx, on=True):
     _check(lib().pga_profile_enable(ctx, int(on)))
 
 
-PHASES = ["fitness", "fitness_fold_fused", "stats", "order_sort", "selection", "mates", "breed", "advance"]
+PHASES = ["fitness", "sparse_pass", "stats", "order_sort", "selection", "mates", "breed", "advance"]
 
 
 def pga_profile_phases(ctx):
@@ -325,6 +327,17 @@ def pga_op_init(seed: int, N: int, P: int, p_off: int = 0, island: int = 0, devi
     out = np.zeros((P, N), np.int32)
     _check(lib().pga_op_init(seed, N, P, p_off, island, device, _p(out)))
     return out
+
+
+def pga_profile_sparse_blocks(ctx) -> int:
+    v = ct.c_int64()
+    _check(lib().pga_profile_sparse_blocks(ctx, ct.byref(v)))
+    return v.value
+
+
+def pga_set_sparse_threshold(ctx, theta: float):
+    """theta: 0 = dense sweep only; 1 = label-sparse whenever N <= 640."""
+    _check(lib().pga_set_sparse_threshold(ctx, float(theta)))
 
 
 def pga_rep_evaluate(ctx, begin: int, end: int, L_dev, top_dev):

@@ -118,7 +118,7 @@ struct Graphs {
 void free_ctx(pga_ctx *c) {
     if (!c) return;
     cudaSetDevice(c->device);
-    void *ptrs[] = {c->C, c->diag, c->lgtab, c->pop[0], c->pop[1], c->popT[0], c->popT[1], c->V, c->L,
+    void *ptrs[] = {c->C, c->diag, c->lgtab, c->sflag, c->sp_live, c->sp_blocks, c->pop[0], c->pop[1], c->popT[0], c->popT[1], c->V, c->L,
                     c->top, c->keys_in, c->keys_out, c->idx_in, c->order, c->q, c->prefix,
                     c->sel, c->mkeys_in, c->mkeys_out, c->m_in, c->sigma, c->cub_tmp, c->st,
                     c->best_labels, c->history, c->stage_i32, c->evCM, c->evGM, c->evL,
@@ -149,6 +149,8 @@ int reset_state(pga_ctx *c, int32_t max_gens) {
     h.best_ever = -1.0;
     *c->h_st = h;
     PGA_CUDA(cudaMemcpyAsync(c->st, c->h_st, sizeof(DevState), cudaMemcpyHostToDevice, c->stream));
+    const int32_t live[3] = {1, 0, 0};   // re-arm the label-sparse check (f2) for a new population
+    PGA_CUDA(cudaMemcpyAsync(c->sp_live, live, sizeof(live), cudaMemcpyHostToDevice, c->stream));
     PGA_CUDA(cudaStreamSynchronize(c->stream));
     (void)max_gens;
     return PGA_OK;
@@ -346,6 +348,11 @@ int pga_create(const double *C, int32_t N, const pga_params *p, pga_ctx **out) {
     rc = rc ? rc : dalloc(&c->C, (size_t)N * c->ldc);
     rc = rc ? rc : dalloc(&c->diag, (size_t)N);
     rc = rc ? rc : dalloc(&c->lgtab, (size_t)2 * (N + 1));
+    rc = rc ? rc : dalloc(&c->sflag, (size_t)(c->Pcap / CB + 1));
+    rc = rc ? rc : dalloc(&c->sp_live, (size_t)3);
+    rc = rc ? rc : dalloc(&c->sp_blocks, (size_t)1);
+    if (!rc && cudaMemset(c->sp_blocks, 0, sizeof(unsigned long long)) != cudaSuccess)
+        rc = fail(PGA_EDEVICE, "memset sp_blocks");
     for (int b = 0; b < 2 && !rc; ++b) {
         rc = rc ? rc : dalloc(&c->pop[b], cm);
         rc = rc ? rc : dalloc(&c->popT[b], gm);
@@ -485,6 +492,13 @@ int pga_gen_evaluate(pga_ctx *c, int32_t *is_migration) {
     return phase_a(c, c->host_gen, is_migration);
 }
 
+int pga_set_sparse_threshold(pga_ctx *c, double theta) {
+    if (!c) return fail(PGA_EINVAL, "ctx is NULL");
+    if (!(theta >= 0.0 && theta <= 1.0)) return fail(PGA_EINVAL, "theta must lie in [0, 1]");
+    c->sparse_theta = theta;
+    return PGA_OK;
+}
+
 int pga_rep_evaluate(pga_ctx *c, int64_t begin, int64_t end, double *L_dev, uint16_t *top_dev) {
     if (!c || !L_dev || !top_dev) return fail(PGA_EINVAL, "NULL argument");
     if (c->p.n_islands != 1) return fail(PGA_ESTATE, "replicated mode needs n_islands = 1 (one population)");
@@ -618,6 +632,18 @@ int pga_profile_enable(pga_ctx *c, int32_t on) {
     c->prof = on != 0;
     c->prof_level = on;
     c->prof_used = 0;
+    PGA_CUDA(cudaSetDevice(c->device));
+    PGA_CUDA(cudaMemsetAsync(c->sp_blocks, 0, sizeof(unsigned long long), c->stream));
+    return PGA_OK;
+}
+
+int pga_profile_sparse_blocks(pga_ctx *c, int64_t *sparse_blocks) {
+    if (!c || !sparse_blocks) return fail(PGA_EINVAL, "NULL argument");
+    PGA_CUDA(cudaSetDevice(c->device));
+    unsigned long long v = 0;
+    PGA_CUDA(cudaMemcpyAsync(&v, c->sp_blocks, sizeof(v), cudaMemcpyDeviceToHost, c->stream));
+    PGA_CUDA(cudaStreamSynchronize(c->stream));
+    *sparse_blocks = (int64_t)v;
     return PGA_OK;
 }
 
@@ -625,18 +651,20 @@ int pga_profile_read(pga_ctx *c, double *sweep_ms, double *fold_ms, double *gen_
     if (!c) return fail(PGA_EINVAL, "ctx is NULL");
     PGA_CUDA(cudaSetDevice(c->device));
     PGA_CUDA(cudaStreamSynchronize(c->stream));
-    double s = 0, g = 0;
+    double s = 0, g = 0, f = 0;
     int32_t n = 0;
     for (size_t k = 0; k + PROF_EV <= c->prof_used; k += PROF_EV) {
-        float a = 0, d = 0;
-        PGA_CUDA(cudaEventElapsedTime(&a, c->prof_ev[k], c->prof_ev[k + 2]));
+        float a = 0, d = 0, sp = 0;
+        PGA_CUDA(cudaEventElapsedTime(&sp, c->prof_ev[k], c->prof_ev[k + 1]));
+        PGA_CUDA(cudaEventElapsedTime(&a, c->prof_ev[k + 1], c->prof_ev[k + 2]));
         PGA_CUDA(cudaEventElapsedTime(&d, c->prof_ev[k], c->prof_ev[k + 8]));
         s += a;
+        f += sp;
         g += d;
         ++n;
     }
     if (sweep_ms) *sweep_ms = s;
-    if (fold_ms) *fold_ms = 0.0;   // the fold is fused into the fitness kernel
+    if (fold_ms) *fold_ms = f;     // label-sparse pre-pass (the fold is fused into k_fitness)
     if (gen_ms) *gen_ms = g;
     if (count) *count = n;
     return PGA_OK;
@@ -651,9 +679,9 @@ int pga_profile_phases(pga_ctx *c, double *ms, int32_t *count) {
     int32_t n = 0;
     for (size_t k = 0; k + PROF_EV <= c->prof_used; k += PROF_EV) {
         for (int j = 0; j < PGA_PROF_PHASES; ++j) {
-            if (j == 1) continue;                       // fused: no separate fold mark
+            // phase 0: dense k_fitness (marks 1..2), phase 1: label-sparse pre-pass (0..1)
             float t = 0;
-            const int a0 = (j == 0) ? 0 : j, a1 = (j == 0) ? 2 : j + 1;
+            const int a0 = (j == 0) ? 1 : (j == 1) ? 0 : j, a1 = (j == 0) ? 2 : (j == 1) ? 1 : j + 1;
             PGA_CUDA(cudaEventElapsedTime(&t, c->prof_ev[k + a0], c->prof_ev[k + a1]));
             acc[j] += t;
         }

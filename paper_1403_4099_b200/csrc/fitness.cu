@@ -133,6 +133,7 @@ struct FitArgs {
     int cb0;                        // first chromosome block (shard offset / 32)
     double fx_scale, fx_inv;        // fold fixed point: 2^S and 2^-S
     const double *lgn, *lgnn;       // log n, log(n^2 - n), n = 0..N (Q30)
+    const uint8_t *sflag;           // per chromosome block: 1 = already evaluated label-sparsely
     int64_t P, Pcap;
     const double *diag;
     double *V;                      // [Pcap][ldn]: V[p][i] = C_ii + 2 r'_i
@@ -166,6 +167,65 @@ __device__ __forceinline__ void pairs16(uint32_t caddr, uint32_t w, const uint32
     const uint32_t col = w | (w << 16);
 #pragma unroll
     for (int q = 0; q < WR / 2; ++q) pair2(caddr + 16 * q, rp[q], col, acc[2 * q], acc[2 * q + 1]);
+}
+
+// Eq. 8 (Q1-Q3) of one chromosome from its per-label tables (warp-wide):
+// cs[k] = c_k in 64-bit fixed point (scale 2^S, read through inv_scale),
+// ns[k] = n_k, labels k < K.  Clusters with n >= 2 and c > n (the only
+// non-zero summands, Q2) are compacted to the front of cs/ns in label order
+// (ns keeps n | label << 16), then the summands are taken lane-parallel as
+// (log n - log c) + (n-1)(log(n^2-n) - log(n^2-c)) with the integer logs from
+// the table (Q30: no divisions), c clamped to n^2 - 1e-9 (Q3); L = half the
+// sum; top = label of the largest summand (smallest label on ties).
+__device__ __forceinline__ void eq8_tables(double *cs, int32_t *ns, int K, int lane, double inv_scale,
+                                           const double *__restrict__ lgn, const double *__restrict__ lgnn,
+                                           double *L_out, uint16_t *top_out) {
+    int M = 0;
+    for (int k0 = 0; k0 < K; k0 += 32) {
+        const int k = k0 + lane;
+        int n = 0;
+        double c = 0.0;
+        if (k < K) {
+            n = ns[k];
+            c = (double)reinterpret_cast<const long long *>(cs)[k] * inv_scale;
+        }
+        const bool act = (n >= 2) && (c > (double)n);
+        const unsigned bal = __ballot_sync(0xFFFFFFFFu, act);   // orders this chunk's reads before its writes
+        if (act) {
+            const int idx = M + __popc(bal & lanemask_lt());
+            cs[idx] = c;
+            ns[idx] = n | (k << 16);
+        }
+        M += __popc(bal);
+    }
+    double fsum = 0.0, fbest = 0.0;
+    int kbest = 0x7FFFFFFF;
+    for (int j = lane; j < M; j += 32) {
+        const int nk = ns[j];
+        const int n = nk & 0xFFFF;
+        const double nd = (double)n, n2 = nd * nd;
+        const double ch = fmin(cs[j], n2 - 1e-9);
+        const double f = (__ldg(lgn + n) - log(ch)) + (nd - 1.0) * (__ldg(lgnn + n) - log(n2 - ch));
+        fsum += f;
+        if (f > fbest) {
+            fbest = f;
+            kbest = nk >> 16;
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        fsum += __shfl_xor_sync(0xFFFFFFFFu, fsum, off);
+        const double of = __shfl_xor_sync(0xFFFFFFFFu, fbest, off);
+        const int ok = __shfl_xor_sync(0xFFFFFFFFu, kbest, off);
+        if (of > fbest || (of == fbest && ok < kbest)) {
+            fbest = of;
+            kbest = ok;
+        }
+    }
+    if (lane == 0) {
+        *L_out = 0.5 * fsum;
+        if (top_out) *top_out = (fbest > 0.0) ? (uint16_t)kbest : (uint16_t)0xFFFF;
+    }
 }
 
 // Fold (warp-wide) of NC chromosomes at once (independent chains -> ILP):
@@ -225,60 +285,8 @@ __device__ __forceinline__ void fold_multi(const uint16_t *const (&lab)[NC], con
     for (int off = 16; off > 0; off >>= 1) kmax = max(kmax, __shfl_xor_sync(0xFFFFFFFFu, kmax, off));
     const int K = (int)min(kmax + 1u, (uint32_t)N);
 #pragma unroll
-    for (int q = 0; q < NC; ++q) {
-        // compact the clusters with n_s >= 2 and c_s > n_s (the only ones with
-        // a non-zero Eq. 8 summand, Q2) to the front of cs/ns, in label order,
-        // so the logs below run on dense lanes; ns keeps n | label << 16.
-        int M = 0;
-        for (int k0 = 0; k0 < K; k0 += 32) {
-            const int k = k0 + lane;
-            int n = 0;
-            double c = 0.0;
-            if (k < K) {
-                n = ns[q][k];
-                c = (double)reinterpret_cast<const long long *>(cs[q])[k] * inv_scale;
-            }
-            const bool act = (n >= 2) && (c > (double)n);
-            const unsigned bal = __ballot_sync(0xFFFFFFFFu, act);   // orders this chunk's reads before its writes
-            if (act) {
-                const int idx = M + __popc(bal & lanemask_lt());
-                cs[q][idx] = c;
-                ns[q][idx] = n | (k << 16);
-            }
-            M += __popc(bal);
-        }
-        double fsum = 0.0, fbest = 0.0;
-        int kbest = 0x7FFFFFFF;
-        for (int j = lane; j < M; j += 32) {
-            // Eq. 8 summand of a compacted cluster (n >= 2, c > n; Q2, Q3),
-            // (log n - log c) + (n-1)(log(n^2-n) - log(n^2-c)) with the integer
-            // logs from the table (Q30: no divisions)
-            const int nk = ns[q][j];
-            const int n = nk & 0xFFFF;
-            const double nd = (double)n, n2 = nd * nd;
-            const double ch = fmin(cs[q][j], n2 - 1e-9);
-            const double f = (__ldg(lgn + n) - log(ch)) + (nd - 1.0) * (__ldg(lgnn + n) - log(n2 - ch));
-            fsum += f;
-            if (f > fbest) {
-                fbest = f;
-                kbest = nk >> 16;
-            }
-        }
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            fsum += __shfl_xor_sync(0xFFFFFFFFu, fsum, off);
-            const double of = __shfl_xor_sync(0xFFFFFFFFu, fbest, off);
-            const int ok = __shfl_xor_sync(0xFFFFFFFFu, kbest, off);
-            if (of > fbest || (of == fbest && ok < kbest)) {
-                fbest = of;
-                kbest = ok;
-            }
-        }
-        if (lane == 0) {
-            *L_out[q] = 0.5 * fsum;
-            if (top_out[q]) *top_out[q] = (fbest > 0.0) ? (uint16_t)kbest : (uint16_t)0xFFFF;
-        }
-    }
+    for (int q = 0; q < NC; ++q)
+        eq8_tables(cs[q], ns[q], K, lane, inv_scale, lgn, lgnn, L_out[q], top_out[q]);
     __syncwarp();
 }
 
@@ -286,6 +294,7 @@ __global__ void __launch_bounds__(FIT_THREADS)
 k_fitness(const __grid_constant__ CUtensorMap tmLab0, const __grid_constant__ CUtensorMap tmLab1,
           const __grid_constant__ CUtensorMap tmC, FitArgs a) {
     if (a.done && *a.done) return;
+    if (a.sflag && a.sflag[a.cb0 + (int)(blockIdx.x / a.nRT)]) return;   // done by k_fitness_sparse
     const int par = (a.gen && (*a.gen & 1)) ? 1 : 0;
     const CUtensorMap *tmLab = par ? &tmLab1 : &tmLab0;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -454,6 +463,213 @@ k_fitness(const __grid_constant__ CUtensorMap tmLab0, const __grid_constant__ CU
     if (tid == 0) a.counters[cb] = 0u;
 }
 
+// ---------------------------------------------------------------------------
+// k_fitness_sparse: label-sparse evaluation of a
+// 32-chromosome block when its clusters are small.  Pass 1 (warp per
+// chromosome, 4 per warp): n_s by shared-memory atomics on packed 16-bit
+// counters; the block's largest sum_s n_s (n_s - 1) / 2.  If that is at most
+// the threshold, pass 2 evaluates every chromosome exactly from its clusters:
+// a counting sort by label, then each member g at position a of its cluster
+// (size n) adds C[g][member (a + d) mod n] for d = 1 .. floor((n-1)/2) (and
+// d = n/2 for the first n/2 members when n is even) -- every unordered pair
+// exactly once -- gathered from L2; c_s = sum of C_gg + 2 sum of pairs in
+// 64-bit fixed point (each term rounded to 2^-S, then integer sums: exact,
+// order-free, deterministic); Eq. 8 from the tables.  The block is then
+// flagged so that k_fitness skips it.  Work ~ sum_s n_s^2 instead of N^2.
+// ---------------------------------------------------------------------------
+constexpr int SP_W = 8, SP_T = SP_W * 32;
+constexpr int SPARSE_MAXN = 640;   // shared-memory footprint (sparse_smem) must fit one CTA
+
+struct SparseArgs {
+    const uint16_t *cm0, *cm1;
+    const double *C;
+    int ldc, N, ldn;
+    int64_t P;
+    int cb0;
+    const double *diag;
+    double *L;
+    uint16_t *top;
+    const int32_t *gen, *done;
+    uint8_t *sflag;
+    uint32_t max_pairs;           // sparse iff every chromosome needs <= max_pairs pair updates
+    int32_t *live;                // GA hysteresis [0]: any block went sparse last launch, [1] any now, [2] CTA count; null = always check
+    unsigned long long *nsparse;  // count of blocks evaluated here (profiling)
+    int nblocks;
+    double fx_scale, fx_inv;
+    const double *lgn, *lgnn;
+};
+
+__host__ __device__ __forceinline__ int sp_words(int N) { return (N + 2) / 2; }   // packed u16 counters for labels 0..N
+
+__host__ __device__ __forceinline__ size_t sp_per_warp(int N) {
+    return (((size_t)N * 8 /*T*/ + (size_t)N * 4 /*ns*/ + (size_t)sp_words(N) * 4 /*cnt*/ +
+             (size_t)sp_words(N) * 4 /*run*/ + (size_t)(N + 1) * 2 /*off*/ + (size_t)N * 2 /*perm*/ + 64) + 15) &
+           ~(size_t)15;
+}
+
+static size_t sparse_smem(int N) { return (size_t)SP_W * sp_per_warp(N) + 64; }
+
+__global__ void __launch_bounds__(SP_T) k_fitness_sparse(SparseArgs a) {
+    if (a.done && *a.done) return;
+    extern __shared__ __align__(16) unsigned char sps[];
+    __shared__ uint32_t s_maxp;
+    __shared__ int s_kmax[pga::CB];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int N = a.N, W = sp_words(N);
+    const int cb = a.cb0 + blockIdx.x;
+    const int par = (a.gen && (*a.gen & 1)) ? 1 : 0;
+    const uint16_t *CM = par ? a.cm1 : a.cm0;
+    unsigned char *wb = sps + (size_t)warp * sp_per_warp(N);
+    long long *T = reinterpret_cast<long long *>(wb);                    // [N] fixed-point c
+    int32_t *ns = reinterpret_cast<int32_t *>(T + N);                    // [N]
+    uint32_t *cq = reinterpret_cast<uint32_t *>(ns + N);                 // [W] packed counts
+    uint32_t *run = cq + W;                                              // [W] packed scatter counters
+    uint16_t *off = reinterpret_cast<uint16_t *>(run + W);              // [N+1]
+    uint16_t *perm = off + (N + 1);                                      // [N]
+    if (a.live && a.live[0] == 0) {     // the population went dense: skip (flags cleared)
+        if (tid == 0) a.sflag[cb] = 0;
+        return;
+    }
+    if (tid == 0) s_maxp = 0u;
+    __syncthreads();
+
+    // ---- pass 1: cluster sizes and pair counts
+    for (int q = warp; q < pga::CB; q += SP_W) {
+        const int64_t p = (int64_t)cb * pga::CB + q;
+        for (int k = lane; k < W; k += 32) cq[k] = 0u;
+        __syncwarp();
+        uint32_t kmax = 0;
+        if (p < a.P)
+            for (int i = lane; i < N; i += 32) {
+                const uint32_t s = CM[p * a.ldn + i];
+                kmax = max(kmax, s);
+                atomicAdd(cq + (s >> 1), 1u << (16 * (s & 1u)));
+            }
+        __syncwarp();
+        uint32_t pairs = 0;
+        for (int k = lane; k < W; k += 32) {
+            const uint32_t w2 = cq[k], n0 = w2 & 0xFFFFu, n1 = w2 >> 16;
+            pairs += n0 * (n0 - (n0 > 0)) / 2 + n1 * (n1 - (n1 > 0)) / 2;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            pairs += __shfl_xor_sync(0xFFFFFFFFu, pairs, o);
+            kmax = max(kmax, __shfl_xor_sync(0xFFFFFFFFu, kmax, o));
+        }
+        if (lane == 0) {
+            atomicMax(&s_maxp, pairs);
+            s_kmax[q] = (int)kmax;
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+    const bool sparse = s_maxp <= a.max_pairs;
+    if (tid == 0) {
+        a.sflag[cb] = sparse ? 1 : 0;
+        if (sparse && a.nsparse) atomicAdd(a.nsparse, 1ull);
+        if (a.live) {                    // last CTA of the launch: keep checking next time iff any block was sparse
+            if (sparse) atomicOr(&a.live[1], 1);
+            __threadfence();
+            if (atomicAdd(&a.live[2], 1) == a.nblocks - 1) {
+                a.live[0] = atomicExch(&a.live[1], 0);
+                a.live[2] = 0;
+            }
+        }
+    }
+    if (!sparse) return;
+
+    // ---- pass 2: exact label-sparse evaluation
+    const double *C = a.C;
+    for (int q = warp; q < pga::CB; q += SP_W) {
+        const int64_t p = (int64_t)cb * pga::CB + q;
+        if (p >= a.P) break;
+        const int K = min(s_kmax[q] + 1, N);
+        // counts again (pass 1 kept only the pair totals)
+        for (int k = lane; k < W; k += 32) cq[k] = 0u;
+        __syncwarp();
+        for (int i = lane; i < N; i += 32) {
+            const uint32_t s = CM[p * a.ldn + i];
+            atomicAdd(cq + (s >> 1), 1u << (16 * (s & 1u)));
+        }
+        __syncwarp();
+        // offsets: exclusive prefix of the counts over labels 0..K-1
+        int base = 0;
+        for (int k0 = 0; k0 < K; k0 += 32) {
+            const int k = k0 + lane;
+            const int n = k < K ? (int)((cq[k >> 1] >> (16 * (k & 1))) & 0xFFFFu) : 0;
+            int incl = n;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                if (lane >= o) incl += t;
+            }
+            if (k < K) {
+                off[k] = (uint16_t)(base + incl - n);
+                ns[k] = n;
+                T[k] = 0;
+            }
+            base += __shfl_sync(0xFFFFFFFFu, incl, 31);
+        }
+        for (int k = lane; k < W; k += 32) run[k] = 0u;
+        __syncwarp();
+        // counting sort of the genes by label (order within a label is free:
+        // the sums below are order-independent)
+        const uint16_t *lab = CM + p * a.ldn;
+        for (int i = lane; i < N; i += 32) {
+            const uint32_t s = lab[i];
+            const uint32_t sh = 16 * (s & 1u);
+            const uint32_t old = (atomicAdd(run + (s >> 1), 1u << sh) >> sh) & 0xFFFFu;
+            perm[off[s] + old] = (uint16_t)i;
+        }
+        __syncwarp();
+        // circulant half pairs of every cluster, members in perm order (so a
+        // cluster's members sit on consecutive lanes: the lanes of one
+        // cluster pre-reduce their integer sums before one shared atomic)
+        for (int t0 = 0; t0 < N; t0 += 32) {
+            const int t = t0 + lane;
+            int s = -1;
+            long long acc = 0;
+            if (t < N) {
+                const int g = perm[t];
+                s = lab[g];
+                const int n = ns[s];
+                if (n >= 2) {
+                    const int st = off[s], av = t - st;
+                    const double *Cg = C + (size_t)g * a.ldc;
+                    acc = __double2ll_rn(__ldg(a.diag + g) * a.fx_scale);
+                    const int h = (n - 1) >> 1;
+                    int bidx = av;
+#pragma unroll 4
+                    for (int d = 1; d <= h; ++d) {
+                        bidx = (bidx + 1 == n) ? 0 : bidx + 1;
+                        acc += 2 * __double2ll_rn(__ldg(Cg + perm[st + bidx]) * a.fx_scale);
+                    }
+                    if (!(n & 1) && av < (n >> 1))
+                        acc += 2 * __double2ll_rn(__ldg(Cg + perm[st + av + (n >> 1)]) * a.fx_scale);
+                } else {
+                    s = -1;
+                }
+            }
+            // segmented sum over runs of equal s (contiguous lanes)
+            const int sprev = __shfl_up_sync(0xFFFFFFFFu, s, 1);
+            const bool head = lane == 0 || sprev != s;
+            const unsigned heads = __ballot_sync(0xFFFFFFFFu, head);
+            // after step o, acc = sum over [lane, min(lane + 2o - 1, end of my run)]
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const long long v = __shfl_down_sync(0xFFFFFFFFu, acc, o);
+                const unsigned span = (unsigned)((((1ull << o) - 1ull) << (lane + 1)) & 0xFFFFFFFFull);  // lanes lane+1..lane+o
+                if (lane + o < 32 && (heads & span) == 0u) acc += v;
+            }
+            if (head && s >= 0) atomicAdd(reinterpret_cast<unsigned long long *>(T) + s, (unsigned long long)acc);
+        }
+        __syncwarp();
+        eq8_tables(reinterpret_cast<double *>(T), ns, K, lane, a.fx_inv, a.lgn, a.lgnn, &a.L[p],
+                   a.top ? &a.top[p] : nullptr);
+        __syncwarp();
+    }
+}
+
 }  // namespace
 
 namespace pga {
@@ -535,6 +751,9 @@ size_t fitness_smem(int N) {
 int prepare_fitness(int N) {
     PGA_CUDA(cudaFuncSetAttribute(k_fitness, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)fitness_smem(N)));
+    if (N <= SPARSE_MAXN)
+        PGA_CUDA(cudaFuncSetAttribute(k_fitness_sparse, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)sparse_smem(N)));
     return PGA_OK;
 }
 
@@ -579,6 +798,38 @@ int launch_fitness_range(pga_ctx *c, const FitBufs &b, int64_t begin, int64_t en
     a.done = b.done;
     a.counters = c->counters;
     if (ev) PGA_CUDA(cudaEventRecord(ev[0], s));
+    a.sflag = nullptr;
+    if (c->sparse_theta > 0.0 && N <= SPARSE_MAXN && c->sflag) {
+        // label-sparse pass first (f2); it flags the blocks it evaluated
+        SparseArgs sp;
+        sp.cm0 = b.cm0;
+        sp.cm1 = b.cm1;
+        sp.C = c->C;
+        sp.ldc = c->ldc;
+        sp.N = N;
+        sp.ldn = c->ldn;
+        sp.P = P;
+        sp.cb0 = a.cb0;
+        sp.diag = c->diag;
+        sp.L = L;
+        sp.top = top;
+        sp.gen = b.gen;
+        sp.done = b.done;
+        sp.sflag = c->sflag;
+        const double dense = 0.5 * (double)N * (double)(N - 1);
+        sp.max_pairs = (uint32_t)fmin(4.0e9, floor(c->sparse_theta * dense));
+        sp.live = b.gen ? c->sp_live : nullptr;     // hysteresis for GA generations only
+        sp.nblocks = a.nCB;
+        sp.nsparse = c->sp_blocks;
+        sp.fx_scale = a.fx_scale;
+        sp.fx_inv = a.fx_inv;
+        sp.lgn = a.lgn;
+        sp.lgnn = a.lgnn;
+        k_fitness_sparse<<<(unsigned)a.nCB, SP_T, sparse_smem(N), s>>>(sp);
+        PGA_LAUNCHED();
+        a.sflag = c->sflag;
+    }
+    if (ev) PGA_CUDA(cudaEventRecord(ev[1], s));   // dense kernel starts here
     k_fitness<<<(unsigned)(a.nRT * a.nCB), FIT_THREADS, fitness_smem(N), s>>>(*b.tm0, *b.tm1, c->tmC, a);
     PGA_LAUNCHED();
     if (ev) PGA_CUDA(cudaEventRecord(ev[2], s));   // sweep and fold are one fused kernel
