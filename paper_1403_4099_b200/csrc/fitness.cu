@@ -501,9 +501,11 @@ struct SparseArgs {
 
 __host__ __device__ __forceinline__ int sp_words(int N) { return (N + 2) / 2; }   // packed u16 counters for labels 0..N
 
+constexpr int SPQ = 64;   // per-warp queue of completed clusters awaiting their Eq. 8 summand
+
 __host__ __device__ __forceinline__ size_t sp_per_warp(int N) {
-    return (((size_t)N * 8 /*T*/ + (size_t)N * 4 /*ns*/ + (size_t)sp_words(N) * 4 /*cnt*/ +
-             (size_t)sp_words(N) * 4 /*run*/ + (size_t)(N + 1) * 2 /*off*/ + (size_t)N * 2 /*perm*/ + 64) + 15) &
+    return (((size_t)sp_words(N) * 4 /*cnt*/ + (size_t)sp_words(N) * 4 /*run*/ + (size_t)(N + 1) * 2 /*off*/ +
+             (size_t)N * 2 /*perm*/ + (size_t)N * 2 /*labels*/ + (size_t)SPQ * 12 /*queue*/ + 64) + 15) &
            ~(size_t)15;
 }
 
@@ -520,12 +522,13 @@ __global__ void __launch_bounds__(SP_T) k_fitness_sparse(SparseArgs a) {
     const int par = (a.gen && (*a.gen & 1)) ? 1 : 0;
     const uint16_t *CM = par ? a.cm1 : a.cm0;
     unsigned char *wb = sps + (size_t)warp * sp_per_warp(N);
-    long long *T = reinterpret_cast<long long *>(wb);                    // [N] fixed-point c
-    int32_t *ns = reinterpret_cast<int32_t *>(T + N);                    // [N]
-    uint32_t *cq = reinterpret_cast<uint32_t *>(ns + N);                 // [W] packed counts
+    double *qc = reinterpret_cast<double *>(wb);                         // [SPQ] queued c
+    uint32_t *qnk = reinterpret_cast<uint32_t *>(qc + SPQ);             // [SPQ] queued n | label << 16
+    uint32_t *cq = qnk + SPQ;                                            // [W] packed counts
     uint32_t *run = cq + W;                                              // [W] packed scatter counters
     uint16_t *off = reinterpret_cast<uint16_t *>(run + W);              // [N+1]
     uint16_t *perm = off + (N + 1);                                      // [N]
+    uint16_t *labs = perm + N;                                           // [N]
     if (a.live && a.live[0] == 0) {     // the population went dense: skip (flags cleared)
         if (tid == 0) a.sflag[cb] = 0;
         return;
@@ -584,11 +587,17 @@ __global__ void __launch_bounds__(SP_T) k_fitness_sparse(SparseArgs a) {
         const int64_t p = (int64_t)cb * pga::CB + q;
         if (p >= a.P) break;
         const int K = min(s_kmax[q] + 1, N);
-        // counts again (pass 1 kept only the pair totals)
-        for (int k = lane; k < W; k += 32) cq[k] = 0u;
+        // counts again (pass 1 kept only the pair totals); labels to shared memory
+        for (int k = lane; k < W; k += 32) {
+            cq[k] = 0u;
+            run[k] = 0u;
+        }
         __syncwarp();
+        const uint16_t *lab = CM + p * a.ldn;
+#pragma unroll 4
         for (int i = lane; i < N; i += 32) {
-            const uint32_t s = CM[p * a.ldn + i];
+            const uint32_t s = lab[i];
+            labs[i] = (uint16_t)s;
             atomicAdd(cq + (s >> 1), 1u << (16 * (s & 1u)));
         }
         __syncwarp();
@@ -603,36 +612,36 @@ __global__ void __launch_bounds__(SP_T) k_fitness_sparse(SparseArgs a) {
                 const int t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
                 if (lane >= o) incl += t;
             }
-            if (k < K) {
-                off[k] = (uint16_t)(base + incl - n);
-                ns[k] = n;
-                T[k] = 0;
-            }
+            if (k < K) off[k] = (uint16_t)(base + incl - n);
             base += __shfl_sync(0xFFFFFFFFu, incl, 31);
         }
-        for (int k = lane; k < W; k += 32) run[k] = 0u;
         __syncwarp();
-        // counting sort of the genes by label (order within a label is free:
-        // the sums below are order-independent)
-        const uint16_t *lab = CM + p * a.ldn;
+        // counting sort of the genes by label: clusters become contiguous runs
+        // in label order (order inside a cluster is free: sums are exact)
+#pragma unroll 4
         for (int i = lane; i < N; i += 32) {
-            const uint32_t s = lab[i];
+            const uint32_t s = labs[i];
             const uint32_t sh = 16 * (s & 1u);
             const uint32_t old = (atomicAdd(run + (s >> 1), 1u << sh) >> sh) & 0xFFFFu;
             perm[off[s] + old] = (uint16_t)i;
         }
         __syncwarp();
-        // circulant half pairs of every cluster, members in perm order (so a
-        // cluster's members sit on consecutive lanes: the lanes of one
-        // cluster pre-reduce their integer sums before one shared atomic)
+        // walk the sorted genes 32 at a time; lanes of one cluster are
+        // consecutive: a segmented sum gives each run's share of c_s, a carry
+        // links clusters that span passes, and every completed cluster with
+        // n >= 2 and c > n (Q2) is queued for its Eq. 8 summand
+        int carry_s = -1, qcnt = 0;
+        long long carry = 0;
+        double fsum = 0.0, fbest = 0.0;
+        int kbest = 0x7FFFFFFF;
         for (int t0 = 0; t0 < N; t0 += 32) {
             const int t = t0 + lane;
-            int s = -1;
+            int s = -1, n = 0;
             long long acc = 0;
             if (t < N) {
                 const int g = perm[t];
-                s = lab[g];
-                const int n = ns[s];
+                s = labs[g];
+                n = (int)((cq[s >> 1] >> (16 * (s & 1))) & 0xFFFFu);
                 if (n >= 2) {
                     const int st = off[s], av = t - st;
                     const double *Cg = C + (size_t)g * a.ldc;
@@ -650,22 +659,85 @@ __global__ void __launch_bounds__(SP_T) k_fitness_sparse(SparseArgs a) {
                     s = -1;
                 }
             }
-            // segmented sum over runs of equal s (contiguous lanes)
             const int sprev = __shfl_up_sync(0xFFFFFFFFu, s, 1);
             const bool head = lane == 0 || sprev != s;
             const unsigned heads = __ballot_sync(0xFFFFFFFFu, head);
-            // after step o, acc = sum over [lane, min(lane + 2o - 1, end of my run)]
+            // after step o: acc = sum over [lane, min(lane + 2o - 1, end of my run)]
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const long long v = __shfl_down_sync(0xFFFFFFFFu, acc, o);
-                const unsigned span = (unsigned)((((1ull << o) - 1ull) << (lane + 1)) & 0xFFFFFFFFull);  // lanes lane+1..lane+o
+                const unsigned span = (unsigned)((((1ull << o) - 1ull) << (lane + 1)) & 0xFFFFFFFFull);
                 if (lane + o < 32 && (heads & span) == 0u) acc += v;
             }
-            if (head && s >= 0) atomicAdd(reinterpret_cast<unsigned long long *>(T) + s, (unsigned long long)acc);
+            if (lane == 0 && s == carry_s && s >= 0) acc += carry;         // continues from the last pass
+            const int lastHead = 31 - __clz(heads);
+            const int sL = __shfl_sync(0xFFFFFFFFu, s, lastHead);
+            const long long accL = __shfl_sync(0xFFFFFFFFu, acc, lastHead);
+            const int nL = __shfl_sync(0xFFFFFFFFu, n, lastHead);
+            const bool openL = sL >= 0 && (int)off[sL] + nL > t0 + 32;    // last cluster goes on
+            // completed clusters of this pass -> queue (label order)
+            double c = 0.0;
+            bool push = false;
+            if (head && s >= 0 && !(openL && lane == lastHead)) {
+                c = (double)acc * a.fx_inv;
+                push = c > (double)n;
+            }
+            const unsigned bal = __ballot_sync(0xFFFFFFFFu, push);
+            if (push) {
+                const int pos = qcnt + __popc(bal & lanemask_lt());
+                qc[pos] = c;
+                qnk[pos] = (uint32_t)n | ((uint32_t)s << 16);
+            }
+            qcnt += __popc(bal);
+            carry_s = openL ? sL : -1;
+            carry = accL;
+            __syncwarp();
+            if (qcnt >= 32) {            // a full batch of Eq. 8 summands, lane-parallel
+                const uint32_t nk = qnk[lane];
+                const int nn = (int)(nk & 0xFFFFu);
+                const double nd = (double)nn, n2 = nd * nd;
+                const double ch = fmin(qc[lane], n2 - 1e-9);
+                const double f = (__ldg(a.lgn + nn) - log(ch)) + (nd - 1.0) * (__ldg(a.lgnn + nn) - log(n2 - ch));
+                fsum += f;
+                if (f > fbest) {
+                    fbest = f;
+                    kbest = (int)(nk >> 16);
+                }
+                __syncwarp();
+                if (lane < qcnt - 32) {
+                    qc[lane] = qc[lane + 32];
+                    qnk[lane] = qnk[lane + 32];
+                }
+                qcnt -= 32;
+                __syncwarp();
+            }
         }
-        __syncwarp();
-        eq8_tables(reinterpret_cast<double *>(T), ns, K, lane, a.fx_inv, a.lgn, a.lgnn, &a.L[p],
-                   a.top ? &a.top[p] : nullptr);
+        if (lane < qcnt) {
+            const uint32_t nk = qnk[lane];
+            const int nn = (int)(nk & 0xFFFFu);
+            const double nd = (double)nn, n2 = nd * nd;
+            const double ch = fmin(qc[lane], n2 - 1e-9);
+            const double f = (__ldg(a.lgn + nn) - log(ch)) + (nd - 1.0) * (__ldg(a.lgnn + nn) - log(n2 - ch));
+            fsum += f;
+            if (f > fbest) {
+                fbest = f;
+                kbest = (int)(nk >> 16);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            fsum += __shfl_xor_sync(0xFFFFFFFFu, fsum, o);
+            const double of = __shfl_xor_sync(0xFFFFFFFFu, fbest, o);
+            const int ok = __shfl_xor_sync(0xFFFFFFFFu, kbest, o);
+            if (of > fbest || (of == fbest && ok < kbest)) {
+                fbest = of;
+                kbest = ok;
+            }
+        }
+        if (lane == 0) {
+            a.L[p] = 0.5 * fsum;
+            if (a.top) a.top[p] = (fbest > 0.0) ? (uint16_t)kbest : (uint16_t)0xFFFF;
+        }
         __syncwarp();
     }
 }
