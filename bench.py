@@ -210,6 +210,9 @@ def main():
                     help="multi-GPU model: islands (population sharded, elite migration; default) or "
                          "replicated master-slave (one population, fitness sharded, L all-gathered; "
                          "SURVEY §8(f) f3)")
+    ap.add_argument("--sparse-theta", type=float, default=None,
+                    help="label-sparse threshold (pga_set_sparse_threshold; default: the library's 0.02; "
+                         "0 = dense sweep only, used to profile the dense kernel)")
     ap.add_argument("--stream", action="store_true",
                     help="F1 only: each step also computes the 1760 windows on the device from one "
                          "return stream (EWMA lambda=0.98 + RMT cleaning, SURVEY §8(f) f4)")
@@ -254,6 +257,8 @@ def main():
     else:
         eng = GpuIsland(C, params)
         runner = IslandRunner(eng)
+    if args.sparse_theta is not None:
+        pga.pga_set_sparse_threshold(eng.ctx, args.sparse_theta)
     eng.init(SEED)
     stream = eng.stream
     for _ in range(W):
@@ -326,7 +331,7 @@ def main():
     e2e = None
     if not args.no_e2e and not replicated:
         eng.close()
-        e2e = e2e_run(pga, torch, dist, C, params, world, min(K, 200), planted)
+        e2e = e2e_run(pga, torch, dist, C, params, world, K, planted, args.sparse_theta)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -372,6 +377,9 @@ def main():
                          "peak": peak, "unit": "pair-updates/s", "frac": achieved / peak,
                          "traffic": traffic,
                          "algorithmic_bytes": dense_blocks / float(ngen) * 32 * (N * 2 + 8 + 2),
+                         "traffic_basis": "ncu dram bytes of one fully dense launch (label-sparse pass off): "
+                                          "compare with algorithmic_bytes_dense_launch",
+                         "algorithmic_bytes_dense_launch": P_eval * (N * 2 + 8 + 2),
                          "traffic_note": "ncu dram bytes of one launch: labels are read twice (gene-major "
                                          "by the sweep's TMA, chromosome-major by the fused fold); the "
                                          "fold scratch V is discarded from L2 after use (no write-back)",
@@ -617,7 +625,7 @@ def bench_f1(args):
     return 0
 
 
-def e2e_run(pga, torch, dist, C, params, world, K, planted):
+def e2e_run(pga, torch, dist, C, params, world, K, planted, theta=None):
     """Same metric through the public API with HOST buffers: C copied from
     pinned host memory (pga_create), K generations, and every step a
     device->host read of the step's result (best L, mean L, best labels)."""
@@ -630,7 +638,9 @@ def e2e_run(pga, torch, dist, C, params, world, K, planted):
     t0 = time.perf_counter()
     eng = GpuIsland(Cp.numpy(), params)
     runner = IslandRunner(eng)
-    eng.init(SEED + 1)
+    if theta is not None:
+        pga.pga_set_sparse_threshold(eng.ctx, theta)
+    eng.init(SEED)
     for _ in range(K):
         runner.step()
         st = eng.state()                 # D2H of the step's result (syncs)

@@ -44,7 +44,7 @@ if os.path.exists(f1csv):
 # 2. full-set metrics of the captured kernels
 kern_rows = []
 hdr = units = None
-for repname in ("prof_full.ncu-rep", "prof_f1.ncu-rep"):
+for repname in ("prof_full.ncu-rep", "prof_sparse.ncu-rep", "prof_f1.ncu-rep"):
     rep = os.path.join(gdir, repname)
     if not os.path.exists(rep):
         continue
