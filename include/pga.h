@@ -232,7 +232,7 @@ int pga_op_init(uint64_t seed, int32_t N, int64_t P, int64_t p_off, int32_t isla
  * label, L2 gathers of C for the pairs inside each cluster) and skipped by
  * the dense sweep.  The result is the same Eq. 5/6/8 value (within the
  * parity tolerance; deterministic).  theta in [0, 1]; 0 = always dense,
- * 1 = sparse whenever N <= 640.  Default 0.02.  During a GA run the check
+ * 1 = sparse whenever N <= 640.  Default 0.04.  During a GA run the check
  * stops once a generation had no sparse block (the population only gets
  * denser); pga_init / pga_set_population re-arm it.  Host only. */
 int pga_set_sparse_threshold(pga_ctx *ctx, double theta);

@@ -560,7 +560,7 @@ int pga_run(pga_ctx *c, int32_t gens, uint64_t seed, int32_t *best_labels, doubl
     const int32_t batch = 8;
     while (!rc) {
         for (int k = 0; k < batch && launched < maxg && !rc; ++k, ++launched)
-            rc = run_one_generation(c, g, true);
+            rc = run_one_generation(c, g, !c->prof);   // profiling events need plain launches
         if (rc) break;
         rc = read_state(c);
         if (rc) break;
