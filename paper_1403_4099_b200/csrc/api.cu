@@ -149,7 +149,7 @@ int reset_state(pga_ctx *c, int32_t max_gens) {
     h.best_ever = -1.0;
     *c->h_st = h;
     PGA_CUDA(cudaMemcpyAsync(c->st, c->h_st, sizeof(DevState), cudaMemcpyHostToDevice, c->stream));
-    const int32_t live[3] = {1, 0, 0};   // re-arm the label-sparse check (f2) for a new population
+    const int32_t live[6] = {1, 0, 0, 0, 0, 0};   // re-arm the label-sparse check (f2) for a new population
     PGA_CUDA(cudaMemcpyAsync(c->sp_live, live, sizeof(live), cudaMemcpyHostToDevice, c->stream));
     PGA_CUDA(cudaStreamSynchronize(c->stream));
     (void)max_gens;
@@ -349,7 +349,7 @@ int pga_create(const double *C, int32_t N, const pga_params *p, pga_ctx **out) {
     rc = rc ? rc : dalloc(&c->diag, (size_t)N);
     rc = rc ? rc : dalloc(&c->lgtab, (size_t)2 * (N + 1));
     rc = rc ? rc : dalloc(&c->sflag, (size_t)(c->Pcap / CB + 1));
-    rc = rc ? rc : dalloc(&c->sp_live, (size_t)3);
+    rc = rc ? rc : dalloc(&c->sp_live, (size_t)6);
     rc = rc ? rc : dalloc(&c->sp_blocks, (size_t)1);
     if (!rc && cudaMemset(c->sp_blocks, 0, sizeof(unsigned long long)) != cudaSuccess)
         rc = fail(PGA_EDEVICE, "memset sp_blocks");

@@ -515,7 +515,6 @@ __global__ void __launch_bounds__(SP_T) k_fitness_sparse(SparseArgs a) {
     if (a.done && *a.done) return;
     extern __shared__ __align__(16) unsigned char sps[];
     __shared__ uint32_t s_maxp;
-    __shared__ int s_kmax[pga::CB];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int N = a.N, W = sp_words(N);
     const int cb = a.cb0 + blockIdx.x;
@@ -533,19 +532,21 @@ __global__ void __launch_bounds__(SP_T) k_fitness_sparse(SparseArgs a) {
         if (tid == 0) a.sflag[cb] = 0;
         return;
     }
+    // every block was sparse at the last check: evaluate sparsely without
+    // checking, except on every 16th launch (the population densifies)
+    const bool skip1 = a.live && a.live[3] != 0 && (a.live[5] & 15) != 0;
     if (tid == 0) s_maxp = 0u;
     __syncthreads();
+    if (!skip1) {
 
     // ---- pass 1: cluster sizes and pair counts
     for (int q = warp; q < pga::CB; q += SP_W) {
         const int64_t p = (int64_t)cb * pga::CB + q;
         for (int k = lane; k < W; k += 32) cq[k] = 0u;
         __syncwarp();
-        uint32_t kmax = 0;
         if (p < a.P)
             for (int i = lane; i < N; i += 32) {
                 const uint32_t s = CM[p * a.ldn + i];
-                kmax = max(kmax, s);
                 atomicAdd(cq + (s >> 1), 1u << (16 * (s & 1u)));
             }
         __syncwarp();
@@ -555,27 +556,32 @@ __global__ void __launch_bounds__(SP_T) k_fitness_sparse(SparseArgs a) {
             pairs += n0 * (n0 - (n0 > 0)) / 2 + n1 * (n1 - (n1 > 0)) / 2;
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            pairs += __shfl_xor_sync(0xFFFFFFFFu, pairs, o);
-            kmax = max(kmax, __shfl_xor_sync(0xFFFFFFFFu, kmax, o));
-        }
-        if (lane == 0) {
-            atomicMax(&s_maxp, pairs);
-            s_kmax[q] = (int)kmax;
-        }
+        for (int o = 16; o > 0; o >>= 1) pairs += __shfl_xor_sync(0xFFFFFFFFu, pairs, o);
+        if (lane == 0) atomicMax(&s_maxp, pairs);
         __syncwarp();
     }
+    }   // !skip1
     __syncthreads();
-    const bool sparse = s_maxp <= a.max_pairs;
+    const bool sparse = skip1 || s_maxp <= a.max_pairs;
     if (tid == 0) {
         a.sflag[cb] = sparse ? 1 : 0;
         if (sparse && a.nsparse) atomicAdd(a.nsparse, 1ull);
-        if (a.live) {                    // last CTA of the launch: keep checking next time iff any block was sparse
+        if (a.live) {
+            // live: [0] any block sparse at the last check, [1] accumulator,
+            // [2] CTA count, [3] every block sparse at the last check, [4]
+            // dense-block count, [5] launch count.  The last CTA publishes.
             if (sparse) atomicOr(&a.live[1], 1);
+            else atomicAdd(&a.live[4], 1);
             __threadfence();
             if (atomicAdd(&a.live[2], 1) == a.nblocks - 1) {
-                a.live[0] = atomicExch(&a.live[1], 0);
+                const int any = atomicExch(&a.live[1], 0);
+                const int dense = atomicExch(&a.live[4], 0);
+                if (!skip1) {
+                    a.live[0] = any;
+                    a.live[3] = dense == 0;
+                }
                 a.live[2] = 0;
+                a.live[5] += 1;
             }
         }
     }
@@ -586,7 +592,6 @@ __global__ void __launch_bounds__(SP_T) k_fitness_sparse(SparseArgs a) {
     for (int q = warp; q < pga::CB; q += SP_W) {
         const int64_t p = (int64_t)cb * pga::CB + q;
         if (p >= a.P) break;
-        const int K = min(s_kmax[q] + 1, N);
         // counts again (pass 1 kept only the pair totals); labels to shared memory
         for (int k = lane; k < W; k += 32) {
             cq[k] = 0u;
@@ -594,12 +599,17 @@ __global__ void __launch_bounds__(SP_T) k_fitness_sparse(SparseArgs a) {
         }
         __syncwarp();
         const uint16_t *lab = CM + p * a.ldn;
+        uint32_t kmax = 0;
 #pragma unroll 4
         for (int i = lane; i < N; i += 32) {
             const uint32_t s = lab[i];
             labs[i] = (uint16_t)s;
+            kmax = max(kmax, s);
             atomicAdd(cq + (s >> 1), 1u << (16 * (s & 1u)));
         }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) kmax = max(kmax, __shfl_xor_sync(0xFFFFFFFFu, kmax, o));
+        const int K = min((int)kmax + 1, N);
         __syncwarp();
         // offsets: exclusive prefix of the counts over labels 0..K-1
         int base = 0;

@@ -85,7 +85,7 @@ struct pga_ctx {
     double *lgtab = nullptr;  // [2 (N+1)]: log n, log(n^2 - n) for the Eq. 8 fold (Q30)
     uint8_t *sflag = nullptr; // [Pcap / CB]: block evaluated by the label-sparse pass (f2)
     double sparse_theta = 0.04;
-    int32_t *sp_live = nullptr;  // device [3]: sparse-pass hysteresis (see k_fitness_sparse)
+    int32_t *sp_live = nullptr;  // device [6]: sparse-pass hysteresis (see k_fitness_sparse)
     unsigned long long *sp_blocks = nullptr;  // device: blocks evaluated label-sparsely (profiling)
     // population: chromosome-major [Pcap][ldn] and gene-major [N][Pcap], double buffered
     uint16_t *pop[2] = {nullptr, nullptr};
