@@ -247,7 +247,7 @@ def main():
     P_local = P_TOTAL if replicated else P_TOTAL // world
     pm = 0.1 if N <= 40 else 2.0 / N            # Table 3 for N <= 40, else 2/N (Q13)
     params = pga.pga_params_default(
-        pop_size=P_local, elite=10, p_mutation=pm, tol=-1.0, max_gens=W + K + 40,
+        pop_size=P_local, elite=10, p_mutation=pm, tol=-1.0, max_gens=W + K + 200,
         device=local, island=0 if replicated else rank, n_islands=1 if replicated else world,
         migrate_every=10, migrants=10, seed=SEED)
 

@@ -482,6 +482,8 @@ constexpr int SPARSE_MAXN = 640;   // shared-memory footprint (sparse_smem) must
 
 struct SparseArgs {
     const uint16_t *cm0, *cm1;
+    uint16_t *gm0, *gm1;          // gene-major labels: written here for blocks found dense (GA mode)
+    int64_t Pcap;
     const double *C;
     int ldc, N, ldn;
     int64_t P;
@@ -509,7 +511,11 @@ __host__ __device__ __forceinline__ size_t sp_per_warp(int N) {
            ~(size_t)15;
 }
 
-static size_t sparse_smem(int N) { return (size_t)SP_W * sp_per_warp(N) + 64; }
+static size_t sparse_smem(int N) {
+    const size_t warps = (size_t)SP_W * sp_per_warp(N) + 64;
+    const size_t tile = (size_t)N * (pga::CB + 2) * sizeof(uint16_t);   // dense-block transpose
+    return warps > tile ? warps : tile;
+}
 
 __global__ void __launch_bounds__(SP_T) k_fitness_sparse(SparseArgs a) {
     if (a.done && *a.done) return;
@@ -563,6 +569,24 @@ __global__ void __launch_bounds__(SP_T) k_fitness_sparse(SparseArgs a) {
     }   // !skip1
     __syncthreads();
     const bool sparse = skip1 || s_maxp <= a.max_pairs;
+    if (!sparse && a.live) {
+        // GA mode: while sparse checks run, the breed leaves the gene-major
+        // copy to us -- transpose this block's labels for the dense sweep
+        uint16_t *GM = par ? a.gm1 : a.gm0;
+        uint16_t *tile = reinterpret_cast<uint16_t *>(sps);          // [N][CB + 2]
+        constexpr int TSP = pga::CB + 2;
+        for (int e = tid; e < pga::CB * N; e += SP_T) {
+            const int q = e / N, i = e - q * N;
+            const int64_t p = (int64_t)cb * pga::CB + q;
+            tile[i * TSP + q] = p < a.P ? CM[p * a.ldn + i] : (uint16_t)0;
+        }
+        __syncthreads();
+        for (int e = tid; e < N * (pga::CB / 2); e += SP_T) {
+            const int i = e / (pga::CB / 2), pr = e - i * (pga::CB / 2);
+            *reinterpret_cast<uint32_t *>(&GM[(int64_t)i * a.Pcap + (int64_t)cb * pga::CB + 2 * pr]) =
+                *reinterpret_cast<const uint32_t *>(&tile[i * TSP + 2 * pr]);
+        }
+    }
     if (tid == 0) {
         a.sflag[cb] = sparse ? 1 : 0;
         if (sparse && a.nsparse) atomicAdd(a.nsparse, 1ull);
@@ -886,6 +910,9 @@ int launch_fitness_range(pga_ctx *c, const FitBufs &b, int64_t begin, int64_t en
         SparseArgs sp;
         sp.cm0 = b.cm0;
         sp.cm1 = b.cm1;
+        sp.gm0 = const_cast<uint16_t *>(b.gm0);
+        sp.gm1 = const_cast<uint16_t *>(b.gm1);
+        sp.Pcap = c->Pcap;
         sp.C = c->C;
         sp.ldc = c->ldc;
         sp.N = N;

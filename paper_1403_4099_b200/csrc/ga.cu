@@ -568,6 +568,7 @@ struct BreedArgs {
     uint64_t seed;
     uint32_t gen, island;
     const int32_t *done, *gen_ptr;
+    const int32_t *gm_skip;            // != 0: the label-sparse pass owns the gene-major copy (f2)
 };
 
 
@@ -858,6 +859,7 @@ __global__ void __launch_bounds__(BW * 32, 3) k_breed2(BreedArgs a) {
         }
     }
     if (HOOK) return;
+    if (a.gm_skip && *a.gm_skip) return;   // sparse mode: k_fitness_sparse transposes dense blocks itself
     __syncthreads();
 
     // ---- phase 3: gene-major rows (BS children = 32 B per gene)
@@ -1221,6 +1223,9 @@ int launch_select_breed(pga_ctx *c, cudaStream_t s) {
     a.ldn = c->ldn;
     a.done = done;
     a.gen_ptr = genp;
+    // the gene-major copy is produced by the label-sparse pass while its
+    // checks are live (it transposes exactly the blocks the dense sweep needs)
+    a.gm_skip = (c->sparse_theta > 0.0 && c->N <= 640) ? c->sp_live : nullptr;
     if (c->N <= BREED2_MAXN)
         k_breed2<false><<<(unsigned)((c->P + BS - 1) / BS), BW * 32, breed2_smem(c->N), s>>>(a);
     else
