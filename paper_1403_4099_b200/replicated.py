@@ -7,8 +7,10 @@ seed).  Per generation rank r evaluates its contiguous shard
 [r*S, min(P, (r+1)*S)) with S = 32 * ceil(P / (32 * world)); the ranks
 all-gather L and the KB top labels (10 bytes per chromosome; NCCL over
 NVLink on GPUs, gloo in CPU tests); every rank installs the full vectors and
-runs the same deterministic operators, so the replicas stay bit-identical
-and the run equals the single-GPU pga_run.
+runs the same deterministic operators, so the replicas stay bit-identical.
+With the label-sparse pass off (pga_set_sparse_threshold(ctx, 0)) the run
+also equals the single-GPU pga_run bit for bit; with it on, a block's path
+(and so the last bits of its L) can depend on the launch history.
 
 The driver only moves bytes and sequences calls.  ``GpuReplica`` is the
 product engine; tests plug in an oracle-backed engine with the same methods.

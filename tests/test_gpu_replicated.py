@@ -35,6 +35,9 @@ def test_replicas_equal_single_gpu_run(pga, orc, cfg, P, W, gens):
     params = pga.pga_params_default(pop_size=P, p_mutation=pm, max_gens=gens, tol=-1.0, seed=3)
     ref_ctx = pga.pga_create(C, params)
     try:
+        # bit-identity with one GPU needs the path choice to be a function of
+        # the block alone: the label-sparse pass's launch-history shortcuts are off
+        pga.pga_set_sparse_threshold(ref_ctx, 0.0)
         ref = pga.pga_run(ref_ctx, gens, 3, N)
         ref_hist = pga.pga_get_history(ref_ctx, gens)
         ref_pop, ref_L = pga.pga_get_population(ref_ctx, P, N)
@@ -44,6 +47,7 @@ def test_replicas_equal_single_gpu_run(pga, orc, cfg, P, W, gens):
     reps = [GpuReplica(C, params) for _ in range(W)]
     try:
         for r in reps:
+            pga.pga_set_sparse_threshold(r.ctx, 0.0)
             r.init(3)
         S = shard(P, W, 0)[2]
         L_all = torch.zeros(S * W, dtype=torch.float64, device="cuda")
