@@ -653,33 +653,46 @@ int pga_batch_run(const double *C, int32_t B, int32_t N, const pga_params *p, in
         a.history = history;
         return launch_batch(a, smem, (cudaStream_t)stream);
     }
-    DBufs d;
-    double *dC, *dL, *dH = nullptr;
-    int32_t *dlab, *dg, *dr;
-    BTRY(d.get(&dC, (size_t)B * N * N));
-    BTRY(d.get(&dL, (size_t)B));
-    BTRY(d.get(&dlab, (size_t)B * N));
-    BTRY(d.get(&dg, (size_t)B));
-    BTRY(d.get(&dr, (size_t)B));
-    if (history) {
-        BTRY(d.get(&dH, (size_t)B * p->max_gens));
-        PGA_CUDA(cudaMemset(dH, 0, sizeof(double) * (size_t)B * p->max_gens));
-    }
-    PGA_CUDA(cudaMemcpy(dC, C, sizeof(double) * (size_t)B * N * N, cudaMemcpyHostToDevice));
+    // host path: one stream, stream-ordered scratch (no device-wide syncs)
+    cudaStream_t st;
+    PGA_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    struct StreamGuard {
+        cudaStream_t s;
+        ~StreamGuard() {
+            cudaStreamSynchronize(s);
+            cudaStreamDestroy(s);
+        }
+    } guard{st};
+    const size_t nC = (size_t)B * N * N, nH = history ? (size_t)B * p->max_gens : 0;
+    unsigned char *blob = nullptr;
+    const size_t bytes = sizeof(double) * (nC + B + nH) + sizeof(int32_t) * ((size_t)B * N + 2 * (size_t)B) + 64;
+    PGA_CUDA(cudaMallocAsync((void **)&blob, bytes, st));
+    struct BlobGuard {
+        void *p;
+        cudaStream_t s;
+        ~BlobGuard() { cudaFreeAsync(p, s); }
+    } bg{blob, st};
+    double *dC = reinterpret_cast<double *>(blob);
+    double *dL = dC + nC;
+    double *dH = history ? dL + B : nullptr;
+    int32_t *dlab = reinterpret_cast<int32_t *>(dL + B + nH);
+    int32_t *dg = dlab + (size_t)B * N;
+    int32_t *dr = dg + B;
+    if (history) PGA_CUDA(cudaMemsetAsync(dH, 0, sizeof(double) * nH, st));
+    PGA_CUDA(cudaMemcpyAsync(dC, C, sizeof(double) * nC, cudaMemcpyHostToDevice, st));
     a.C = dC;
     a.best_labels = dlab;
     a.best_L = dL;
     a.gens = dg;
     a.reason = dr;
     a.history = dH;
-    BTRY(launch_batch(a, smem, 0));
-    PGA_CUDA(cudaDeviceSynchronize());
-    PGA_CUDA(cudaMemcpy(best_L, dL, sizeof(double) * B, cudaMemcpyDeviceToHost));
-    if (best_labels) PGA_CUDA(cudaMemcpy(best_labels, dlab, sizeof(int32_t) * (size_t)B * N, cudaMemcpyDeviceToHost));
-    if (gens) PGA_CUDA(cudaMemcpy(gens, dg, sizeof(int32_t) * B, cudaMemcpyDeviceToHost));
-    if (reason) PGA_CUDA(cudaMemcpy(reason, dr, sizeof(int32_t) * B, cudaMemcpyDeviceToHost));
-    if (history)
-        PGA_CUDA(cudaMemcpy(history, dH, sizeof(double) * (size_t)B * p->max_gens, cudaMemcpyDeviceToHost));
+    BTRY(launch_batch(a, smem, st));
+    PGA_CUDA(cudaMemcpyAsync(best_L, dL, sizeof(double) * B, cudaMemcpyDeviceToHost, st));
+    if (best_labels) PGA_CUDA(cudaMemcpyAsync(best_labels, dlab, sizeof(int32_t) * (size_t)B * N, cudaMemcpyDeviceToHost, st));
+    if (gens) PGA_CUDA(cudaMemcpyAsync(gens, dg, sizeof(int32_t) * B, cudaMemcpyDeviceToHost, st));
+    if (reason) PGA_CUDA(cudaMemcpyAsync(reason, dr, sizeof(int32_t) * B, cudaMemcpyDeviceToHost, st));
+    if (history) PGA_CUDA(cudaMemcpyAsync(history, dH, sizeof(double) * nH, cudaMemcpyDeviceToHost, st));
+    PGA_CUDA(cudaStreamSynchronize(st));
     return PGA_OK;
 }
 

@@ -251,20 +251,6 @@ __global__ void __launch_bounds__(JT) k_clean(const double *__restrict__ R, int 
 
 int stream_count(int T, int warm, int stride) { return T < warm ? 0 : (T - warm) / stride + 1; }
 
-struct SBufs {
-    std::vector<void *> ptrs;
-    ~SBufs() {
-        for (void *p : ptrs) cudaFree(p);
-    }
-    template <typename T>
-    int get(T **p, size_t n) {
-        cudaError_t e = cudaMalloc((void **)p, sizeof(T) * (n ? n : 1));
-        if (e != cudaSuccess) return pga::fail(PGA_ENOMEM, std::string("cudaMalloc failed: ") + cudaGetErrorString(e));
-        ptrs.push_back((void *)*p);
-        return PGA_OK;
-    }
-};
-
 #define STRY(x)              \
     do {                     \
         int _rc = (x);       \
@@ -319,23 +305,36 @@ int pga_corr_stream(const double *X, int32_t T, int32_t N, double lambda, int32_
         cudaFreeAsync(R, st);
         return rc;
     }
-    SBufs d;
-    double *R;
-    STRY(d.get(&R, (size_t)B * N * N));
-    double *dX, *dC;
-    int32_t *dst;
-    STRY(d.get(&dX, (size_t)T * N));
-    STRY(d.get(&dC, (size_t)B * N * N));
-    STRY(d.get(&dst, 1));
-    PGA_CUDA(cudaMemset(dst, 0, sizeof(int32_t)));
-    PGA_CUDA(cudaMemcpy(dX, X, sizeof(double) * (size_t)T * N, cudaMemcpyHostToDevice));
-    STRY(launch_stream(dX, T, N, lambda, warm, stride, qq, clean, dC, dst, R, 0));
-    PGA_CUDA(cudaDeviceSynchronize());
+    // host path: one stream, stream-ordered scratch
+    cudaStream_t st;
+    PGA_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    struct StreamGuard {
+        cudaStream_t s;
+        ~StreamGuard() {
+            cudaStreamSynchronize(s);
+            cudaStreamDestroy(s);
+        }
+    } guard{st};
+    const size_t nX = (size_t)T * N, nR = (size_t)B * N * N;
+    unsigned char *blob = nullptr;
+    PGA_CUDA(cudaMallocAsync((void **)&blob, sizeof(double) * (nX + 2 * nR) + 64, st));
+    struct BlobGuard {
+        void *p;
+        cudaStream_t s;
+        ~BlobGuard() { cudaFreeAsync(p, s); }
+    } bg{blob, st};
+    double *dX = reinterpret_cast<double *>(blob), *R = dX + nX, *dC = R + nR;
+    int32_t *dst = reinterpret_cast<int32_t *>(dC + nR);
+    PGA_CUDA(cudaMemsetAsync(dst, 0, sizeof(int32_t), st));
+    PGA_CUDA(cudaMemcpyAsync(dX, X, sizeof(double) * nX, cudaMemcpyHostToDevice, st));
+    STRY(launch_stream(dX, T, N, lambda, warm, stride, qq, clean, dC, dst, R, st));
     int32_t h = 0;
-    PGA_CUDA(cudaMemcpy(&h, dst, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    PGA_CUDA(cudaMemcpyAsync(&h, dst, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    PGA_CUDA(cudaStreamSynchronize(st));
     if (status) *status = h;
     if (h) return pga::fail(PGA_ENUMERIC, "non-positive EWMA variance at an emission");
-    PGA_CUDA(cudaMemcpy(C_out, dC, sizeof(double) * (size_t)B * N * N, cudaMemcpyDeviceToHost));
+    PGA_CUDA(cudaMemcpyAsync(C_out, dC, sizeof(double) * nR, cudaMemcpyDeviceToHost, st));
+    PGA_CUDA(cudaStreamSynchronize(st));
     return PGA_OK;
 }
 
