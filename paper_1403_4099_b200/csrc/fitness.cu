@@ -239,10 +239,10 @@ __device__ __forceinline__ void eq8_tables(double *cs, int32_t *ns, int K, int l
 template <int NC>
 __device__ __forceinline__ void fold_multi(const uint16_t *const (&lab)[NC], const double *const (&v)[NC],
                                            int N, double *const (&cs)[NC], int32_t *const (&ns)[NC],
-                                           double *gbuf, int lane, double *const (&L_out)[NC],
+                                           int lane, double *const (&L_out)[NC],
                                            uint16_t *const (&top_out)[NC], double scale, double inv_scale,
                                            const double *__restrict__ lgn, const double *__restrict__ lgnn) {
-    (void)gbuf;   // cs / ns were zeroed by the caller (all-zero bits == integer 0)
+    // cs / ns were zeroed by the caller (all-zero bits == integer 0)
     // software pipeline: loads of chunk c+2 are issued while chunk c folds
     uint32_t s_n1[NC], s_n2[NC];
     double v_n1[NC], v_n2[NC];
@@ -421,7 +421,6 @@ k_fitness(const __grid_constant__ CUtensorMap tmLab0, const __grid_constant__ CU
         double *csb = reinterpret_cast<double *>(smem) + (size_t)warp * NCF * N;
         int32_t *nsb = reinterpret_cast<int32_t *>(reinterpret_cast<double *>(smem) + (size_t)a.fold_warps * NCF * N) +
                        (size_t)warp * NCF * N;
-        double *gbuf = reinterpret_cast<double *>(nsb + (size_t)(a.fold_warps - warp) * NCF * N) + warp * NCF * 32;
         for (int q = NCF * warp; q < pga::CB; q += NCF * a.fold_warps) {
             const int64_t p = (int64_t)cb * pga::CB + q;
             if (p >= a.P) break;
@@ -448,7 +447,7 @@ k_fitness(const __grid_constant__ CUtensorMap tmLab0, const __grid_constant__ CU
                 for (int k = lane; k < N * NCF / 2; k += 32) n2[k] = make_uint2(0u, 0u);
                 __syncwarp();
             }
-            fold_multi<NCF>(lab, vv, N, cs, ns, gbuf, lane, Lo, to, a.fx_scale, a.fx_inv, a.lgn, a.lgnn);
+            fold_multi<NCF>(lab, vv, N, cs, ns, lane, Lo, to, a.fx_scale, a.fx_inv, a.lgn, a.lgnn);
             // V of these chromosomes is dead: drop its L2 lines without a
             // DRAM write-back (rows are 128-byte aligned, ldn % 16 == 0)
 #pragma unroll
@@ -842,14 +841,14 @@ int launch_logtab(pga_ctx *c, cudaStream_t s) {
 }
 
 int fold_warps(int N) {
-    const size_t per = 2 * (size_t)N * (sizeof(double) + sizeof(int32_t)) + 2 * 32 * sizeof(double);
+    const size_t per = 2 * (size_t)N * (sizeof(double) + sizeof(int32_t));   // NCF = 2 chromosomes per warp
     int w = (int)((size_t)(NSTAGE * STAGE_BYTES) / per);
     if (w < 1) w = 1;
     return w > CW + 1 ? CW + 1 : w;
 }
 
 size_t fitness_smem(int N) {
-    const size_t fold = (size_t)fold_warps(N) * (2 * N * (sizeof(double) + sizeof(int32_t)) + 2 * 32 * sizeof(double)) + 16;
+    const size_t fold = (size_t)fold_warps(N) * (2 * N * (sizeof(double) + sizeof(int32_t))) + 16;
     const size_t pipe = (size_t)NSTAGE * STAGE_BYTES;
     return (fold > pipe ? fold : pipe) + 2 * NSTAGE * sizeof(uint64_t) + 128;
 }
