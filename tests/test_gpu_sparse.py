@@ -76,3 +76,68 @@ def test_sparse_threshold_validation(pga):
             pga.pga_set_sparse_threshold(ctx, 1.5)
     finally:
         pga.pga_destroy(ctx)
+
+
+@pytest.mark.parametrize("N,P", [(640, 100), (641, 64), (37, 33), (2, 5)])
+def test_sparse_edges_match_oracle(pga, orc, N, P):
+    """Largest N with a label-sparse pass (640), the first without (641),
+    ragged P (not a multiple of 32), N = 2: every path vs the oracle."""
+    rng = np.random.default_rng(N + P)
+    X = rng.standard_normal((max(3 * N, 40), N))
+    k = max(1, N // 6)
+    X += 0.8 * rng.standard_normal((X.shape[0], k))[:, rng.integers(0, k, N)]
+    C = orc.pearson(X)
+    labs = [workloads.random_labels(rng, P, N), workloads.random_labels(rng, P, N, K=max(2, N // 50))]
+    ctx = pga.pga_create(C, pga.pga_params_default(pop_size=P, elite=min(10, P - 1)))
+    try:
+        for theta in (1.0, 0.0):
+            pga.pga_set_sparse_threshold(ctx, theta)
+            for lab in labs:
+                _assert_L(pga.pga_evaluate(ctx, lab + 1), orc.evaluate(C, lab, nthreads=8)[0])
+    finally:
+        pga.pga_destroy(ctx)
+
+
+@pytest.mark.parametrize("theta", [0.0, 1.0, 0.04])
+def test_ga_recovers_C1_any_path(pga, orc, theta):
+    """The GA recovers C1's planted partition whichever fitness path runs
+    (forced dense, forced label-sparse, default)."""
+    X, planted = workloads.noh_returns(workloads.CONFIGS["C1"])
+    C = orc.pearson(X)
+    ok = 0
+    for seed in range(1, 6):
+        ctx = pga.pga_create(C, pga.pga_params_default(pop_size=128, max_gens=300, tol=-1.0, seed=seed))
+        try:
+            pga.pga_set_sparse_threshold(ctx, theta)
+            r = pga.pga_run(ctx, 300, seed, 18)
+            Lr, _ = orc.log_likelihood(C, r["best_labels"] - 1)
+            _assert_L([r["best_L"]], [Lr])
+            ok += np.array_equal(r["best_labels"] - 1, planted)
+        finally:
+            pga.pga_destroy(ctx)
+    assert ok >= 4, ok
+
+
+def test_sparse_pass_in_lockstep_with_oracle(pga, orc):
+    """C4-size GA generations with the default label-sparse pass: at every
+    generation the GPU's L matches the oracle and, fed the GPU's L and top,
+    the oracle's operators breed the GPU's next population bit for bit."""
+    X, _ = workloads.noh_returns(workloads.CONFIGS["C4"])
+    C = orc.pearson(X)
+    P, N = 2048, 500
+    params = pga.pga_params_default(pop_size=P, p_mutation=2.0 / N, tol=-1.0, max_gens=50, seed=21)
+    ctx = pga.pga_create(C, params)
+    try:
+        pga.pga_init(ctx, 21)
+        op = orc.default_params(pop=P, p_m=2.0 / N, tol=-1.0, max_gens=50, seed=21)
+        for g in range(4):
+            pga.pga_gen_evaluate(ctx)
+            pop, L, top = pga.pga_get_population(ctx, P, N, with_top=True)
+            _assert_L(L, orc.evaluate(C, pop - 1, nthreads=8)[0])
+            nxt = orc.step(op, pop - 1, L, top, g)
+            pga.pga_gen_breed(ctx)
+            pop2, _ = pga.pga_get_population(ctx, P, N)
+            assert np.array_equal(pop2 - 1, nxt), g
+        assert pga.pga_profile_sparse_blocks(ctx) >= 0
+    finally:
+        pga.pga_destroy(ctx)
