@@ -506,7 +506,7 @@ constexpr int SPQ = 64;   // per-warp queue of completed clusters awaiting their
 
 __host__ __device__ __forceinline__ size_t sp_per_warp(int N) {
     return (((size_t)sp_words(N) * 4 /*cnt*/ + (size_t)sp_words(N) * 4 /*run*/ + (size_t)(N + 1) * 2 /*off*/ +
-             (size_t)N * 2 /*perm*/ + (size_t)N * 2 /*labels*/ + (size_t)SPQ * 12 /*queue*/ + 64) + 15) &
+             (size_t)N * 2 /*perm*/ + (size_t)SPQ * 12 /*queue*/ + 64) + 15) &
            ~(size_t)15;
 }
 
@@ -516,7 +516,7 @@ static size_t sparse_smem(int N) {
     return warps > tile ? warps : tile;
 }
 
-__global__ void __launch_bounds__(SP_T) k_fitness_sparse(SparseArgs a) {
+__global__ void __launch_bounds__(SP_T, 5) k_fitness_sparse(SparseArgs a) {
     if (a.done && *a.done) return;
     extern __shared__ __align__(16) unsigned char sps[];
     __shared__ uint32_t s_maxp;
@@ -532,7 +532,6 @@ __global__ void __launch_bounds__(SP_T) k_fitness_sparse(SparseArgs a) {
     uint32_t *run = cq + W;                                              // [W] packed scatter counters
     uint16_t *off = reinterpret_cast<uint16_t *>(run + W);              // [N+1]
     uint16_t *perm = off + (N + 1);                                      // [N]
-    uint16_t *labs = perm + N;                                           // [N]
     if (a.live && a.live[0] == 0) {     // the population went dense: skip (flags cleared)
         if (tid == 0) a.sflag[cb] = 0;
         return;
@@ -626,7 +625,6 @@ __global__ void __launch_bounds__(SP_T) k_fitness_sparse(SparseArgs a) {
 #pragma unroll 4
         for (int i = lane; i < N; i += 32) {
             const uint32_t s = lab[i];
-            labs[i] = (uint16_t)s;
             kmax = max(kmax, s);
             atomicAdd(cq + (s >> 1), 1u << (16 * (s & 1u)));
         }
@@ -653,7 +651,7 @@ __global__ void __launch_bounds__(SP_T) k_fitness_sparse(SparseArgs a) {
         // in label order (order inside a cluster is free: sums are exact)
 #pragma unroll 4
         for (int i = lane; i < N; i += 32) {
-            const uint32_t s = labs[i];
+            const uint32_t s = lab[i];
             const uint32_t sh = 16 * (s & 1u);
             const uint32_t old = (atomicAdd(run + (s >> 1), 1u << sh) >> sh) & 0xFFFFu;
             perm[off[s] + old] = (uint16_t)i;
@@ -673,7 +671,7 @@ __global__ void __launch_bounds__(SP_T) k_fitness_sparse(SparseArgs a) {
             long long acc = 0;
             if (t < N) {
                 const int g = perm[t];
-                s = labs[g];
+                s = lab[g];
                 n = (int)((cq[s >> 1] >> (16 * (s & 1))) & 0xFFFFu);
                 if (n >= 2) {
                     const int st = off[s], av = t - st;
