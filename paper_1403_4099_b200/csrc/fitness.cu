@@ -505,7 +505,7 @@ __host__ __device__ __forceinline__ int sp_words(int N) { return (N + 2) / 2; } 
 constexpr int SPQ = 64;   // per-warp queue of completed clusters awaiting their Eq. 8 summand
 
 __host__ __device__ __forceinline__ size_t sp_per_warp(int N) {
-    return (((size_t)sp_words(N) * 4 /*cnt*/ + (size_t)sp_words(N) * 4 /*run*/ + (size_t)(N + 1) * 2 /*off*/ +
+    return (((size_t)sp_words(N) * 4 /*cnt, then scatter counters*/ + (size_t)(N + 2) * 2 /*off*/ +
              (size_t)N * 2 /*perm*/ + (size_t)SPQ * 12 /*queue*/ + 64) + 15) &
            ~(size_t)15;
 }
@@ -529,9 +529,9 @@ __global__ void __launch_bounds__(SP_T, 5) k_fitness_sparse(SparseArgs a) {
     double *qc = reinterpret_cast<double *>(wb);                         // [SPQ] queued c
     uint32_t *qnk = reinterpret_cast<uint32_t *>(qc + SPQ);             // [SPQ] queued n | label << 16
     uint32_t *cq = qnk + SPQ;                                            // [W] packed counts
-    uint32_t *run = cq + W;                                              // [W] packed scatter counters
-    uint16_t *off = reinterpret_cast<uint16_t *>(run + W);              // [N+1]
-    uint16_t *perm = off + (N + 1);                                      // [N]
+    uint32_t *run = cq;                                                  // [W] scatter counters (after the offsets)
+    uint16_t *off = reinterpret_cast<uint16_t *>(cq + W);               // [N+2]
+    uint16_t *perm = off + (N + 2);                                      // [N]
     if (a.live && a.live[0] == 0) {     // the population went dense: skip (flags cleared)
         if (tid == 0) a.sflag[cb] = 0;
         return;
@@ -614,11 +614,8 @@ __global__ void __launch_bounds__(SP_T, 5) k_fitness_sparse(SparseArgs a) {
     for (int q = warp; q < pga::CB; q += SP_W) {
         const int64_t p = (int64_t)cb * pga::CB + q;
         if (p >= a.P) break;
-        // counts again (pass 1 kept only the pair totals); labels to shared memory
-        for (int k = lane; k < W; k += 32) {
-            cq[k] = 0u;
-            run[k] = 0u;
-        }
+        // counts again (pass 1 kept only the pair totals)
+        for (int k = lane; k < W; k += 32) cq[k] = 0u;
         __syncwarp();
         const uint16_t *lab = CM + p * a.ldn;
         uint32_t kmax = 0;
@@ -646,6 +643,9 @@ __global__ void __launch_bounds__(SP_T, 5) k_fitness_sparse(SparseArgs a) {
             if (k < K) off[k] = (uint16_t)(base + incl - n);
             base += __shfl_sync(0xFFFFFFFFu, incl, 31);
         }
+        if (lane == 0) off[K] = (uint16_t)base;      // n_s = off[s + 1] - off[s]
+        __syncwarp();
+        for (int k = lane; k < W; k += 32) run[k] = 0u;   // the counts become scatter counters
         __syncwarp();
         // counting sort of the genes by label: clusters become contiguous runs
         // in label order (order inside a cluster is free: sums are exact)
@@ -672,7 +672,7 @@ __global__ void __launch_bounds__(SP_T, 5) k_fitness_sparse(SparseArgs a) {
             if (t < N) {
                 const int g = perm[t];
                 s = lab[g];
-                n = (int)((cq[s >> 1] >> (16 * (s & 1))) & 0xFFFFu);
+                n = (int)off[s + 1] - (int)off[s];
                 if (n >= 2) {
                     const int st = off[s], av = t - st;
                     const double *Cg = C + (size_t)g * a.ldc;
