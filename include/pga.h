@@ -95,9 +95,11 @@ int pga_evaluate(pga_ctx *ctx, const int32_t *labels, int64_t P, double *out_L);
 
 /* Device fast path, stream-ordered on `stream` (cudaStream_t, NULL = the
  * ctx's stream):  labels_dev: device uint16 [P][N] row-major, 0-based values
- * < N (unchecked);  L_dev: device fp64 [P];  top_dev: device uint16 [P] or
+ * < N;  L_dev: device fp64 [P];  top_dev: device uint16 [P] or
  * NULL — label of the cluster with the largest Eq. 8 summand, 0xFFFF if none.
- * 1 <= P <= the ctx's capacity (pop_size rounded up to 64). */
+ * 1 <= P <= the ctx's capacity (pop_size rounded up to 32).  A label >= N is
+ * evaluated as label 0 (that chromosome's L is then meaningless; the others
+ * are unaffected). */
 int pga_evaluate_device(pga_ctx *ctx, const uint16_t *labels_dev, int64_t P,
                         double *L_dev, uint16_t *top_dev, void *stream);
 

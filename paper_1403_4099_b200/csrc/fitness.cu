@@ -40,6 +40,10 @@ __global__ void k_pack(const uint16_t *__restrict__ lab16, const int32_t *__rest
         if (p < P && i < N) {
             if (lab16) {
                 v = lab16[p * ld_in + i];
+                if (v >= (uint16_t)N) {    // out of range: flagged, evaluated as label 0 (no stray table index)
+                    atomicExch(&st->pack_error, 1);
+                    v = 0;
+                }
             } else {
                 const int32_t x = lab32[p * (int64_t)N + i];
                 if (x < 1 || x > N) {

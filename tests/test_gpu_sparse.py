@@ -141,3 +141,29 @@ def test_sparse_pass_in_lockstep_with_oracle(pga, orc):
         assert pga.pga_profile_sparse_blocks(ctx) >= 0
     finally:
         pga.pga_destroy(ctx)
+
+
+@pytest.mark.parametrize("theta", [0.0, 1.0])
+def test_out_of_range_device_label_is_contained(pga, orc, theta):
+    """A label >= N in one chromosome (device fast path, unchecked input)
+    must not disturb the other chromosomes' L on either fitness path."""
+    import torch
+    X, planted = workloads.noh_returns(workloads.CONFIGS["C3"])
+    C = orc.pearson(X)
+    N, P = C.shape[0], 96
+    lab = workloads.population_mix(5, planted, P)
+    bad = lab.copy()
+    bad[7, 3] = N + 5
+    ctx = pga.pga_create(C, pga.pga_params_default(pop_size=P))
+    try:
+        pga.pga_set_sparse_threshold(ctx, theta)
+        L = torch.zeros(P, dtype=torch.float64, device="cuda")
+        s = torch.cuda.Stream()
+        pga.pga_evaluate_device(ctx, torch.from_numpy(bad.astype(np.int16)).cuda(), L, stream=s.cuda_stream)
+        s.synchronize()
+        Lg = L.cpu().numpy()
+    finally:
+        pga.pga_destroy(ctx)
+    Lo, _ = orc.evaluate(C, lab)
+    keep = np.arange(P) != 7
+    _assert_L(Lg[keep], Lo[keep])
