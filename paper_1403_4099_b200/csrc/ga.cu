@@ -1172,7 +1172,11 @@ int launch_breed_hook(const int32_t *pop, const int32_t *top, const int32_t *ord
     return PGA_OK;
 }
 
-bool small_select(const pga_ctx *c) { return c->P <= SMALL_P; }
+// GA generations: one CTA up to 1024 (bitonic); above that the multi-CTA
+// path (run sort + merge tree, weights, scan, SUS, mates) is faster than the
+// single-CTA block radix sort (pga_op_select still uses it up to SMALL_P)
+constexpr int SMALL_GA_P = 1024;
+bool small_select(const pga_ctx *c) { return c->P <= SMALL_GA_P; }
 
 int launch_sort_order(pga_ctx *c, cudaStream_t s) {
     if (small_select(c))
