@@ -778,19 +778,25 @@ __global__ void __launch_bounds__(BW * 32, 3) k_breed2(BreedArgs a) {
     const int64_t o = o0 + slot;
     const ChildPlan p = plan_child(a, o, gen);
 
-    // ---- phase 1: crossover + mutation -> pre-canonical genes in the tile
+    // ---- phase 1: crossover + mutation -> pre-canonical genes in the tile.
+    // Lane l takes the gene pair (b0 + 64h + 2l, +1): one 32-bit load per
+    // parent, both mutation bits from one shuffle, and at most one MUTV
+    // block (both genes share Philox block (g >> 2)).
     for (int b0 = 0; b0 < N; b0 += GCH) {
-        uint32_t ga[GCH / 32], gb[GCH / 32];
+        uint32_t ga[GCH / 64], gb[GCH / 64];
 #pragma unroll
-        for (int sc = 0; sc < GCH / 32; ++sc) {
-            const int i = b0 + 32 * sc + lane;
-            const bool valid = p.valid && i < N;
+        for (int h = 0; h < GCH / 64; ++h) {
+            const int g0 = b0 + 64 * h + 2 * lane;
+            const bool v0 = p.valid && g0 < N, v1 = p.valid && g0 + 1 < N;
             if (HOOK) {
-                ga[sc] = valid ? (uint32_t)a.i32_in[p.pa * N + i] : 0u;
-                gb[sc] = (valid && p.mode != 0) ? (uint32_t)a.i32_in[p.pb * N + i] : 0u;
+                ga[h] = (v0 ? (uint32_t)a.i32_in[p.pa * N + g0] : 0u) |
+                        ((v1 ? (uint32_t)a.i32_in[p.pa * N + g0 + 1] : 0u) << 16);
+                gb[h] = (p.mode != 0) ? ((v0 ? (uint32_t)a.i32_in[p.pb * N + g0] : 0u) |
+                                         ((v1 ? (uint32_t)a.i32_in[p.pb * N + g0 + 1] : 0u) << 16)) : 0u;
             } else {
-                ga[sc] = valid ? (uint32_t)cm_in[p.pa * a.ldn + i] : 0u;
-                gb[sc] = (valid && p.mode != 0) ? (uint32_t)cm_in[p.pb * a.ldn + i] : 0u;
+                // ldn is even and g0 is even: the pair is one aligned 32-bit word
+                ga[h] = v0 ? *reinterpret_cast<const uint32_t *>(cm_in + p.pa * a.ldn + g0) : 0u;
+                gb[h] = (v0 && p.mode != 0) ? *reinterpret_cast<const uint32_t *>(cm_in + p.pb * a.ldn + g0) : 0u;
             }
         }
         uint32_t mbits = 0;
@@ -800,21 +806,30 @@ __global__ void __launch_bounds__(BW * 32, 3) k_breed2(BreedArgs a) {
                     ((uint64_t)u.z < a.thr_m ? 4u : 0u) | ((uint64_t)u.w < a.thr_m ? 8u : 0u);
         }
 #pragma unroll
-        for (int sc = 0; sc < GCH / 32; ++sc) {
-            const int i = b0 + 32 * sc + lane;
-            const bool valid = p.valid && i < N;
-            const uint32_t mb = __shfl_sync(0xFFFFFFFFu, mbits, 8 * sc + (lane >> 2));
-            uint32_t s = ga[sc];
-            if (p.mode == 1) {
-                if (p.kb_top >= 0 && (int)gb[sc] == p.kb_top) s = (uint32_t)N;
-            } else if (p.mode == 2) {
-                if (i >= p.cut) s = gb[sc];
+        for (int h = 0; h < GCH / 64; ++h) {
+            const int g0 = b0 + 64 * h + 2 * lane;
+            const uint32_t mb = (__shfl_sync(0xFFFFFFFFu, mbits, 16 * h + (lane >> 1)) >> (2 * (lane & 1))) & 3u;
+            uint32_t s[2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int i = g0 + e;
+                uint32_t x = (ga[h] >> (16 * e)) & 0xFFFFu;
+                const uint32_t y = (gb[h] >> (16 * e)) & 0xFFFFu;
+                if (p.mode == 1) {
+                    if (p.kb_top >= 0 && (int)y == p.kb_top) x = (uint32_t)N;
+                } else if (p.mode == 2) {
+                    if (i >= p.cut) x = y;
+                }
+                s[e] = x;
             }
-            if (valid && ((mb >> (lane & 3)) & 1u)) {
-                const U4 v = draw(a.seed, pga::TAG_MUTV, a.island, gen, (uint32_t)(i >> 2), p.og);
-                s = scale_u32(word(v, i & 3), (uint32_t)N);
+            if (p.valid && mb) {
+                const U4 v = draw(a.seed, pga::TAG_MUTV, a.island, gen, (uint32_t)(g0 >> 2), p.og);
+#pragma unroll
+                for (int e = 0; e < 2; ++e)
+                    if ((mb >> e) & 1u) s[e] = scale_u32(word(v, (g0 + e) & 3), (uint32_t)N);
             }
-            if (i < N) tile[i * TS + slot] = (uint16_t)s;
+            if (g0 < N) tile[g0 * TS + slot] = (uint16_t)s[0];
+            if (g0 + 1 < N) tile[(g0 + 1) * TS + slot] = (uint16_t)s[1];
         }
     }
     __syncwarp();
