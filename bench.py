@@ -41,6 +41,9 @@ FP64_LANES_PER_SM = 64           # DFMA lanes / clk / SM (B200: 37 TF fp64 = 148
 # (tools/mb_pairloop.cu, shared-memory resident, no pipeline/fold): 26.8
 # executed pair-updates per SM-clock, register-file-read bound.
 LOOP_PAIRS_PER_CLK = 26.8
+# Measured random 8-byte gather rate from an L2-resident 2 MB fp64 array (C at
+# N = 500) on this pool (tools/mb_l2gather.cu): the label-sparse pass's bound.
+L2_GATHERS_PER_S = 3.03e11
 
 METRIC = ("GA generation throughput, nominal pair-updates/s (N^2 * P per generation; "
           "fitness + all operators)")
@@ -289,7 +292,7 @@ def main():
     launches = pga.pga_launch_count() - launches0
     ms = ev0.elapsed_time(ev1)
     prof = pga.pga_profile_read(eng.ctx)
-    sparse_blocks = pga.pga_profile_sparse_blocks(eng.ctx)
+    sparse_blocks, sparse_gathers = pga.pga_profile_sparse(eng.ctx)
     pga.pga_profile_enable(eng.ctx, False)
     # roofline pass for the dense sweep kernel, right after the timed region:
     # the same population with the label-sparse pre-pass off, so every block
@@ -419,6 +422,18 @@ def main():
                          "frac_of_loop_ceiling": achieved / (LOOP_PAIRS_PER_CLK * SM_COUNT * sm_max * 1e6),
                          "loop_ceiling_basis": "measured bare inner loop (tools/mb_pairloop.cu): "
                                                "26.8 pairs/clk/SM, register-file-read bound"},
+            "roofline_sparse_pass": ({
+                "bound": "l2", "kernel": "k_fitness_sparse",
+                "achieved": sparse_gathers / (prof["fold_ms"] / 1000.0),
+                "peak": L2_GATHERS_PER_S, "unit": "C-entry gathers/s",
+                "frac": sparse_gathers / (prof["fold_ms"] / 1000.0) / L2_GATHERS_PER_S,
+                "work_per_launch": "%.4g gathers (sum over the blocks it evaluated of n_s(n_s-1)/2 + n_s "
+                                   "per cluster), average over the timed launches"
+                                   % (sparse_gathers / float(ngen)),
+                "peak_basis": "measured random 8-byte gathers from an L2-resident 2 MB fp64 array "
+                              "(tools/mb_l2gather.cu): 3.03e11/s = 9.7 TB/s of 32-byte sectors",
+                "share_of_timed_generation": sparse_ms / gen_ms}
+                if sparse_gathers > 0 and prof["fold_ms"] > 0 else None),
             "gpu_launches": int(launches),
             "clocks": clk,
             "best_L": st["best_L"],

@@ -82,6 +82,7 @@ _SIGS = {
     "pga_launch_count": (ct.c_int64, []),
     "pga_set_sparse_threshold": (ct.c_int, [ct.c_void_p, ct.c_double]),
     "pga_profile_sparse_blocks": (ct.c_int, [ct.c_void_p, ct.c_void_p]),
+    "pga_profile_sparse": (ct.c_int, [ct.c_void_p, ct.c_void_p, ct.c_void_p]),
     "pga_rep_evaluate": (ct.c_int, [ct.c_void_p, ct.c_int64, ct.c_int64, ct.c_void_p, ct.c_void_p]),
     "pga_rep_commit": (ct.c_int, [ct.c_void_p, ct.c_void_p, ct.c_void_p]),
     "pga_stream_count": (ct.c_int, [ct.c_int32, ct.c_int32, ct.c_int32]),
@@ -333,6 +334,13 @@ def pga_profile_sparse_blocks(ctx) -> int:
     v = ct.c_int64()
     _check(lib().pga_profile_sparse_blocks(ctx, ct.byref(v)))
     return v.value
+
+
+def pga_profile_sparse(ctx):
+    """(blocks evaluated by the label-sparse pre-pass, C entries it gathered)."""
+    v, g = ct.c_int64(), ct.c_int64()
+    _check(lib().pga_profile_sparse(ctx, ct.byref(v), ct.byref(g)))
+    return v.value, g.value
 
 
 def pga_set_sparse_threshold(ctx, theta: float):

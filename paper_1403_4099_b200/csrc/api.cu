@@ -350,8 +350,8 @@ int pga_create(const double *C, int32_t N, const pga_params *p, pga_ctx **out) {
     rc = rc ? rc : dalloc(&c->lgtab, (size_t)2 * (N + 1));
     rc = rc ? rc : dalloc(&c->sflag, (size_t)(c->Pcap / CB + 1));
     rc = rc ? rc : dalloc(&c->sp_live, (size_t)6);
-    rc = rc ? rc : dalloc(&c->sp_blocks, (size_t)1);
-    if (!rc && cudaMemset(c->sp_blocks, 0, sizeof(unsigned long long)) != cudaSuccess)
+    rc = rc ? rc : dalloc(&c->sp_blocks, (size_t)2);
+    if (!rc && cudaMemset(c->sp_blocks, 0, 2 * sizeof(unsigned long long)) != cudaSuccess)
         rc = fail(PGA_EDEVICE, "memset sp_blocks");
     for (int b = 0; b < 2 && !rc; ++b) {
         rc = rc ? rc : dalloc(&c->pop[b], cm);
@@ -633,17 +633,22 @@ int pga_profile_enable(pga_ctx *c, int32_t on) {
     c->prof_level = on;
     c->prof_used = 0;
     PGA_CUDA(cudaSetDevice(c->device));
-    PGA_CUDA(cudaMemsetAsync(c->sp_blocks, 0, sizeof(unsigned long long), c->stream));
+    PGA_CUDA(cudaMemsetAsync(c->sp_blocks, 0, 2 * sizeof(unsigned long long), c->stream));
     return PGA_OK;
 }
 
 int pga_profile_sparse_blocks(pga_ctx *c, int64_t *sparse_blocks) {
+    return pga_profile_sparse(c, sparse_blocks, nullptr);
+}
+
+int pga_profile_sparse(pga_ctx *c, int64_t *sparse_blocks, int64_t *gathered) {
     if (!c || !sparse_blocks) return fail(PGA_EINVAL, "NULL argument");
     PGA_CUDA(cudaSetDevice(c->device));
-    unsigned long long v = 0;
-    PGA_CUDA(cudaMemcpyAsync(&v, c->sp_blocks, sizeof(v), cudaMemcpyDeviceToHost, c->stream));
+    unsigned long long v[2] = {0, 0};
+    PGA_CUDA(cudaMemcpyAsync(v, c->sp_blocks, sizeof(v), cudaMemcpyDeviceToHost, c->stream));
     PGA_CUDA(cudaStreamSynchronize(c->stream));
-    *sparse_blocks = (int64_t)v;
+    *sparse_blocks = (int64_t)v[0];
+    if (gathered) *gathered = (int64_t)v[1];
     return PGA_OK;
 }
 

@@ -498,7 +498,7 @@ struct SparseArgs {
     uint8_t *sflag;
     uint32_t max_pairs;           // sparse iff every chromosome needs <= max_pairs pair updates
     int32_t *live;                // GA hysteresis [0]: any block went sparse last launch, [1] any now, [2] CTA count; null = always check
-    unsigned long long *nsparse;  // count of blocks evaluated here (profiling)
+    unsigned long long *nsparse;  // [0] blocks evaluated here, [1] C entries gathered (profiling)
     int nblocks;
     double fx_scale, fx_inv;
     const double *lgn, *lgnn;
@@ -666,6 +666,7 @@ __global__ void __launch_bounds__(SP_T, 5) k_fitness_sparse(SparseArgs a) {
         // links clusters that span passes, and every completed cluster with
         // n >= 2 and c > n (Q2) is queued for its Eq. 8 summand
         int carry_s = -1, qcnt = 0;
+        unsigned long long npair = 0;
         long long carry = 0;
         double fsum = 0.0, fbest = 0.0;
         int kbest = 0x7FFFFFFF;
@@ -679,6 +680,7 @@ __global__ void __launch_bounds__(SP_T, 5) k_fitness_sparse(SparseArgs a) {
                 n = (int)off[s + 1] - (int)off[s];
                 if (n >= 2) {
                     const int st = off[s], av = t - st;
+                    if (av == 0) npair += (unsigned long long)n * (n - 1) / 2 + n;   // pairs + diagonal, once per cluster
                     const double *Cg = C + (size_t)g * a.ldc;
                     acc = __double2ll_rn(__ldg(a.diag + g) * a.fx_scale);
                     const int h = (n - 1) >> 1;
@@ -768,6 +770,11 @@ __global__ void __launch_bounds__(SP_T, 5) k_fitness_sparse(SparseArgs a) {
                 fbest = of;
                 kbest = ok;
             }
+        }
+        if (a.nsparse) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) npair += __shfl_xor_sync(0xFFFFFFFFu, npair, o);
+            if (lane == 0) atomicAdd(a.nsparse + 1, npair);
         }
         if (lane == 0) {
             a.L[p] = 0.5 * fsum;
