@@ -427,8 +427,9 @@ def main():
                 "achieved": sparse_gathers / (prof["fold_ms"] / 1000.0),
                 "peak": L2_GATHERS_PER_S, "unit": "C-entry gathers/s",
                 "frac": sparse_gathers / (prof["fold_ms"] / 1000.0) / L2_GATHERS_PER_S,
-                "work_per_launch": "%.4g gathers (sum over the blocks it evaluated of n_s(n_s-1)/2 + n_s "
-                                   "per cluster), average over the timed launches"
+                "work_per_launch": "%.4g gathers (sum over the blocks it evaluated of n_s(n_s-1)/2 per "
+                                   "cluster; the diagonal comes from a 4 KB array in L1), average over the "
+                                   "timed launches"
                                    % (sparse_gathers / float(ngen)),
                 "peak_basis": "measured random 8-byte gathers from an L2-resident 2 MB fp64 array "
                               "(tools/mb_l2gather.cu): 3.03e11/s = 9.7 TB/s of 32-byte sectors",

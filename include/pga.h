@@ -371,8 +371,8 @@ int pga_profile_enable(pga_ctx *ctx, int32_t on);
 int pga_profile_read(pga_ctx *ctx, double *sweep_ms, double *fold_ms, double *gen_ms,
                      int32_t *count);
 int pga_profile_sparse_blocks(pga_ctx *ctx, int64_t *sparse_blocks);
-/* Same, plus the C entries the pre-pass gathered (sum over its chromosomes'
- * clusters of n_s(n_s-1)/2 + n_s); gathered may be NULL. */
+/* Same, plus the off-diagonal C entries the pre-pass gathered (sum over its
+ * chromosomes' clusters of n_s(n_s-1)/2); gathered may be NULL. */
 int pga_profile_sparse(pga_ctx *ctx, int64_t *sparse_blocks, int64_t *gathered);
 
 /* Level-2 profiling: per-phase AVERAGE milliseconds, ms[PGA_PROF_PHASES]:

@@ -680,7 +680,7 @@ __global__ void __launch_bounds__(SP_T, 5) k_fitness_sparse(SparseArgs a) {
                 n = (int)off[s + 1] - (int)off[s];
                 if (n >= 2) {
                     const int st = off[s], av = t - st;
-                    if (av == 0) npair += (unsigned long long)n * (n - 1) / 2 + n;   // pairs + diagonal, once per cluster
+                    if (av == 0) npair += (unsigned long long)n * (n - 1) / 2;   // C pairs gathered (diag: L1), once per cluster
                     const double *Cg = C + (size_t)g * a.ldc;
                     acc = __double2ll_rn(__ldg(a.diag + g) * a.fx_scale);
                     const int h = (n - 1) >> 1;
