@@ -234,10 +234,27 @@ int pga_op_init(uint64_t seed, int32_t N, int64_t P, int64_t p_off, int32_t isla
  * label, L2 gathers of C for the pairs inside each cluster) and skipped by
  * the dense sweep.  The result is the same Eq. 5/6/8 value (within the
  * parity tolerance; deterministic).  theta in [0, 1]; 0 = always dense,
- * 1 = sparse whenever N <= 640.  Default 0.04.  During a GA run the check
+ * 1 = sparse whenever N <= 640; negative = automatic, the default: 0.25
+ * with the cluster cache on (pga_set_cluster_cache), 0.04 with it off.  The
+ * pass is cheaper than the dense sweep up to about 4% of the pairs when
+ * every pair is gathered, and up to a quarter when most clusters are cache
+ * hits, as in GA generations.  During a GA run the check
  * stops once a generation had no sparse block (the population only gets
  * denser); pga_init / pga_set_population re-arm it.  Host only. */
 int pga_set_sparse_threshold(pga_ctx *ctx, double theta);
+
+/* Cluster cache of the label-sparse pass (on by default; N <= 640).  c_s
+ * (Eq. 6) depends only on the member set of cluster s, and a GA generation
+ * repeats almost every cluster of the one before (elites are copied,
+ * knowledge-based crossover transplants whole clusters, mutation moves a
+ * few genes).  Clusters with at least 6 members are keyed by two 64-bit
+ * Zobrist sums of their members plus n_s, and their exact 64-bit
+ * fixed-point c_s is kept in a device hash table (64 slots per chromosome,
+ * 2^12..2^22 slots of 32 B; cleared by the pass itself when half full).  A
+ * hit replaces the cluster's n_s(n_s-1)/2 gathers.  Results are
+ * bit-identical with the cache on or off (a wrong hit needs a 128-bit key
+ * collision).  on: 0 = off, else on.  Host only. */
+int pga_set_cluster_cache(pga_ctx *ctx, int32_t on);
 
 /* ---------------------------------------------------------------------
  * Replicated master-slave across GPUs.  The paper's
@@ -374,6 +391,9 @@ int pga_profile_sparse_blocks(pga_ctx *ctx, int64_t *sparse_blocks);
 /* Same, plus the off-diagonal C entries the pre-pass gathered (sum over its
  * chromosomes' clusters of n_s(n_s-1)/2); gathered may be NULL. */
 int pga_profile_sparse(pga_ctx *ctx, int64_t *sparse_blocks, int64_t *gathered);
+/* Cluster-cache hits since profiling was enabled, and the off-diagonal pair
+ * updates they replaced (pga_set_cluster_cache).  Synchronises. */
+int pga_profile_cache(pga_ctx *ctx, int64_t *hits, int64_t *saved);
 
 /* Level-2 profiling: per-phase AVERAGE milliseconds, ms[PGA_PROF_PHASES]:
  * 0 dense fitness kernel (sweep + fused fold), 1 label-sparse pre-pass, 2 statistics/termination,

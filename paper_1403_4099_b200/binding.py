@@ -83,6 +83,8 @@ _SIGS = {
     "pga_set_sparse_threshold": (ct.c_int, [ct.c_void_p, ct.c_double]),
     "pga_profile_sparse_blocks": (ct.c_int, [ct.c_void_p, ct.c_void_p]),
     "pga_profile_sparse": (ct.c_int, [ct.c_void_p, ct.c_void_p, ct.c_void_p]),
+    "pga_set_cluster_cache": (ct.c_int, [ct.c_void_p, ct.c_int32]),
+    "pga_profile_cache": (ct.c_int, [ct.c_void_p, ct.c_void_p, ct.c_void_p]),
     "pga_rep_evaluate": (ct.c_int, [ct.c_void_p, ct.c_int64, ct.c_int64, ct.c_void_p, ct.c_void_p]),
     "pga_rep_commit": (ct.c_int, [ct.c_void_p, ct.c_void_p, ct.c_void_p]),
     "pga_stream_count": (ct.c_int, [ct.c_int32, ct.c_int32, ct.c_int32]),
@@ -346,6 +348,18 @@ def pga_profile_sparse(ctx):
 def pga_set_sparse_threshold(ctx, theta: float):
     """theta: 0 = dense sweep only; 1 = label-sparse whenever N <= 640."""
     _check(lib().pga_set_sparse_threshold(ctx, float(theta)))
+
+
+def pga_set_cluster_cache(ctx, on: bool):
+    """Cluster cache of the label-sparse pass (default on); results are identical either way."""
+    _check(lib().pga_set_cluster_cache(ctx, 1 if on else 0))
+
+
+def pga_profile_cache(ctx):
+    """(cluster-cache hits, pair updates they replaced) since profiling was enabled."""
+    h, v = ct.c_int64(), ct.c_int64()
+    _check(lib().pga_profile_cache(ctx, ct.byref(h), ct.byref(v)))
+    return h.value, v.value
 
 
 def pga_rep_evaluate(ctx, begin: int, end: int, L_dev, top_dev):

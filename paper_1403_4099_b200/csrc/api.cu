@@ -36,7 +36,8 @@ int launch_init_raw(uint64_t seed, int N, int ldn, int64_t P, int64_t Pcap, int6
 int run_select_ops(const double *L, int64_t P, const pga_params &p, int32_t gen, int32_t island,
                    int32_t *order, int32_t *sel, uint64_t *keys_in, uint64_t *keys_out,
                    int32_t *idx_in, uint64_t *q, uint64_t *prefix, void *tmp, size_t tmp_bytes,
-                   const int32_t *done, cudaStream_t s, const int32_t *gen_ptr, bool sorted);
+                   const int32_t *done, cudaStream_t s, const int32_t *gen_ptr, bool sorted,
+                   int32_t *sigma);
 int run_mates(int64_t M, const pga_params &p, int32_t gen, int32_t island, uint32_t *k_in,
               uint32_t *k_out, int32_t *m_in, int32_t *sigma, void *tmp, size_t tmp_bytes,
               const int32_t *done, cudaStream_t s, const int32_t *gen_ptr);
@@ -118,7 +119,8 @@ struct Graphs {
 void free_ctx(pga_ctx *c) {
     if (!c) return;
     cudaSetDevice(c->device);
-    void *ptrs[] = {c->C, c->diag, c->lgtab, c->sflag, c->sp_live, c->sp_blocks, c->pop[0], c->pop[1], c->popT[0], c->popT[1], c->V, c->L,
+    void *ptrs[] = {c->C, c->diag, c->lgtab, c->sflag, c->sp_live, c->sp_blocks, c->cc, c->cc_state,
+                    c->cc_keys, c->pop[0], c->pop[1], c->popT[0], c->popT[1], c->V, c->L,
                     c->top, c->keys_in, c->keys_out, c->idx_in, c->order, c->q, c->prefix,
                     c->sel, c->mkeys_in, c->mkeys_out, c->m_in, c->sigma, c->cub_tmp, c->st,
                     c->best_labels, c->history, c->stage_i32, c->evCM, c->evGM, c->evL,
@@ -350,9 +352,34 @@ int pga_create(const double *C, int32_t N, const pga_params *p, pga_ctx **out) {
     rc = rc ? rc : dalloc(&c->lgtab, (size_t)2 * (N + 1));
     rc = rc ? rc : dalloc(&c->sflag, (size_t)(c->Pcap / CB + 1));
     rc = rc ? rc : dalloc(&c->sp_live, (size_t)6);
-    rc = rc ? rc : dalloc(&c->sp_blocks, (size_t)2);
-    if (!rc && cudaMemset(c->sp_blocks, 0, 2 * sizeof(unsigned long long)) != cudaSuccess)
+    rc = rc ? rc : dalloc(&c->sp_blocks, (size_t)4);
+    if (!rc && cudaMemset(c->sp_blocks, 0, 4 * sizeof(unsigned long long)) != cudaSuccess)
         rc = fail(PGA_EDEVICE, "memset sp_blocks");
+    if (!rc && N <= 640) {
+        // cluster cache: 64 slots per chromosome, 2^12 .. 2^22 slots (32 B each)
+        uint32_t slots = 1u << 12;
+        while (slots < (1u << 22) && (int64_t)slots < 64 * c->P) slots <<= 1;
+        c->cc_mask = slots - 1u;
+        rc = rc ? rc : dalloc(&c->cc, (size_t)slots);
+        rc = rc ? rc : dalloc(&c->cc_state, (size_t)4);
+        rc = rc ? rc : dalloc(&c->cc_keys, (size_t)2 * N);
+        if (!rc && (cudaMemset(c->cc, 0, sizeof(CCSlot) * slots) != cudaSuccess ||
+                    cudaMemset(c->cc_state, 0, 4 * sizeof(uint32_t)) != cudaSuccess))
+            rc = fail(PGA_EDEVICE, "memset cluster cache");
+        if (!rc) {
+            // Zobrist keys: splitmix64 of a fixed seed (any fixed keys do)
+            std::vector<uint64_t> k(2 * (size_t)N);
+            uint64_t x = 0x1403409900000001ull;
+            for (auto &v : k) {
+                uint64_t z = (x += 0x9E3779B97F4A7C15ull);
+                z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+                z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+                v = z ^ (z >> 31);
+            }
+            if (cudaMemcpy(c->cc_keys, k.data(), sizeof(uint64_t) * k.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+                rc = fail(PGA_EDEVICE, "copy cache keys");
+        }
+    }
     for (int b = 0; b < 2 && !rc; ++b) {
         rc = rc ? rc : dalloc(&c->pop[b], cm);
         rc = rc ? rc : dalloc(&c->popT[b], gm);
@@ -494,8 +521,8 @@ int pga_gen_evaluate(pga_ctx *c, int32_t *is_migration) {
 
 int pga_set_sparse_threshold(pga_ctx *c, double theta) {
     if (!c) return fail(PGA_EINVAL, "ctx is NULL");
-    if (!(theta >= 0.0 && theta <= 1.0)) return fail(PGA_EINVAL, "theta must lie in [0, 1]");
-    c->sparse_theta = theta;
+    if (!(theta <= 1.0)) return fail(PGA_EINVAL, "theta must lie in [0, 1] (negative = automatic)");
+    c->sparse_theta = theta < 0.0 ? -1.0 : theta;
     return PGA_OK;
 }
 
@@ -633,7 +660,24 @@ int pga_profile_enable(pga_ctx *c, int32_t on) {
     c->prof_level = on;
     c->prof_used = 0;
     PGA_CUDA(cudaSetDevice(c->device));
-    PGA_CUDA(cudaMemsetAsync(c->sp_blocks, 0, 2 * sizeof(unsigned long long), c->stream));
+    PGA_CUDA(cudaMemsetAsync(c->sp_blocks, 0, 4 * sizeof(unsigned long long), c->stream));
+    return PGA_OK;
+}
+
+int pga_set_cluster_cache(pga_ctx *c, int32_t on) {
+    if (!c) return fail(PGA_EINVAL, "ctx is NULL");
+    c->cc_on = on != 0;
+    return PGA_OK;
+}
+
+int pga_profile_cache(pga_ctx *c, int64_t *hits, int64_t *saved) {
+    if (!c || !hits || !saved) return fail(PGA_EINVAL, "NULL argument");
+    PGA_CUDA(cudaSetDevice(c->device));
+    unsigned long long v[4] = {0, 0, 0, 0};
+    PGA_CUDA(cudaMemcpyAsync(v, c->sp_blocks, sizeof(v), cudaMemcpyDeviceToHost, c->stream));
+    PGA_CUDA(cudaStreamSynchronize(c->stream));
+    *hits = (int64_t)v[2];
+    *saved = (int64_t)v[3];
     return PGA_OK;
 }
 
@@ -804,7 +848,7 @@ int pga_op_select(const double *L, int64_t P, const pga_params *p, int32_t gen, 
     TRY(hb.get((unsigned char **)&tmp, tb));
     PGA_CUDA(cudaMemcpy(dL, L, sizeof(double) * P, cudaMemcpyHostToDevice));
     TRY(run_select_ops(dL, P, *p, gen, island, dorder, dsel, k1, k2, didx, q, pre, tmp, tb, nullptr,
-                       0, nullptr, false));
+                       0, nullptr, false, nullptr));
     PGA_CUDA(cudaDeviceSynchronize());
     PGA_CUDA(cudaMemcpy(order_out, dorder, sizeof(int32_t) * P, cudaMemcpyDeviceToHost));
     PGA_CUDA(cudaMemcpy(sel_out, dsel, sizeof(int32_t) * M, cudaMemcpyDeviceToHost));

@@ -479,9 +479,85 @@ k_fitness(const __grid_constant__ CUtensorMap tmLab0, const __grid_constant__ CU
 // 64-bit fixed point (each term rounded to 2^-S, then integer sums: exact,
 // order-free, deterministic); Eq. 8 from the tables.  The block is then
 // flagged so that k_fitness skips it.  Work ~ sum_s n_s^2 instead of N^2.
+//
+// Cluster cache: c_s is a function of the member set alone (C is fixed for
+// the ctx), and a GA generation repeats almost all of the previous one's
+// clusters (elites, knowledge-based crossover transplants whole clusters,
+// mutation moves ~2 genes; tools/cache_hit.py measures 93-99 % of the C4
+// pairs).  A cluster with n >= CC_NMIN is keyed by the XOR of its members'
+// 128-bit Zobrist keys (plus n) and looked up in a device hash table of exact
+// fixed-point c_s; a hit replaces its n(n-1)/2 gathers, a miss is gathered
+// and inserted.  The value is bit-identical either way (the fixed-point sum
+// is order-free), so the cache changes cost, never results, short of a
+// 128-bit key collision.
 // ---------------------------------------------------------------------------
 constexpr int SP_W = 8, SP_T = SP_W * 32;
 constexpr int SPARSE_MAXN = 640;   // shared-memory footprint (sparse_smem) must fit one CTA
+#ifndef PGA_CC_NMIN
+#define PGA_CC_NMIN 6
+#endif
+#ifndef PGA_SP_MINB
+#define PGA_SP_MINB 3
+#endif
+constexpr int CC_NMIN = PGA_CC_NMIN;   // clusters this large go through the cache
+constexpr int CC_PROBE = 8;        // linear-probe length
+
+__host__ __device__ __forceinline__ int cc_entries(int N) { return N / CC_NMIN + 1; }
+
+__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t *p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// slot: k1 claimed by CAS (0 = empty); k2, v and chk = cc_mix(k1, k2, v, n)
+// are then written once.  A reader takes the slot only if k1, k2 and the
+// checksum agree, so a half-written slot reads as a miss without any
+// ordering between the fields (relaxed L2 loads; no L1 invalidation).
+__device__ __forceinline__ uint64_t cc_mix(uint64_t k1, uint64_t k2, long long v, uint32_t n) {
+    uint64_t z = k1 ^ (k2 * 0x9E3779B97F4A7C15ull) ^ ((uint64_t)v * 0xBF58476D1CE4E5B9ull) ^ ((uint64_t)n << 47);
+    z ^= z >> 31;
+    z *= 0x94D049BB133111EBull;
+    z ^= z >> 29;
+    return z | 1ull;
+}
+
+__device__ __forceinline__ bool cc_find(pga::CCSlot *T, uint32_t mask, uint64_t k1, uint64_t k2, uint32_t n,
+                                        long long *v) {
+    uint32_t i = (uint32_t)(k1 >> 17) & mask;
+    for (int r = 0; r < CC_PROBE; ++r) {
+        const uint64_t s1 = ld_relaxed_u64(&T[i].k1);
+        if (s1 == 0) return false;
+        if (s1 == k1) {
+            const uint64_t s2 = ld_relaxed_u64(&T[i].k2);
+            const long long sv = (long long)ld_relaxed_u64(reinterpret_cast<const uint64_t *>(&T[i].v));
+            const uint64_t sc = ld_relaxed_u64(&T[i].chk);
+            if (s2 != k2 || sc != cc_mix(k1, k2, sv, n)) return false;
+            *v = sv;
+            return true;
+        }
+        i = (i + 1) & mask;
+    }
+    return false;
+}
+
+__device__ __forceinline__ void cc_insert(pga::CCSlot *T, uint32_t mask, uint32_t *fill, uint64_t k1,
+                                          uint64_t k2, uint32_t n, long long v) {
+    uint32_t i = (uint32_t)(k1 >> 17) & mask;
+    for (int r = 0; r < CC_PROBE; ++r) {
+        const unsigned long long old =
+            atomicCAS(reinterpret_cast<unsigned long long *>(&T[i].k1), 0ull, (unsigned long long)k1);
+        if (old == 0ull) {
+            T[i].k2 = k2;
+            T[i].v = v;
+            T[i].chk = cc_mix(k1, k2, v, n);
+            atomicAdd(fill, 1u);
+            return;
+        }
+        if (old == k1) return;   // inserted by another chromosome
+        i = (i + 1) & mask;
+    }
+}
 
 struct SparseArgs {
     const uint16_t *cm0, *cm1;
@@ -498,10 +574,14 @@ struct SparseArgs {
     uint8_t *sflag;
     uint32_t max_pairs;           // sparse iff every chromosome needs <= max_pairs pair updates
     int32_t *live;                // GA hysteresis [0]: any block went sparse last launch, [1] any now, [2] CTA count; null = always check
-    unsigned long long *nsparse;  // [0] blocks evaluated here, [1] C entries gathered (profiling)
+    unsigned long long *nsparse;  // [0] blocks evaluated here, [1] C entries gathered, [2] cache hits, [3] pairs they saved (profiling)
     int nblocks;
     double fx_scale, fx_inv;
     const double *lgn, *lgnn;
+    pga::CCSlot *cc;              // cluster cache (null = off)
+    uint32_t cc_mask;             // slots - 1
+    uint32_t *cc_state;           // [0] fill, [1] clear request, [2] CTA count
+    const uint64_t *cc_keys;      // [N][2] Zobrist keys
 };
 
 __host__ __device__ __forceinline__ int sp_words(int N) { return (N + 2) / 2; }   // packed u16 counters for labels 0..N
@@ -509,8 +589,9 @@ __host__ __device__ __forceinline__ int sp_words(int N) { return (N + 2) / 2; } 
 constexpr int SPQ = 64;   // per-warp queue of completed clusters awaiting their Eq. 8 summand
 
 __host__ __device__ __forceinline__ size_t sp_per_warp(int N) {
-    return (((size_t)sp_words(N) * 4 /*cnt, then scatter counters*/ + (size_t)(N + 2) * 2 /*off*/ +
-             (size_t)N * 2 /*perm*/ + (size_t)SPQ * 12 /*queue*/ + 64) + 15) &
+    return (((size_t)sp_words(N) * 4 /*counts, then ordinals*/ + (size_t)(N + 2) * 4 /*off*/ +
+             (size_t)N * 4 /*perm2*/ + (size_t)SPQ * 12 /*queue*/ + (size_t)cc_entries(N) * 18 /*cache entries, n*/ +
+             64) + 15) &
            ~(size_t)15;
 }
 
@@ -520,7 +601,7 @@ static size_t sparse_smem(int N) {
     return warps > tile ? warps : tile;
 }
 
-__global__ void __launch_bounds__(SP_T, 5) k_fitness_sparse(SparseArgs a) {
+__global__ void __launch_bounds__(SP_T, PGA_SP_MINB) k_fitness_sparse(SparseArgs a) {
     if (a.done && *a.done) return;
     extern __shared__ __align__(16) unsigned char sps[];
     __shared__ uint32_t s_maxp;
@@ -531,11 +612,12 @@ __global__ void __launch_bounds__(SP_T, 5) k_fitness_sparse(SparseArgs a) {
     const uint16_t *CM = par ? a.cm1 : a.cm0;
     unsigned char *wb = sps + (size_t)warp * sp_per_warp(N);
     double *qc = reinterpret_cast<double *>(wb);                         // [SPQ] queued c
-    uint32_t *qnk = reinterpret_cast<uint32_t *>(qc + SPQ);             // [SPQ] queued n | label << 16
-    uint32_t *cq = qnk + SPQ;                                            // [W] packed counts
-    uint32_t *run = cq;                                                  // [W] scatter counters (after the offsets)
-    uint16_t *off = reinterpret_cast<uint16_t *>(cq + W);               // [N+2]
-    uint16_t *perm = off + (N + 2);                                      // [N]
+    ulonglong2 *cent = reinterpret_cast<ulonglong2 *>(qc + SPQ);        // [E] Zobrist sums, then hit {c, 0} / miss {k1, k2}
+    uint32_t *qnk = reinterpret_cast<uint32_t *>(cent + cc_entries(N)); // [SPQ] queued n | label << 16
+    uint32_t *cq = qnk + SPQ;                                            // [W] packed u16 counts, then ordinals
+    uint32_t *off = cq + W;                                              // [N+2] cluster starts, then ends
+    uint32_t *perm2 = off + (N + 2);                                     // [N] sorted genes: g | s << 16
+    uint16_t *cn = reinterpret_cast<uint16_t *>(perm2 + N);             // [E] n of each cached cluster
     if (a.live && a.live[0] == 0) {     // the population went dense: skip (flags cleared)
         if (tid == 0) a.sflag[cb] = 0;
         return;
@@ -543,6 +625,10 @@ __global__ void __launch_bounds__(SP_T, 5) k_fitness_sparse(SparseArgs a) {
     // every block was sparse at the last check: evaluate sparsely without
     // checking, except on every 16th launch (the population densifies)
     const bool skip1 = a.live && a.live[3] != 0 && (a.live[5] & 15) != 0;
+    // cache clear request (the table is half full): this launch clears it
+    // and neither reads nor writes it
+    const bool cc_clear = a.cc && *reinterpret_cast<volatile uint32_t *>(a.cc_state + 1) != 0u;
+    const bool use_cache = a.cc && !cc_clear;
     if (tid == 0) s_maxp = 0u;
     __syncthreads();
     if (!skip1) {
@@ -589,6 +675,25 @@ __global__ void __launch_bounds__(SP_T, 5) k_fitness_sparse(SparseArgs a) {
                 *reinterpret_cast<const uint32_t *>(&tile[i * TSP + 2 * pr]);
         }
     }
+    if (cc_clear) {
+        const uint32_t slots = a.cc_mask + 1u, per = (slots + gridDim.x - 1) / gridDim.x;
+        const uint32_t lo = blockIdx.x * per, hi = min(slots, lo + per);
+        for (uint32_t i = lo + tid; i < hi; i += SP_T) a.cc[i] = pga::CCSlot{};
+    }
+    if (a.cc && tid == 0) {
+        // the last CTA to get here toggles the clear request (CTAs read it at
+        // their start, and all have started by then)
+        __threadfence();
+        if (atomicAdd(a.cc_state + 2, 1u) == gridDim.x - 1) {
+            if (cc_clear) {
+                a.cc_state[0] = 0u;
+                a.cc_state[1] = 0u;
+            } else if (atomicAdd(a.cc_state, 0u) > (a.cc_mask >> 1)) {
+                a.cc_state[1] = 1u;
+            }
+            a.cc_state[2] = 0u;
+        }
+    }
     if (tid == 0) {
         a.sflag[cb] = sparse ? 1 : 0;
         if (sparse && a.nsparse) atomicAdd(a.nsparse, 1ull);
@@ -615,6 +720,8 @@ __global__ void __launch_bounds__(SP_T, 5) k_fitness_sparse(SparseArgs a) {
 
     // ---- pass 2: exact label-sparse evaluation
     const double *C = a.C;
+    const uint4 *keys4 = reinterpret_cast<const uint4 *>(a.cc_keys);
+    uint16_t *ordm = reinterpret_cast<uint16_t *>(cq);
     for (int q = warp; q < pga::CB; q += SP_W) {
         const int64_t p = (int64_t)cb * pga::CB + q;
         if (p >= a.P) break;
@@ -633,54 +740,102 @@ __global__ void __launch_bounds__(SP_T, 5) k_fitness_sparse(SparseArgs a) {
         for (int o = 16; o > 0; o >>= 1) kmax = max(kmax, __shfl_xor_sync(0xFFFFFFFFu, kmax, o));
         const int K = min((int)kmax + 1, N);
         __syncwarp();
-        // offsets: exclusive prefix of the counts over labels 0..K-1
-        int base = 0;
+        // offsets (exclusive prefix of the counts over labels 0..K-1), and the
+        // cache ordinals: a label with n >= CC_NMIN gets the next ordinal (in
+        // label order) and a zeroed Zobrist accumulator; ordm[k] (in place
+        // over its 16-bit count) = ordinal, or 0xFFFF
+        int base = 0, ecnt = 0;
         for (int k0 = 0; k0 < K; k0 += 32) {
             const int k = k0 + lane;
-            const int n = k < K ? (int)((cq[k >> 1] >> (16 * (k & 1))) & 0xFFFFu) : 0;
+            const int n = k < K ? (int)ordm[k] : 0;
             int incl = n;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const int t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
                 if (lane >= o) incl += t;
             }
-            if (k < K) off[k] = (uint16_t)(base + incl - n);
+            const bool el = use_cache && n >= CC_NMIN;
+            const unsigned bal = __ballot_sync(0xFFFFFFFFu, el);
+            if (k < K) {
+                off[k] = (uint32_t)(base + incl - n);
+                uint16_t om = 0xFFFFu;
+                if (el) {
+                    const int ord = ecnt + __popc(bal & lanemask_lt());
+                    om = (uint16_t)ord;
+                    cent[ord] = make_ulonglong2(0ull, 0ull);
+                    cn[ord] = (uint16_t)n;
+                }
+                ordm[k] = om;
+            }
+            ecnt += __popc(bal);
             base += __shfl_sync(0xFFFFFFFFu, incl, 31);
         }
-        if (lane == 0) off[K] = (uint16_t)base;      // n_s = off[s + 1] - off[s]
         __syncwarp();
-        for (int k = lane; k < W; k += 32) run[k] = 0u;   // the counts become scatter counters
-        __syncwarp();
-        // counting sort of the genes by label: clusters become contiguous runs
-        // in label order (order inside a cluster is free: sums are exact)
+        // counting sort of the genes by label (clusters become contiguous runs
+        // in label order; order inside a cluster is free: sums are exact), and
+        // the Zobrist XOR of each cached cluster's members.  Afterwards off[s]
+        // is the END of cluster s and its start is off[s - 1] (0 for s = 0).
 #pragma unroll 4
         for (int i = lane; i < N; i += 32) {
             const uint32_t s = lab[i];
-            const uint32_t sh = 16 * (s & 1u);
-            const uint32_t old = (atomicAdd(run + (s >> 1), 1u << sh) >> sh) & 0xFFFFu;
-            perm[off[s] + old] = (uint16_t)i;
+            const uint32_t pos = atomicAdd(off + s, 1u);
+            perm2[pos] = (uint32_t)i | (s << 16);
+            const uint32_t om = ordm[s];
+            if (om != 0xFFFFu) {
+                uint32_t *h = reinterpret_cast<uint32_t *>(cent + om);
+                const uint4 kk = __ldg(keys4 + i);
+                atomicXor(h, kk.x);
+                atomicXor(h + 1, kk.y);
+                atomicXor(h + 2, kk.z);
+                atomicXor(h + 3, kk.w);
+            }
         }
         __syncwarp();
-        // walk the sorted genes 32 at a time; lanes of one cluster are
-        // consecutive: a segmented sum gives each run's share of c_s, a carry
-        // links clusters that span passes, and every completed cluster with
-        // n >= 2 and c > n (Q2) is queued for its Eq. 8 summand
-        int carry_s = -1, qcnt = 0;
+        // one lookup per cached cluster, lane-parallel: a hit leaves {c, 0},
+        // a miss {k1, k2} (k2 != 0) for the insert once c is gathered
+        unsigned long long nhit = 0, nsaved = 0;
+        for (int o = lane; o < ecnt; o += 32) {
+            const ulonglong2 h = cent[o];
+            const uint64_t k1 = h.x | 1ull, k2 = h.y | 1ull;
+            const uint32_t n = cn[o];
+            long long v = 0;
+            if (cc_find(a.cc, a.cc_mask, k1, k2, n, &v)) {
+                cent[o] = make_ulonglong2((unsigned long long)v, 0ull);
+                nhit += 1;
+                nsaved += (unsigned long long)n * (n - 1) / 2;
+            } else {
+                cent[o] = make_ulonglong2(k1, k2);
+            }
+        }
+        __syncwarp();
+        // walk the sorted genes 32 at a time.  A lane's group is the window's
+        // lanes of its cluster (contiguous); the cluster open at the window's
+        // end carries on.
+        // Every completed cluster with n >= 2 and c > n (Q2) is queued for its
+        // Eq. 8 summand.
+        int qcnt = 0;
         unsigned long long npair = 0;
         long long carry = 0;
         double fsum = 0.0, fbest = 0.0;
         int kbest = 0x7FFFFFFF;
         for (int t0 = 0; t0 < N; t0 += 32) {
             const int t = t0 + lane;
-            int s = -1, n = 0;
+            int s = -1, st = t, en = t + 1, n = 0;
+            uint32_t om = 0xFFFFu;
             long long acc = 0;
             if (t < N) {
-                const int g = perm[t];
-                s = lab[g];
-                n = (int)off[s + 1] - (int)off[s];
-                if (n >= 2) {
-                    const int st = off[s], av = t - st;
-                    if (av == 0) npair += (unsigned long long)n * (n - 1) / 2;   // C pairs gathered (diag: L1), once per cluster
+                const uint32_t pg = perm2[t];
+                const int g = (int)(pg & 0xFFFFu);
+                s = (int)(pg >> 16);
+                en = (int)off[s];
+                st = s ? (int)off[s - 1] : 0;
+                n = en - st;
+                om = ordm[s];
+                if (om != 0xFFFFu && cent[om].y == 0ull) {        // cache hit: the head carries c_s
+                    acc = (t == st) ? (long long)cent[om].x : 0ll;
+                } else if (n >= 2) {
+                    const int av = t - st;
+                    if (av == 0) npair += (unsigned long long)n * (n - 1) / 2;   // C pairs gathered, once per cluster
                     const double *Cg = C + (size_t)g * a.ldc;
                     acc = __double2ll_rn(__ldg(a.diag + g) * a.fx_scale);
                     const int h = (n - 1) >> 1;
@@ -688,36 +843,43 @@ __global__ void __launch_bounds__(SP_T, 5) k_fitness_sparse(SparseArgs a) {
 #pragma unroll 4
                     for (int d = 1; d <= h; ++d) {
                         bidx = (bidx + 1 == n) ? 0 : bidx + 1;
-                        acc += 2 * __double2ll_rn(__ldg(Cg + perm[st + bidx]) * a.fx_scale);
+                        acc += 2 * __double2ll_rn(__ldg(Cg + (perm2[st + bidx] & 0xFFFFu)) * a.fx_scale);
                     }
                     if (!(n & 1) && av < (n >> 1))
-                        acc += 2 * __double2ll_rn(__ldg(Cg + perm[st + av + (n >> 1)]) * a.fx_scale);
+                        acc += 2 * __double2ll_rn(__ldg(Cg + (perm2[st + av + (n >> 1)] & 0xFFFFu)) * a.fx_scale);
                 } else {
                     s = -1;
+                    st = t;
+                    en = t + 1;
                 }
             }
-            const int sprev = __shfl_up_sync(0xFFFFFFFFu, s, 1);
-            const bool head = lane == 0 || sprev != s;
-            const unsigned heads = __ballot_sync(0xFFFFFFFFu, head);
-            // after step o: acc = sum over [lane, min(lane + 2o - 1, end of my run)]
+            // group sum = difference of the window's inclusive prefix sums at
+            // the group's ends (mod 2^64: exact)
+            const int lo = max(st - t0, 0), hi = min(en - t0, 32);
+            unsigned long long pre = (unsigned long long)acc;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                const long long v = __shfl_down_sync(0xFFFFFFFFu, acc, o);
-                const unsigned span = (unsigned)((((1ull << o) - 1ull) << (lane + 1)) & 0xFFFFFFFFull);
-                if (lane + o < 32 && (heads & span) == 0u) acc += v;
+                const unsigned long long v = __shfl_up_sync(0xFFFFFFFFu, pre, o);
+                if (lane >= o) pre += v;
             }
-            if (lane == 0 && s == carry_s && s >= 0) acc += carry;         // continues from the last pass
-            const int lastHead = 31 - __clz(heads);
-            const int sL = __shfl_sync(0xFFFFFFFFu, s, lastHead);
-            const long long accL = __shfl_sync(0xFFFFFFFFu, acc, lastHead);
-            const int nL = __shfl_sync(0xFFFFFFFFu, n, lastHead);
-            const bool openL = sL >= 0 && (int)off[sL] + nL > t0 + 32;    // last cluster goes on
-            // completed clusters of this pass -> queue (label order)
+            const unsigned long long phi = __shfl_sync(0xFFFFFFFFu, pre, hi - 1);
+            const unsigned long long plo = __shfl_sync(0xFFFFFFFFu, pre, lo > 0 ? lo - 1 : 0);
+            long long tot = (long long)(phi - (lo > 0 ? plo : 0ull));
+            if (s >= 0 && st < t0) tot += carry;                 // continues from the last window
+            const int s31 = __shfl_sync(0xFFFFFFFFu, s, 31);
+            const int en31 = __shfl_sync(0xFFFFFFFFu, en, 31);
+            const long long tot31 = __shfl_sync(0xFFFFFFFFu, tot, 31);
+            carry = (s31 >= 0 && en31 > t0 + 32) ? tot31 : 0ll;
+            // completed clusters of this window -> queue (label order)
             double c = 0.0;
             bool push = false;
-            if (head && s >= 0 && !(openL && lane == lastHead)) {
-                c = (double)acc * a.fx_inv;
+            if (s >= 0 && lane == lo && en <= t0 + 32) {
+                c = (double)tot * a.fx_inv;
                 push = c > (double)n;
+                if (om != 0xFFFFu) {
+                    const ulonglong2 e = cent[om];
+                    if (e.y != 0ull) cc_insert(a.cc, a.cc_mask, a.cc_state, e.x, e.y, (uint32_t)n, tot);
+                }
             }
             const unsigned bal = __ballot_sync(0xFFFFFFFFu, push);
             if (push) {
@@ -726,8 +888,6 @@ __global__ void __launch_bounds__(SP_T, 5) k_fitness_sparse(SparseArgs a) {
                 qnk[pos] = (uint32_t)n | ((uint32_t)s << 16);
             }
             qcnt += __popc(bal);
-            carry_s = openL ? sL : -1;
-            carry = accL;
             __syncwarp();
             if (qcnt >= 32) {            // a full batch of Eq. 8 summands, lane-parallel
                 const uint32_t nk = qnk[lane];
@@ -773,8 +933,16 @@ __global__ void __launch_bounds__(SP_T, 5) k_fitness_sparse(SparseArgs a) {
         }
         if (a.nsparse) {
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) npair += __shfl_xor_sync(0xFFFFFFFFu, npair, o);
-            if (lane == 0) atomicAdd(a.nsparse + 1, npair);
+            for (int o = 16; o > 0; o >>= 1) {
+                npair += __shfl_xor_sync(0xFFFFFFFFu, npair, o);
+                nhit += __shfl_xor_sync(0xFFFFFFFFu, nhit, o);
+                nsaved += __shfl_xor_sync(0xFFFFFFFFu, nsaved, o);
+            }
+            if (lane == 0) {
+                atomicAdd(a.nsparse + 1, npair);
+                atomicAdd(a.nsparse + 2, nhit);
+                atomicAdd(a.nsparse + 3, nsaved);
+            }
         }
         if (lane == 0) {
             a.L[p] = 0.5 * fsum;
@@ -913,7 +1081,7 @@ int launch_fitness_range(pga_ctx *c, const FitBufs &b, int64_t begin, int64_t en
     a.counters = c->counters;
     if (ev) PGA_CUDA(cudaEventRecord(ev[0], s));
     a.sflag = nullptr;
-    if (c->sparse_theta > 0.0 && N <= SPARSE_MAXN && c->sflag) {
+    if (sparse_theta_eff(c) > 0.0 && N <= SPARSE_MAXN && c->sflag) {
         // label-sparse pass first (f2); it flags the blocks it evaluated
         SparseArgs sp;
         sp.cm0 = b.cm0;
@@ -934,7 +1102,7 @@ int launch_fitness_range(pga_ctx *c, const FitBufs &b, int64_t begin, int64_t en
         sp.done = b.done;
         sp.sflag = c->sflag;
         const double dense = 0.5 * (double)N * (double)(N - 1);
-        sp.max_pairs = (uint32_t)fmin(4.0e9, floor(c->sparse_theta * dense));
+        sp.max_pairs = (uint32_t)fmin(4.0e9, floor(sparse_theta_eff(c) * dense));
         sp.live = b.gen ? c->sp_live : nullptr;     // hysteresis for GA generations only
         sp.nblocks = a.nCB;
         sp.nsparse = c->sp_blocks;
@@ -942,6 +1110,10 @@ int launch_fitness_range(pga_ctx *c, const FitBufs &b, int64_t begin, int64_t en
         sp.fx_inv = a.fx_inv;
         sp.lgn = a.lgn;
         sp.lgnn = a.lgnn;
+        sp.cc = c->cc_on ? c->cc : nullptr;
+        sp.cc_mask = c->cc_mask;
+        sp.cc_state = c->cc_state;
+        sp.cc_keys = c->cc_keys;
         k_fitness_sparse<<<(unsigned)a.nCB, SP_T, sparse_smem(N), s>>>(sp);
         PGA_LAUNCHED();
         a.sflag = c->sflag;

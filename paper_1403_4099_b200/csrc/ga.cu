@@ -228,11 +228,12 @@ __global__ void k_weights(const double *__restrict__ L, const int32_t *__restric
 __global__ void k_sus(const uint64_t *__restrict__ prefix, const double *__restrict__ L,
                       const int32_t *__restrict__ order, int64_t P, int64_t M, int scaling,
                       uint64_t seed, uint32_t gen, uint32_t island, int32_t *sel,
-                      const int32_t *done, const int32_t *gen_ptr) {
+                      const int32_t *done, const int32_t *gen_ptr, int32_t *sigma) {
     if (done && *done) return;
     const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (m >= M) return;
     if (gen_ptr) gen = (uint32_t)*gen_ptr;
+    if (sigma) sigma[m] = feistel_slot(m, M, seed, gen, island);   // mates fused (Q10)
     const double wmax = (scaling == PGA_SCALE_RANK) ? 1.0 : L[order[0]];
     if (!(wmax > 0.0)) {  // all-zero fitness: uniform fallback
         const U4 u = draw(seed, pga::TAG_SUS, island, gen, (uint32_t)m, 0u);
@@ -257,11 +258,12 @@ __global__ void k_sus(const uint64_t *__restrict__ prefix, const double *__restr
 
 __global__ void k_tournament(const double *__restrict__ L, int64_t P, int64_t M, int k,
                              uint64_t seed, uint32_t gen, uint32_t island, int32_t *sel,
-                             const int32_t *done, const int32_t *gen_ptr) {
+                             const int32_t *done, const int32_t *gen_ptr, int32_t *sigma) {
     if (done && *done) return;
     const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (m >= M) return;
     if (gen_ptr) gen = (uint32_t)*gen_ptr;
+    if (sigma) sigma[m] = feistel_slot(m, M, seed, gen, island);   // mates fused (Q10)
     const U4 u = draw(seed, pga::TAG_TOUR, island, gen, (uint32_t)m, 0u);
     int best = (int)scale_u32(u.x, (uint32_t)P);
     for (int t = 1; t < k; ++t) {
@@ -1108,7 +1110,8 @@ int launch_select_small(int what, const double *L, int64_t P, const pga_params &
 int run_select_ops(const double *L, int64_t P, const pga_params &p, int32_t gen, int32_t island,
                    int32_t *order, int32_t *sel, uint64_t *keys_in, uint64_t *keys_out,
                    int32_t *idx_in, uint64_t *q, uint64_t *prefix, void *tmp, size_t tmp_bytes,
-                   const int32_t *done, cudaStream_t s, const int32_t *gen_ptr, bool sorted) {
+                   const int32_t *done, cudaStream_t s, const int32_t *gen_ptr, bool sorted,
+                   int32_t *sigma) {
     const int64_t M = 2 * ((P - p.elite + 1) / 2);
     const unsigned nb = (unsigned)((P + 255) / 256);
     if (!sorted && P <= SMALL_P)   // one CTA; mates go to scratch (q)
@@ -1122,7 +1125,7 @@ int run_select_ops(const double *L, int64_t P, const pga_params &p, int32_t gen,
     if (p.selection == PGA_SEL_TOURNAMENT) {
         k_tournament<<<(unsigned)((M + 255) / 256), 256, 0, s>>>(L, P, M, p.tournament_k, p.seed,
                                                                 (uint32_t)gen, (uint32_t)island,
-                                                                sel, done, gen_ptr);
+                                                                sel, done, gen_ptr, sigma);
         PGA_LAUNCHED();
         return PGA_OK;
     }
@@ -1133,7 +1136,7 @@ int run_select_ops(const double *L, int64_t P, const pga_params &p, int32_t gen,
     count_launch();
     k_sus<<<(unsigned)((M + 255) / 256), 256, 0, s>>>(prefix, L, order, P, M, p.scaling, p.seed,
                                                       (uint32_t)gen, (uint32_t)island, sel, done,
-                                                      gen_ptr);
+                                                      gen_ptr, sigma);
     PGA_LAUNCHED();
     return PGA_OK;
 }
@@ -1214,15 +1217,12 @@ int launch_select_breed(pga_ctx *c, cudaStream_t s) {
         PGA_MARK(c, 5, s);
         PGA_MARK(c, 6, s);
     } else {
+        // selection with the Feistel mates fused into the same kernel
         rc = run_select_ops(c->L, c->P, p, 0, p.island, c->order, c->sel, c->keys_in, c->keys_out,
                             c->idx_in, c->q, c->prefix, c->cub_tmp, c->cub_tmp_bytes, done, s,
-                            genp, true);
+                            genp, true, c->sigma);
         if (rc) return rc;
         PGA_MARK(c, 5, s);
-        const int64_t M = 2 * ((c->P - p.elite + 1) / 2);
-        rc = run_mates(M, p, 0, p.island, c->mkeys_in, c->mkeys_out, c->m_in, c->sigma, c->cub_tmp,
-                       c->cub_tmp_bytes, done, s, genp);
-        if (rc) return rc;
         PGA_MARK(c, 6, s);
     }
     BreedArgs a{};
@@ -1244,7 +1244,7 @@ int launch_select_breed(pga_ctx *c, cudaStream_t s) {
     a.gen_ptr = genp;
     // the gene-major copy is produced by the label-sparse pass while its
     // checks are live (it transposes exactly the blocks the dense sweep needs)
-    a.gm_skip = (c->sparse_theta > 0.0 && c->N <= 640) ? c->sp_live : nullptr;
+    a.gm_skip = (sparse_theta_eff(c) > 0.0 && c->N <= 640) ? c->sp_live : nullptr;
     if (c->N <= BREED2_MAXN)
         k_breed2<false><<<(unsigned)((c->P + BS - 1) / BS), BW * 32, breed2_smem(c->N), s>>>(a);
     else

@@ -49,6 +49,15 @@ enum : uint32_t {
 constexpr int PROF_EV = 9;     // phase marks per profiled generation
 constexpr int CB = 32;         // chromosomes per fitness CTA tile (one per lane)
 
+// Cluster-cache slot (k_fitness_sparse): exact fixed-point c_s of a member
+// set keyed by two 64-bit Zobrist words; k1 == 0 empty; chk validates.
+struct alignas(32) CCSlot {
+    uint64_t k1;
+    uint64_t k2;
+    long long v;
+    uint64_t chk;
+};
+
 // Device-resident GA state (one island).  Read/written only by kernels.
 struct DevState {
     int32_t gen;          // generation about to be / being evaluated
@@ -84,9 +93,14 @@ struct pga_ctx {
     double *diag = nullptr;
     double *lgtab = nullptr;  // [2 (N+1)]: log n, log(n^2 - n) for the Eq. 8 fold (Q30)
     uint8_t *sflag = nullptr; // [Pcap / CB]: block evaluated by the label-sparse pass (f2)
-    double sparse_theta = 0.04;
+    double sparse_theta = -1.0;   // < 0: automatic (sparse_theta_eff)
     int32_t *sp_live = nullptr;  // device [6]: sparse-pass hysteresis (see k_fitness_sparse)
-    unsigned long long *sp_blocks = nullptr;  // device: blocks evaluated label-sparsely (profiling)
+    unsigned long long *sp_blocks = nullptr;  // device [4]: sparse blocks, gathers, cache hits, pairs saved (profiling)
+    pga::CCSlot *cc = nullptr;     // cluster cache table (N <= 640)
+    uint32_t cc_mask = 0;          // slots - 1
+    uint32_t *cc_state = nullptr;  // device [4]: fill, clear request, CTA count
+    uint64_t *cc_keys = nullptr;   // device [N][2] Zobrist keys
+    bool cc_on = true;
     // population: chromosome-major [Pcap][ldn] and gene-major [N][Pcap], double buffered
     uint16_t *pop[2] = {nullptr, nullptr};
     uint16_t *popT[2] = {nullptr, nullptr};
@@ -130,6 +144,14 @@ struct pga_ctx {
     size_t prof_used = 0;
     cudaEvent_t *pev = nullptr;         // this generation's events while profiling, else null
 };
+
+// Label-sparse threshold in effect: the caller's, else 0.25 with the cluster
+// cache (hits make a sparse block cheap up to a quarter of the dense pairs)
+// and 0.04 without it.
+inline double sparse_theta_eff(const pga_ctx *c) {
+    if (c->sparse_theta >= 0.0) return c->sparse_theta;
+    return (c->cc && c->cc_on) ? 0.25 : 0.04;
+}
 
 namespace pga {
 
