@@ -497,9 +497,10 @@ constexpr int SPARSE_MAXN = 640;   // shared-memory footprint (sparse_smem) must
 #define PGA_CC_NMIN 6
 #endif
 #ifndef PGA_SP_MINB
-#define PGA_SP_MINB 3
+#define PGA_SP_MINB 4
 #endif
 constexpr int CC_NMIN = PGA_CC_NMIN;   // clusters this large go through the cache
+static_assert(CC_NMIN >= 2, "large clusters must have pairs");
 constexpr int CC_PROBE = 8;        // linear-probe length
 
 __host__ __device__ __forceinline__ int cc_entries(int N) { return N / CC_NMIN + 1; }
@@ -589,9 +590,9 @@ __host__ __device__ __forceinline__ int sp_words(int N) { return (N + 2) / 2; } 
 constexpr int SPQ = 64;   // per-warp queue of completed clusters awaiting their Eq. 8 summand
 
 __host__ __device__ __forceinline__ size_t sp_per_warp(int N) {
-    return (((size_t)sp_words(N) * 4 /*counts, then ordinals*/ + (size_t)(N + 2) * 4 /*off*/ +
-             (size_t)N * 4 /*perm2*/ + (size_t)SPQ * 12 /*queue*/ + (size_t)cc_entries(N) * 18 /*cache entries, n*/ +
-             64) + 15) &
+    return (((size_t)sp_words(N) * 4 /*counts, then ordinals*/ + (size_t)sp_words(N + 2) * 4 /*off*/ +
+             (size_t)N * 4 /*perm2*/ + (size_t)SPQ * 12 /*queue*/ +
+             (size_t)cc_entries(N) * 20 /*hash/keys then f, n, label per large cluster*/ + 64) + 15) &
            ~(size_t)15;
 }
 
@@ -611,13 +612,16 @@ __global__ void __launch_bounds__(SP_T, PGA_SP_MINB) k_fitness_sparse(SparseArgs
     const int par = (a.gen && (*a.gen & 1)) ? 1 : 0;
     const uint16_t *CM = par ? a.cm1 : a.cm0;
     unsigned char *wb = sps + (size_t)warp * sp_per_warp(N);
-    double *qc = reinterpret_cast<double *>(wb);                         // [SPQ] queued c
-    ulonglong2 *cent = reinterpret_cast<ulonglong2 *>(qc + SPQ);        // [E] Zobrist sums, then hit {c, 0} / miss {k1, k2}
-    uint32_t *qnk = reinterpret_cast<uint32_t *>(cent + cc_entries(N)); // [SPQ] queued n | label << 16
-    uint32_t *cq = qnk + SPQ;                                            // [W] packed u16 counts, then ordinals
-    uint32_t *off = cq + W;                                              // [N+2] cluster starts, then ends
-    uint32_t *perm2 = off + (N + 2);                                     // [N] sorted genes: g | s << 16
-    uint16_t *cn = reinterpret_cast<uint16_t *>(perm2 + N);             // [E] n of each cached cluster
+    const int E = cc_entries(N);
+    double *qc = reinterpret_cast<double *>(wb);                         // [SPQ] queued c (small clusters)
+    ulonglong2 *cent = reinterpret_cast<ulonglong2 *>(qc + SPQ);        // [E] Zobrist XOR, keys {k1, k2}, then {f, -}
+    uint32_t *qnk = reinterpret_cast<uint32_t *>(cent + E);             // [SPQ] queued n | label << 16
+    uint32_t *cq = qnk + SPQ;                                            // [W] packed u16 counts, then ordm
+    uint32_t *offw = cq + W;                                             // [sp_words(N+2)] packed u16 walk starts, then ends
+    uint16_t *off = reinterpret_cast<uint16_t *>(offw);
+    uint32_t *perm2 = offw + sp_words(N + 2);                            // [N] walked genes: g | s << 16
+    uint16_t *cn = reinterpret_cast<uint16_t *>(perm2 + N);             // [E] n (| 0x8000: cache hit)
+    uint16_t *clab = cn + E;                                             // [E] label
     if (a.live && a.live[0] == 0) {     // the population went dense: skip (flags cleared)
         if (tid == 0) a.sflag[cb] = 0;
         return;
@@ -718,7 +722,10 @@ __global__ void __launch_bounds__(SP_T, PGA_SP_MINB) k_fitness_sparse(SparseArgs
     }
     if (!sparse) return;
 
-    // ---- pass 2: exact label-sparse evaluation
+    // ---- pass 2: exact label-sparse evaluation.  Large clusters (n >=
+    // CC_NMIN) get ordinals (label order) and their Eq. 8 terms are summed per
+    // ordinal, separately from the small clusters' queue: the summation order
+    // is the same whether a term came from the cache or was gathered.
     const double *C = a.C;
     const uint4 *keys4 = reinterpret_cast<const uint4 *>(a.cc_keys);
     uint16_t *ordm = reinterpret_cast<uint16_t *>(cq);
@@ -740,118 +747,130 @@ __global__ void __launch_bounds__(SP_T, PGA_SP_MINB) k_fitness_sparse(SparseArgs
         for (int o = 16; o > 0; o >>= 1) kmax = max(kmax, __shfl_xor_sync(0xFFFFFFFFu, kmax, o));
         const int K = min((int)kmax + 1, N);
         __syncwarp();
-        // offsets (exclusive prefix of the counts over labels 0..K-1), and the
-        // cache ordinals: a label with n >= CC_NMIN gets the next ordinal (in
-        // label order) and a zeroed Zobrist accumulator; ordm[k] (in place
-        // over its 16-bit count) = ordinal, or 0xFFFF
-        int base = 0, ecnt = 0;
+        // ordinals: ordm[k] (in place over the 16-bit count) = ordinal of a
+        // large cluster, else 0x8000 | n
+        int ecnt = 0;
         for (int k0 = 0; k0 < K; k0 += 32) {
             const int k = k0 + lane;
             const int n = k < K ? (int)ordm[k] : 0;
-            int incl = n;
+            const bool el = n >= CC_NMIN;
+            const unsigned bal = __ballot_sync(0xFFFFFFFFu, el);
+            if (el) {
+                const int ord = ecnt + __popc(bal & lanemask_lt());
+                ordm[k] = (uint16_t)ord;
+                cent[ord] = make_ulonglong2(0ull, 0ull);
+                cn[ord] = (uint16_t)n;
+                clab[ord] = (uint16_t)k;
+            } else if (k < K) {
+                ordm[k] = (uint16_t)(0x8000 | n);
+            }
+            ecnt += __popc(bal);
+        }
+        __syncwarp();
+        unsigned long long nhit = 0, nsaved = 0;
+        if (use_cache && ecnt > 0) {
+            // Zobrist XOR of each large cluster's members
+#pragma unroll 4
+            for (int i = lane; i < N; i += 32) {
+                const uint32_t om = ordm[lab[i]];
+                if (!(om & 0x8000u)) {
+                    uint32_t *h = reinterpret_cast<uint32_t *>(cent + om);
+                    const uint4 kk = __ldg(keys4 + i);
+                    atomicXor(h, kk.x);
+                    atomicXor(h + 1, kk.y);
+                    atomicXor(h + 2, kk.z);
+                    atomicXor(h + 3, kk.w);
+                }
+            }
+            __syncwarp();
+            // one lookup per large cluster, lane-parallel; a hit is its Eq. 8
+            // term and the cluster is not walked
+            for (int o = lane; o < ecnt; o += 32) {
+                const ulonglong2 h = cent[o];
+                const uint64_t k1 = h.x | 1ull, k2 = h.y | 1ull;
+                const uint32_t n = cn[o];
+                long long v = 0;
+                cent[o] = make_ulonglong2(k1, k2);
+                if (cc_find(a.cc, a.cc_mask, k1, k2, n, &v)) {
+                    cent[o].x = (unsigned long long)v;          // the cached Eq. 8 term
+                    cn[o] = (uint16_t)(n | 0x8000u);
+                    nhit += 1;
+                    nsaved += (unsigned long long)n * (n - 1) / 2;
+                }
+            }
+            __syncwarp();
+        }
+        // walk offsets: clusters with n >= 2 that are not cache hits, in label
+        // order (exclusive prefix over labels 0..K-1)
+        int base = 0;
+        for (int k0 = 0; k0 < K; k0 += 32) {
+            const int k = k0 + lane;
+            int w = 0;
+            if (k < K) {
+                const uint32_t om = ordm[k];
+                w = (om & 0x8000u) ? (int)(om & 0x7FFFu) : ((cn[om] & 0x8000u) ? 0 : (int)cn[om]);
+                if (w < 2) w = 0;
+            }
+            int incl = w;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const int t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
                 if (lane >= o) incl += t;
             }
-            const bool el = use_cache && n >= CC_NMIN;
-            const unsigned bal = __ballot_sync(0xFFFFFFFFu, el);
-            if (k < K) {
-                off[k] = (uint32_t)(base + incl - n);
-                uint16_t om = 0xFFFFu;
-                if (el) {
-                    const int ord = ecnt + __popc(bal & lanemask_lt());
-                    om = (uint16_t)ord;
-                    cent[ord] = make_ulonglong2(0ull, 0ull);
-                    cn[ord] = (uint16_t)n;
-                }
-                ordm[k] = om;
-            }
-            ecnt += __popc(bal);
+            if (k < K) off[k] = (uint16_t)(base + incl - w);
             base += __shfl_sync(0xFFFFFFFFu, incl, 31);
         }
+        const int Nw = base;
         __syncwarp();
-        // counting sort of the genes by label (clusters become contiguous runs
-        // in label order; order inside a cluster is free: sums are exact), and
-        // the Zobrist XOR of each cached cluster's members.  Afterwards off[s]
-        // is the END of cluster s and its start is off[s - 1] (0 for s = 0).
+        // counting sort of the walked genes by label (order inside a cluster
+        // is free: sums are exact); afterwards off[s] is the END of cluster s
+        // and its start is off[s - 1] (0 for s = 0)
 #pragma unroll 4
         for (int i = lane; i < N; i += 32) {
             const uint32_t s = lab[i];
-            const uint32_t pos = atomicAdd(off + s, 1u);
-            perm2[pos] = (uint32_t)i | (s << 16);
             const uint32_t om = ordm[s];
-            if (om != 0xFFFFu) {
-                uint32_t *h = reinterpret_cast<uint32_t *>(cent + om);
-                const uint4 kk = __ldg(keys4 + i);
-                atomicXor(h, kk.x);
-                atomicXor(h + 1, kk.y);
-                atomicXor(h + 2, kk.z);
-                atomicXor(h + 3, kk.w);
-            }
-        }
-        __syncwarp();
-        // one lookup per cached cluster, lane-parallel: a hit leaves {c, 0},
-        // a miss {k1, k2} (k2 != 0) for the insert once c is gathered
-        unsigned long long nhit = 0, nsaved = 0;
-        for (int o = lane; o < ecnt; o += 32) {
-            const ulonglong2 h = cent[o];
-            const uint64_t k1 = h.x | 1ull, k2 = h.y | 1ull;
-            const uint32_t n = cn[o];
-            long long v = 0;
-            if (cc_find(a.cc, a.cc_mask, k1, k2, n, &v)) {
-                cent[o] = make_ulonglong2((unsigned long long)v, 0ull);
-                nhit += 1;
-                nsaved += (unsigned long long)n * (n - 1) / 2;
-            } else {
-                cent[o] = make_ulonglong2(k1, k2);
+            const bool walked = (om & 0x8000u) ? (om & 0x7FFFu) >= 2u : !(cn[om] & 0x8000u);
+            if (walked) {
+                const uint32_t sh = 16 * (s & 1u);
+                const uint32_t pos = (atomicAdd(offw + (s >> 1), 1u << sh) >> sh) & 0xFFFFu;
+                perm2[pos] = (uint32_t)i | (s << 16);
             }
         }
         __syncwarp();
         // walk the sorted genes 32 at a time.  A lane's group is the window's
         // lanes of its cluster (contiguous); the cluster open at the window's
-        // end carries on.
-        // Every completed cluster with n >= 2 and c > n (Q2) is queued for its
-        // Eq. 8 summand.
+        // end carries on.  A completed large cluster stores its Eq. 8 term
+        // (and inserts it into the cache); a completed small one with c > n
+        // (Q2) is queued for its term.
         int qcnt = 0;
         unsigned long long npair = 0;
         long long carry = 0;
         double fsum = 0.0, fbest = 0.0;
         int kbest = 0x7FFFFFFF;
-        for (int t0 = 0; t0 < N; t0 += 32) {
+        for (int t0 = 0; t0 < Nw; t0 += 32) {
             const int t = t0 + lane;
             int s = -1, st = t, en = t + 1, n = 0;
-            uint32_t om = 0xFFFFu;
             long long acc = 0;
-            if (t < N) {
+            if (t < Nw) {
                 const uint32_t pg = perm2[t];
                 const int g = (int)(pg & 0xFFFFu);
                 s = (int)(pg >> 16);
                 en = (int)off[s];
                 st = s ? (int)off[s - 1] : 0;
                 n = en - st;
-                om = ordm[s];
-                if (om != 0xFFFFu && cent[om].y == 0ull) {        // cache hit: the head carries c_s
-                    acc = (t == st) ? (long long)cent[om].x : 0ll;
-                } else if (n >= 2) {
-                    const int av = t - st;
-                    if (av == 0) npair += (unsigned long long)n * (n - 1) / 2;   // C pairs gathered, once per cluster
-                    const double *Cg = C + (size_t)g * a.ldc;
-                    acc = __double2ll_rn(__ldg(a.diag + g) * a.fx_scale);
-                    const int h = (n - 1) >> 1;
-                    int bidx = av;
+                const int av = t - st;
+                if (av == 0) npair += (unsigned long long)n * (n - 1) / 2;   // C pairs gathered, once per cluster
+                const double *Cg = C + (size_t)g * a.ldc;
+                acc = __double2ll_rn(__ldg(a.diag + g) * a.fx_scale);
+                const int h = (n - 1) >> 1;
+                int bidx = av;
 #pragma unroll 4
-                    for (int d = 1; d <= h; ++d) {
-                        bidx = (bidx + 1 == n) ? 0 : bidx + 1;
-                        acc += 2 * __double2ll_rn(__ldg(Cg + (perm2[st + bidx] & 0xFFFFu)) * a.fx_scale);
-                    }
-                    if (!(n & 1) && av < (n >> 1))
-                        acc += 2 * __double2ll_rn(__ldg(Cg + (perm2[st + av + (n >> 1)] & 0xFFFFu)) * a.fx_scale);
-                } else {
-                    s = -1;
-                    st = t;
-                    en = t + 1;
+                for (int d = 1; d <= h; ++d) {
+                    bidx = (bidx + 1 == n) ? 0 : bidx + 1;
+                    acc += 2 * __double2ll_rn(__ldg(Cg + (perm2[st + bidx] & 0xFFFFu)) * a.fx_scale);
                 }
+                if (!(n & 1) && av < (n >> 1))
+                    acc += 2 * __double2ll_rn(__ldg(Cg + (perm2[st + av + (n >> 1)] & 0xFFFFu)) * a.fx_scale);
             }
             // group sum = difference of the window's inclusive prefix sums at
             // the group's ends (mod 2^64: exact)
@@ -870,15 +889,25 @@ __global__ void __launch_bounds__(SP_T, PGA_SP_MINB) k_fitness_sparse(SparseArgs
             const int en31 = __shfl_sync(0xFFFFFFFFu, en, 31);
             const long long tot31 = __shfl_sync(0xFFFFFFFFu, tot, 31);
             carry = (s31 >= 0 && en31 > t0 + 32) ? tot31 : 0ll;
-            // completed clusters of this window -> queue (label order)
             double c = 0.0;
             bool push = false;
             if (s >= 0 && lane == lo && en <= t0 + 32) {
                 c = (double)tot * a.fx_inv;
-                push = c > (double)n;
-                if (om != 0xFFFFu) {
-                    const ulonglong2 e = cent[om];
-                    if (e.y != 0ull) cc_insert(a.cc, a.cc_mask, a.cc_state, e.x, e.y, (uint32_t)n, tot);
+                const uint32_t om = ordm[s];
+                if (om & 0x8000u) {
+                    push = c > (double)n;
+                } else {
+                    double f = 0.0;
+                    if (c > (double)n) {
+                        const double nd = (double)n, n2 = nd * nd;
+                        const double ch = fmin(c, n2 - 1e-9);
+                        f = (__ldg(a.lgn + n) - log(ch)) + (nd - 1.0) * (__ldg(a.lgnn + n) - log(n2 - ch));
+                    }
+                    if (use_cache) {
+                        const ulonglong2 e = cent[om];
+                        cc_insert(a.cc, a.cc_mask, a.cc_state, e.x, e.y, (uint32_t)n, __double_as_longlong(f));
+                    }
+                    cent[om].x = (unsigned long long)__double_as_longlong(f);
                 }
             }
             const unsigned bal = __ballot_sync(0xFFFFFFFFu, push);
@@ -919,6 +948,17 @@ __global__ void __launch_bounds__(SP_T, PGA_SP_MINB) k_fitness_sparse(SparseArgs
             if (f > fbest) {
                 fbest = f;
                 kbest = (int)(nk >> 16);
+            }
+        }
+        __syncwarp();
+        // the large clusters' terms, in ordinal (= label) order per lane
+        for (int o = lane; o < ecnt; o += 32) {
+            const double f = __longlong_as_double((long long)cent[o].x);
+            fsum += f;
+            const int kl = (int)clab[o];
+            if (f > fbest || (f == fbest && f > 0.0 && kl < kbest)) {
+                fbest = f;
+                kbest = kl;
             }
         }
 #pragma unroll
