@@ -748,7 +748,7 @@ __global__ void __launch_bounds__(SP_T, PGA_SP_MINB) k_fitness_sparse(SparseArgs
         const int K = min((int)kmax + 1, N);
         __syncwarp();
         // ordinals: ordm[k] (in place over the 16-bit count) = ordinal of a
-        // large cluster, else 0x8000 | n
+        // large cluster, else 0x8000 | n; bit 14 is set below for walked labels
         int ecnt = 0;
         for (int k0 = 0; k0 < K; k0 += 32) {
             const int k = k0 + lane;
@@ -810,6 +810,7 @@ __global__ void __launch_bounds__(SP_T, PGA_SP_MINB) k_fitness_sparse(SparseArgs
                 const uint32_t om = ordm[k];
                 w = (om & 0x8000u) ? (int)(om & 0x7FFFu) : ((cn[om] & 0x8000u) ? 0 : (int)cn[om]);
                 if (w < 2) w = 0;
+                else ordm[k] = (uint16_t)(om | 0x4000u);     // walked
             }
             int incl = w;
 #pragma unroll
@@ -828,9 +829,7 @@ __global__ void __launch_bounds__(SP_T, PGA_SP_MINB) k_fitness_sparse(SparseArgs
 #pragma unroll 4
         for (int i = lane; i < N; i += 32) {
             const uint32_t s = lab[i];
-            const uint32_t om = ordm[s];
-            const bool walked = (om & 0x8000u) ? (om & 0x7FFFu) >= 2u : !(cn[om] & 0x8000u);
-            if (walked) {
+            if (ordm[s] & 0x4000u) {
                 const uint32_t sh = 16 * (s & 1u);
                 const uint32_t pos = (atomicAdd(offw + (s >> 1), 1u << sh) >> sh) & 0xFFFFu;
                 perm2[pos] = (uint32_t)i | (s << 16);
@@ -893,7 +892,7 @@ __global__ void __launch_bounds__(SP_T, PGA_SP_MINB) k_fitness_sparse(SparseArgs
             bool push = false;
             if (s >= 0 && lane == lo && en <= t0 + 32) {
                 c = (double)tot * a.fx_inv;
-                const uint32_t om = ordm[s];
+                const uint32_t om = ordm[s] & 0xBFFFu;
                 if (om & 0x8000u) {
                     push = c > (double)n;
                 } else {
