@@ -293,6 +293,7 @@ def main():
     ms = ev0.elapsed_time(ev1)
     prof = pga.pga_profile_read(eng.ctx)
     sparse_blocks, sparse_gathers = pga.pga_profile_sparse(eng.ctx)
+    cache_hits, cache_saved = pga.pga_profile_cache(eng.ctx)
     pga.pga_profile_enable(eng.ctx, False)
     # roofline pass for the dense sweep kernel, right after the timed region:
     # the same population with the label-sparse pre-pass off, so every block
@@ -304,7 +305,7 @@ def main():
         runner.step()
     dprof = pga.pga_profile_read(eng.ctx)
     pga.pga_profile_enable(eng.ctx, False)
-    pga.pga_set_sparse_threshold(eng.ctx, 0.04 if args.sparse_theta is None else args.sparse_theta)
+    pga.pga_set_sparse_threshold(eng.ctx, -1.0 if args.sparse_theta is None else args.sparse_theta)
     # diagnostic per-phase breakdown, OUTSIDE the timed region (level-2 marks)
     pga.pga_profile_enable(eng.ctx, 2)
     for _ in range(min(K, 20)):
@@ -339,11 +340,13 @@ def main():
     peaks = measured_peaks()
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
     peak = FP64_LANES_PER_SM * SM_COUNT * sm_max * 1e6
-    traffic = None
+    traffic = sp_inst = sp_dram = None
     if CONFIG == "C4" and world == 1:      # profiles/ hold one ncu capture of the C4 launch
         try:
             tj = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
             traffic = tj.get("k_sweep", {}).get("dram_bytes_per_launch")
+            sp_inst = tj.get("k_fitness_sparse", {}).get("inst_per_launch")
+            sp_dram = tj.get("k_fitness_sparse", {}).get("dram_bytes_per_launch")
         except Exception:
             pass
 
@@ -366,6 +369,65 @@ def main():
         eng.close()
 
     if rank == 0:
+        rl_dense = {"bound": "alu", "kernel": "k_fitness (dense sweep + fused fold)", "achieved": achieved,
+                         "peak": peak, "unit": "pair-updates/s", "frac": achieved / peak,
+                         "measured": "CUDA events on the library stream over %d generations right after the "
+                                     "timed region, same population, label-sparse pre-pass off (every block "
+                                     "through k_fitness); in the timed region itself k_fitness ran %.1f%% of "
+                                     "the blocks and took %.3f of %.3f ms per generation, the label-sparse "
+                                     "pre-pass (k_fitness_sparse) %.3f ms"
+                                     % (dprof["count"], 100.0 * dense_blocks / float(nblk * ngen), sweep_ms,
+                                        gen_ms, sparse_ms),
+                         "traffic": traffic,
+                         "algorithmic_bytes": P_eval * (N * 2 + 8 + 2),
+                         "traffic_note": "ncu dram bytes of one launch: labels are read twice (gene-major "
+                                         "by the sweep's TMA, chromosome-major by the fused fold); the "
+                                         "fold scratch V is discarded from L2 after use (no write-back)",
+                         "work_per_launch": "%d chromosomes x N(N-1)/2 = %.4g executed pair-updates"
+                                            % (P_eval, executed_local),
+                         "peak_basis": "1 DFMA per executed pair; 64 FP64 lanes/clk/SM x 148 SMs "
+                                       "x %.0f MHz (sm_max_mhz)" % sm_max,
+                         "frac_at_measured_clock": (achieved / (FP64_LANES_PER_SM * SM_COUNT *
+                                                    clk["sm_mhz"] * 1e6))
+                         if clk and clk.get("sm_mhz") else None,
+                         "loop_ceiling": LOOP_PAIRS_PER_CLK * SM_COUNT * sm_max * 1e6,
+                         "frac_of_loop_ceiling": achieved / (LOOP_PAIRS_PER_CLK * SM_COUNT * sm_max * 1e6),
+                         "loop_ceiling_basis": "measured bare inner loop (tools/mb_pairloop.cu): "
+                                               "26.8 pairs/clk/SM, register-file-read bound"}
+        rl_sparse = ({
+                "bound": "issue", "kernel": "k_fitness_sparse",
+                "achieved": sp_inst / (sparse_ms / 1000.0),
+                "peak": 4.0 * SM_COUNT * sm_max * 1e6, "unit": "warp-instructions/s",
+                "frac": sp_inst / (sparse_ms / 1000.0) / (4.0 * SM_COUNT * sm_max * 1e6),
+                "work_per_launch": "%.4g warp-instructions (ncu smsp__inst_executed.sum of one launch at "
+                                   "generation ~400, profiles/traffic.json) / the timed mean launch time "
+                                   "%.3f ms" % (sp_inst, sparse_ms),
+                "peak_basis": "4 warp-instructions/clk/SM (one per SMSP) x 148 SMs x %.0f MHz; the pass is "
+                              "latency/issue bound (shared-memory atomics, dependent label loads), not "
+                              "bandwidth bound: its DRAM traffic is the labels (%.0f MB per launch)"
+                              % (sm_max, (sp_dram or 0) / 1e6),
+                "gathers": {"per_launch": sparse_gathers / float(ngen),
+                            "per_s": sparse_gathers / (prof["fold_ms"] / 1000.0),
+                            "frac_of_l2_gather_peak": sparse_gathers / (prof["fold_ms"] / 1000.0) /
+                                                      L2_GATHERS_PER_S,
+                            "l2_gather_peak_basis": "tools/mb_l2gather.cu: 3.03e11 random 8-byte gathers/s"},
+                "cluster_cache": {"hits_per_launch": cache_hits / float(ngen),
+                                  "pair_updates_saved_per_launch": cache_saved / float(ngen),
+                                  "hit_share_of_pairs": cache_saved / float(max(1, cache_saved + sparse_gathers))},
+                "measured": "CUDA events on the library stream around every k_fitness_sparse launch of the "
+                            "timed region (mean %.3f of %.3f ms per generation)" % (sparse_ms, gen_ms),
+                "traffic": sp_dram,
+                "algorithmic_bytes": P_eval * (N * 2 + 8 + 2),
+                "traffic_note": "ncu dram bytes of one launch: the chromosome-major labels (2N bytes per "
+                                "chromosome) plus L and top; C, the cache table's hot slots and the "
+                                "cache keys stay in L2",
+                "share_of_timed_generation": sparse_ms / gen_ms}
+                if sp_inst and prof["fold_ms"] > 0 else None)
+        # the top-level roofline is the kernel that dominated the timed region
+        if rl_sparse is not None and sparse_ms > sweep_ms:
+            rl_main, rl_other = rl_sparse, rl_dense
+        else:
+            rl_main, rl_other = rl_dense, rl_sparse
         line = {
             "metric": METRIC, "value": value, "unit": "pair-updates/s", "n_gpus": world,
             "steps": K, "warmup": W, "ms_per_step": ms_step, "higher_is_better": True,
@@ -390,51 +452,16 @@ def main():
                                          "k_fitness_dense_pass": dense_sweep_ms},
             "sparse_pass": {"blocks_evaluated_sparsely": sparse_blocks,
                             "fraction_of_blocks": sparse_blocks / float(nblk * ngen),
-                            "note": "SURVEY §8(f) f2: blocks of 32 chromosomes whose clusters need <= 4% "
-                                    "of the dense pair updates are evaluated label-sparsely (L2 "
-                                    "gathers) and skipped by k_fitness; the check stops once a "
-                                    "generation has no sparse block"},
+                            "note": "SURVEY §8(f) f2: blocks of 32 chromosomes whose clusters need <= 25% "
+                                    "of the dense pair updates (automatic threshold with the cluster "
+                                    "cache on) are evaluated label-sparsely and skipped by k_fitness; "
+                                    "clusters of >= 6 genes come from the cluster cache when an earlier "
+                                    "generation had the same member set, the rest are gathered from L2"},
             "phase_ms_per_generation": {k: round(v, 4) for k, v in phases.items()
                                         if k != "fitness_fold_fused"},
             "phase_note": "diagnostic pass after the timed region (phase events add ~3 us/gen)",
-            "roofline": {"bound": "alu", "kernel": "k_fitness (dense sweep + fused fold)", "achieved": achieved,
-                         "peak": peak, "unit": "pair-updates/s", "frac": achieved / peak,
-                         "measured": "CUDA events on the library stream over %d generations right after the "
-                                     "timed region, same population, label-sparse pre-pass off (every block "
-                                     "through k_fitness); in the timed region itself k_fitness ran %.1f%% of "
-                                     "the blocks and took %.3f of %.3f ms per generation, the label-sparse "
-                                     "pre-pass (k_fitness_sparse) %.3f ms"
-                                     % (dprof["count"], 100.0 * dense_blocks / float(nblk * ngen), sweep_ms,
-                                        gen_ms, sparse_ms),
-                         "traffic": traffic,
-                         "algorithmic_bytes": P_eval * (N * 2 + 8 + 2),
-                         "traffic_note": "ncu dram bytes of one launch: labels are read twice (gene-major "
-                                         "by the sweep's TMA, chromosome-major by the fused fold); the "
-                                         "fold scratch V is discarded from L2 after use (no write-back)",
-                         "work_per_launch": "%d chromosomes x N(N-1)/2 = %.4g executed pair-updates"
-                                            % (P_eval, executed_local),
-                         "peak_basis": "1 DFMA per executed pair; 64 FP64 lanes/clk/SM x 148 SMs "
-                                       "x %.0f MHz (sm_max_mhz)" % sm_max,
-                         "frac_at_measured_clock": (achieved / (FP64_LANES_PER_SM * SM_COUNT *
-                                                    clk["sm_mhz"] * 1e6))
-                         if clk and clk.get("sm_mhz") else None,
-                         "loop_ceiling": LOOP_PAIRS_PER_CLK * SM_COUNT * sm_max * 1e6,
-                         "frac_of_loop_ceiling": achieved / (LOOP_PAIRS_PER_CLK * SM_COUNT * sm_max * 1e6),
-                         "loop_ceiling_basis": "measured bare inner loop (tools/mb_pairloop.cu): "
-                                               "26.8 pairs/clk/SM, register-file-read bound"},
-            "roofline_sparse_pass": ({
-                "bound": "l2", "kernel": "k_fitness_sparse",
-                "achieved": sparse_gathers / (prof["fold_ms"] / 1000.0),
-                "peak": L2_GATHERS_PER_S, "unit": "C-entry gathers/s",
-                "frac": sparse_gathers / (prof["fold_ms"] / 1000.0) / L2_GATHERS_PER_S,
-                "work_per_launch": "%.4g gathers (sum over the blocks it evaluated of n_s(n_s-1)/2 per "
-                                   "cluster; the diagonal comes from a 4 KB array in L1), average over the "
-                                   "timed launches"
-                                   % (sparse_gathers / float(ngen)),
-                "peak_basis": "measured random 8-byte gathers from an L2-resident 2 MB fp64 array "
-                              "(tools/mb_l2gather.cu): 3.03e11/s = 9.7 TB/s of 32-byte sectors",
-                "share_of_timed_generation": sparse_ms / gen_ms}
-                if sparse_gathers > 0 and prof["fold_ms"] > 0 else None),
+            "roofline": rl_main,
+            "roofline_other": rl_other,
             "gpu_launches": int(launches),
             "clocks": clk,
             "best_L": st["best_L"],

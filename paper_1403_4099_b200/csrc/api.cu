@@ -31,6 +31,7 @@ int cuda_fail(cudaError_t e, const char *what) {
 void count_launch(int n) { g_launches += n; }
 
 // declared in ga.cu / fitness.cu
+int launch_resync_gm(pga_ctx *c, cudaStream_t s);
 int launch_init_raw(uint64_t seed, int N, int ldn, int64_t P, int64_t Pcap, int64_t p_off,
                     uint32_t island, uint16_t *CM, uint16_t *GM, int32_t *out32, cudaStream_t s);
 int run_select_ops(const double *L, int64_t P, const pga_params &p, int32_t gen, int32_t island,
@@ -522,7 +523,13 @@ int pga_gen_evaluate(pga_ctx *c, int32_t *is_migration) {
 int pga_set_sparse_threshold(pga_ctx *c, double theta) {
     if (!c) return fail(PGA_EINVAL, "ctx is NULL");
     if (!(theta <= 1.0)) return fail(PGA_EINVAL, "theta must lie in [0, 1] (negative = automatic)");
+    const bool was_on = sparse_theta_eff(c) > 0.0;
     c->sparse_theta = theta < 0.0 ? -1.0 : theta;
+    if (was_on && !(sparse_theta_eff(c) > 0.0) && c->has_pop && c->N <= 640) {
+        // the breed may have left the gene-major copy to the sparse pass
+        PGA_CUDA(cudaSetDevice(c->device));
+        TRY(launch_resync_gm(c, c->stream));
+    }
     return PGA_OK;
 }
 

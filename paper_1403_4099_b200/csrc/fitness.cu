@@ -466,6 +466,33 @@ k_fitness(const __grid_constant__ CUtensorMap tmLab0, const __grid_constant__ CU
     if (tid == 0) a.counters[cb] = 0u;
 }
 
+// k_resync_gm: rebuild the gene-major copy of the CURRENT population (buffer
+// gen & 1) from the chromosome-major one.  While the label-sparse pass runs,
+// the breed leaves the gene-major copy to it; when the pass is switched off
+// mid-run (pga_set_sparse_threshold(0)) the dense sweep needs it back.
+__global__ void k_resync_gm(const uint16_t *__restrict__ CM0, const uint16_t *__restrict__ CM1,
+                            uint16_t *GM0, uint16_t *GM1, const pga::DevState *st, int64_t P, int N,
+                            int ldn, int64_t Pcap) {
+    __shared__ uint16_t tile[32][33];
+    const int par = st->gen & 1;
+    const uint16_t *CM = par ? CM1 : CM0;
+    uint16_t *GM = par ? GM1 : GM0;
+    const int64_t p0 = (int64_t)blockIdx.x * 32;
+    const int i0 = blockIdx.y * 32;
+    const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+    for (int r = ty; r < 32; r += 8) {
+        const int64_t p = p0 + r;
+        const int i = i0 + tx;
+        tile[r][tx] = (p < P && i < N) ? CM[p * ldn + i] : (uint16_t)0;
+    }
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {
+        const int i = i0 + r;
+        const int64_t p = p0 + tx;
+        if (i < N && p < P) GM[(int64_t)i * Pcap + p] = tile[tx][r];
+    }
+}
+
 // ---------------------------------------------------------------------------
 // k_fitness_sparse: label-sparse evaluation of a
 // 32-chromosome block when its clusters are small.  Pass 1 (warp per
@@ -994,6 +1021,14 @@ __global__ void __launch_bounds__(SP_T, PGA_SP_MINB) k_fitness_sparse(SparseArgs
 }  // namespace
 
 namespace pga {
+
+int launch_resync_gm(pga_ctx *c, cudaStream_t s) {
+    dim3 grid((unsigned)((c->P + 31) / 32), (unsigned)((c->N + 31) / 32));
+    k_resync_gm<<<grid, dim3(32, 8), 0, s>>>(c->pop[0], c->pop[1], c->popT[0], c->popT[1], c->st, c->P, c->N,
+                                             c->ldn, c->Pcap);
+    PGA_LAUNCHED();
+    return PGA_OK;
+}
 
 int launch_pack(pga_ctx *c, const uint16_t *lab16, const int32_t *lab32, int64_t P, int ld_in,
                 uint16_t *CM, uint16_t *GM, cudaStream_t s) {

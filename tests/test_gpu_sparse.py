@@ -167,3 +167,29 @@ def test_out_of_range_device_label_is_contained(pga, orc, theta):
     Lo, _ = orc.evaluate(C, lab)
     keep = np.arange(P) != 7
     _assert_L(Lg[keep], Lo[keep])
+
+
+def test_switching_the_sparse_pass_off_mid_run(pga, orc):
+    """While the label-sparse pass runs, the breed leaves the gene-major copy
+    to it; switching the pass off between generations must hand the dense
+    sweep a current copy (the L of the next evaluation matches the oracle)."""
+    X, _ = workloads.noh_returns(workloads.CONFIGS["C4"])
+    C = orc.pearson(X)
+    P, N = 2048, 500
+    ctx = pga.pga_create(C, pga.pga_params_default(pop_size=P, p_mutation=2.0 / N, tol=-1.0, max_gens=60, seed=4))
+    try:
+        pga.pga_init(ctx, 4)
+        for _ in range(12):
+            pga.pga_gen_evaluate(ctx)
+            pga.pga_gen_breed(ctx)
+        pga.pga_set_sparse_threshold(ctx, 0.0)
+        pga.pga_gen_evaluate(ctx)
+        pop, L = pga.pga_get_population(ctx, P, N)
+        _assert_L(L, orc.evaluate(C, pop - 1, nthreads=8)[0])
+        pga.pga_gen_breed(ctx)
+        pga.pga_set_sparse_threshold(ctx, -1.0)     # and back on (automatic)
+        pga.pga_gen_evaluate(ctx)
+        pop, L = pga.pga_get_population(ctx, P, N)
+        _assert_L(L, orc.evaluate(C, pop - 1, nthreads=8)[0])
+    finally:
+        pga.pga_destroy(ctx)

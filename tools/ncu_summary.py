@@ -89,6 +89,8 @@ for hdr, units, d in kern_rows:
         traffic[name] = {"dram_bytes_per_launch": tobytes(vals["dram__bytes_read.sum"]) +
                          tobytes(vals["dram__bytes_write.sum"]),
                          "source": "profiles/%s_full.md (ncu --set full, one launch)" % tag}
+        if "smsp__inst_executed.sum" in vals:
+            traffic[name]["inst_per_launch"] = float(vals["smsp__inst_executed.sum"][0].replace(",", ""))
 open(os.path.join(out_dir, "%s_full.md" % tag), "w").write("\n".join(md) + "\n")
 if "k_fitness" in traffic:
     traffic["k_sweep"] = traffic["k_fitness"]      # bench.py key (sweep + fused fold kernel)

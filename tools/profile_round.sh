@@ -16,7 +16,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none -k regex:k_batch --csv
     --log-file gpurun_out/launches_f1.csv $F1 > gpurun_out/prof_launches_f1.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"k_fitness$|k_breed" -s 4 -c 2 \
     -o gpurun_out/prof_full $DENSE > gpurun_out/prof_full.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k_fitness_sparse -s 400 -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:k_fitness_sparse -s 403 -c 1 \
     -o gpurun_out/prof_sparse python bench.py --steps 3 --warmup 410 --no-cpu --no-e2e \
     > gpurun_out/prof_sparse.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_batch -c 1 \
