@@ -749,8 +749,11 @@ constexpr int BREED2_MAXN = 1024;
 
 __host__ __device__ __forceinline__ int breed2_nch(int N) { return (N + 31) / 32; }
 
+// tile rows padded to whole 128-gene chunks: phase 1 stores unconditionally
+__host__ __device__ __forceinline__ int breed2_rows(int N) { return (N + GCH - 1) / GCH * GCH; }
+
 static size_t breed2_smem(int N) {
-    const size_t tile = (size_t)N * TS * sizeof(uint16_t);
+    const size_t tile = (size_t)breed2_rows(N) * TS * sizeof(uint16_t);
     const size_t fp = (size_t)BS * ((N + 1 + 3) & ~3) * sizeof(uint32_t);
     const size_t bal = (size_t)BS * breed2_nch(N) * (sizeof(uint32_t) + sizeof(uint16_t));
     return ((tile + 15) & ~(size_t)15) + ((fp + 15) & ~(size_t)15) + bal + 16;
@@ -767,8 +770,8 @@ __global__ void __launch_bounds__(BW * 32, 3) k_breed2(BreedArgs a) {
     const uint16_t *cm_in = par ? a.cm_in1 : a.cm_in0;
     uint16_t *cm_out = par ? a.cm_out0 : a.cm_out1;
     uint16_t *gm_out = par ? a.gm_out0 : a.gm_out1;
-    uint16_t *tile = reinterpret_cast<uint16_t *>(sm2);                               // [N][TS]
-    const size_t tile_b = ((size_t)N * TS * sizeof(uint16_t) + 15) & ~(size_t)15;
+    uint16_t *tile = reinterpret_cast<uint16_t *>(sm2);                               // [rows][TS]
+    const size_t tile_b = ((size_t)breed2_rows(N) * TS * sizeof(uint16_t) + 15) & ~(size_t)15;
     const int fpn = (N + 1 + 3) & ~3;
     uint32_t *fp = reinterpret_cast<uint32_t *>(sm2 + tile_b) + (size_t)warp * fpn;    // [BS][fpn]
     const size_t fp_b = ((size_t)BS * fpn * sizeof(uint32_t) + 15) & ~(size_t)15;
@@ -830,8 +833,8 @@ __global__ void __launch_bounds__(BW * 32, 3) k_breed2(BreedArgs a) {
                 for (int e = 0; e < 2; ++e)
                     if ((mb >> e) & 1u) s[e] = scale_u32(word(v, (g0 + e) & 3), (uint32_t)N);
             }
-            if (g0 < N) tile[g0 * TS + slot] = (uint16_t)s[0];
-            if (g0 + 1 < N) tile[(g0 + 1) * TS + slot] = (uint16_t)s[1];
+            tile[g0 * TS + slot] = (uint16_t)s[0];          // rows >= N are padding
+            tile[(g0 + 1) * TS + slot] = (uint16_t)s[1];
         }
     }
     __syncwarp();
@@ -846,9 +849,15 @@ __global__ void __launch_bounds__(BW * 32, 3) k_breed2(BreedArgs a) {
             for (int c = 0; c < nch; ++c) {           // independent chunks: atomics return nothing
                 const int i = 32 * c + lane;
                 const bool valid = i < N;
+#ifdef PGA_BREED_MATCH
                 const uint32_t s = valid ? (uint32_t)tile[i * TS + slot] : 0x10000u + (uint32_t)lane;
                 const unsigned m = __match_any_sync(0xFFFFFFFFu, s);
                 if (valid && lane == __ffs(m) - 1) atomicMin(&fp[s], (uint32_t)i);
+#else
+                // every lane: the shared-memory atomic unit resolves equal
+                // labels in a chunk (cheaper than waiting for MATCH.ANY)
+                if (valid) atomicMin(&fp[tile[i * TS + slot]], (uint32_t)i);
+#endif
             }
             __syncwarp();
         }

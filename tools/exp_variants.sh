@@ -1,6 +1,7 @@
-python tools/sp_prof.py save 500 > /dev/null
+#!/bin/bash
+# time each experimental build in exp_libs/ with the default C4 bench
 for f in exp_libs/*.so; do
   echo "== $f"
-  PGA_LIB=$f python tools/sp_prof.py load 500
-  PGA_LIB=$f timeout 300 python tools/theta_scan.py 1000 -1 cache 2>&1 | tail -1
+  PGA_LIB=$f timeout 300 python bench.py --no-cpu --no-e2e 2>/dev/null | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['phase_ms_per_generation'])"
 done
