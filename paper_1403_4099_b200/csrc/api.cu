@@ -121,6 +121,7 @@ void free_ctx(pga_ctx *c) {
     if (!c) return;
     cudaSetDevice(c->device);
     void *ptrs[] = {c->C, c->diag, c->lgtab, c->sflag, c->sp_live, c->sp_blocks, c->cc, c->cc_state,
+                    c->stats_part, c->stats_ctr,
                     c->cc_keys, c->pop[0], c->pop[1], c->popT[0], c->popT[1], c->V, c->L,
                     c->top, c->keys_in, c->keys_out, c->idx_in, c->order, c->q, c->prefix,
                     c->sel, c->mkeys_in, c->mkeys_out, c->m_in, c->sigma, c->cub_tmp, c->st,
@@ -354,6 +355,9 @@ int pga_create(const double *C, int32_t N, const pga_params *p, pga_ctx **out) {
     rc = rc ? rc : dalloc(&c->sflag, (size_t)(c->Pcap / CB + 1));
     rc = rc ? rc : dalloc(&c->sp_live, (size_t)6);
     rc = rc ? rc : dalloc(&c->sp_blocks, (size_t)4);
+    rc = rc ? rc : dalloc(&c->stats_part, (size_t)3 * 1024);
+    rc = rc ? rc : dalloc(&c->stats_ctr, (size_t)1);
+    if (!rc && cudaMemset(c->stats_ctr, 0, sizeof(uint32_t)) != cudaSuccess) rc = fail(PGA_EDEVICE, "memset stats_ctr");
     if (!rc && cudaMemset(c->sp_blocks, 0, 4 * sizeof(unsigned long long)) != cudaSuccess)
         rc = fail(PGA_EDEVICE, "memset sp_blocks");
     if (!rc && N <= 640) {

@@ -521,12 +521,12 @@ __global__ void k_resync_gm(const uint16_t *__restrict__ CM0, const uint16_t *__
 constexpr int SP_W = 8, SP_T = SP_W * 32;
 constexpr int SPARSE_MAXN = 640;   // shared-memory footprint (sparse_smem) must fit one CTA
 #ifndef PGA_CC_NMIN
-#define PGA_CC_NMIN 6
+#define PGA_CC_NMIN 5
 #endif
 #ifndef PGA_SP_MINB
 #define PGA_SP_MINB 4
 #endif
-constexpr int CC_NMIN = PGA_CC_NMIN;   // clusters this large go through the cache
+constexpr int CC_NMIN = PGA_CC_NMIN;   // clusters this large go through the cache (5: best of 3..8 at C4)
 static_assert(CC_NMIN >= 2, "large clusters must have pairs");
 constexpr int CC_PROBE = 8;        // linear-probe length
 

@@ -106,31 +106,19 @@ __global__ void k_canon_i32(int32_t *lab, int64_t P, int N, int tab) {
 }
 
 // ---------------------------------------------------------------------------
-// k_stats: one block.  best (lowest index on ties), mean, stall counter,
-// termination flag, best-ever labels, history (Alg. 1; Q16, Q17).
+// k_stats: best (lowest index on ties), mean, stall counter, termination
+// flag, best-ever labels, history (Alg. 1; Q16, Q17).  Each CTA
+// reduces a fixed contiguous slice; the last CTA to finish reduces the
+// partials in CTA order (deterministic) and updates the state.
 // mode 0: single island, update stall every generation
 // mode 1: multi-island non-migration generation: statistics only
 // mode 2: multi-island migration generation: stall on the (global) best
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(1024)
-k_stats(const double *__restrict__ L, int64_t P, const uint16_t *CM0, const uint16_t *CM1,
-        int ldn, int N, pga::DevState *st, uint16_t *best_labels, double *history,
-        int hist_cap, double tol, int stall_gens, int max_gens, int mode, int migrate_every) {
-    __shared__ double sb[32], ss[32];
-    __shared__ int si[32];
-    __shared__ int s_improved, s_bi;
-    if (st->done) return;
+constexpr int STATS_T = 1024, STATS_PER_CTA = 4096, STATS_MAXG = 1024;
+
+__device__ __forceinline__ void stats_reduce(double &best, int &bi, double &sum, double *sb, int *si,
+                                             double *ss) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    double best = -1.0, sum = 0.0;
-    int bi = 0x7FFFFFFF;
-    for (int64_t i = tid; i < P; i += blockDim.x) {
-        const double v = L[i];
-        sum += v;
-        if (v > best) {  // ascending i per thread -> first max kept
-            best = v;
-            bi = (int)i;
-        }
-    }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
         const double ob = __shfl_xor_sync(0xFFFFFFFFu, best, off);
@@ -162,32 +150,81 @@ k_stats(const double *__restrict__ L, int64_t P, const uint16_t *CM0, const uint
                 bi = oi;
             }
         }
-        if (lane == 0) {
-            const int g = st->gen;
-            st->best = best;
-            st->best_idx = bi;
-            st->mean = sum / (double)P;
-            if (g < hist_cap) history[g] = best;
-            if (mode == 0) {
-                if (g > 0) st->stall = (best - st->prev_best < tol) ? st->stall + 1 : 0;
-                st->prev_best = best;
-            } else if (mode == 2) {
-                if (g + 1 > migrate_every)
-                    st->stall = (best - st->prev_best < tol) ? st->stall + migrate_every : 0;
-                st->prev_best = best;
-            }
-            int done = 0;
-            if (tol >= 0.0 && st->stall >= stall_gens) {
-                done = 1;
-                st->reason = PGA_REASON_STALLED;
-            }
-            if (g + 1 >= max_gens) done = 1;
-            st->done = done;
-            const int improved = (best > st->best_ever) ? 1 : 0;
-            if (improved) st->best_ever = best;
-            s_improved = improved;
-            s_bi = bi;               // broadcast the block-wide argmax
+    }
+}
+
+__global__ void __launch_bounds__(STATS_T)
+k_stats(const double *__restrict__ L, int64_t P, const uint16_t *CM0, const uint16_t *CM1,
+        int ldn, int N, pga::DevState *st, uint16_t *best_labels, double *history,
+        int hist_cap, double tol, int stall_gens, int max_gens, int mode, int migrate_every,
+        double *part, uint32_t *counter, int64_t per) {
+    __shared__ double sb[32], ss[32];
+    __shared__ int si[32];
+    __shared__ int s_improved, s_bi, s_last;
+    if (st->done) return;
+    const int tid = threadIdx.x, lane = tid & 31;
+    double best = -1.0, sum = 0.0;
+    int bi = 0x7FFFFFFF;
+    const int64_t lo = (int64_t)blockIdx.x * per, hi = min(P, lo + per);
+    for (int64_t i = lo + tid; i < hi; i += blockDim.x) {
+        const double v = L[i];
+        sum += v;
+        if (v > best) {  // ascending i per thread -> first max kept
+            best = v;
+            bi = (int)i;
         }
+    }
+    stats_reduce(best, bi, sum, sb, si, ss);
+    if (gridDim.x > 1) {
+        if (tid == 0) {
+            part[3 * blockIdx.x] = best;
+            part[3 * blockIdx.x + 1] = sum;
+            part[3 * blockIdx.x + 2] = (double)bi;   // exact: |bi| < 2^31
+            __threadfence();
+            s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+        }
+        __syncthreads();
+        if (!s_last) return;
+        __threadfence();
+        // partials in CTA order: thread t takes CTA t (<= STATS_MAXG), then the same tree
+        best = -1.0;
+        sum = 0.0;
+        bi = 0x7FFFFFFF;
+        if (tid < (int)gridDim.x) {
+            const volatile double *vp = part;
+            best = vp[3 * tid];
+            sum = vp[3 * tid + 1];
+            bi = (int)vp[3 * tid + 2];
+        }
+        __syncthreads();
+        stats_reduce(best, bi, sum, sb, si, ss);
+        if (tid == 0) *counter = 0u;
+    }
+    if (tid == 0) {
+        const int g = st->gen;
+        st->best = best;
+        st->best_idx = bi;
+        st->mean = sum / (double)P;
+        if (g < hist_cap) history[g] = best;
+        if (mode == 0) {
+            if (g > 0) st->stall = (best - st->prev_best < tol) ? st->stall + 1 : 0;
+            st->prev_best = best;
+        } else if (mode == 2) {
+            if (g + 1 > migrate_every)
+                st->stall = (best - st->prev_best < tol) ? st->stall + migrate_every : 0;
+            st->prev_best = best;
+        }
+        int done = 0;
+        if (tol >= 0.0 && st->stall >= stall_gens) {
+            done = 1;
+            st->reason = PGA_REASON_STALLED;
+        }
+        if (g + 1 >= max_gens) done = 1;
+        st->done = done;
+        const int improved = (best > st->best_ever) ? 1 : 0;
+        if (improved) st->best_ever = best;
+        s_improved = improved;
+        s_bi = bi;               // broadcast the argmax
     }
     __syncthreads();
     if (s_improved) {
@@ -1051,9 +1088,13 @@ int launch_init(pga_ctx *c, uint64_t seed, cudaStream_t s) {
 }
 
 int launch_stats(pga_ctx *c, int mode, cudaStream_t s) {
-    k_stats<<<1, 1024, 0, s>>>(c->L, c->P, c->pop[0], c->pop[1], c->ldn, c->N, c->st,
-                               c->best_labels, c->history, c->hist_cap, c->p.tol,
-                               c->p.stall_gens, c->p.max_gens, mode, c->p.migrate_every);
+    int64_t g = (c->P + STATS_PER_CTA - 1) / STATS_PER_CTA;
+    if (g > STATS_MAXG) g = STATS_MAXG;
+    const int64_t per = (c->P + g - 1) / g;
+    k_stats<<<(unsigned)g, STATS_T, 0, s>>>(c->L, c->P, c->pop[0], c->pop[1], c->ldn, c->N, c->st,
+                                            c->best_labels, c->history, c->hist_cap, c->p.tol,
+                                            c->p.stall_gens, c->p.max_gens, mode, c->p.migrate_every,
+                                            c->stats_part, c->stats_ctr, per);
     PGA_LAUNCHED();
     return PGA_OK;
 }

@@ -129,6 +129,8 @@ struct pga_ctx {
     // TMA descriptors (sweep) and fold counters
     CUtensorMap tmC{}, tmLab[2]{}, tmLabEv{};
     uint32_t *counters = nullptr;      // [Pcap / CB]
+    double *stats_part = nullptr;      // [3 x 1024] k_stats partials
+    uint32_t *stats_ctr = nullptr;     // k_stats CTA counter
     // migration scratch
     int64_t mig_bytes = 0;
     // host mirror
