@@ -509,7 +509,11 @@ k_select_small(int what, const double *__restrict__ L, int P, int M, int selecti
 // The last level writes the indices to order.  1 + ceil(log2(P / RUN))
 // launches, each spread over the whole GPU.
 // ---------------------------------------------------------------------------
-constexpr int RUN = 1024, RUN_T = 512;
+#ifndef PGA_SORT_RUN
+#define PGA_SORT_RUN 1024
+#endif
+// bitonic runs in shared memory (RUN * 12 B); 1024 measured best of 1024..4096
+constexpr int RUN = PGA_SORT_RUN, RUN_T = RUN / 2 < 1024 ? RUN / 2 : 1024;
 
 __global__ void __launch_bounds__(RUN_T)
 k_sort_runs(const double *__restrict__ L, int64_t P, uint64_t *keys, int32_t *idx, const int32_t *done) {
@@ -533,16 +537,19 @@ k_sort_runs(const double *__restrict__ L, int64_t P, uint64_t *keys, int32_t *id
     __syncthreads();
     for (int size = 2; size <= RUN; size <<= 1)
         for (int stride = size >> 1; stride > 0; stride >>= 1) {
-            const int t = tid;
-            const int i = 2 * t - (t & (stride - 1)), j = i + stride;
-            const bool up = (i & size) == 0;
-            const uint64_t ki = sk[i], kj = sk[j];
-            const uint32_t vi = sv[i], vj = sv[j];
-            if (kv_less(kj, vj, ki, vi) == up) {
-                sk[i] = kj;
-                sk[j] = ki;
-                sv[i] = vj;
-                sv[j] = vi;
+#pragma unroll
+            for (int r = 0; r < RUN / (2 * RUN_T); ++r) {
+                const int t = tid + r * RUN_T;
+                const int i = 2 * t - (t & (stride - 1)), j = i + stride;
+                const bool up = (i & size) == 0;
+                const uint64_t ki = sk[i], kj = sk[j];
+                const uint32_t vi = sv[i], vj = sv[j];
+                if (kv_less(kj, vj, ki, vi) == up) {
+                    sk[i] = kj;
+                    sk[j] = ki;
+                    sv[i] = vj;
+                    sv[j] = vi;
+                }
             }
             __syncthreads();
         }
