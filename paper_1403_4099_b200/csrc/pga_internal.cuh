@@ -147,11 +147,13 @@ struct pga_ctx {
     cudaEvent_t *pev = nullptr;         // this generation's events while profiling, else null
 };
 
-// Label-sparse threshold in effect: the caller's, else 0.25 with the cluster
-// cache (hits make a sparse block cheap up to a quarter of the dense pairs)
-// and 0.04 without it.
+// Label-sparse threshold in effect: the caller's, else automatic: off below
+// N = 160 (the dense sweep is cheaper there: C1-C3 measured), 0.25 with the
+// cluster cache (hits make a sparse block cheap up to a quarter of the dense
+// pairs) and 0.04 without it.
 inline double sparse_theta_eff(const pga_ctx *c) {
     if (c->sparse_theta >= 0.0) return c->sparse_theta;
+    if (c->N < 160) return 0.0;
     return (c->cc && c->cc_on) ? 0.25 : 0.04;
 }
 
