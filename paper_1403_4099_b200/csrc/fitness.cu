@@ -520,6 +520,7 @@ __global__ void k_resync_gm(const uint16_t *__restrict__ CM0, const uint16_t *__
 // ---------------------------------------------------------------------------
 constexpr int SP_W = 8, SP_T = SP_W * 32;
 constexpr int SPARSE_MAXN = 640;   // shared-memory footprint (sparse_smem) must fit one CTA
+constexpr int SP_LREG = SPARSE_MAXN / 64;   // label registers per lane (two 16-bit labels each)
 #ifndef PGA_CC_NMIN
 #define PGA_CC_NMIN 5
 #endif
@@ -764,11 +765,23 @@ __global__ void __launch_bounds__(SP_T, PGA_SP_MINB) k_fitness_sparse(SparseArgs
         __syncwarp();
         const uint16_t *lab = CM + p * a.ldn;
         uint32_t kmax = 0;
-#pragma unroll 4
-        for (int i = lane; i < N; i += 32) {
-            const uint32_t s = lab[i];
-            kmax = max(kmax, s);
-            atomicAdd(cq + (s >> 1), 1u << (16 * (s & 1u)));
+        // the chromosome's labels stay in registers for the three passes over
+        // them: gene lane + 32 k is half (k & 1) of labr[k >> 1]
+        uint32_t labr[SP_LREG];
+#pragma unroll
+        for (int k = 0; k < 2 * SP_LREG; ++k) {
+            const int i = lane + 32 * k;
+            const uint32_t v = i < N ? (uint32_t)lab[i] : 0u;
+            if (k & 1) labr[k >> 1] |= v << 16;
+            else labr[k >> 1] = v;
+        }
+#pragma unroll
+        for (int k = 0; k < 2 * SP_LREG; ++k) {
+            if (lane + 32 * k < N) {
+                const uint32_t s = (labr[k >> 1] >> (16 * (k & 1))) & 0xFFFFu;
+                kmax = max(kmax, s);
+                atomicAdd(cq + (s >> 1), 1u << (16 * (s & 1u)));
+            }
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) kmax = max(kmax, __shfl_xor_sync(0xFFFFFFFFu, kmax, o));
@@ -797,9 +810,11 @@ __global__ void __launch_bounds__(SP_T, PGA_SP_MINB) k_fitness_sparse(SparseArgs
         unsigned long long nhit = 0, nsaved = 0;
         if (use_cache && ecnt > 0) {
             // Zobrist XOR of each large cluster's members
-#pragma unroll 4
-            for (int i = lane; i < N; i += 32) {
-                const uint32_t om = ordm[lab[i]];
+#pragma unroll
+            for (int k = 0; k < 2 * SP_LREG; ++k) {
+                const int i = lane + 32 * k;
+                if (i >= N) continue;
+                const uint32_t om = ordm[(labr[k >> 1] >> (16 * (k & 1))) & 0xFFFFu];
                 if (!(om & 0x8000u)) {
                     uint32_t *h = reinterpret_cast<uint32_t *>(cent + om);
                     const uint4 kk = __ldg(keys4 + i);
@@ -853,9 +868,11 @@ __global__ void __launch_bounds__(SP_T, PGA_SP_MINB) k_fitness_sparse(SparseArgs
         // counting sort of the walked genes by label (order inside a cluster
         // is free: sums are exact); afterwards off[s] is the END of cluster s
         // and its start is off[s - 1] (0 for s = 0)
-#pragma unroll 4
-        for (int i = lane; i < N; i += 32) {
-            const uint32_t s = lab[i];
+#pragma unroll
+        for (int k = 0; k < 2 * SP_LREG; ++k) {
+            const int i = lane + 32 * k;
+            if (i >= N) continue;
+            const uint32_t s = (labr[k >> 1] >> (16 * (k & 1))) & 0xFFFFu;
             if (ordm[s] & 0x4000u) {
                 const uint32_t sh = 16 * (s & 1u);
                 const uint32_t pos = (atomicAdd(offw + (s >> 1), 1u << sh) >> sh) & 0xFFFFu;
