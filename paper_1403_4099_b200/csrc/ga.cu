@@ -262,35 +262,43 @@ __global__ void k_weights(const double *__restrict__ L, const int32_t *__restric
     q[i] = qi;
 }
 
+// SUS (Q9) without a search: the M pointers start + m * step are sorted and
+// evenly spaced, so individual i (wheel segment [prefix[i-1], prefix[i])) owns
+// exactly the pointers m in [ceil((lo - start) / step), ceil((hi - start) /
+// step)) -- the same min{i : prefix[i] > ptr} as a binary search, in exact
+// u64 arithmetic.  Thread t: the mates slot sigma[t] (t < M, fused) and the
+// pointers of individual t (t < P).
+__device__ __forceinline__ uint64_t sus_first(uint64_t x, uint64_t start, uint64_t step) {
+    return x <= start ? 0ull : (x - start + step - 1) / step;
+}
+
 __global__ void k_sus(const uint64_t *__restrict__ prefix, const double *__restrict__ L,
                       const int32_t *__restrict__ order, int64_t P, int64_t M, int scaling,
                       uint64_t seed, uint32_t gen, uint32_t island, int32_t *sel,
                       const int32_t *done, const int32_t *gen_ptr, int32_t *sigma) {
     if (done && *done) return;
-    const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (m >= M) return;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= P && t >= M) return;
     if (gen_ptr) gen = (uint32_t)*gen_ptr;
-    if (sigma) sigma[m] = feistel_slot(m, M, seed, gen, island);   // mates fused (Q10)
+    if (sigma && t < M) sigma[t] = feistel_slot(t, M, seed, gen, island);   // mates fused (Q10)
     const double wmax = (scaling == PGA_SCALE_RANK) ? 1.0 : L[order[0]];
     if (!(wmax > 0.0)) {  // all-zero fitness: uniform fallback
-        const U4 u = draw(seed, pga::TAG_SUS, island, gen, (uint32_t)m, 0u);
-        sel[m] = (int32_t)scale_u32(u.x, (uint32_t)P);
+        if (t < M) {
+            const U4 u = draw(seed, pga::TAG_SUS, island, gen, (uint32_t)t, 0u);
+            sel[t] = (int32_t)scale_u32(u.x, (uint32_t)P);
+        }
         return;
     }
+    if (t >= P) return;
     const uint64_t Q = prefix[P - 1];
     const uint64_t step = Q / (uint64_t)M;
     const U4 u = draw(seed, pga::TAG_SUS, island, gen, 0u, 0xFFFFFFFFu);
     const uint64_t x = ((uint64_t)u.x << 32) | (uint64_t)u.y;
     const uint64_t start = __umul64hi(x, step);
-    const uint64_t ptr = start + (uint64_t)m * step;
-    // min{i : prefix[i] > ptr}
-    int64_t lo = 0, hi = P - 1;
-    while (lo < hi) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (prefix[mid] > ptr) hi = mid;
-        else lo = mid + 1;
-    }
-    sel[m] = (int32_t)lo;
+    const uint64_t lo = t ? prefix[t - 1] : 0ull, hi = prefix[t];
+    const int64_t m0 = (int64_t)min(sus_first(lo, start, step), (uint64_t)M);
+    const int64_t m1 = (int64_t)min(sus_first(hi, start, step), (uint64_t)M);
+    for (int64_t m = m0; m < m1; ++m) sel[m] = (int32_t)t;
 }
 
 __global__ void k_tournament(const double *__restrict__ L, int64_t P, int64_t M, int k,
@@ -1191,7 +1199,7 @@ int run_select_ops(const double *L, int64_t P, const pga_params &p, int32_t gen,
     size_t tb = tmp_bytes;
     PGA_CUDA(cub::DeviceScan::InclusiveSum(tmp, tb, q, prefix, (int)P, s));
     count_launch();
-    k_sus<<<(unsigned)((M + 255) / 256), 256, 0, s>>>(prefix, L, order, P, M, p.scaling, p.seed,
+    k_sus<<<(unsigned)((max(P, M) + 255) / 256), 256, 0, s>>>(prefix, L, order, P, M, p.scaling, p.seed,
                                                       (uint32_t)gen, (uint32_t)island, sel, done,
                                                       gen_ptr, sigma);
     PGA_LAUNCHED();
