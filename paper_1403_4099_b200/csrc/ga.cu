@@ -787,36 +787,41 @@ __global__ void __launch_bounds__(BW * 32, 3) k_breed(BreedArgs a) {
 
 // ---------------------------------------------------------------------------
 // k_breed2 (N <= BREED2_MAXN): the same operators and outputs as k_breed with
-// a canonicalisation that has no dependency chain across gene chunks.
-// Phase 1 writes every child's pre-canonical genes to a shared tile [N][BS].
-// Phase 2 (warp per child): (a) first-occurrence positions fp[v] = min i --
-// each chunk's match_any leader (its first lane with that value) does a
-// shared atomicMin, so the chunks do not wait on one another;
-// (b) one ballot per chunk marks the genes i with fp[s_i] == i, and a running
-// count gives each chunk's base; (c) canonical(s_i) = rank of fp[s_i] among
-// the first occurrences = base[chunk] + popc(ballot[chunk] below fp's lane).
-// Phase 3 writes the gene-major rows of the CTA's 16 children from the tile.
+// a canonicalisation that has no dependency chain across gene chunks, and the
+// child's labels held in registers from crossover to the store.  Lane l owns
+// the gene pairs (128 b + 64 h + 2 l, +1) of its warp's child (NB = ceil(N /
+// 128) chunks b, h = 0, 1: one 32-bit word per pair).
+// Phase 1: crossover + mutation -> pre-canonical pair words.
+// Phase 2 (canonical form, Q7): (a) first-occurrence positions fp[v] = min i
+// by shared atomicMin (order-free, so no chunk waits on another); (b) per
+// 64-gene group G two ballots (even / odd genes) mark the genes i with
+// fp[s_i] == i, and a running count gives each group's base; (c) canonical(s_i)
+// = rank of f = fp[s_i] among the first occurrences = base[G'] + firsts of
+// group G' = f >> 6 below f (even genes with lane <= / < (f >> 1) & 31,
+// odd genes with lane <).  The canonical pair is one 32-bit store.
+// Phase 3 (dense mode only) writes the gene-major rows of the CTA's 16
+// children through the shared tile.
 // ---------------------------------------------------------------------------
 constexpr int BREED2_MAXN = 1024;
 
-__host__ __device__ __forceinline__ int breed2_nch(int N) { return (N + 31) / 32; }
+__host__ __device__ __forceinline__ int breed2_ngrp(int N) { return (N + 63) / 64; }
 
-// tile rows padded to whole 128-gene chunks: phase 1 stores unconditionally
+// tile rows padded to whole 128-gene chunks
 __host__ __device__ __forceinline__ int breed2_rows(int N) { return (N + GCH - 1) / GCH * GCH; }
 
 static size_t breed2_smem(int N) {
     const size_t tile = (size_t)breed2_rows(N) * TS * sizeof(uint16_t);
     const size_t fp = (size_t)BS * ((N + 1 + 3) & ~3) * sizeof(uint32_t);
-    const size_t bal = (size_t)BS * breed2_nch(N) * (sizeof(uint32_t) + sizeof(uint16_t));
-    return ((tile + 15) & ~(size_t)15) + ((fp + 15) & ~(size_t)15) + bal + 16;
+    const size_t grp = (size_t)BS * breed2_ngrp(N) * sizeof(uint4);
+    return ((tile + 15) & ~(size_t)15) + ((fp + 15) & ~(size_t)15) + grp + 16;
 }
 
-template <bool HOOK>
-__global__ void __launch_bounds__(BW * 32, 3) k_breed2(BreedArgs a) {
+template <bool HOOK, int NB>
+__global__ void __launch_bounds__(BW * 32, NB <= 2 ? 3 : 2) k_breed2(BreedArgs a) {
     if (a.done && *a.done) return;
     extern __shared__ __align__(16) unsigned char sm2[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int N = a.N, nch = breed2_nch(N);
+    const int N = a.N;
     const uint32_t gen = a.gen_ptr ? (uint32_t)*a.gen_ptr : a.gen;
     const int par = a.gen_ptr ? (int)(gen & 1u) : 0;
     const uint16_t *cm_in = par ? a.cm_in1 : a.cm_in0;
@@ -827,22 +832,22 @@ __global__ void __launch_bounds__(BW * 32, 3) k_breed2(BreedArgs a) {
     const int fpn = (N + 1 + 3) & ~3;
     uint32_t *fp = reinterpret_cast<uint32_t *>(sm2 + tile_b) + (size_t)warp * fpn;    // [BS][fpn]
     const size_t fp_b = ((size_t)BS * fpn * sizeof(uint32_t) + 15) & ~(size_t)15;
-    uint32_t *balv = reinterpret_cast<uint32_t *>(sm2 + tile_b + fp_b) + (size_t)warp * nch;
-    uint16_t *base = reinterpret_cast<uint16_t *>(sm2 + tile_b + fp_b + (size_t)BS * nch * sizeof(uint32_t)) +
-                     (size_t)warp * nch;
+    uint4 *grp = reinterpret_cast<uint4 *>(sm2 + tile_b + fp_b) + (size_t)warp * breed2_ngrp(N);  // {even, odd, base, -}
     const int64_t o0 = (int64_t)blockIdx.x * BS;
     const int slot = warp;
     const int64_t o = o0 + slot;
     const ChildPlan p = plan_child(a, o, gen);
 
-    // ---- phase 1: crossover + mutation -> pre-canonical genes in the tile.
-    // Lane l takes the gene pair (b0 + 64h + 2l, +1): one 32-bit load per
-    // parent, both mutation bits from one shuffle, and at most one MUTV
-    // block (both genes share Philox block (g >> 2)).
-    for (int b0 = 0; b0 < N; b0 += GCH) {
-        uint32_t ga[GCH / 64], gb[GCH / 64];
+    // ---- phase 1: crossover + mutation -> pre-canonical pair words.  Both
+    // mutation bits of a pair come from one shuffle, and there is at most one
+    // MUTV block per pair (both genes share Philox block (g >> 2)).
+    uint32_t w[NB][2];
 #pragma unroll
-        for (int h = 0; h < GCH / 64; ++h) {
+    for (int b = 0; b < NB; ++b) {
+        const int b0 = GCH * b;
+        uint32_t ga[2], gb[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
             const int g0 = b0 + 64 * h + 2 * lane;
             const bool v0 = p.valid && g0 < N, v1 = p.valid && g0 + 1 < N;
             if (HOOK) {
@@ -863,7 +868,7 @@ __global__ void __launch_bounds__(BW * 32, 3) k_breed2(BreedArgs a) {
                     ((uint64_t)u.z < a.thr_m ? 4u : 0u) | ((uint64_t)u.w < a.thr_m ? 8u : 0u);
         }
 #pragma unroll
-        for (int h = 0; h < GCH / 64; ++h) {
+        for (int h = 0; h < 2; ++h) {
             const int g0 = b0 + 64 * h + 2 * lane;
             const uint32_t mb = (__shfl_sync(0xFFFFFFFFu, mbits, 16 * h + (lane >> 1)) >> (2 * (lane & 1))) & 3u;
             uint32_t s[2];
@@ -885,59 +890,70 @@ __global__ void __launch_bounds__(BW * 32, 3) k_breed2(BreedArgs a) {
                 for (int e = 0; e < 2; ++e)
                     if ((mb >> e) & 1u) s[e] = scale_u32(word(v, (g0 + e) & 3), (uint32_t)N);
             }
-            tile[g0 * TS + slot] = (uint16_t)s[0];          // rows >= N are padding
-            tile[(g0 + 1) * TS + slot] = (uint16_t)s[1];
+            w[b][h] = s[0] | (s[1] << 16);
         }
     }
-    __syncwarp();
 
     // ---- phase 2: canonical form (Q7), no chain across chunks
+    const bool gm = !HOOK && !(a.gm_skip && *a.gm_skip);   // dense mode: gene-major rows wanted
     if (p.valid) {
         {                                             // (a) first occurrences: fp[v] = min i
             uint4 *f4 = reinterpret_cast<uint4 *>(fp);
             const uint4 inf = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
             for (int k = lane; k < fpn / 4; k += 32) f4[k] = inf;
             __syncwarp();
-            for (int c = 0; c < nch; ++c) {           // independent chunks: atomics return nothing
-                const int i = 32 * c + lane;
-                const bool valid = i < N;
-#ifdef PGA_BREED_MATCH
-                const uint32_t s = valid ? (uint32_t)tile[i * TS + slot] : 0x10000u + (uint32_t)lane;
-                const unsigned m = __match_any_sync(0xFFFFFFFFu, s);
-                if (valid && lane == __ffs(m) - 1) atomicMin(&fp[s], (uint32_t)i);
-#else
-                // every lane: the shared-memory atomic unit resolves equal
-                // labels in a chunk (cheaper than waiting for MATCH.ANY)
-                if (valid) atomicMin(&fp[tile[i * TS + slot]], (uint32_t)i);
-#endif
-            }
+#pragma unroll
+            for (int b = 0; b < NB; ++b)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int g0 = GCH * b + 64 * h + 2 * lane;
+                    if (g0 < N) atomicMin(&fp[w[b][h] & 0xFFFFu], (uint32_t)g0);
+                    if (g0 + 1 < N) atomicMin(&fp[w[b][h] >> 16], (uint32_t)(g0 + 1));
+                }
             __syncwarp();
         }
-        int run = 0;
-        for (int c = 0; c < nch; ++c) {               // (b) first-occurrence ballots, chunk bases
-            const int i = 32 * c + lane;
-            const bool first = i < N && fp[tile[i * TS + slot]] == (uint32_t)i;
-            const unsigned bal = __ballot_sync(0xFFFFFFFFu, first);
-            if (lane == 0) {
-                balv[c] = bal;
-                base[c] = (uint16_t)run;
+        uint32_t run = 0;
+#pragma unroll
+        for (int b = 0; b < NB; ++b)                  // (b) first-occurrence ballots, group bases
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int G = 2 * b + h, g0 = 64 * G + 2 * lane;
+                if (64 * G >= N) continue;            // warp-uniform
+                const bool f0 = g0 < N && fp[w[b][h] & 0xFFFFu] == (uint32_t)g0;
+                const bool f1 = g0 + 1 < N && fp[w[b][h] >> 16] == (uint32_t)(g0 + 1);
+                const unsigned be = __ballot_sync(0xFFFFFFFFu, f0), bo = __ballot_sync(0xFFFFFFFFu, f1);
+                if (lane == 0) grp[G] = make_uint4(be, bo, run, 0u);
+                run += (uint32_t)(__popc(be) + __popc(bo));
             }
-            run += __popc(bal);
-        }
         __syncwarp();
-        for (int c = 0; c < nch; ++c) {               // (c) canonical labels
-            const int i = 32 * c + lane;
-            if (i < N) {
-                const int f = (int)fp[tile[i * TS + slot]];
-                const uint32_t cv = (uint32_t)base[f >> 5] + __popc(balv[f >> 5] & ((1u << (f & 31)) - 1u));
-                tile[i * TS + slot] = (uint16_t)cv;
-                if (HOOK) a.i32_out[o * N + i] = (int32_t)cv;
-                else cm_out[o * a.ldn + i] = (uint16_t)cv;
+#pragma unroll
+        for (int b = 0; b < NB; ++b)                  // (c) canonical labels
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int g0 = GCH * b + 64 * h + 2 * lane;
+                if (g0 >= N) continue;
+                uint32_t cv[2];
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const uint32_t f = (g0 + e < N) ? fp[(w[b][h] >> (16 * e)) & 0xFFFFu] : 0u;
+                    const uint4 gr = grp[f >> 6];
+                    const uint32_t l = (f >> 1) & 31u, below = (1u << l) - 1u;
+                    cv[e] = gr.z + __popc(gr.x & (below | ((f & 1u) << l))) + __popc(gr.y & below);
+                }
+                if (g0 + 1 >= N) cv[1] = 0u;
+                if (HOOK) {
+                    a.i32_out[o * N + g0] = (int32_t)cv[0];
+                    if (g0 + 1 < N) a.i32_out[o * N + g0 + 1] = (int32_t)cv[1];
+                } else {
+                    *reinterpret_cast<uint32_t *>(cm_out + o * a.ldn + g0) = cv[0] | (cv[1] << 16);
+                    if (gm) {
+                        tile[g0 * TS + slot] = (uint16_t)cv[0];
+                        tile[(g0 + 1) * TS + slot] = (uint16_t)cv[1];   // rows >= N are padding
+                    }
+                }
             }
-        }
     }
-    if (HOOK) return;
-    if (a.gm_skip && *a.gm_skip) return;   // sparse mode: k_fitness_sparse transposes dense blocks itself
+    if (!gm) return;   // sparse mode: k_fitness_sparse transposes dense blocks itself
     __syncthreads();
 
     // ---- phase 3: gene-major rows (BS children = 32 B per gene)
@@ -950,6 +966,29 @@ __global__ void __launch_bounds__(BW * 32, 3) k_breed2(BreedArgs a) {
             else gm_out[(int64_t)i * a.Pcap + oo] = (uint16_t)(two & 0xFFFF);
         }
     }
+}
+
+// one instantiation per chunk count NB = ceil(N / 128) (labels stay in registers)
+template <bool HOOK>
+static void launch_breed2(const BreedArgs &a, int64_t P, int N, cudaStream_t s) {
+    const unsigned grid = (unsigned)((P + BS - 1) / BS);
+    const size_t sm = breed2_smem(N);
+    switch ((N + GCH - 1) / GCH) {
+#define PGA_B2(nb) case nb: k_breed2<HOOK, nb><<<grid, BW * 32, sm, s>>>(a); break;
+        PGA_B2(1) PGA_B2(2) PGA_B2(3) PGA_B2(4) PGA_B2(5) PGA_B2(6) PGA_B2(7) PGA_B2(8)
+#undef PGA_B2
+    }
+}
+
+template <bool HOOK>
+static cudaError_t prepare_breed2(int N) {
+    const int sm = (int)breed2_smem(N);
+    switch ((N + GCH - 1) / GCH) {
+#define PGA_B2(nb) case nb: return cudaFuncSetAttribute(k_breed2<HOOK, nb>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+        PGA_B2(1) PGA_B2(2) PGA_B2(3) PGA_B2(4) PGA_B2(5) PGA_B2(6) PGA_B2(7) PGA_B2(8)
+#undef PGA_B2
+    }
+    return cudaSuccess;
 }
 
 // k_set_pop: int32 1-based labels (validated on the host) -> canonical
@@ -1081,10 +1120,8 @@ int prepare_breed(int N) {
     PGA_CUDA(cudaFuncSetAttribute(k_breed<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)breed_smem(N)));
     PGA_CUDA(cudaFuncSetAttribute(k_breed<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)breed_smem(N)));
     if (N <= BREED2_MAXN) {
-        PGA_CUDA(cudaFuncSetAttribute(k_breed2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)breed2_smem(N)));
-        PGA_CUDA(cudaFuncSetAttribute(k_breed2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)breed2_smem(N)));
+        PGA_CUDA(prepare_breed2<true>(N));
+        PGA_CUDA(prepare_breed2<false>(N));
     }
     return PGA_OK;
 }
@@ -1249,7 +1286,7 @@ int launch_breed_hook(const int32_t *pop, const int32_t *top, const int32_t *ord
     a.island = (uint32_t)island;
     a.ldn = N;
     a.Pcap = P;
-    if (N <= BREED2_MAXN) k_breed2<true><<<(unsigned)((P + BS - 1) / BS), BW * 32, breed2_smem(N), s>>>(a);
+    if (N <= BREED2_MAXN) launch_breed2<true>(a, P, N, s);
     else k_breed<true><<<(unsigned)((P + BS - 1) / BS), BW * 32, breed_smem(N), s>>>(a);
     PGA_LAUNCHED();
     return PGA_OK;
@@ -1311,7 +1348,7 @@ int launch_select_breed(pga_ctx *c, cudaStream_t s) {
     // checks are live (it transposes exactly the blocks the dense sweep needs)
     a.gm_skip = (sparse_theta_eff(c) > 0.0 && c->N <= 640) ? c->sp_live : nullptr;
     if (c->N <= BREED2_MAXN)
-        k_breed2<false><<<(unsigned)((c->P + BS - 1) / BS), BW * 32, breed2_smem(c->N), s>>>(a);
+        launch_breed2<false>(a, c->P, c->N, s);
     else
         k_breed<false><<<(unsigned)((c->P + BS - 1) / BS), BW * 32, breed_smem(c->N), s>>>(a);
     PGA_LAUNCHED();
