@@ -1,3 +1,4 @@
+#include <cstdlib>
 // api.cu — the C ABI declared in include/pga.h.  Argument validation, the
 // per-island runtime (buffers, stream, CUDA graph of one generation) and the
 // host<->device marshalling.  Every step of the method runs in the kernels of
@@ -29,6 +30,14 @@ int cuda_fail(cudaError_t e, const char *what) {
     return PGA_EDEVICE;
 }
 void count_launch(int n) { g_launches += n; }
+
+cudaError_t prof_record(cudaEvent_t e, cudaStream_t s) {
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    cudaError_t r = cudaStreamIsCapturing(s, &st);
+    if (r != cudaSuccess) return r;
+    return st == cudaStreamCaptureStatusActive ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal)
+                                               : cudaEventRecord(e, s);
+}
 
 // declared in ga.cu / fitness.cu
 int launch_resync_gm(pga_ctx *c, cudaStream_t s);
@@ -113,13 +122,23 @@ using namespace pga;
 
 namespace {
 
-struct Graphs {
-    cudaGraphExec_t gen = nullptr;
-};
+
+void drop_graph(GExec &g) {
+    if (g.x) cudaGraphExecDestroy(g.x);
+    if (g.g) cudaGraphDestroy(g.g);
+    g = GExec{};
+}
+
+void drop_graphs(pga_ctx *c) {
+    drop_graph(c->gx_eval[0]);
+    drop_graph(c->gx_eval[1]);
+    drop_graph(c->gx_breed);
+}
 
 void free_ctx(pga_ctx *c) {
     if (!c) return;
     cudaSetDevice(c->device);
+    drop_graphs(c);
     void *ptrs[] = {c->C, c->diag, c->lgtab, c->sflag, c->sp_live, c->sp_blocks, c->cc, c->cc_state,
                     c->stats_part, c->stats_ctr,
                     c->cc_keys, c->pop[0], c->pop[1], c->popT[0], c->popT[1], c->V, c->L,
@@ -231,34 +250,79 @@ int phase_b(pga_ctx *c) {
     PGA_MARK(c, 4, c->stream);
     TRY(launch_select_breed(c, c->stream));
     if (c->pev) {
-        PGA_CUDA(cudaEventRecord(c->pev[8], c->stream));
+        PGA_CUDA(prof_record(c->pev[8], c->stream));
         c->prof_used += PROF_EV;
         c->pev = nullptr;
     }
     return PGA_OK;
 }
 
+// Capture fn()'s launches on c->stream into *g.  Profiling: the events fn()
+// records (this generation's slot of prof_ev) become event-record nodes,
+// remembered with their phase-mark index so that every replay records into
+// that generation's own slot (launch_graph).
+template <class F>
+int capture_graph(pga_ctx *c, GExec *g, F fn) {
+    drop_graph(*g);
+    const size_t base = c->prof_used;
+    const size_t pu = c->prof_used;
+    const int64_t k0 = g_launches;
+    PGA_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    const int rc = fn();
+    g->nk = (int)(g_launches - k0);
+    g_launches -= g->nk;   // counted at every replay instead
+    c->prof_used = pu;     // fn()'s bookkeeping is redone per replay
+    cudaError_t e = cudaStreamEndCapture(c->stream, &g->g);
+    if (rc || e != cudaSuccess) {
+        drop_graph(*g);
+        return rc ? rc : cuda_fail(e, "cudaStreamEndCapture");
+    }
+    if (c->prof) {
+        size_t n = 0;
+        PGA_CUDA(cudaGraphGetNodes(g->g, nullptr, &n));
+        std::vector<cudaGraphNode_t> nodes(n);
+        PGA_CUDA(cudaGraphGetNodes(g->g, nodes.data(), &n));
+        for (cudaGraphNode_t nd : nodes) {
+            cudaGraphNodeType t;
+            PGA_CUDA(cudaGraphNodeGetType(nd, &t));
+            if (t != cudaGraphNodeTypeEventRecord) continue;
+            cudaEvent_t ev;
+            PGA_CUDA(cudaGraphEventRecordNodeGetEvent(nd, &ev));
+            for (int k = 0; k < PROF_EV; ++k)
+                if (base + k < c->prof_ev.size() && c->prof_ev[base + k] == ev) g->evn.emplace_back(nd, k);
+        }
+    }
+    e = cudaGraphInstantiate(&g->x, g->g, 0);
+    if (e != cudaSuccess) {
+        drop_graph(*g);
+        return cuda_fail(e, "cudaGraphInstantiate");
+    }
+    return PGA_OK;
+}
+
+int launch_graph(pga_ctx *c, GExec &g) {
+    if (!g.evn.empty()) {
+        cudaEvent_t *slot = prof_slot(c);
+        if (!slot) return fail(PGA_EDEVICE, "profiling events unavailable");
+        for (auto &ne : g.evn) PGA_CUDA(cudaGraphExecEventRecordNodeSetEvent(g.x, ne.first, slot[ne.second]));
+    }
+    PGA_CUDA(cudaGraphLaunch(g.x, c->stream));
+    count_launch(g.nk);
+    return PGA_OK;
+}
+
 // one single-island generation, captured once into a CUDA graph
-int run_one_generation(pga_ctx *c, Graphs &g, bool use_graph) {
+int run_one_generation(pga_ctx *c, GExec &g, bool use_graph) {
     if (!use_graph) {
         TRY(phase_a(c, 0, nullptr));
         return phase_b(c);
     }
-    if (!g.gen) {
-        cudaGraph_t graph;
-        PGA_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-        int rc = phase_a(c, 0, nullptr);
-        if (!rc) rc = phase_b(c);
-        cudaError_t e = cudaStreamEndCapture(c->stream, &graph);
-        if (rc) return rc;
-        if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
-        e = cudaGraphInstantiate(&g.gen, graph, 0);
-        cudaGraphDestroy(graph);
-        if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
-    }
-    PGA_CUDA(cudaGraphLaunch(g.gen, c->stream));
-    count_launch(0);
-    return PGA_OK;
+    if (!g.x)
+        TRY(capture_graph(c, &g, [&] {
+            int rc = phase_a(c, 0, nullptr);
+            return rc ? rc : phase_b(c);
+        }));
+    return launch_graph(c, g);
 }
 
 void to_one_based(const std::vector<uint16_t> &src, int32_t *dst, size_t n) {
@@ -521,7 +585,16 @@ int pga_gen_evaluate(pga_ctx *c, int32_t *is_migration) {
     if (!c->has_pop) return fail(PGA_ESTATE, "no population: call pga_init first");
     if (c->pending_migration) return fail(PGA_ESTATE, "migration pending: call pga_import_migrants");
     PGA_CUDA(cudaSetDevice(c->device));
-    return phase_a(c, c->host_gen, is_migration);
+    // replay of the cached graph for this kind of generation (the host
+    // decides migration generations, so each kind has its own graph)
+    const bool mig = is_migration_gen(c, c->host_gen);
+    GExec &g = c->gx_eval[mig ? 1 : 0];
+    if (!g.x) TRY(capture_graph(c, &g, [&] { return phase_a(c, c->host_gen, nullptr); }));
+    TRY(launch_graph(c, g));
+    c->pev = prof_slot(c);   // this generation's slot (null unless profiling)
+    c->pending_migration = mig;
+    if (is_migration) *is_migration = mig ? 1 : 0;
+    return PGA_OK;
 }
 
 int pga_set_sparse_threshold(pga_ctx *c, double theta) {
@@ -529,6 +602,7 @@ int pga_set_sparse_threshold(pga_ctx *c, double theta) {
     if (!(theta <= 1.0)) return fail(PGA_EINVAL, "theta must lie in [0, 1] (negative = automatic)");
     const bool was_on = sparse_theta_eff(c) > 0.0;
     c->sparse_theta = theta < 0.0 ? -1.0 : theta;
+    drop_graphs(c);   // the launch sequence depends on it
     if (was_on && !(sparse_theta_eff(c) > 0.0) && c->has_pop && c->N <= 640) {
         // the breed may have left the gene-major copy to the sparse pass
         PGA_CUDA(cudaSetDevice(c->device));
@@ -566,7 +640,11 @@ int pga_gen_breed(pga_ctx *c) {
     if (!c->has_pop) return fail(PGA_ESTATE, "no population: call pga_init first");
     if (c->pending_migration) return fail(PGA_ESTATE, "migration pending: call pga_import_migrants");
     PGA_CUDA(cudaSetDevice(c->device));
-    TRY(phase_b(c));
+    const bool profiled = c->pev != nullptr;   // phase_b clears it while being captured
+    if (!c->gx_breed.x) TRY(capture_graph(c, &c->gx_breed, [&] { return phase_b(c); }));
+    TRY(launch_graph(c, c->gx_breed));
+    if (profiled) c->prof_used += PROF_EV;   // as phase_b does in plain launches
+    c->pev = nullptr;
     c->host_gen += 1;
     return PGA_OK;
 }
@@ -588,12 +666,13 @@ int pga_run(pga_ctx *c, int32_t gens, uint64_t seed, int32_t *best_labels, doubl
     if (!c) return fail(PGA_EINVAL, "ctx is NULL");
     if (c->p.n_islands > 1) return fail(PGA_ESTATE, "pga_run is single-island; drive islands with pga_gen_evaluate/breed");
     PGA_CUDA(cudaSetDevice(c->device));
+    drop_graphs(c);   // max_gens is changed for this run (a kernel argument)
     const int32_t saved_max = c->p.max_gens;
     const int32_t maxg = gens > 0 ? gens : c->p.max_gens;
     TRY(ensure_history(c, maxg));
     c->p.max_gens = maxg;
     int rc = pga_init(c, seed);
-    Graphs g;
+    GExec g;
     int32_t launched = 0;
     const int32_t batch = 8;
     while (!rc) {
@@ -604,7 +683,7 @@ int pga_run(pga_ctx *c, int32_t gens, uint64_t seed, int32_t *best_labels, doubl
         if (rc) break;
         if (c->h_st->done || launched >= maxg) break;
     }
-    if (g.gen) cudaGraphExecDestroy(g.gen);
+    drop_graph(g);
     c->p.max_gens = saved_max;
     if (rc) return rc;
     c->host_gen = c->h_st->gen;
@@ -669,6 +748,7 @@ int pga_profile_enable(pga_ctx *c, int32_t on) {
     if (!c) return fail(PGA_EINVAL, "ctx is NULL");
     c->prof = on != 0;
     c->prof_level = on;
+    drop_graphs(c);
     c->prof_used = 0;
     PGA_CUDA(cudaSetDevice(c->device));
     PGA_CUDA(cudaMemsetAsync(c->sp_blocks, 0, 4 * sizeof(unsigned long long), c->stream));
@@ -678,6 +758,7 @@ int pga_profile_enable(pga_ctx *c, int32_t on) {
 int pga_set_cluster_cache(pga_ctx *c, int32_t on) {
     if (!c) return fail(PGA_EINVAL, "ctx is NULL");
     c->cc_on = on != 0;
+    drop_graphs(c);
     return PGA_OK;
 }
 

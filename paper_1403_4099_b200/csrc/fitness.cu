@@ -297,8 +297,12 @@ __device__ __forceinline__ void fold_multi(const uint16_t *const (&lab)[NC], con
 __global__ void __launch_bounds__(FIT_THREADS)
 k_fitness(const __grid_constant__ CUtensorMap tmLab0, const __grid_constant__ CUtensorMap tmLab1,
           const __grid_constant__ CUtensorMap tmC, FitArgs a) {
-    if (a.done && *a.done) return;
-    if (a.sflag && a.sflag[a.cb0 + (int)(blockIdx.x / a.nRT)]) return;   // done by k_fitness_sparse
+    {   // both exit tests from one round trip (independent loads): with every
+        // block evaluated label-sparsely, this is all a CTA does
+        const int32_t dn = a.done ? __ldg(a.done) : 0;
+        const uint8_t sf = a.sflag ? a.sflag[a.cb0 + (int)(blockIdx.x / a.nRT)] : (uint8_t)0;
+        if (dn | sf) return;   // stopped, or done by k_fitness_sparse
+    }
     const int par = (a.gen && (*a.gen & 1)) ? 1 : 0;
     const CUtensorMap *tmLab = par ? &tmLab1 : &tmLab0;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -1170,7 +1174,7 @@ int launch_fitness_range(pga_ctx *c, const FitBufs &b, int64_t begin, int64_t en
     a.gen = b.gen;
     a.done = b.done;
     a.counters = c->counters;
-    if (ev) PGA_CUDA(cudaEventRecord(ev[0], s));
+    if (ev) PGA_CUDA(prof_record(ev[0], s));
     a.sflag = nullptr;
     if (sparse_theta_eff(c) > 0.0 && N <= SPARSE_MAXN && c->sflag) {
         // label-sparse pass first (f2); it flags the blocks it evaluated
@@ -1209,10 +1213,10 @@ int launch_fitness_range(pga_ctx *c, const FitBufs &b, int64_t begin, int64_t en
         PGA_LAUNCHED();
         a.sflag = c->sflag;
     }
-    if (ev) PGA_CUDA(cudaEventRecord(ev[1], s));   // dense kernel starts here
+    if (ev) PGA_CUDA(prof_record(ev[1], s));   // dense kernel starts here
     k_fitness<<<(unsigned)(a.nRT * a.nCB), FIT_THREADS, fitness_smem(N), s>>>(*b.tm0, *b.tm1, c->tmC, a);
     PGA_LAUNCHED();
-    if (ev) PGA_CUDA(cudaEventRecord(ev[2], s));   // sweep and fold are one fused kernel
+    if (ev) PGA_CUDA(prof_record(ev[2], s));   // sweep and fold are one fused kernel
     return PGA_OK;
 }
 

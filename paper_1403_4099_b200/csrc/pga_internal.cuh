@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/pga.h"
@@ -19,6 +20,9 @@ void set_error(const std::string &msg);
 int fail(int code, const std::string &msg);
 int cuda_fail(cudaError_t e, const char *what);
 void count_launch(int n = 1);
+// profiling event record; under stream capture it becomes an event-record
+// node of the graph (cudaEventRecordExternal), re-targeted per replay
+cudaError_t prof_record(cudaEvent_t e, cudaStream_t s);
 int check_params(const pga_params *p);       // api.cu: pga_params validation
 int check_corr(const double *C, int32_t N);  // api.cu: C finite, unit diagonal, symmetric
 int ensure_device(int dev);                  // api.cu: device present, made current
@@ -31,7 +35,7 @@ int ensure_device(int dev);                  // api.cu: device present, made cur
 
 #define PGA_MARK(c, k, s)                                                  \
     do {                                                                   \
-        if ((c)->pev && (c)->prof_level >= 2) PGA_CUDA(cudaEventRecord((c)->pev[k], (s))); \
+        if ((c)->pev && (c)->prof_level >= 2) PGA_CUDA(::pga::prof_record((c)->pev[k], (s))); \
     } while (0)
 
 #define PGA_LAUNCHED()                                                     \
@@ -79,6 +83,18 @@ struct Migrant;  // layout documented in api.cu
 }  // namespace pga
 
 // The context (opaque at the ABI).
+namespace pga {
+// a captured launch sequence: the executable graph, its template (kept for
+// the event-record node handles), the kernel launches it holds, and its
+// profiling event-record nodes with their phase-mark index
+struct GExec {
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t x = nullptr;
+    int nk = 0;
+    std::vector<std::pair<cudaGraphNode_t, int>> evn;
+};
+}  // namespace pga
+
 struct pga_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -95,6 +111,11 @@ struct pga_ctx {
     uint8_t *sflag = nullptr; // [Pcap / CB]: block evaluated by the label-sparse pass (f2)
     double sparse_theta = -1.0;   // < 0: automatic (sparse_theta_eff)
     int32_t *sp_live = nullptr;  // device [6]: sparse-pass hysteresis (see k_fitness_sparse)
+    // cached graphs of pga_gen_evaluate (plain / migration generation) and
+    // pga_gen_breed; dropped whenever a setting that changes the launch
+    // sequence does (drop_graphs)
+    pga::GExec gx_eval[2];
+    pga::GExec gx_breed;
     unsigned long long *sp_blocks = nullptr;  // device [4]: sparse blocks, gathers, cache hits, pairs saved (profiling)
     pga::CCSlot *cc = nullptr;     // cluster cache table (N <= 640)
     uint32_t cc_mask = 0;          // slots - 1
