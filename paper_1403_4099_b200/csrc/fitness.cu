@@ -555,16 +555,25 @@ __device__ __forceinline__ uint64_t cc_mix(uint64_t k1, uint64_t k2, long long v
     return z | 1ull;
 }
 
+__device__ __forceinline__ ulonglong2 ld_relaxed_u64x2(const uint64_t *p) {
+    ulonglong2 v;
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p) : "memory");
+    return v;
+}
+
 __device__ __forceinline__ bool cc_find(pga::CCSlot *T, uint32_t mask, uint64_t k1, uint64_t k2, uint32_t n,
                                         long long *v) {
     uint32_t i = (uint32_t)(k1 >> 17) & mask;
     for (int r = 0; r < CC_PROBE; ++r) {
-        const uint64_t s1 = ld_relaxed_u64(&T[i].k1);
+        // the whole 32-byte slot in one round trip (two 16-byte loads in flight)
+        const ulonglong2 h = ld_relaxed_u64x2(&T[i].k1);
+        const ulonglong2 t = ld_relaxed_u64x2(reinterpret_cast<const uint64_t *>(&T[i].v));
+        const uint64_t s1 = h.x;
         if (s1 == 0) return false;
         if (s1 == k1) {
-            const uint64_t s2 = ld_relaxed_u64(&T[i].k2);
-            const long long sv = (long long)ld_relaxed_u64(reinterpret_cast<const uint64_t *>(&T[i].v));
-            const uint64_t sc = ld_relaxed_u64(&T[i].chk);
+            const uint64_t s2 = h.y;
+            const long long sv = (long long)t.x;
+            const uint64_t sc = t.y;
             if (s2 != k2 || sc != cc_mix(k1, k2, sv, n)) return false;
             *v = sv;
             return true;

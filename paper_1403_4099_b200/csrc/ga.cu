@@ -571,25 +571,89 @@ k_sort_runs(const double *__restrict__ L, int64_t P, uint64_t *keys, int32_t *id
 }
 
 // one merge level at run width w: (ks, is) -> (kd, id); kd may be null (last level)
-__global__ void k_merge_level(const uint64_t *__restrict__ ks, const int32_t *__restrict__ is, int64_t P,
-                              int64_t w, uint64_t *kd, int32_t *id, const int32_t *done) {
+// One merge level.  A CTA's 256 items lie in one run (w is a multiple of
+// 256), so their ranks in the sibling run are monotone and cover one
+// contiguous range.  Rank = number of sibling items before the item in
+// (key, index) order: (1) a sample of every MS-th sibling item is staged in
+// shared memory (one coalesced round trip) and searched there, which bounds
+// the rank to a window of MS; (2) the union of the CTA's windows is staged in
+// shared memory and each item finishes its search there.  Spans too large
+// to stage fall back to searches in global memory.  The result is the same
+// permutation as a plain per-item binary search.
+constexpr int MERGE_T = 256, MERGE_MS = 64, MERGE_CAP = 2048;
+static_assert(RUN % MERGE_T == 0, "a CTA of the merge must lie in one run");
+
+__device__ __forceinline__ bool key_before(uint64_t ka, uint32_t ia, uint64_t kb, uint32_t ib) {
+    return ka < kb || (ka == kb && ia < ib);
+}
+
+__global__ void __launch_bounds__(MERGE_T) k_merge_level(const uint64_t *__restrict__ ks,
+                                                         const int32_t *__restrict__ is, int64_t P, int64_t w,
+                                                         uint64_t *kd, int32_t *id, const int32_t *done) {
     if (done && *done) return;
-    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= P) return;
-    const int64_t blk = g / (2 * w) * (2 * w);
-    const bool left = g - blk < w;
+    __shared__ uint64_t sk[MERGE_CAP];
+    __shared__ uint32_t si[MERGE_CAP];
+    __shared__ int64_t s_lo, s_hi;
+    const int tid = threadIdx.x;
+    const int64_t c0 = (int64_t)blockIdx.x * MERGE_T;
+    if (c0 >= P) return;
+    const int64_t g = c0 + tid;
+    const bool valid = g < P;
+    const int64_t blk = c0 / (2 * w) * (2 * w);
+    const bool left = c0 - blk < w;
     const int64_t sib = left ? blk + w : blk;
-    const int64_t off = left ? g - blk : g - blk - w;
+    const int64_t off = (left ? c0 - blk : c0 - blk - w) + tid;
     const int64_t slen = max((int64_t)0, min(w, P - sib));
-    const uint64_t ke = ks[g];
-    const uint32_t ie = (uint32_t)is[g];
+    const int64_t last = min((int64_t)MERGE_T, P - c0) - 1;   // last valid thread
+    const uint64_t ke = valid ? ks[g] : ~0ull;
+    const uint32_t ie = valid ? (uint32_t)is[g] : 0xFFFFFFFFu;
+    const uint64_t *sk_g = ks + sib;
+    const int32_t *si_g = is + sib;
+
+    // (1) window [lo, hi) of the rank from the sibling's MS-sample
     int64_t lo = 0, hi = slen;
-    while (lo < hi) {            // sibling items before (ke, ie)
-        const int64_t mid = (lo + hi) >> 1;
-        const uint64_t km = __ldg(ks + sib + mid);
-        if (km < ke || (km == ke && (uint32_t)__ldg(is + sib + mid) < ie)) lo = mid + 1;
-        else hi = mid;
+    const int64_t ns = (slen + MERGE_MS - 1) / MERGE_MS;
+    if (ns > 0 && ns <= MERGE_CAP) {
+        for (int64_t j = tid; j < ns; j += MERGE_T) {
+            sk[j] = __ldg(sk_g + j * MERGE_MS);
+            si[j] = (uint32_t)__ldg(si_g + j * MERGE_MS);
+        }
+        __syncthreads();
+        int64_t a = 0, b = ns;                        // samples before the item
+        while (a < b) {
+            const int64_t m = (a + b) >> 1;
+            if (key_before(sk[m], si[m], ke, ie)) a = m + 1;
+            else b = m;
+        }
+        lo = a > 0 ? (a - 1) * MERGE_MS + 1 : 0;
+        hi = min(slen, a * MERGE_MS);
+        __syncthreads();                              // samples read: the buffer is reused
     }
+    // (2) the CTA's span of windows, staged when it fits
+    if (tid == 0) s_lo = lo;
+    if (tid == last) s_hi = hi;
+    __syncthreads();
+    const int64_t Lo = s_lo, Hi = s_hi;
+    if (!valid) lo = hi = Lo;                         // beyond P: no search
+    if (Hi - Lo <= MERGE_CAP) {
+        for (int64_t p = Lo + tid; p < Hi; p += MERGE_T) {
+            sk[p - Lo] = __ldg(sk_g + p);
+            si[p - Lo] = (uint32_t)__ldg(si_g + p);
+        }
+        __syncthreads();
+        while (lo < hi) {
+            const int64_t m = (lo + hi) >> 1;
+            if (key_before(sk[m - Lo], si[m - Lo], ke, ie)) lo = m + 1;
+            else hi = m;
+        }
+    } else {
+        while (lo < hi) {
+            const int64_t m = (lo + hi) >> 1;
+            if (key_before(__ldg(sk_g + m), (uint32_t)__ldg(si_g + m), ke, ie)) lo = m + 1;
+            else hi = m;
+        }
+    }
+    if (!valid) return;
     const int64_t pos = blk + off + lo;
     if (kd) kd[pos] = ke;
     id[pos] = (int32_t)ie;
@@ -1173,13 +1237,13 @@ static int sort_order(const double *L, int64_t P, int32_t *order, uint64_t *keys
     PGA_LAUNCHED();
     const unsigned nb = (unsigned)((P + 255) / 256);
     if (nruns == 1) {   // one run: copy its indices out through a width-P "merge"
-        k_merge_level<<<nb, 256, 0, s>>>(kA, iA, P, P, nullptr, order, done);
+        k_merge_level<<<nb, MERGE_T, 0, s>>>(kA, iA, P, P, nullptr, order, done);
         PGA_LAUNCHED();
         return PGA_OK;
     }
     for (int64_t w = RUN; w < P; w *= 2) {
         const bool last = 2 * w >= P;
-        k_merge_level<<<nb, 256, 0, s>>>(kA, iA, P, w, last ? nullptr : kB, last ? order : iB, done);
+        k_merge_level<<<nb, MERGE_T, 0, s>>>(kA, iA, P, w, last ? nullptr : kB, last ? order : iB, done);
         PGA_LAUNCHED();
         uint64_t *tk = kA;
         kA = kB;
