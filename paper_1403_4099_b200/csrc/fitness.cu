@@ -779,18 +779,17 @@ __global__ void __launch_bounds__(SP_T, PGA_SP_MINB) k_fitness_sparse(SparseArgs
         const uint16_t *lab = CM + p * a.ldn;
         uint32_t kmax = 0;
         // the chromosome's labels stay in registers for the three passes over
-        // them: gene lane + 32 k is half (k & 1) of labr[k >> 1]
+        // them: gene 64 (k >> 1) + 2 lane + (k & 1) is half (k & 1) of
+        // labr[k >> 1] (one aligned 32-bit load per gene pair; ldn is even)
         uint32_t labr[SP_LREG];
 #pragma unroll
-        for (int k = 0; k < 2 * SP_LREG; ++k) {
-            const int i = lane + 32 * k;
-            const uint32_t v = i < N ? (uint32_t)lab[i] : 0u;
-            if (k & 1) labr[k >> 1] |= v << 16;
-            else labr[k >> 1] = v;
+        for (int k = 0; k < SP_LREG; ++k) {
+            const int i = 64 * k + 2 * lane;
+            labr[k] = i < N ? *reinterpret_cast<const uint32_t *>(lab + i) : 0u;
         }
 #pragma unroll
         for (int k = 0; k < 2 * SP_LREG; ++k) {
-            if (lane + 32 * k < N) {
+            if (64 * (k >> 1) + 2 * lane + (k & 1) < N) {
                 const uint32_t s = (labr[k >> 1] >> (16 * (k & 1))) & 0xFFFFu;
                 kmax = max(kmax, s);
                 atomicAdd(cq + (s >> 1), 1u << (16 * (s & 1u)));
@@ -825,7 +824,7 @@ __global__ void __launch_bounds__(SP_T, PGA_SP_MINB) k_fitness_sparse(SparseArgs
             // Zobrist XOR of each large cluster's members
 #pragma unroll
             for (int k = 0; k < 2 * SP_LREG; ++k) {
-                const int i = lane + 32 * k;
+                const int i = 64 * (k >> 1) + 2 * lane + (k & 1);
                 if (i >= N) continue;
                 const uint32_t om = ordm[(labr[k >> 1] >> (16 * (k & 1))) & 0xFFFFu];
                 if (!(om & 0x8000u)) {
@@ -883,7 +882,7 @@ __global__ void __launch_bounds__(SP_T, PGA_SP_MINB) k_fitness_sparse(SparseArgs
         // and its start is off[s - 1] (0 for s = 0)
 #pragma unroll
         for (int k = 0; k < 2 * SP_LREG; ++k) {
-            const int i = lane + 32 * k;
+            const int i = 64 * (k >> 1) + 2 * lane + (k & 1);
             if (i >= N) continue;
             const uint32_t s = (labr[k >> 1] >> (16 * (k & 1))) & 0xFFFFu;
             if (ordm[s] & 0x4000u) {
