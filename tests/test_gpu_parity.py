@@ -181,6 +181,43 @@ def test_fitness_full_size_sampled(pga, orc, cfg, P, sample):
     assert N == planted.shape[0] and Lp > 0
 
 
+def test_fitness_full_size_C5_tiled(pga, orc):
+    """C5 at its full BASELINE size (N=2000, P=262144: 1 GB of u16 labels, one
+    evaluate launch as in the bench).  The population is an 8192-row mix
+    repeated 32 times on the device, each copy under its own label
+    permutation, so every row is distinct as data; sampled rows from all
+    copies (and both ends) are rebuilt on the host and evaluated by the
+    oracle one by one."""
+    import torch
+    C, planted = _corr(orc, workloads.CONFIGS["C5"])
+    N = C.shape[0]
+    base_P, reps = 8192, 32
+    P = base_P * reps
+    base = workloads.population_mix(123, planted, base_P)
+    rng = np.random.default_rng(17)
+    perms = np.stack([rng.permutation(N) for _ in range(reps)]).astype(np.int64)
+    ctx = pga.pga_create(C, _par(pga, P))
+    try:
+        db = torch.from_numpy(base.astype(np.int64)).cuda()
+        dp = torch.from_numpy(perms).cuda()
+        dl = torch.empty((P, N), dtype=torch.int16, device="cuda")
+        for t in range(reps):
+            dl[t * base_P:(t + 1) * base_P] = torch.gather(
+                dp[t].expand(base_P, N), 1, db).to(torch.int16)
+        del db
+        L = torch.zeros(P, dtype=torch.float64, device="cuda")
+        pga.pga_evaluate_device(ctx, dl, L)
+        torch.cuda.synchronize()
+        Lg = L.cpu().numpy()
+    finally:
+        pga.pga_destroy(ctx)
+    idx = np.concatenate([rng.choice(P, 40, replace=False), [0, 1, base_P - 1, base_P, P - 1]])
+    rows = np.stack([perms[i // base_P][base[i % base_P]] for i in idx]).astype(np.int32)
+    Lo, _ = orc.evaluate(C, rows, nthreads=8)
+    _assert_L(Lg[idx], Lo)
+    assert np.all(np.isfinite(Lg))
+
+
 def test_pearson_parity(pga, orc):
     X, _ = workloads.noh_returns(workloads.CONFIGS["C3"])
     Cg = pga.pga_correlation(X)
