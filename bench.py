@@ -213,6 +213,8 @@ def main():
     ap.add_argument("--impl", default="pga", choices=["pga", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--island-load", type=int, default=0,
+                    help="diagnostic only: run ONE island of the G-GPU split (P/G chromosomes) on one GPU")
     ap.add_argument("--mode", default="islands", choices=["islands", "replicated"],
                     help="multi-GPU model: islands (population sharded, elite migration; default) or "
                          "replicated master-slave (one population, fitness sharded, L all-gathered; "
@@ -251,7 +253,7 @@ def main():
     X, planted = workloads.noh_returns(workloads.CONFIGS[CONFIG])
     N = X.shape[1]
     C = pga.pga_correlation(X, device=local)        # Eq. 7 on the device
-    P_local = P_TOTAL if replicated else P_TOTAL // world
+    P_local = P_TOTAL if replicated else P_TOTAL // max(world, args.island_load)
     pm = 0.1 if N <= 40 else 2.0 / N            # Table 3 for N <= 40, else 2/N (Q13)
     params = pga.pga_params_default(
         pop_size=P_local, elite=10, p_mutation=pm, tol=-1.0, max_gens=W + K + 200,
@@ -437,6 +439,7 @@ def main():
             "config": {"workload": "%s: N=%d, P=%d total (%d per GPU), 1 step = 1 generation"
                                    % (CONFIG, N, P_TOTAL, P_local), "N": N, "population": P_TOTAL,
                        "population_per_gpu": P_local,
+                       **({"diagnostic_island_load_of_gpus": args.island_load} if args.island_load else {}),
                        "parallelism": ("replicated master-slave x%d (fitness shard %d per GPU)"
                                        % (world, P_eval)) if replicated else "islands x%d" % world,
                        "migration": "none: L and top all-gathered every generation (NCCL)"

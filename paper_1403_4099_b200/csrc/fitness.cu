@@ -522,14 +522,17 @@ __global__ void k_resync_gm(const uint16_t *__restrict__ CM0, const uint16_t *__
 // is order-free), so the cache changes cost, never results, short of a
 // 128-bit key collision.
 // ---------------------------------------------------------------------------
-constexpr int SP_W = 8, SP_T = SP_W * 32;
+#ifndef PGA_SP_W
+#define PGA_SP_W 16
+#endif
+constexpr int SP_W = PGA_SP_W, SP_T = SP_W * 32;   // warps per CTA (a CTA owns one 32-chromosome block)
 constexpr int SPARSE_MAXN = 640;   // shared-memory footprint (sparse_smem) must fit one CTA
 constexpr int SP_LREG = SPARSE_MAXN / 64;   // label registers per lane (two 16-bit labels each)
 #ifndef PGA_CC_NMIN
 #define PGA_CC_NMIN 5
 #endif
 #ifndef PGA_SP_MINB
-#define PGA_SP_MINB 4
+#define PGA_SP_MINB 2
 #endif
 constexpr int CC_NMIN = PGA_CC_NMIN;   // clusters this large go through the cache (5: best of 3..8 at C4)
 static_assert(CC_NMIN >= 2, "large clusters must have pairs");
