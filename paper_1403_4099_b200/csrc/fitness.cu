@@ -805,6 +805,11 @@ __global__ void __launch_bounds__(SP_T, PGA_SP_MINB) k_fitness_sparse(SparseArgs
         // ordinals: ordm[k] (in place over the 16-bit count) = ordinal of a
         // large cluster, else 0x8000 | n; bit 14 is set below for walked labels
         int ecnt = 0;
+        // second copy of the Zobrist accumulators in perm2 (free until the
+        // walk): odd lanes XOR into it, halving same-address collisions of the
+        // shared atomics; the copies are XORed at the lookup (order-free)
+        const bool dup = use_cache && (size_t)E * 16 <= (size_t)N * 4;
+        uint32_t *cent2 = perm2;
         for (int k0 = 0; k0 < K; k0 += 32) {
             const int k = k0 + lane;
             const int n = k < K ? (int)ordm[k] : 0;
@@ -814,6 +819,7 @@ __global__ void __launch_bounds__(SP_T, PGA_SP_MINB) k_fitness_sparse(SparseArgs
                 const int ord = ecnt + __popc(bal & lanemask_lt());
                 ordm[k] = (uint16_t)ord;
                 cent[ord] = make_ulonglong2(0ull, 0ull);
+                if (dup) cent2[4 * ord] = cent2[4 * ord + 1] = cent2[4 * ord + 2] = cent2[4 * ord + 3] = 0u;   // 4-byte aligned only
                 cn[ord] = (uint16_t)n;
                 clab[ord] = (uint16_t)k;
             } else if (k < K) {
@@ -831,7 +837,7 @@ __global__ void __launch_bounds__(SP_T, PGA_SP_MINB) k_fitness_sparse(SparseArgs
                 if (i >= N) continue;
                 const uint32_t om = ordm[(labr[k >> 1] >> (16 * (k & 1))) & 0xFFFFu];
                 if (!(om & 0x8000u)) {
-                    uint32_t *h = reinterpret_cast<uint32_t *>(cent + om);
+                    uint32_t *h = (dup && (lane & 1)) ? cent2 + 4 * om : reinterpret_cast<uint32_t *>(cent + om);
                     const uint4 kk = __ldg(keys4 + i);
                     atomicXor(h, kk.x);
                     atomicXor(h + 1, kk.y);
@@ -843,7 +849,12 @@ __global__ void __launch_bounds__(SP_T, PGA_SP_MINB) k_fitness_sparse(SparseArgs
             // one lookup per large cluster, lane-parallel; a hit is its Eq. 8
             // term and the cluster is not walked
             for (int o = lane; o < ecnt; o += 32) {
-                const ulonglong2 h = cent[o];
+                ulonglong2 h = cent[o];
+                if (dup) {
+                    const uint32_t *c2 = cent2 + 4 * o;
+                    h.x ^= (unsigned long long)c2[0] | ((unsigned long long)c2[1] << 32);
+                    h.y ^= (unsigned long long)c2[2] | ((unsigned long long)c2[3] << 32);
+                }
                 const uint64_t k1 = h.x | 1ull, k2 = h.y | 1ull;
                 const uint32_t n = cn[o];
                 long long v = 0;

@@ -867,6 +867,9 @@ __global__ void __launch_bounds__(BW * 32, 3) k_breed(BreedArgs a) {
 // children through the shared tile.
 // ---------------------------------------------------------------------------
 constexpr int BREED2_MAXN = 1024;
+#ifndef PGA_B2_MINB
+#define PGA_B2_MINB 2
+#endif
 
 __host__ __device__ __forceinline__ int breed2_ngrp(int N) { return (N + 63) / 64; }
 
@@ -881,7 +884,7 @@ static size_t breed2_smem(int N) {
 }
 
 template <bool HOOK, int NB>
-__global__ void __launch_bounds__(BW * 32, NB <= 2 ? 3 : 2) k_breed2(BreedArgs a) {
+__global__ void __launch_bounds__(BW * 32, NB <= 2 ? 3 : PGA_B2_MINB) k_breed2(BreedArgs a) {
     if (a.done && *a.done) return;
     extern __shared__ __align__(16) unsigned char sm2[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
