@@ -299,6 +299,72 @@ def test_run_stall_termination(orc):
     assert r["reason"] == 1 and r["gens_run"] == 51 and r["best_L"] == 0.0
 
 
+def _q28_gens(M, S):
+    """Hand-worked Q28: with G > 1 islands the stall counter
+    is updated only at migration generations g = kM - 1 (k = 1, 2, ...), on
+    the global best, adding M per epoch without improvement; the first
+    epoch (g + 1 = M) only records prev_best.  If the best never improves,
+    the k-th increment happens at g = (k + 1) M - 1, the counter reaches S
+    after ceil(S / M) increments, so the run stops after
+    (ceil(S / M) + 1) M generations."""
+    return (-(-S // M) + 1) * M
+
+
+@pytest.mark.parametrize("G,M,S", [(2, 10, 50), (2, 7, 50), (3, 5, 12), (2, 4, 4)])
+def test_island_stall_rule_never_improving(orc, G, M, S):
+    """Q28 pinned on the identity C: every partition has L = 0, so
+    the global best never improves and stalls from the first update."""
+    pr = orc.default_params(pop=16, max_gens=1000, tol=1e-5, stall_gens=S, seed=5,
+                            n_islands=G, migrate_every=M, migrants=3)
+    r = orc.run(np.eye(6), pr)
+    assert r["reason"] == 1
+    assert r["gens_run"] == _q28_gens(M, S)
+    assert r["best_L"] == 0.0
+
+
+def test_island_stall_rule_tolerance_semantics(orc):
+    """Q28 + Q16 on a structured C.  (a) tol = 0: with elitism and
+    migration the global best never drops, so 'best - prev < 0'
+    never holds and the run reaches max_gens.  (b) a tolerance larger than
+    any possible gain (|L| <= N ln N / 2 ... far below 1e9) makes every
+    epoch 'unimproved': the same stop generation as the identity case.
+    (c) single population (G = 1): the per-generation rule stops at
+    S + 1 generations, the case the hand-worked Q28 count reduces to with
+    M = 1 minus the skipped first epoch."""
+    X, _ = workloads.noh_returns(workloads.CONFIGS["C1"])
+    C = orc.pearson(X)
+    a = orc.run(C, orc.default_params(pop=32, max_gens=90, tol=0.0, stall_gens=20, seed=2,
+                                      n_islands=2, migrate_every=5, migrants=3))
+    assert a["reason"] == 0 and a["gens_run"] == 90
+    b = orc.run(C, orc.default_params(pop=32, max_gens=500, tol=1e9, stall_gens=20, seed=2,
+                                      n_islands=2, migrate_every=5, migrants=3))
+    assert b["reason"] == 1 and b["gens_run"] == _q28_gens(5, 20) == 25
+    c = orc.run(C, orc.default_params(pop=32, max_gens=500, tol=1e9, stall_gens=20, seed=2))
+    assert c["reason"] == 1 and c["gens_run"] == 21
+
+
+def test_island_stall_rule_counts_only_unimproved_epochs(orc):
+    """Q28 with a real improvement: on C1 the global best rises during the
+    first epochs, so the run must outlast the never-improving count, and
+    when it stops the last S/M epochs (the migration generations' history
+    entries) show gains below tol while the epoch before shows a gain of
+    at least tol."""
+    X, _ = workloads.noh_returns(workloads.CONFIGS["C1"])
+    C = orc.pearson(X)
+    M, S, tol = 5, 15, 1e-5
+    r = orc.run(C, orc.default_params(pop=32, max_gens=2000, tol=tol, stall_gens=S, seed=4,
+                                      n_islands=2, migrate_every=M, migrants=3))
+    assert r["reason"] == 1
+    g = r["gens_run"]
+    assert g % M == 0 and g > _q28_gens(M, S)
+    h = r["history"]
+    mig = [k for k in range(g) if (k + 1) % M == 0]       # migration generations
+    k = -(-S // M)                                         # unimproved epochs needed
+    tail = [h[mig[-j]] - h[mig[-j - 1]] for j in range(1, k + 1)]
+    assert all(d < tol for d in tail)
+    assert h[mig[-k - 1]] - h[mig[-k - 2]] >= tol
+
+
 def test_islands_migration_keeps_global_best(orc):
     X, planted = workloads.noh_returns(workloads.CONFIGS["C1"])
     C = orc.pearson(X)
@@ -375,3 +441,24 @@ def test_run_f1_windows_local_optimum(orc):
                     cand.append(m)
         Lc, _ = orc.evaluate(C, np.asarray(cand, np.int32))
         assert Lc.max() <= L0, b
+
+
+def test_c2_set_oracle_ga_reaches_brute_force(orc):
+    """C2's exhaustive set: 50 matrices with n
+    in {6, 8, 10}, seeds 2000..2049.  The enumeration visits Bell(n)
+    partitions (203, 4140, 115975); the oracle GA (P = 1024, Table 3
+    termination) never exceeds the exhaustive maximum and reaches it on at
+    least 90% of the matrices (50/50 when this test was written)."""
+    bell = {6: 203, 8: 4140, 10: 115975}
+    hits = 0
+    for k in range(workloads.C2_SET["count"]):
+        spec = workloads.c2_set_spec(k)
+        assert spec.N in bell
+        X, _ = workloads.noh_returns(spec)
+        C = orc.pearson(X)
+        best, Lb, count = orc.brute_force(C)
+        assert count == bell[spec.N]
+        r = orc.run(C, orc.default_params(pop=1024, seed=workloads.C2_SET["seed0"] + k))
+        assert r["best_L"] <= Lb + 1e-9 * max(1.0, Lb)
+        hits += abs(r["best_L"] - Lb) <= 1e-9 * max(1.0, Lb)
+    assert hits >= 45

@@ -82,6 +82,30 @@ def noh_returns(spec: PlantedSpec):
     return X, planted
 
 
+# C2's exhaustive-check set (SPEC S:536 acceptance 2):
+# 50 matrices, n in {6, 8, 10}, GA seeds / matrix seeds 2000..2049.  Every
+# fifth matrix is pure noise (independent assets); the others plant 1..3
+# clusters of 2..n/2 stocks with loadings g ~ U(0.55, 0.85), the remaining
+# assets independent.  T = 250 as in C1/C2.
+C2_SET = dict(count=50, seed0=2000, sizes=(6, 8, 10), T=250)
+
+
+def c2_set_spec(k: int) -> PlantedSpec:
+    seed = C2_SET["seed0"] + k
+    n = C2_SET["sizes"][k % 3]
+    if k % 5 == 4:
+        return PlantedSpec((), (), C2_SET["T"], seed, singletons=n)
+    rng = np.random.Generator(np.random.PCG64(seed))
+    sizes = []
+    for _ in range(int(rng.integers(1, 4))):
+        m = int(rng.integers(2, n // 2 + 1))
+        if sum(sizes) + m > n:
+            break
+        sizes.append(m)
+    g = tuple(float(x) for x in rng.uniform(0.55, 0.85, len(sizes)))
+    return PlantedSpec(tuple(sizes), g, C2_SET["T"], seed, singletons=n - sum(sizes))
+
+
 def random_labels(rng, P, N, K=None):
     """Labels uniform over [0, K) (K = N: 'looks like initialisation')."""
     K = N if K is None else K
