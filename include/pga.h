@@ -57,7 +57,11 @@ typedef struct {
     int32_t  max_gens;      /* default 400 */
     int32_t  selection;     /* PGA_SEL_SUS (default) or PGA_SEL_TOURNAMENT */
     int32_t  tournament_k;  /* 1..4, default 2 */
-    int32_t  scaling;       /* PGA_SCALE_RANK (default) or PGA_SCALE_NONE */
+    int32_t  scaling;       /* PGA_SCALE_RANK (default) or PGA_SCALE_NONE.  RANK
+                             * (w = 1/sqrt(rank)) is this library's reading Q9 of
+                             * Alg. 1's separate "Apply scaling" step; it
+                             * deliberately differs from SPEC S:151's identity
+                             * scaling, which PGA_SCALE_NONE selects. */
     int32_t  device;        /* CUDA device ordinal, default 0 */
     int32_t  island;        /* this island's id, 0 <= island < n_islands */
     int32_t  n_islands;     /* islands in the run (1 = single population) */
@@ -75,6 +79,12 @@ int pga_params_default(pga_params *out);
  * finite (Eq. 7; reading Q4); otherwise PGA_EINVAL.  2 <= N <= 16384.
  * The ctx owns its copy of C; the caller's buffer may be freed on return. */
 int pga_create(const double *C, int32_t N, const pga_params *p, pga_ctx **out);
+
+/* The ctx's sizes (host only, no device call): N, pop_size (this island's
+ * population) and the evaluation capacity (pop_size rounded up to 32, the
+ * largest P pga_evaluate_device accepts).  Any output pointer may be NULL.
+ * Bindings use it to check caller arrays before passing them. */
+int pga_get_dims(pga_ctx *ctx, int32_t *N, int64_t *pop_size, int64_t *capacity);
 
 /* Free everything owned by ctx.  NULL-safe. */
 void pga_destroy(pga_ctx *ctx);
@@ -94,8 +104,13 @@ const char *pga_last_error(void);
 int pga_evaluate(pga_ctx *ctx, const int32_t *labels, int64_t P, double *out_L);
 
 /* Device fast path, stream-ordered on `stream` (cudaStream_t, NULL = the
- * ctx's stream):  labels_dev: device uint16 [P][N] row-major, 0-based values
- * < N;  L_dev: device fp64 [P];  top_dev: device uint16 [P] or
+ * ctx's stream).  The call uses the ctx's evaluation scratch (staging
+ * layouts, fold scratch, block flags and counters), so when `stream` is not
+ * the ctx's stream it is joined to it with events in both directions: the
+ * launch waits for all work already queued on the ctx's stream, and later
+ * ctx work waits for the launch.  Concurrent calls on one ctx are therefore
+ * serialised on the device, never interleaved (no wrong-result race).
+ * labels_dev: device uint16 [P][N] row-major, 0-based values < N;  L_dev: device fp64 [P];  top_dev: device uint16 [P] or
  * NULL — label of the cluster with the largest Eq. 8 summand, 0xFFFF if none.
  * 1 <= P <= the ctx's capacity (pop_size rounded up to 32).  A label >= N is
  * evaluated as label 0 (that chromosome's L is then meaningless; the others
@@ -248,7 +263,7 @@ int pga_set_sparse_threshold(pga_ctx *ctx, double theta);
  * (Eq. 6) depends only on the member set of cluster s, and a GA generation
  * repeats almost every cluster of the one before (elites are copied,
  * knowledge-based crossover transplants whole clusters, mutation moves a
- * few genes).  Clusters with at least 6 members are keyed by two 64-bit
+ * few genes).  Clusters with at least 5 members are keyed by two 64-bit
  * Zobrist sums of their members plus n_s, and their exact 64-bit
  * fixed-point c_s is kept in a device hash table (64 slots per chromosome,
  * 2^12..2^22 slots of 32 B; cleared by the pass itself when half full).  A
@@ -256,6 +271,13 @@ int pga_set_sparse_threshold(pga_ctx *ctx, double theta);
  * bit-identical with the cache on or off (a wrong hit needs a 128-bit key
  * collision).  on: 0 = off, else on.  Host only. */
 int pga_set_cluster_cache(pga_ctx *ctx, int32_t on);
+
+/* Cluster-cache occupancy (measurement and tests; synchronises): slots
+ * filled since the last clear, table size in slots (0 when the ctx has no
+ * cache, N > 640), and how many times the table was cleared (a launch
+ * clears it when more than half the slots are filled).  Any pointer may be
+ * NULL. */
+int pga_cache_stats(pga_ctx *ctx, int64_t *fill, int64_t *slots, int64_t *clears);
 
 /* ---------------------------------------------------------------------
  * Replicated master-slave across GPUs.  The paper's
@@ -357,10 +379,12 @@ int pga_batch_op_step(int32_t B, int32_t N, const pga_params *params, const int3
  * C_out   fp64 [B][N][N], B = pga_stream_count(T, warm, stride).
  * on_device 0: X, C_out host, synchronous; a non-positive variance at an
  *         emission -> PGA_ENUMERIC (and *status = 1 if status != NULL).
- *         1: X, C_out, status device memory on `device`; work is ordered on
- *         `stream` and the call returns after it completes (its scratch is
- *         freed); *status (caller-zeroed) is set to 1 on a non-positive
- *         variance.
+ *         1: X, C_out, status device memory on `device`; the call is
+ *         ASYNCHRONOUS and stream-ordered: it enqueues the kernels and the
+ *         stream-ordered release of its scratch (cudaFreeAsync) on `stream`
+ *         and returns; C_out and *status (caller-zeroed, set to 1 on a
+ *         non-positive variance) are valid only once `stream` has reached
+ *         that point (synchronise it, or order later work on it).
  * The EWMA recurrences and the uncleaned correlation are computed without
  * FMA contraction in the SPEC's operation order (bit-identical to a plain
  * fp64 evaluation); the cleaning uses a two-sided Jacobi eigensolver.

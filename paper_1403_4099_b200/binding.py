@@ -80,6 +80,8 @@ _SIGS = {
     "pga_op_init": (ct.c_int, [ct.c_uint64, ct.c_int32, ct.c_int64, ct.c_int64, ct.c_int32,
                                ct.c_int32, ct.c_void_p]),
     "pga_launch_count": (ct.c_int64, []),
+    "pga_get_dims": (ct.c_int, [ct.c_void_p, ct.c_void_p, ct.c_void_p, ct.c_void_p]),
+    "pga_cache_stats": (ct.c_int, [ct.c_void_p, ct.c_void_p, ct.c_void_p, ct.c_void_p]),
     "pga_set_sparse_threshold": (ct.c_int, [ct.c_void_p, ct.c_double]),
     "pga_profile_sparse_blocks": (ct.c_int, [ct.c_void_p, ct.c_void_p]),
     "pga_profile_sparse": (ct.c_int, [ct.c_void_p, ct.c_void_p, ct.c_void_p]),
@@ -140,6 +142,26 @@ def _c(a, dt):
     return np.ascontiguousarray(a, dtype=dt)
 
 
+def pga_get_dims(ctx):
+    """(N, pop_size, capacity) of a ctx."""
+    n, p, c = ct.c_int32(), ct.c_int64(), ct.c_int64()
+    _check(lib().pga_get_dims(ctx, ct.byref(n), ct.byref(p), ct.byref(c)))
+    return n.value, p.value, c.value
+
+
+def _need(cond, msg):
+    if not cond:
+        raise ValueError(msg)
+
+
+def _dev_tensor(t, dtypes, numel, what):
+    """Check a torch CUDA tensor argument before its pointer crosses the ABI."""
+    _need(hasattr(t, "data_ptr") and getattr(t, "is_cuda", False), "%s must be a CUDA tensor" % what)
+    _need(str(t.dtype).replace("torch.", "") in dtypes, "%s must have dtype %s (got %s)"
+          % (what, "/".join(dtypes), t.dtype))
+    _need(t.numel() >= numel, "%s holds %d elements, needs %d" % (what, t.numel(), numel))
+
+
 def pga_params_default(**kw) -> pga_params:
     p = pga_params()
     _check(lib().pga_params_default(ct.byref(p)))
@@ -165,6 +187,8 @@ def pga_evaluate(ctx, labels_1based) -> np.ndarray:
     lab = _c(labels_1based, np.int32)
     if lab.ndim == 1:
         lab = lab[None, :]
+    N = pga_get_dims(ctx)[0]
+    _need(lab.ndim == 2 and lab.shape[1] == N, "labels must be [P][%d]" % N)
     L = np.zeros(lab.shape[0], np.float64)
     _check(lib().pga_evaluate(ctx, _p(lab), lab.shape[0], _p(L)))
     return L
@@ -172,7 +196,15 @@ def pga_evaluate(ctx, labels_1based) -> np.ndarray:
 
 def pga_evaluate_device(ctx, labels_dev, L_dev, top_dev=None, stream=None):
     """labels_dev: torch uint16-compatible (int16) CUDA tensor [P][N] 0-based."""
+    N, _, cap = pga_get_dims(ctx)
+    _need(labels_dev.dim() == 2 and labels_dev.shape[1] == N, "labels_dev must be [P][%d]" % N)
     P = labels_dev.shape[0]
+    _need(1 <= P <= cap, "P must lie in [1, %d]" % cap)
+    _dev_tensor(labels_dev, ("int16", "uint16"), P * N, "labels_dev")
+    _need(labels_dev.is_contiguous(), "labels_dev must be contiguous")
+    _dev_tensor(L_dev, ("float64",), P, "L_dev")
+    if top_dev is not None:
+        _dev_tensor(top_dev, ("int16", "uint16"), P, "top_dev")
     _check(lib().pga_evaluate_device(ctx, _p(labels_dev), P, _p(L_dev), _p(top_dev),
                                      None if stream is None else ct.c_void_p(stream)))
 
@@ -197,7 +229,9 @@ def pga_generation(ctx) -> bool:
     return bool(d.value)
 
 
-def pga_run(ctx, gens: int, seed: int, N: int):
+def pga_run(ctx, gens: int, seed: int, N: int = None):
+    N = pga_get_dims(ctx)[0] if N is None else N
+    _need(N == pga_get_dims(ctx)[0], "N differs from the ctx's")
     best = np.zeros(N, np.int32)
     L = ct.c_double(0)
     g = ct.c_int32(0)
@@ -206,7 +240,9 @@ def pga_run(ctx, gens: int, seed: int, N: int):
     return dict(best_labels=best, best_L=L.value, gens_run=g.value, reason=r.value)
 
 
-def pga_get_state(ctx, N: int):
+def pga_get_state(ctx, N: int = None):
+    N = pga_get_dims(ctx)[0] if N is None else N
+    _need(N == pga_get_dims(ctx)[0], "N differs from the ctx's")
     gen, done, reason = ct.c_int32(), ct.c_int32(), ct.c_int32()
     best, mean = ct.c_double(), ct.c_double()
     lab = np.zeros(N, np.int32)
@@ -222,7 +258,10 @@ def pga_get_history(ctx, n: int) -> np.ndarray:
     return h
 
 
-def pga_get_population(ctx, P: int, N: int, with_top: bool = False):
+def pga_get_population(ctx, P: int = None, N: int = None, with_top: bool = False):
+    Nc, Pc, _ = pga_get_dims(ctx)
+    P, N = (Pc if P is None else P), (Nc if N is None else N)
+    _need((P, N) == (Pc, Nc), "population is [%d][%d], not [%d][%d]" % (Pc, Nc, P, N))
     lab = np.zeros((P, N), np.int32)
     L = np.zeros(P, np.float64)
     top = np.zeros(P, np.int32)
@@ -254,6 +293,8 @@ def pga_profile_read(ctx):
 
 def pga_set_population(ctx, labels_1based, generation: int = 0):
     lab = _c(labels_1based, np.int32)
+    N, P, _ = pga_get_dims(ctx)
+    _need(lab.shape == (P, N), "labels must be [%d][%d]" % (P, N))
     _check(lib().pga_set_population(ctx, _p(lab), generation))
 
 
@@ -355,6 +396,13 @@ def pga_set_cluster_cache(ctx, on: bool):
     _check(lib().pga_set_cluster_cache(ctx, 1 if on else 0))
 
 
+def pga_cache_stats(ctx):
+    """dict(fill, slots, clears) of the cluster cache (slots 0: no cache)."""
+    f, s, c = ct.c_int64(), ct.c_int64(), ct.c_int64()
+    _check(lib().pga_cache_stats(ctx, ct.byref(f), ct.byref(s), ct.byref(c)))
+    return dict(fill=f.value, slots=s.value, clears=c.value)
+
+
 def pga_profile_cache(ctx):
     """(cluster-cache hits, pair updates they replaced) since profiling was enabled."""
     h, v = ct.c_int64(), ct.c_int64()
@@ -365,10 +413,15 @@ def pga_profile_cache(ctx):
 def pga_rep_evaluate(ctx, begin: int, end: int, L_dev, top_dev):
     """Fitness of chromosomes [begin, end) into device buffers (torch tensors:
     float64 [end-begin], int16/uint16 [end-begin])."""
+    _dev_tensor(L_dev, ("float64",), max(0, end - begin), "L_dev")
+    _dev_tensor(top_dev, ("int16", "uint16"), max(0, end - begin), "top_dev")
     _check(lib().pga_rep_evaluate(ctx, begin, end, _p(L_dev), _p(top_dev)))
 
 
 def pga_rep_commit(ctx, L_dev, top_dev):
+    P = pga_get_dims(ctx)[1]
+    _dev_tensor(L_dev, ("float64",), P, "L_dev")
+    _dev_tensor(top_dev, ("int16", "uint16"), P, "top_dev")
     _check(lib().pga_rep_commit(ctx, _p(L_dev), _p(top_dev)))
 
 

@@ -150,6 +150,7 @@ void free_ctx(pga_ctx *c) {
         if (p) cudaFree(p);
     if (c->h_st) cudaFreeHost(c->h_st);
     for (cudaEvent_t e : c->prof_ev) cudaEventDestroy(e);
+    if (c->join_ev) cudaEventDestroy(c->join_ev);
     if (c->stream) cudaStreamDestroy(c->stream);
 }
 
@@ -411,6 +412,8 @@ int pga_create(const double *C, int32_t N, const pga_params *p, pga_ctx **out) {
     };
     cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) return bail(cuda_fail(e, "cudaStreamCreate"));
+    e = cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming);
+    if (e != cudaSuccess) return bail(cuda_fail(e, "cudaEventCreate"));
     const size_t cm = (size_t)c->Pcap * c->ldn, gm = (size_t)N * c->Pcap;
     int rc = 0;
     rc = rc ? rc : dalloc(&c->C, (size_t)N * c->ldc);
@@ -524,6 +527,14 @@ void pga_destroy(pga_ctx *c) {
     delete c;
 }
 
+int pga_get_dims(pga_ctx *c, int32_t *N, int64_t *pop_size, int64_t *capacity) {
+    if (!c) return fail(PGA_EINVAL, "ctx is NULL");
+    if (N) *N = c->N;
+    if (pop_size) *pop_size = c->P;
+    if (capacity) *capacity = c->Pcap;
+    return PGA_OK;
+}
+
 int pga_get_stream(pga_ctx *c, void **stream) {
     if (!c || !stream) return fail(PGA_EINVAL, "NULL argument");
     *stream = (void *)c->stream;
@@ -563,9 +574,21 @@ int pga_evaluate_device(pga_ctx *c, const uint16_t *labels_dev, int64_t P, doubl
         PGA_CUDA(cudaSetDevice(c->device));
         TRY(ensure_eval_bufs(c));
     }
+    // the evaluation scratch (evCM/evGM, V, counters, sflag, cache state) is
+    // per ctx: join a foreign stream to the ctx's stream in both directions
+    const bool foreign = s != c->stream;
+    if (foreign) {
+        PGA_CUDA(cudaEventRecord(c->join_ev, c->stream));
+        PGA_CUDA(cudaStreamWaitEvent(s, c->join_ev, 0));
+    }
     TRY(launch_pack(c, labels_dev, nullptr, P, c->N, c->evCM, c->evGM, s));
     FitBufs b{c->evCM, c->evCM, c->evGM, c->evGM, &c->tmLabEv, &c->tmLabEv, nullptr, nullptr};
-    return launch_fitness(c, b, P, L_dev, top_dev, s);
+    TRY(launch_fitness(c, b, P, L_dev, top_dev, s));
+    if (foreign) {
+        PGA_CUDA(cudaEventRecord(c->join_ev, s));
+        PGA_CUDA(cudaStreamWaitEvent(c->stream, c->join_ev, 0));
+    }
+    return PGA_OK;
 }
 
 int pga_init(pga_ctx *c, uint64_t seed) {
@@ -770,6 +793,24 @@ int pga_profile_cache(pga_ctx *c, int64_t *hits, int64_t *saved) {
     PGA_CUDA(cudaStreamSynchronize(c->stream));
     *hits = (int64_t)v[2];
     *saved = (int64_t)v[3];
+    return PGA_OK;
+}
+
+int pga_cache_stats(pga_ctx *c, int64_t *fill, int64_t *slots, int64_t *clears) {
+    if (!c) return fail(PGA_EINVAL, "ctx is NULL");
+    if (!c->cc) {
+        if (fill) *fill = 0;
+        if (slots) *slots = 0;
+        if (clears) *clears = 0;
+        return PGA_OK;
+    }
+    PGA_CUDA(cudaSetDevice(c->device));
+    uint32_t v[4] = {0, 0, 0, 0};
+    PGA_CUDA(cudaMemcpyAsync(v, c->cc_state, sizeof(v), cudaMemcpyDeviceToHost, c->stream));
+    PGA_CUDA(cudaStreamSynchronize(c->stream));
+    if (fill) *fill = (int64_t)v[0];
+    if (slots) *slots = (int64_t)c->cc_mask + 1;
+    if (clears) *clears = (int64_t)v[3];
     return PGA_OK;
 }
 

@@ -625,7 +625,7 @@ struct SparseArgs {
     const double *lgn, *lgnn;
     pga::CCSlot *cc;              // cluster cache (null = off)
     uint32_t cc_mask;             // slots - 1
-    uint32_t *cc_state;           // [0] fill, [1] clear request, [2] CTA count
+    uint32_t *cc_state;           // [0] fill, [1] clear request, [2] CTA count, [3] clears done
     const uint64_t *cc_keys;      // [N][2] Zobrist keys
 };
 
@@ -736,6 +736,7 @@ __global__ void __launch_bounds__(SP_T, PGA_SP_MINB) k_fitness_sparse(SparseArgs
             if (cc_clear) {
                 a.cc_state[0] = 0u;
                 a.cc_state[1] = 0u;
+                a.cc_state[3] += 1u;   // clears so far (pga_cache_stats)
             } else if (atomicAdd(a.cc_state, 0u) > (a.cc_mask >> 1)) {
                 a.cc_state[1] = 1u;
             }

@@ -1094,7 +1094,7 @@ __global__ void k_export(const double *__restrict__ L, const uint16_t *__restric
                          const uint16_t *CM1, const pga::DevState *st, int ldn, int N, int Em,
                          int64_t rec_bytes, unsigned char *out) {
     const int r = blockIdx.x;
-    if (r >= Em) return;
+    if (r >= Em || st->done) return;   // stopped: the population is final (every island agrees, Q28)
     const uint16_t *CM = (st->gen & 1) ? CM1 : CM0;
     const int p = order[r];
     unsigned char *rec = out + (int64_t)r * rec_bytes;
@@ -1113,6 +1113,7 @@ __global__ void k_import(const unsigned char *__restrict__ in, int G, int Em, in
                          uint16_t *CM0, uint16_t *CM1, uint16_t *GM0, uint16_t *GM1,
                          const pga::DevState *st, int ldn, int N, int64_t Pcap) {
     __shared__ int chosen[256];
+    if (st->done) return;   // stopped: the population is final (every island agrees, Q28)
     const int total = G * Em;
     if (threadIdx.x == 0) {
         // selection by repeated scans (total <= 8 * 256); strict '>' keeps

@@ -98,6 +98,7 @@ struct GExec {
 struct pga_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaEvent_t join_ev = nullptr;   // joins a caller's stream to `stream` (pga_evaluate_device)
     pga_params p{};
     int32_t N = 0;
     int32_t ldn = 0;       // padded gene stride of chromosome-major labels / V
