@@ -37,6 +37,9 @@ CFG_POP = {"C1": 128, "C2": 1024, "C3": 4096, "C4": 65536, "C5": 262144}
 SEED = 2024
 SM_COUNT = 148
 FP64_LANES_PER_SM = 64           # DFMA lanes / clk / SM (B200: 37 TF fp64 = 148*64*2*1.965G)
+# SURVEY §8(d) headline ceiling for executed pair-updates: ISETP + SEL per
+# pair on the 64-op/clk/SM integer/logic pipe = 32 pairs per SM-clock.
+ALU_PAIRS_PER_CLK = 32
 # Measured ceiling of the exact fp64 masked-accumulate inner loop on this pool
 # (tools/mb_pairloop.cu, shared-memory resident, no pipeline/fold): 26.8
 # executed pair-updates per SM-clock, register-file-read bound.
@@ -153,6 +156,23 @@ def oracle_rate(C, planted, target_s=12.0, max_P=65536):
     return N * N * P * g / dt, P, g, dt, N * N * sub.shape[0] / d1
 
 
+def parity_probe(C, pop, L_gpu, cores, rows=4096):
+    """The oracle (cpu_baseline leg) re-evaluates a sample of the GPU's last
+    evaluated population: max |dL| / max(1, |L|) against north_star's 1e-9."""
+    import oracle as orc
+    orc.build()
+    P = pop.shape[0]
+    idx = np.unique(np.concatenate([np.linspace(0, P - 1, min(rows, P)).astype(np.int64), [0, P - 1]]))
+    t0 = time.perf_counter()
+    Lo, _ = orc.evaluate(C, pop[idx], nthreads=cores)
+    dt = time.perf_counter() - t0
+    err = np.abs(L_gpu[idx] - Lo) / np.maximum(1.0, np.abs(Lo))
+    return {"rows": int(idx.size), "max_rel_dL": float(err.max()), "tolerance": 1e-9,
+            "pass": bool(err.max() <= 1e-9), "oracle_seconds": dt,
+            "what": "oracle orc_evaluate of evenly spaced rows of the GPU's last evaluated population "
+                    "(labels and L read back together after the timed region)"}
+
+
 def run_reference(args):
     rank = env_int("RANK", 0)
     if rank != 0:
@@ -190,7 +210,7 @@ def run_reference(args):
         "data": "synthetic (Noh-model returns, seed 50004)",
         "config": {"workload": "C4 (N=500; oracle on a bounded sample of P=%d chromosomes per "
                                "generation)" % P, "N": N, "population": P},
-        "cpu_baseline": {"value": value, "unit": "pair-updates/s", "cores": cores,
+        "cpu_baseline": {"value": value, "unit": "pair-updates/s", "cores": cores, "cpu_model": cpu_model(),
                          "kind": "oracle",
                          "sample": "%d-chromosome C4 population, full generation (evaluate on %d "
                                    "threads + single-threaded operators)" % (P, cores)},
@@ -204,6 +224,34 @@ def run_reference(args):
 # ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
+def spawn_ranks(n):
+    """`bench.py --gpus N` without a launcher: re-run this command under
+    torch.distributed.run with N ranks on this node (rank 0 prints the line)."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(n),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def cpu_model():
+    try:
+        for line in subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
 def main():
     global CONFIG, P_TOTAL
     ap = argparse.ArgumentParser()
@@ -220,8 +268,8 @@ def main():
                          "replicated master-slave (one population, fitness sharded, L all-gathered; "
                          "SURVEY §8(f) f3)")
     ap.add_argument("--sparse-theta", type=float, default=None,
-                    help="label-sparse threshold (pga_set_sparse_threshold; default: the library's 0.02; "
-                         "0 = dense sweep only, used to profile the dense kernel)")
+                    help="label-sparse threshold (pga_set_sparse_threshold; default: the library's automatic "
+                         "choice, 0.25 with the cluster cache at N >= 160; 0 = dense sweep only)")
     ap.add_argument("--stream", action="store_true",
                     help="F1 only: each step also computes the 1760 windows on the device from one "
                          "return stream (EWMA lambda=0.98 + RMT cleaning, SURVEY §8(f) f4)")
@@ -231,6 +279,13 @@ def main():
     args = ap.parse_args()
     CONFIG = args.config
     args.warmup = max(3, args.warmup)
+    ws = os.environ.get("WORLD_SIZE")
+    if ws is None and args.gpus > 1:
+        return spawn_ranks(args.gpus)
+    if ws is not None and int(ws) != args.gpus:
+        print("bench.py: WORLD_SIZE=%s but --gpus %d; launch one rank per GPU" % (ws, args.gpus),
+              file=sys.stderr)
+        return 2
     if CONFIG == "F1":
         return reference_f1(args) if args.impl == "reference" else bench_f1(args)
     P_TOTAL = CFG_POP[CONFIG]
@@ -314,6 +369,12 @@ def main():
         runner.step()
     phases, _ = pga.pga_profile_phases(eng.ctx)
     pga.pga_profile_enable(eng.ctx, False)
+    # parity probe for the report (checked by the oracle in the cpu_baseline
+    # leg): one more evaluation, whose labels and L are read back together
+    probe = None
+    if not replicated and world == 1:
+        runner.e.gen_evaluate()
+        probe = pga.pga_get_population(eng.ctx)
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -329,8 +390,8 @@ def main():
     executed_local = N * (N - 1) / 2.0 * P_eval
     value = nominal / (ms_step / 1000.0)
 
-    # roofline of the dominant kernel (the dense k_fitness), from live CUDA
-    # events; blocks the label-sparse pre-pass evaluated are skipped by it
+    # rooflines of the two fitness kernels from live CUDA events on the
+    # library's stream (pga_profile_*), averaged over the timed generations
     ngen = max(1, prof["count"])
     sweep_ms = prof["sweep_ms"] / ngen
     sparse_ms = prof["fold_ms"] / ngen
@@ -338,19 +399,85 @@ def main():
     nblk = (P_eval + 31) // 32
     dense_blocks = nblk * prof["count"] - sparse_blocks
     dense_sweep_ms = dprof["sweep_ms"] / max(1, dprof["count"])       # dense roofline pass
-    achieved = executed_local / (dense_sweep_ms / 1000.0)
     peaks = measured_peaks()
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
-    peak = FP64_LANES_PER_SM * SM_COUNT * sm_max * 1e6
-    traffic = sp_inst = sp_dram = None
-    if CONFIG == "C4" and world == 1:      # profiles/ hold one ncu capture of the C4 launch
+    hbm_gbs = float(peaks.get("hbm_gbs", 6542.7))
+    alu_peak = ALU_PAIRS_PER_CLK * SM_COUNT * sm_max * 1e6          # SURVEY §8(d) headline ceiling
+    fp64_peak = FP64_LANES_PER_SM * SM_COUNT * sm_max * 1e6
+    issue_peak = 4.0 * SM_COUNT * sm_max * 1e6
+    alg_bytes = P_eval * (N * 2 + 8 + 2)       # §8(d): N u16 labels read, L (f64) + top (u16) written
+    tj = {}
+    if world == 1:
         try:
             tj = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
-            traffic = tj.get("k_sweep", {}).get("dram_bytes_per_launch")
-            sp_inst = tj.get("k_fitness_sparse", {}).get("inst_per_launch")
-            sp_dram = tj.get("k_fitness_sparse", {}).get("dram_bytes_per_launch")
         except Exception:
-            pass
+            tj = {}
+    cfg_key = "%s_w%d" % (CONFIG, 1)
+    sp_ncu = tj.get("k_fitness_sparse", {}).get(cfg_key, {})
+    dn_ncu = tj.get("k_fitness", {}).get(cfg_key, {})
+
+    achieved = executed_local / (dense_sweep_ms / 1000.0)
+    rl_dense = {
+        "bound": "alu", "kernel": "k_fitness (TMA pair sweep + fused fold)",
+        "achieved": achieved, "peak": alu_peak, "unit": "pair-updates/s", "frac": achieved / alu_peak,
+        "traffic": dn_ncu.get("dram_bytes_per_launch"), "algorithmic_bytes": alg_bytes,
+        "work_per_launch": "%d chromosomes x N(N-1)/2 = %.4g executed pair-updates" % (P_eval, executed_local),
+        "peak_basis": "SURVEY §8(d): ISETP+SEL per pair on the 64-op/clk/SM INT pipe = 32 pairs/clk/SM "
+                      "x 148 SMs x %.0f MHz (sm_max_mhz)" % sm_max,
+        "measured": "CUDA events on the library stream over %d generations right after the timed region "
+                    "(same population, label-sparse pass off, so every block runs k_fitness): %.4f ms "
+                    "per launch.  In the timed region k_fitness ran %.1f%% of the blocks (%.4f ms per "
+                    "generation)" % (dprof["count"], dense_sweep_ms, 100.0 * dense_blocks / float(nblk * ngen),
+                                     sweep_ms),
+        "other_bounds": [
+            {"bound": "fp64", "peak": fp64_peak, "frac": achieved / fp64_peak,
+             "basis": "1 DADD per executed pair, 64 FP64 lanes/clk/SM"},
+            {"bound": "measured_loop", "peak": LOOP_PAIRS_PER_CLK * SM_COUNT * sm_max * 1e6,
+             "frac": achieved / (LOOP_PAIRS_PER_CLK * SM_COUNT * sm_max * 1e6),
+             "basis": "tools/mb_pairloop.cu bare inner loop: 26.8 pairs/clk/SM"},
+            {"bound": "hbm", "achieved_gbs": alg_bytes / (dense_sweep_ms / 1000.0) / 1e9, "peak_gbs": hbm_gbs,
+             "frac": alg_bytes / (dense_sweep_ms / 1000.0) / 1e9 / hbm_gbs},
+        ],
+    }
+    rl_sparse = None
+    if prof["fold_ms"] > 0 and sparse_blocks > 0:
+        sp_s = sparse_ms / 1000.0
+        pairs_needed = (sparse_gathers + cache_saved) / float(ngen)   # sum n_s(n_s-1)/2 per launch
+        gbs = alg_bytes / sp_s / 1e9
+        others = [
+            {"bound": "alu", "what": "necessary pair-updates per launch (C entries gathered + pair updates "
+                                     "served by the cluster cache) = %.4g" % pairs_needed,
+             "achieved": pairs_needed / sp_s, "peak": alu_peak, "unit": "pair-updates/s",
+             "frac": pairs_needed / sp_s / alu_peak},
+            {"bound": "l2_gather", "what": "C entries gathered from L2 per launch = %.4g"
+                                           % (sparse_gathers / float(ngen)),
+             "achieved": sparse_gathers / float(ngen) / sp_s, "peak": L2_GATHERS_PER_S, "unit": "gathers/s",
+             "frac": sparse_gathers / float(ngen) / sp_s / L2_GATHERS_PER_S,
+             "basis": "tools/mb_l2gather.cu: 3.03e11 random 8-byte gathers/s from an L2-resident C"},
+        ]
+        if sp_ncu.get("inst_per_launch"):
+            others.append({"bound": "issue", "what": "%.4g warp-instructions per launch (ncu "
+                                                      "smsp__inst_executed.sum, %s)" % (sp_ncu["inst_per_launch"],
+                                                                                        sp_ncu.get("source", "")),
+                           "achieved": sp_ncu["inst_per_launch"] / sp_s, "peak": issue_peak,
+                           "unit": "warp-instructions/s", "frac": sp_ncu["inst_per_launch"] / sp_s / issue_peak,
+                           "basis": "1 warp-instruction/clk per SMSP, 4 per SM"})
+        rl_sparse = {
+            "bound": "hbm", "kernel": "k_fitness_sparse (label-sparse pass + cluster cache)",
+            "achieved": gbs, "peak": hbm_gbs, "unit": "GB/s", "frac": gbs / hbm_gbs,
+            "traffic": sp_ncu.get("dram_bytes_per_launch"), "algorithmic_bytes": alg_bytes,
+            "work_per_launch": "%d chromosomes x (2N label bytes + 8 B L + 2 B top) = %d algorithmic bytes"
+                               % (P_eval, alg_bytes),
+            "measured": "CUDA events on the library stream around every k_fitness_sparse launch of the timed "
+                        "region: %.4f ms per launch of %.4f ms per generation" % (sparse_ms, gen_ms),
+            "traffic_note": "ncu dram__bytes_read+write of one launch inside the bench window (%s)"
+                            % sp_ncu.get("source", "no capture for this config"),
+            "other_bounds": others,
+            "cluster_cache": {"hits_per_launch": cache_hits / float(ngen),
+                              "pair_updates_saved_per_launch": cache_saved / float(ngen),
+                              "hit_share_of_pairs": cache_saved / float(max(1, cache_saved + sparse_gathers))},
+            "share_of_timed_generation": sparse_ms / gen_ms,
+        }
 
     # end-to-end through the public API from host memory (rank-local), see DESIGN.md §7
     e2e = None
@@ -361,70 +488,19 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         v, Ps, ng, dt, v1 = oracle_rate(C, planted, max_P=P_TOTAL)
-        cpu = {"value": v, "unit": "pair-updates/s", "cores": os.cpu_count() or 1,
+        cores = os.cpu_count() or 1
+        cpu = {"value": v, "unit": "pair-updates/s", "cores": cores, "cpu_model": cpu_model(),
                "kind": "oracle",
-               "sample": "%d-chromosome C4 population, %d full oracle generations (evaluate on "
+               "sample": "%d-chromosome %s population, %d full oracle generations (evaluate on "
                          "%d host threads + single-threaded operators), %.1f s"
-                         % (Ps, ng, os.cpu_count() or 1, dt),
+                         % (Ps, CONFIG, ng, cores, dt),
                "single_thread_evaluate": {"value": v1, "unit": "pair-updates/s", "cores": 1}}
+        if probe is not None:
+            cpu["parity"] = parity_probe(C, probe[0] - 1, probe[1], cores)
     if eng.ctx is not None:
         eng.close()
 
     if rank == 0:
-        rl_dense = {"bound": "alu", "kernel": "k_fitness (dense sweep + fused fold)", "achieved": achieved,
-                         "peak": peak, "unit": "pair-updates/s", "frac": achieved / peak,
-                         "measured": "CUDA events on the library stream over %d generations right after the "
-                                     "timed region, same population, label-sparse pre-pass off (every block "
-                                     "through k_fitness); in the timed region itself k_fitness ran %.1f%% of "
-                                     "the blocks and took %.3f of %.3f ms per generation, the label-sparse "
-                                     "pre-pass (k_fitness_sparse) %.3f ms"
-                                     % (dprof["count"], 100.0 * dense_blocks / float(nblk * ngen), sweep_ms,
-                                        gen_ms, sparse_ms),
-                         "traffic": traffic,
-                         "algorithmic_bytes": P_eval * (N * 2 + 8 + 2),
-                         "traffic_note": "ncu dram bytes of one launch: labels are read twice (gene-major "
-                                         "by the sweep's TMA, chromosome-major by the fused fold); the "
-                                         "fold scratch V is discarded from L2 after use (no write-back)",
-                         "work_per_launch": "%d chromosomes x N(N-1)/2 = %.4g executed pair-updates"
-                                            % (P_eval, executed_local),
-                         "peak_basis": "1 DFMA per executed pair; 64 FP64 lanes/clk/SM x 148 SMs "
-                                       "x %.0f MHz (sm_max_mhz)" % sm_max,
-                         "frac_at_measured_clock": (achieved / (FP64_LANES_PER_SM * SM_COUNT *
-                                                    clk["sm_mhz"] * 1e6))
-                         if clk and clk.get("sm_mhz") else None,
-                         "loop_ceiling": LOOP_PAIRS_PER_CLK * SM_COUNT * sm_max * 1e6,
-                         "frac_of_loop_ceiling": achieved / (LOOP_PAIRS_PER_CLK * SM_COUNT * sm_max * 1e6),
-                         "loop_ceiling_basis": "measured bare inner loop (tools/mb_pairloop.cu): "
-                                               "26.8 pairs/clk/SM, register-file-read bound"}
-        rl_sparse = ({
-                "bound": "issue", "kernel": "k_fitness_sparse",
-                "achieved": sp_inst / (sparse_ms / 1000.0),
-                "peak": 4.0 * SM_COUNT * sm_max * 1e6, "unit": "warp-instructions/s",
-                "frac": sp_inst / (sparse_ms / 1000.0) / (4.0 * SM_COUNT * sm_max * 1e6),
-                "work_per_launch": "%.4g warp-instructions (ncu smsp__inst_executed.sum of one launch at "
-                                   "generation ~400, profiles/traffic.json) / the timed mean launch time "
-                                   "%.3f ms" % (sp_inst, sparse_ms),
-                "peak_basis": "4 warp-instructions/clk/SM (one per SMSP) x 148 SMs x %.0f MHz; the pass is "
-                              "latency/issue bound (shared-memory atomics, dependent label loads), not "
-                              "bandwidth bound: its DRAM traffic is the labels (%.0f MB per launch)"
-                              % (sm_max, (sp_dram or 0) / 1e6),
-                "gathers": {"per_launch": sparse_gathers / float(ngen),
-                            "per_s": sparse_gathers / (prof["fold_ms"] / 1000.0),
-                            "frac_of_l2_gather_peak": sparse_gathers / (prof["fold_ms"] / 1000.0) /
-                                                      L2_GATHERS_PER_S,
-                            "l2_gather_peak_basis": "tools/mb_l2gather.cu: 3.03e11 random 8-byte gathers/s"},
-                "cluster_cache": {"hits_per_launch": cache_hits / float(ngen),
-                                  "pair_updates_saved_per_launch": cache_saved / float(ngen),
-                                  "hit_share_of_pairs": cache_saved / float(max(1, cache_saved + sparse_gathers))},
-                "measured": "CUDA events on the library stream around every k_fitness_sparse launch of the "
-                            "timed region (mean %.3f of %.3f ms per generation)" % (sparse_ms, gen_ms),
-                "traffic": sp_dram,
-                "algorithmic_bytes": P_eval * (N * 2 + 8 + 2),
-                "traffic_note": "ncu dram bytes of one launch: the chromosome-major labels (2N bytes per "
-                                "chromosome) plus L and top; C, the cache table's hot slots and the "
-                                "cache keys stay in L2",
-                "share_of_timed_generation": sparse_ms / gen_ms}
-                if sp_inst and prof["fold_ms"] > 0 else None)
         # the top-level roofline is the kernel that dominated the timed region
         if rl_sparse is not None and sparse_ms > sweep_ms:
             rl_main, rl_other = rl_sparse, rl_dense
@@ -474,6 +550,12 @@ def main():
                                 "(tests/test_gpu_parity.py::test_run_recovers_planted_C4)"},
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "parity": (cpu or {}).get("parity"),
+            "paper_context": "Table 4 (P:369, P:373): the paper's CUDA PGA clusters one 18-stock JSE "
+                             "correlation matrix in 0.80 s median on a GTX Titan Black (1.39 s on a Tesla "
+                             "C2050; serial MATLAB 7.77 s), population 1000, <= 400 generations; at most "
+                             "~5e5 fitness evaluations/s (BASELINE.md §1).  Other hardware, data and "
+                             "workload: context, not a target.",
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -248,21 +248,28 @@ def test_run_table3_termination_equals_oracle(pga, orc):
 # C4 at full size, mid-run, across cluster-cache clears
 # ---------------------------------------------------------------------------
 def test_C4_full_size_midrun_sample(pga, orc):
-    """C4 (N = 500, P = 65536, p_m = 2/N) after ~500 generations with the
+    """C4 (N = 500, P = 65536, p_m = 2/N) after ~800 generations with the
     automatic label-sparse pass and the cluster cache, including at least
     one cache clear and the pass's unchecked launches: 1024 sampled
     chromosomes of the evaluated generation (plus both ends) against the
     oracle, and the next population (all 65536 rows) equal to orc_step on
     the GPU's L and top."""
     C, _ = _corr(orc, workloads.CONFIGS["C4"])
-    N, P, gens = C.shape[0], 65536, 520
-    params = _par(pga, P, max_gens=gens + 5, tol=-1.0, p_mutation=2.0 / N, seed=12)
+    N, P = C.shape[0], 65536
+    params = _par(pga, P, max_gens=4000, tol=-1.0, p_mutation=2.0 / N, seed=12)
     ctx = pga.pga_create(C, params)
     try:
         pga.pga_init(ctx, 12)
-        for _ in range(gens):
-            pga.pga_gen_evaluate(ctx)
-            pga.pga_gen_breed(ctx)
+        gens, after = 0, None
+        # run until the cache table has been cleared (half full: ~700
+        # generations at C4), then 60 generations more
+        while gens < 3500 and (after is None or gens < after + 60):
+            for _ in range(20):
+                pga.pga_gen_evaluate(ctx)
+                pga.pga_gen_breed(ctx)
+            gens += 20
+            if after is None and pga.pga_cache_stats(ctx)["clears"] >= 1:
+                after = gens
         pga.pga_gen_evaluate(ctx)
         pop, L, top = pga.pga_get_population(ctx, with_top=True)
         cache = pga.pga_cache_stats(ctx)
@@ -279,7 +286,7 @@ def test_C4_full_size_midrun_sample(pga, orc):
     Lo, to = orc.evaluate(C, pop[idx] - 1, nthreads=NT)
     _assert_L(L[idx], Lo)
     assert np.all(np.isfinite(L)) and L.min() > 0.0
-    op = orc.default_params(pop=P, max_gens=gens + 5, tol=-1.0, p_m=2.0 / N, seed=12)
+    op = orc.default_params(pop=P, max_gens=4000, tol=-1.0, p_m=2.0 / N, seed=12)
     assert np.array_equal(nxt - 1, orc.step(op, pop - 1, L, top, gen=gens))
 
 
