@@ -104,7 +104,7 @@ const char *pga_last_error(void);
 int pga_evaluate(pga_ctx *ctx, const int32_t *labels, int64_t P, double *out_L);
 
 /* Device fast path, stream-ordered on `stream` (cudaStream_t, NULL = the
- * ctx's stream).  The call uses the ctx's evaluation scratch (staging
+ * ctx's stream; cudaStreamLegacy selects the legacy default stream).  The call uses the ctx's evaluation scratch (staging
  * layouts, fold scratch, block flags and counters), so when `stream` is not
  * the ctx's stream it is joined to it with events in both directions: the
  * launch waits for all work already queued on the ctx's stream, and later
@@ -422,7 +422,8 @@ int pga_profile_cache(pga_ctx *ctx, int64_t *hits, int64_t *saved);
 
 /* Level-2 profiling: per-phase AVERAGE milliseconds, ms[PGA_PROF_PHASES]:
  * 0 dense fitness kernel (sweep + fused fold), 1 label-sparse pre-pass, 2 statistics/termination,
- * 3 order sort, 4 scaling+selection, 5 mate pairing, 6 breed, 7 advance. */
+ * 3 order sort, 4 scaling+selection, 5 mate pairing, 6 breed, 7 advance (fused into the
+ * breed's last CTA since round 2: ~0). */
 #define PGA_PROF_PHASES 8
 int pga_profile_phases(pga_ctx *ctx, double *ms, int32_t *count);
 

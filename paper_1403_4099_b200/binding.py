@@ -194,8 +194,23 @@ def pga_evaluate(ctx, labels_1based) -> np.ndarray:
     return L
 
 
+CUDA_STREAM_LEGACY = 1   # cudaStreamLegacy: the legacy default stream as an explicit handle
+
+
+def _caller_stream(stream):
+    """The stream a device-pointer call is ordered on: the caller's, else
+    torch's current stream (the legacy default stream is passed as
+    cudaStreamLegacy, since NULL means the ctx's own stream at this ABI)."""
+    if stream is None:
+        import torch
+        stream = torch.cuda.current_stream().cuda_stream
+    return stream if stream else CUDA_STREAM_LEGACY
+
+
 def pga_evaluate_device(ctx, labels_dev, L_dev, top_dev=None, stream=None):
-    """labels_dev: torch uint16-compatible (int16) CUDA tensor [P][N] 0-based."""
+    """labels_dev: torch uint16-compatible (int16) CUDA tensor [P][N] 0-based.
+    Ordered on `stream` (default: torch's current stream, so tensors made
+    just before are complete); the library joins it to the ctx's stream."""
     N, _, cap = pga_get_dims(ctx)
     _need(labels_dev.dim() == 2 and labels_dev.shape[1] == N, "labels_dev must be [P][%d]" % N)
     P = labels_dev.shape[0]
@@ -206,7 +221,7 @@ def pga_evaluate_device(ctx, labels_dev, L_dev, top_dev=None, stream=None):
     if top_dev is not None:
         _dev_tensor(top_dev, ("int16", "uint16"), P, "top_dev")
     _check(lib().pga_evaluate_device(ctx, _p(labels_dev), P, _p(L_dev), _p(top_dev),
-                                     None if stream is None else ct.c_void_p(stream)))
+                                     ct.c_void_p(_caller_stream(stream))))
 
 
 def pga_init(ctx, seed: int):

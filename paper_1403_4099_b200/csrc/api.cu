@@ -31,6 +31,14 @@ int cuda_fail(cudaError_t e, const char *what) {
 }
 void count_launch(int n) { g_launches += n; }
 
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char *e = std::getenv("PGA_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 cudaError_t prof_record(cudaEvent_t e, cudaStream_t s) {
     cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
     cudaError_t r = cudaStreamIsCapturing(s, &st);
@@ -45,12 +53,9 @@ int launch_init_raw(uint64_t seed, int N, int ldn, int64_t P, int64_t Pcap, int6
                     uint32_t island, uint16_t *CM, uint16_t *GM, int32_t *out32, cudaStream_t s);
 int run_select_ops(const double *L, int64_t P, const pga_params &p, int32_t gen, int32_t island,
                    int32_t *order, int32_t *sel, uint64_t *keys_in, uint64_t *keys_out,
-                   int32_t *idx_in, uint64_t *q, uint64_t *prefix, void *tmp, size_t tmp_bytes,
-                   const int32_t *done, cudaStream_t s, const int32_t *gen_ptr, bool sorted,
-                   int32_t *sigma);
-int run_mates(int64_t M, const pga_params &p, int32_t gen, int32_t island, uint32_t *k_in,
-              uint32_t *k_out, int32_t *m_in, int32_t *sigma, void *tmp, size_t tmp_bytes,
-              const int32_t *done, cudaStream_t s, const int32_t *gen_ptr);
+                   int32_t *idx_in, int32_t *rank, uint64_t *q, uint64_t *bsum, const int32_t *done,
+                   cudaStream_t s, const int32_t *gen_ptr, bool sorted, int32_t *sigma);
+int run_mates(int64_t M, const pga_params &p, int32_t gen, int32_t island, int32_t *sigma, cudaStream_t s);
 int launch_breed_hook(const int32_t *pop, const int32_t *top, const int32_t *order, int64_t P,
                       int N, const int32_t *sel, const int32_t *sigma, const pga_params &p,
                       int32_t gen, int32_t island, int64_t p_off, int32_t *next, cudaStream_t s);
@@ -141,9 +146,9 @@ void free_ctx(pga_ctx *c) {
     drop_graphs(c);
     void *ptrs[] = {c->C, c->diag, c->lgtab, c->sflag, c->sp_live, c->sp_blocks, c->cc, c->cc_state,
                     c->stats_part, c->stats_ctr,
-                    c->cc_keys, c->pop[0], c->pop[1], c->popT[0], c->popT[1], c->V, c->L,
-                    c->top, c->keys_in, c->keys_out, c->idx_in, c->order, c->q, c->prefix,
-                    c->sel, c->mkeys_in, c->mkeys_out, c->m_in, c->sigma, c->cub_tmp, c->st,
+                    c->cc_keys, c->ptab, c->pop[0], c->pop[1], c->popT[0], c->popT[1], c->V, c->L,
+                    c->top, c->keys_in, c->keys_out, c->idx_in, c->order, c->q, c->rank,
+                    c->sel, c->sigma, c->breed_ctr, c->st,
                     c->best_labels, c->history, c->stage_i32, c->evCM, c->evGM, c->evL,
                     c->counters};
     for (void *p : ptrs)
@@ -435,6 +440,7 @@ int pga_create(const double *C, int32_t N, const pga_params *p, pga_ctx **out) {
         rc = rc ? rc : dalloc(&c->cc, (size_t)slots);
         rc = rc ? rc : dalloc(&c->cc_state, (size_t)4);
         rc = rc ? rc : dalloc(&c->cc_keys, (size_t)2 * N);
+        rc = rc ? rc : dalloc(&c->ptab, (size_t)N * c->ldc);
         if (!rc && (cudaMemset(c->cc, 0, sizeof(CCSlot) * slots) != cudaSuccess ||
                     cudaMemset(c->cc_state, 0, 4 * sizeof(uint32_t)) != cudaSuccess))
             rc = fail(PGA_EDEVICE, "memset cluster cache");
@@ -464,21 +470,17 @@ int pga_create(const double *C, int32_t N, const pga_params *p, pga_ctx **out) {
     rc = rc ? rc : dalloc(&c->idx_in, (size_t)c->Pcap);
     rc = rc ? rc : dalloc(&c->order, (size_t)c->Pcap);
     rc = rc ? rc : dalloc(&c->q, (size_t)c->Pcap);
-    rc = rc ? rc : dalloc(&c->prefix, (size_t)c->Pcap);
+    rc = rc ? rc : dalloc(&c->rank, (size_t)c->Pcap);
     rc = rc ? rc : dalloc(&c->sel, (size_t)c->Pcap + 2);
-    rc = rc ? rc : dalloc(&c->mkeys_in, (size_t)c->Pcap + 2);
-    rc = rc ? rc : dalloc(&c->mkeys_out, (size_t)c->Pcap + 2);
-    rc = rc ? rc : dalloc(&c->m_in, (size_t)c->Pcap + 2);
     rc = rc ? rc : dalloc(&c->sigma, (size_t)c->Pcap + 2);
+    rc = rc ? rc : dalloc(&c->breed_ctr, (size_t)1);
     rc = rc ? rc : dalloc(&c->st, 1);
     rc = rc ? rc : dalloc(&c->best_labels, (size_t)c->ldn);
     rc = rc ? rc : dalloc(&c->counters, (size_t)(c->Pcap / CB));
     if (rc) return bail(rc);
     e = cudaMemsetAsync(c->counters, 0, sizeof(uint32_t) * (size_t)(c->Pcap / CB), c->stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(c->breed_ctr, 0, sizeof(uint32_t), c->stream);
     if (e != cudaSuccess) return bail(cuda_fail(e, "cudaMemset counters"));
-    c->cub_tmp_bytes = cub_tmp_needed(c->Pcap + 2);
-    rc = dalloc((unsigned char **)&c->cub_tmp, c->cub_tmp_bytes);
-    if (rc) return bail(rc);
     e = cudaMallocHost((void **)&c->h_st, sizeof(DevState));
     if (e != cudaSuccess) return bail(fail(PGA_ENOMEM, "cudaMallocHost failed"));
     // population buffers: zero so padding chromosomes hold valid labels
@@ -502,6 +504,7 @@ int pga_create(const double *C, int32_t N, const pga_params *p, pga_ctx **out) {
     }
     rc = prepare_fitness(N);
     if (!rc) rc = launch_logtab(c, c->stream);
+    if (!rc) rc = launch_pairtab(c, c->stream);
     if (!rc && cudaStreamSynchronize(c->stream) != cudaSuccess) rc = cuda_fail(cudaGetLastError(), "log table");
     if (!rc) rc = prepare_breed(N);
     if (!rc) rc = prepare_select_small();
@@ -966,21 +969,19 @@ int pga_op_select(const double *L, int64_t P, const pga_params *p, int32_t gen, 
     const int64_t M = 2 * ((P - p->elite + 1) / 2);
     HookBufs hb;
     double *dL;
-    int32_t *dorder, *dsel, *didx;
-    uint64_t *k1, *k2, *q, *pre;
-    void *tmp;
-    const size_t tb = cub_tmp_needed(P + 2);
+    int32_t *dorder, *dsel, *didx, *drank;
+    uint64_t *k1, *k2, *q, *bsum;
     TRY(hb.get(&dL, P));
     TRY(hb.get(&dorder, P));
     TRY(hb.get(&dsel, M));
     TRY(hb.get(&didx, P));
+    TRY(hb.get(&drank, P));
     TRY(hb.get(&k1, P));
     TRY(hb.get(&k2, P));
     TRY(hb.get(&q, P));
-    TRY(hb.get(&pre, P));
-    TRY(hb.get((unsigned char **)&tmp, tb));
+    TRY(hb.get(&bsum, P / 1024 + 2));
     PGA_CUDA(cudaMemcpy(dL, L, sizeof(double) * P, cudaMemcpyHostToDevice));
-    TRY(run_select_ops(dL, P, *p, gen, island, dorder, dsel, k1, k2, didx, q, pre, tmp, tb, nullptr,
+    TRY(run_select_ops(dL, P, *p, gen, island, dorder, dsel, k1, k2, didx, drank, q, bsum, nullptr,
                        0, nullptr, false, nullptr));
     PGA_CUDA(cudaDeviceSynchronize());
     PGA_CUDA(cudaMemcpy(order_out, dorder, sizeof(int32_t) * P, cudaMemcpyDeviceToHost));
@@ -993,16 +994,9 @@ int pga_op_mates(int64_t M, const pga_params *p, int32_t gen, int32_t island, in
     if (M < 1) return fail(PGA_EINVAL, "M must be >= 1");
     TRY(ensure_device(p->device));
     HookBufs hb;
-    uint32_t *k1, *k2;
-    int32_t *m1, *sig;
-    void *tmp;
-    const size_t tb = cub_tmp_needed(M + 2);
-    TRY(hb.get(&k1, M));
-    TRY(hb.get(&k2, M));
-    TRY(hb.get(&m1, M));
+    int32_t *sig;
     TRY(hb.get(&sig, M));
-    TRY(hb.get((unsigned char **)&tmp, tb));
-    TRY(run_mates(M, *p, gen, island, k1, k2, m1, sig, tmp, tb, nullptr, 0, nullptr));
+    TRY(run_mates(M, *p, gen, island, sig, 0));
     PGA_CUDA(cudaDeviceSynchronize());
     PGA_CUDA(cudaMemcpy(sigma_out, sig, sizeof(int32_t) * M, cudaMemcpyDeviceToHost));
     return PGA_OK;

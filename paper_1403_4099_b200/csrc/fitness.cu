@@ -232,6 +232,17 @@ __device__ __forceinline__ void eq8_tables(double *cs, int32_t *ns, int K, int l
     }
 }
 
+// Summand of Eq. 8 (Q1-Q3) for a cluster of n >= 2 members with intra-
+// cluster sum c: 0 unless c > n (Q2); c clamped to n^2 - 1e-9 (Q3); the
+// integer logs from the table (Q30).
+__device__ __forceinline__ double eq8_term(int n, double c, const double *__restrict__ lgn,
+                                           const double *__restrict__ lgnn) {
+    if (!(c > (double)n)) return 0.0;
+    const double nd = (double)n, n2 = nd * nd;
+    const double ch = fmin(c, n2 - 1e-9);
+    return (__ldg(lgn + n) - log(ch)) + (nd - 1.0) * (__ldg(lgnn + n) - log(n2 - ch));
+}
+
 // Fold (warp-wide) of NC chromosomes at once (independent chains -> ILP):
 // lane per gene; n_s by a shared-memory integer atomic, and c_s = sum of V_i
 // over the cluster accumulated in 64-bit fixed point (V * 2^S, S = 62 -
@@ -297,6 +308,8 @@ __device__ __forceinline__ void fold_multi(const uint16_t *const (&lab)[NC], con
 __global__ void __launch_bounds__(FIT_THREADS)
 k_fitness(const __grid_constant__ CUtensorMap tmLab0, const __grid_constant__ CUtensorMap tmLab1,
           const __grid_constant__ CUtensorMap tmC, FitArgs a) {
+    pdl_wait();
+    pdl_trigger();
     {   // both exit tests from one round trip (independent loads): with every
         // block evaluated label-sparsely, this is all a CTA does
         const int32_t dn = a.done ? __ldg(a.done) : 0;
@@ -538,7 +551,14 @@ constexpr int CC_NMIN = PGA_CC_NMIN;   // clusters this large go through the cac
 static_assert(CC_NMIN >= 2, "large clusters must have pairs");
 constexpr int CC_PROBE = 8;        // linear-probe length
 
-__host__ __device__ __forceinline__ int cc_entries(int N) { return N / CC_NMIN + 1; }
+// Cluster classes of the label-sparse pass: n = 2 .. WALK_N-1 ("small") are
+// evaluated lane-parallel from their recorded members (n = 2 from the pair-
+// term table); n >= WALK_N ("walk class") get an ordinal, go through the
+// cache when n >= CC_NMIN, and are walked when not a hit.
+constexpr int WALK_N = 4;
+constexpr int SMALL_N = WALK_N - 1;   // members recorded per label
+static_assert(CC_NMIN >= WALK_N, "cacheable clusters are in the walk class");
+__host__ __device__ __forceinline__ int cc_entries(int N) { return N / WALK_N + 1; }
 
 __device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t *p) {
     uint64_t v;
@@ -623,6 +643,7 @@ struct SparseArgs {
     int nblocks;
     double fx_scale, fx_inv;
     const double *lgn, *lgnn;
+    const double *ptab;           // [N][ldc] Eq. 8 term of every pair cluster {i, j} (k_pairtab)
     pga::CCSlot *cc;              // cluster cache (null = off)
     uint32_t cc_mask;             // slots - 1
     uint32_t *cc_state;           // [0] fill, [1] clear request, [2] CTA count, [3] clears done
@@ -631,13 +652,19 @@ struct SparseArgs {
 
 __host__ __device__ __forceinline__ int sp_words(int N) { return (N + 2) / 2; }   // packed u16 counters for labels 0..N
 
-constexpr int SPQ = 64;   // per-warp queue of completed clusters awaiting their Eq. 8 summand
-
+// Per-warp shared memory of the label-sparse pass (bytes, 16-aligned):
+//   A [16 E]  cent: Zobrist keys {k1, k2} per ordinal, then the Eq. 8 term
+//   B [16 E]  perm2: walked genes (g | ordinal << 16); before that the
+//             second Zobrist copy
+//   (during counting and the small pass A+B hold mem [SMALL_N (N+1)] u16,
+//    the first members of every label, and slist [N/2 + 1] u16)
+//   cq [4 (W + 1)]  packed u16 counts, then ordm (u16 per label); during the
+//             walk, c of every walked cluster (fp64 per ordinal: 8 E <= 4 (W + 1))
+//   wen [4 E] walk range ends per ordinal
+//   cn, clab [2 E each] n (| 0x8000: cache hit), label per ordinal
 __host__ __device__ __forceinline__ size_t sp_per_warp(int N) {
-    return (((size_t)sp_words(N) * 4 /*counts, then ordinals*/ + (size_t)sp_words(N + 2) * 4 /*off*/ +
-             (size_t)N * 4 /*perm2*/ + (size_t)SPQ * 12 /*queue*/ +
-             (size_t)cc_entries(N) * 20 /*hash/keys then f, n, label per large cluster*/ + 64) + 15) &
-           ~(size_t)15;
+    const size_t E = (size_t)cc_entries(N);
+    return ((32 * E + ((size_t)sp_words(N) + 1) * 4 + 8 * E + 64) + 15) & ~(size_t)15;
 }
 
 static size_t sparse_smem(int N) {
@@ -647,6 +674,8 @@ static size_t sparse_smem(int N) {
 }
 
 __global__ void __launch_bounds__(SP_T, PGA_SP_MINB) k_fitness_sparse(SparseArgs a) {
+    pdl_wait();
+    pdl_trigger();
     if (a.done && *a.done) return;
     extern __shared__ __align__(16) unsigned char sps[];
     __shared__ uint32_t s_maxp;
@@ -657,14 +686,15 @@ __global__ void __launch_bounds__(SP_T, PGA_SP_MINB) k_fitness_sparse(SparseArgs
     const uint16_t *CM = par ? a.cm1 : a.cm0;
     unsigned char *wb = sps + (size_t)warp * sp_per_warp(N);
     const int E = cc_entries(N);
-    double *qc = reinterpret_cast<double *>(wb);                         // [SPQ] queued c (small clusters)
-    ulonglong2 *cent = reinterpret_cast<ulonglong2 *>(qc + SPQ);        // [E] Zobrist XOR, keys {k1, k2}, then {f, -}
-    uint32_t *qnk = reinterpret_cast<uint32_t *>(cent + E);             // [SPQ] queued n | label << 16
-    uint32_t *cq = qnk + SPQ;                                            // [W] packed u16 counts, then ordm
-    uint32_t *offw = cq + W;                                             // [sp_words(N+2)] packed u16 walk starts, then ends
-    uint16_t *off = reinterpret_cast<uint16_t *>(offw);
-    uint32_t *perm2 = offw + sp_words(N + 2);                            // [N] walked genes: g | s << 16
-    uint16_t *cn = reinterpret_cast<uint16_t *>(perm2 + N);             // [E] n (| 0x8000: cache hit)
+    ulonglong2 *cent = reinterpret_cast<ulonglong2 *>(wb);              // A [E] Zobrist keys {k1, k2}, then {f, -}
+    uint32_t *perm2 = reinterpret_cast<uint32_t *>(cent + E);           // B [4 E] walked genes g | ordinal << 16
+    uint32_t *cent2 = perm2;                                             // B: second Zobrist copy (before the walk)
+    uint16_t *mem = reinterpret_cast<uint16_t *>(wb);                   // A+B [SMALL_N (N+1)]: first members per label
+    uint16_t *slist = mem + SMALL_N * (N + 1);                           // A+B [N/2 + 1]: small labels
+    uint32_t *cq = perm2 + 4 * E;                                        // [W] packed u16 counts, then ordm
+    uint32_t *wen = cq + W + 1;                                          // [E] walk range ends
+    double *cval = reinterpret_cast<double *>(cq);                       // [E] walked clusters' c (after the sort)
+    uint16_t *cn = reinterpret_cast<uint16_t *>(wen + E);               // [E] n (| 0x8000: cache hit)
     uint16_t *clab = cn + E;                                             // [E] label
     if (a.live && a.live[0] == 0) {     // the population went dense: skip (flags cleared)
         if (tid == 0) a.sflag[cb] = 0;
@@ -767,22 +797,30 @@ __global__ void __launch_bounds__(SP_T, PGA_SP_MINB) k_fitness_sparse(SparseArgs
     }
     if (!sparse) return;
 
-    // ---- pass 2: exact label-sparse evaluation.  Large clusters (n >=
-    // CC_NMIN) get ordinals (label order) and their Eq. 8 terms are summed per
-    // ordinal, separately from the small clusters' queue: the summation order
-    // is the same whether a term came from the cache or was gathered.
+    // ---- pass 2: exact label-sparse evaluation.  Per chromosome: (1) counts,
+    // recording each label's first SMALL_N members; (2) classes: small
+    // clusters (2 <= n < WALK_N) are listed, walk-class clusters (n >=
+    // WALK_N) get ordinals in label order; (3) small clusters lane-parallel:
+    // c from their recorded members (n = 2: the pair-term table), Eq. 8 term
+    // at once; (4) Zobrist keys of cacheable clusters (n >= CC_NMIN) and one
+    // lookup each; (5)-(7) the walk-class clusters that were not hits are
+    // counting-sorted by ordinal and walked (every unordered pair once, L2
+    // gathers of C, exact fixed-point sums), their terms stored per ordinal
+    // (and inserted into the cache); (8) the walk-class terms are summed in
+    // ordinal (= label) order, so L does not depend on which came from the
+    // cache.  c sums are exact fixed-point integers (order-free), so every
+    // term is deterministic.
     const double *C = a.C;
     const uint4 *keys4 = reinterpret_cast<const uint4 *>(a.cc_keys);
     uint16_t *ordm = reinterpret_cast<uint16_t *>(cq);
     for (int q = warp; q < pga::CB; q += SP_W) {
         const int64_t p = (int64_t)cb * pga::CB + q;
         if (p >= a.P) break;
-        // counts again (pass 1 kept only the pair totals)
         for (int k = lane; k < W; k += 32) cq[k] = 0u;
         __syncwarp();
         const uint16_t *lab = CM + p * a.ldn;
         uint32_t kmax = 0;
-        // the chromosome's labels stay in registers for the three passes over
+        // the chromosome's labels stay in registers for the passes over
         // them: gene 64 (k >> 1) + 2 lane + (k & 1) is half (k & 1) of
         // labr[k >> 1] (one aligned 32-bit load per gene pair; ldn is even)
         uint32_t labr[SP_LREG];
@@ -791,54 +829,91 @@ __global__ void __launch_bounds__(SP_T, PGA_SP_MINB) k_fitness_sparse(SparseArgs
             const int i = 64 * k + 2 * lane;
             labr[k] = i < N ? *reinterpret_cast<const uint32_t *>(lab + i) : 0u;
         }
+        // (1) counts; the count before a gene's increment is its slot
 #pragma unroll
         for (int k = 0; k < 2 * SP_LREG; ++k) {
-            if (64 * (k >> 1) + 2 * lane + (k & 1) < N) {
+            const int i = 64 * (k >> 1) + 2 * lane + (k & 1);
+            if (i < N) {
                 const uint32_t s = (labr[k >> 1] >> (16 * (k & 1))) & 0xFFFFu;
                 kmax = max(kmax, s);
-                atomicAdd(cq + (s >> 1), 1u << (16 * (s & 1u)));
+                const uint32_t sh = 16 * (s & 1u);
+                const uint32_t slot = (atomicAdd(cq + (s >> 1), 1u << sh) >> sh) & 0xFFFFu;
+                if (slot < (uint32_t)SMALL_N) mem[SMALL_N * s + slot] = (uint16_t)i;
             }
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) kmax = max(kmax, __shfl_xor_sync(0xFFFFFFFFu, kmax, o));
         const int K = min((int)kmax + 1, N);
         __syncwarp();
-        // ordinals: ordm[k] (in place over the 16-bit count) = ordinal of a
-        // large cluster, else 0x8000 | n; bit 14 is set below for walked labels
-        int ecnt = 0;
-        // second copy of the Zobrist accumulators in perm2 (free until the
-        // walk): odd lanes XOR into it, halving same-address collisions of the
-        // shared atomics; the copies are XORed at the lookup (order-free)
-        const bool dup = use_cache && (size_t)E * 16 <= (size_t)N * 4;
-        uint32_t *cent2 = perm2;
+        // (2) classes.  ordm[k] (in place over the 16-bit count): 0x8000 | n
+        // below the walk class, else the ordinal | 0x2000 if cacheable;
+        // bit 0x4000 is set below for cache hits
+        int ecnt = 0, scnt = 0;
         for (int k0 = 0; k0 < K; k0 += 32) {
             const int k = k0 + lane;
             const int n = k < K ? (int)ordm[k] : 0;
-            const bool el = n >= CC_NMIN;
-            const unsigned bal = __ballot_sync(0xFFFFFFFFu, el);
+            const bool el = n >= WALK_N, sm = n >= 2 && n < WALK_N;
+            const unsigned be = __ballot_sync(0xFFFFFFFFu, el), bs = __ballot_sync(0xFFFFFFFFu, sm);
             if (el) {
-                const int ord = ecnt + __popc(bal & lanemask_lt());
-                ordm[k] = (uint16_t)ord;
-                cent[ord] = make_ulonglong2(0ull, 0ull);
-                if (dup) cent2[4 * ord] = cent2[4 * ord + 1] = cent2[4 * ord + 2] = cent2[4 * ord + 3] = 0u;   // 4-byte aligned only
+                const int ord = ecnt + __popc(be & lanemask_lt());
+                ordm[k] = (uint16_t)(ord | (n >= CC_NMIN ? 0x2000 : 0));
                 cn[ord] = (uint16_t)n;
                 clab[ord] = (uint16_t)k;
             } else if (k < K) {
                 ordm[k] = (uint16_t)(0x8000 | n);
+                if (sm) slist[scnt + __popc(bs & lanemask_lt())] = (uint16_t)k;
             }
-            ecnt += __popc(bal);
+            ecnt += __popc(be);
+            scnt += __popc(bs);
         }
         __syncwarp();
-        unsigned long long nhit = 0, nsaved = 0;
+        // (3) small clusters, one per lane: no walk, no queue
+        uint32_t nhit = 0, nsaved = 0, npair = 0;   // per chromosome: < 2^32 (N <= 640)
+        double fsum = 0.0, fbest = 0.0;
+        int kbest = 0x7FFFFFFF;
+        for (int j = lane; j < scnt; j += 32) {
+            const int sl = (int)slist[j];
+            const int n = (int)(ordm[sl] & 0x7FFFu);
+            const int g0 = mem[SMALL_N * sl], g1 = mem[SMALL_N * sl + 1];
+            double f;
+            if (n == 2) {
+                f = __ldg(a.ptab + (size_t)g0 * a.ldc + g1);
+                npair += 1;
+            } else {
+                const int g2 = mem[SMALL_N * sl + 2];
+                const long long acc =
+                    __double2ll_rn(__ldg(a.diag + g0) * a.fx_scale) + __double2ll_rn(__ldg(a.diag + g1) * a.fx_scale) +
+                    __double2ll_rn(__ldg(a.diag + g2) * a.fx_scale) +
+                    2 * (__double2ll_rn(__ldg(C + (size_t)g0 * a.ldc + g1) * a.fx_scale) +
+                         __double2ll_rn(__ldg(C + (size_t)g0 * a.ldc + g2) * a.fx_scale) +
+                         __double2ll_rn(__ldg(C + (size_t)g1 * a.ldc + g2) * a.fx_scale));
+                f = eq8_term(n, (double)acc * a.fx_inv, a.lgn, a.lgnn);
+                npair += 3;
+            }
+            fsum += f;
+            if (f > fbest || (f == fbest && f > 0.0 && sl < kbest)) {
+                fbest = f;
+                kbest = sl;
+            }
+        }
+        __syncwarp();   // mem and slist (regions A+B) are dead from here
+        // (4) Zobrist XOR of each cacheable cluster's members; the odd lanes
+        // XOR into the second copy (halves same-address collisions of the
+        // shared atomics); the copies are XORed at the lookup (order-free)
         if (use_cache && ecnt > 0) {
-            // Zobrist XOR of each large cluster's members
+            for (int o = lane; o < ecnt; o += 32) {
+                cent[o] = make_ulonglong2(0ull, 0ull);
+                cent2[4 * o] = cent2[4 * o + 1] = cent2[4 * o + 2] = cent2[4 * o + 3] = 0u;
+            }
+            __syncwarp();
 #pragma unroll
             for (int k = 0; k < 2 * SP_LREG; ++k) {
                 const int i = 64 * (k >> 1) + 2 * lane + (k & 1);
                 if (i >= N) continue;
                 const uint32_t om = ordm[(labr[k >> 1] >> (16 * (k & 1))) & 0xFFFFu];
-                if (!(om & 0x8000u)) {
-                    uint32_t *h = (dup && (lane & 1)) ? cent2 + 4 * om : reinterpret_cast<uint32_t *>(cent + om);
+                if ((om & 0xA000u) == 0x2000u) {
+                    const uint32_t o = om & 0x1FFFu;
+                    uint32_t *h = (lane & 1) ? cent2 + 4 * o : reinterpret_cast<uint32_t *>(cent + o);
                     const uint4 kk = __ldg(keys4 + i);
                     atomicXor(h, kk.x);
                     atomicXor(h + 1, kk.y);
@@ -847,89 +922,84 @@ __global__ void __launch_bounds__(SP_T, PGA_SP_MINB) k_fitness_sparse(SparseArgs
                 }
             }
             __syncwarp();
-            // one lookup per large cluster, lane-parallel; a hit is its Eq. 8
-            // term and the cluster is not walked
+            // one lookup per cacheable cluster, lane-parallel; a hit is its
+            // Eq. 8 term and the cluster is not walked
             for (int o = lane; o < ecnt; o += 32) {
-                ulonglong2 h = cent[o];
-                if (dup) {
-                    const uint32_t *c2 = cent2 + 4 * o;
-                    h.x ^= (unsigned long long)c2[0] | ((unsigned long long)c2[1] << 32);
-                    h.y ^= (unsigned long long)c2[2] | ((unsigned long long)c2[3] << 32);
-                }
-                const uint64_t k1 = h.x | 1ull, k2 = h.y | 1ull;
                 const uint32_t n = cn[o];
+                if (n < (uint32_t)CC_NMIN) continue;
+                ulonglong2 h = cent[o];
+                const uint32_t *c2 = cent2 + 4 * o;
+                h.x ^= (unsigned long long)c2[0] | ((unsigned long long)c2[1] << 32);
+                h.y ^= (unsigned long long)c2[2] | ((unsigned long long)c2[3] << 32);
+                const uint64_t k1 = h.x | 1ull, k2 = h.y | 1ull;
                 long long v = 0;
                 cent[o] = make_ulonglong2(k1, k2);
                 if (cc_find(a.cc, a.cc_mask, k1, k2, n, &v)) {
                     cent[o].x = (unsigned long long)v;          // the cached Eq. 8 term
                     cn[o] = (uint16_t)(n | 0x8000u);
+                    ordm[clab[o]] |= 0x4000u;
                     nhit += 1;
-                    nsaved += (unsigned long long)n * (n - 1) / 2;
+                    nsaved += n * (n - 1) / 2;
                 }
             }
             __syncwarp();
         }
-        // walk offsets: clusters with n >= 2 that are not cache hits, in label
-        // order (exclusive prefix over labels 0..K-1)
+        // (5) walk ranges: walk-class clusters that are not hits, in ordinal
+        // order (exclusive prefix); wen[o] = start, the end after (6)
         int base = 0;
-        for (int k0 = 0; k0 < K; k0 += 32) {
-            const int k = k0 + lane;
+        for (int o0 = 0; o0 < ecnt; o0 += 32) {
+            const int o = o0 + lane;
             int w = 0;
-            if (k < K) {
-                const uint32_t om = ordm[k];
-                w = (om & 0x8000u) ? (int)(om & 0x7FFFu) : ((cn[om] & 0x8000u) ? 0 : (int)cn[om]);
-                if (w < 2) w = 0;
-                else ordm[k] = (uint16_t)(om | 0x4000u);     // walked
+            if (o < ecnt) {
+                const uint32_t n = cn[o];
+                w = (n & 0x8000u) ? 0 : (int)n;
             }
             int incl = w;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-                if (lane >= o) incl += t;
+            for (int d = 1; d < 32; d <<= 1) {
+                const int t = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+                if (lane >= d) incl += t;
             }
-            if (k < K) off[k] = (uint16_t)(base + incl - w);
+            if (o < ecnt) wen[o] = (uint32_t)(base + incl - w);
             base += __shfl_sync(0xFFFFFFFFu, incl, 31);
         }
         const int Nw = base;
         __syncwarp();
-        // counting sort of the walked genes by label (order inside a cluster
-        // is free: sums are exact); afterwards off[s] is the END of cluster s
-        // and its start is off[s - 1] (0 for s = 0)
+        // (6) counting sort of the walked genes by ordinal (order inside a
+        // cluster is free: sums are exact)
+        if (Nw > 0) {
 #pragma unroll
-        for (int k = 0; k < 2 * SP_LREG; ++k) {
-            const int i = 64 * (k >> 1) + 2 * lane + (k & 1);
-            if (i >= N) continue;
-            const uint32_t s = (labr[k >> 1] >> (16 * (k & 1))) & 0xFFFFu;
-            if (ordm[s] & 0x4000u) {
-                const uint32_t sh = 16 * (s & 1u);
-                const uint32_t pos = (atomicAdd(offw + (s >> 1), 1u << sh) >> sh) & 0xFFFFu;
-                perm2[pos] = (uint32_t)i | (s << 16);
+            for (int k = 0; k < 2 * SP_LREG; ++k) {
+                const int i = 64 * (k >> 1) + 2 * lane + (k & 1);
+                if (i >= N) continue;
+                const uint32_t om = ordm[(labr[k >> 1] >> (16 * (k & 1))) & 0xFFFFu];
+                if (!(om & 0xC000u)) {
+                    const uint32_t o = om & 0x1FFFu;
+                    const uint32_t pos = atomicAdd(wen + o, 1u);
+                    perm2[pos] = (uint32_t)i | (o << 16);
+                }
             }
+            __syncwarp();
         }
-        __syncwarp();
-        // walk the sorted genes 32 at a time.  A lane's group is the window's
-        // lanes of its cluster (contiguous); the cluster open at the window's
-        // end carries on.  A completed large cluster stores its Eq. 8 term
-        // (and inserts it into the cache); a completed small one with c > n
-        // (Q2) is queued for its term.
-        int qcnt = 0;
-        unsigned long long npair = 0;
+        // (7) walk the sorted genes 32 at a time.  A lane's group is the
+        // window's lanes of its cluster (contiguous); the cluster open at the
+        // window's end carries on.  A completed cluster stores its c at its
+        // ordinal (ordm is dead: cval overlays it); its Eq. 8 term is taken
+        // lane-parallel in (8).
         long long carry = 0;
-        double fsum = 0.0, fbest = 0.0;
-        int kbest = 0x7FFFFFFF;
         for (int t0 = 0; t0 < Nw; t0 += 32) {
             const int t = t0 + lane;
-            int s = -1, st = t, en = t + 1, n = 0;
+            int o = -1, st = t, en = t + 1, n = 0;
             long long acc = 0;
             if (t < Nw) {
                 const uint32_t pg = perm2[t];
                 const int g = (int)(pg & 0xFFFFu);
-                s = (int)(pg >> 16);
-                en = (int)off[s];
-                st = s ? (int)off[s - 1] : 0;
-                n = en - st;
+                o = (int)(pg >> 16);
+                en = (int)wen[o];
+                n = (int)cn[o];
+                st = en - n;
                 const int av = t - st;
-                if (av == 0) npair += (unsigned long long)n * (n - 1) / 2;   // C pairs gathered, once per cluster
+                if (av == 0) npair += (uint32_t)(n * (n - 1) / 2);   // C pairs gathered, once per cluster
                 const double *Cg = C + (size_t)g * a.ldc;
                 acc = __double2ll_rn(__ldg(a.diag + g) * a.fx_scale);
                 const int h = (n - 1) >> 1;
@@ -947,83 +1017,36 @@ __global__ void __launch_bounds__(SP_T, PGA_SP_MINB) k_fitness_sparse(SparseArgs
             const int lo = max(st - t0, 0), hi = min(en - t0, 32);
             unsigned long long pre = (unsigned long long)acc;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const unsigned long long v = __shfl_up_sync(0xFFFFFFFFu, pre, o);
-                if (lane >= o) pre += v;
+            for (int d = 1; d < 32; d <<= 1) {
+                const unsigned long long v = __shfl_up_sync(0xFFFFFFFFu, pre, d);
+                if (lane >= d) pre += v;
             }
             const unsigned long long phi = __shfl_sync(0xFFFFFFFFu, pre, hi - 1);
             const unsigned long long plo = __shfl_sync(0xFFFFFFFFu, pre, lo > 0 ? lo - 1 : 0);
             long long tot = (long long)(phi - (lo > 0 ? plo : 0ull));
-            if (s >= 0 && st < t0) tot += carry;                 // continues from the last window
-            const int s31 = __shfl_sync(0xFFFFFFFFu, s, 31);
+            if (o >= 0 && st < t0) tot += carry;                 // continues from the last window
+            const int o31 = __shfl_sync(0xFFFFFFFFu, o, 31);
             const int en31 = __shfl_sync(0xFFFFFFFFu, en, 31);
             const long long tot31 = __shfl_sync(0xFFFFFFFFu, tot, 31);
-            carry = (s31 >= 0 && en31 > t0 + 32) ? tot31 : 0ll;
-            double c = 0.0;
-            bool push = false;
-            if (s >= 0 && lane == lo && en <= t0 + 32) {
-                c = (double)tot * a.fx_inv;
-                const uint32_t om = ordm[s] & 0xBFFFu;
-                if (om & 0x8000u) {
-                    push = c > (double)n;
-                } else {
-                    double f = 0.0;
-                    if (c > (double)n) {
-                        const double nd = (double)n, n2 = nd * nd;
-                        const double ch = fmin(c, n2 - 1e-9);
-                        f = (__ldg(a.lgn + n) - log(ch)) + (nd - 1.0) * (__ldg(a.lgnn + n) - log(n2 - ch));
-                    }
-                    if (use_cache) {
-                        const ulonglong2 e = cent[om];
-                        cc_insert(a.cc, a.cc_mask, a.cc_state, e.x, e.y, (uint32_t)n, __double_as_longlong(f));
-                    }
-                    cent[om].x = (unsigned long long)__double_as_longlong(f);
-                }
-            }
-            const unsigned bal = __ballot_sync(0xFFFFFFFFu, push);
-            if (push) {
-                const int pos = qcnt + __popc(bal & lanemask_lt());
-                qc[pos] = c;
-                qnk[pos] = (uint32_t)n | ((uint32_t)s << 16);
-            }
-            qcnt += __popc(bal);
-            __syncwarp();
-            if (qcnt >= 32) {            // a full batch of Eq. 8 summands, lane-parallel
-                const uint32_t nk = qnk[lane];
-                const int nn = (int)(nk & 0xFFFFu);
-                const double nd = (double)nn, n2 = nd * nd;
-                const double ch = fmin(qc[lane], n2 - 1e-9);
-                const double f = (__ldg(a.lgn + nn) - log(ch)) + (nd - 1.0) * (__ldg(a.lgnn + nn) - log(n2 - ch));
-                fsum += f;
-                if (f > fbest) {
-                    fbest = f;
-                    kbest = (int)(nk >> 16);
-                }
-                __syncwarp();
-                if (lane < qcnt - 32) {
-                    qc[lane] = qc[lane + 32];
-                    qnk[lane] = qnk[lane + 32];
-                }
-                qcnt -= 32;
-                __syncwarp();
-            }
-        }
-        if (lane < qcnt) {
-            const uint32_t nk = qnk[lane];
-            const int nn = (int)(nk & 0xFFFFu);
-            const double nd = (double)nn, n2 = nd * nd;
-            const double ch = fmin(qc[lane], n2 - 1e-9);
-            const double f = (__ldg(a.lgn + nn) - log(ch)) + (nd - 1.0) * (__ldg(a.lgnn + nn) - log(n2 - ch));
-            fsum += f;
-            if (f > fbest) {
-                fbest = f;
-                kbest = (int)(nk >> 16);
-            }
+            carry = (o31 >= 0 && en31 > t0 + 32) ? tot31 : 0ll;
+            if (o >= 0 && lane == lo && en <= t0 + 32) cval[o] = (double)tot * a.fx_inv;
         }
         __syncwarp();
-        // the large clusters' terms, in ordinal (= label) order per lane
+        // (8) the walk-class terms, in ordinal (= label) order per lane: a hit
+        // is the cached term; a walked cluster's term is computed here (and
+        // inserted into the cache when cacheable)
         for (int o = lane; o < ecnt; o += 32) {
-            const double f = __longlong_as_double((long long)cent[o].x);
+            const uint32_t nh = cn[o];
+            double f;
+            if (nh & 0x8000u) {
+                f = __longlong_as_double((long long)cent[o].x);
+            } else {
+                f = eq8_term((int)nh, cval[o], a.lgn, a.lgnn);
+                if (use_cache && nh >= (uint32_t)CC_NMIN) {
+                    const ulonglong2 e = cent[o];
+                    cc_insert(a.cc, a.cc_mask, a.cc_state, e.x, e.y, nh, __double_as_longlong(f));
+                }
+            }
             fsum += f;
             const int kl = (int)clab[o];
             if (f > fbest || (f == fbest && f > 0.0 && kl < kbest)) {
@@ -1049,9 +1072,9 @@ __global__ void __launch_bounds__(SP_T, PGA_SP_MINB) k_fitness_sparse(SparseArgs
                 nsaved += __shfl_xor_sync(0xFFFFFFFFu, nsaved, o);
             }
             if (lane == 0) {
-                atomicAdd(a.nsparse + 1, npair);
-                atomicAdd(a.nsparse + 2, nhit);
-                atomicAdd(a.nsparse + 3, nsaved);
+                atomicAdd(a.nsparse + 1, (unsigned long long)npair);
+                atomicAdd(a.nsparse + 2, (unsigned long long)nhit);
+                atomicAdd(a.nsparse + 3, (unsigned long long)nsaved);
             }
         }
         if (lane == 0) {
@@ -1060,6 +1083,19 @@ __global__ void __launch_bounds__(SP_T, PGA_SP_MINB) k_fitness_sparse(SparseArgs
         }
         __syncwarp();
     }
+}
+
+// Eq. 8 term of every pair cluster {i, j} (the label-sparse pass's n = 2
+// clusters): c = C_ii + C_jj + 2 C_ij in the pass's fixed point, then the
+// same eq8_term -- identical to what a walk of that pair would give.
+__global__ void k_pairtab(const double *__restrict__ C, int ldc, const double *__restrict__ diag, int N,
+                          double fx_scale, double fx_inv, const double *__restrict__ lgn,
+                          const double *__restrict__ lgnn, double *T) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y;
+    if (j >= N) return;
+    const long long acc = __double2ll_rn(diag[i] * fx_scale) + __double2ll_rn(diag[j] * fx_scale) +
+                          2 * __double2ll_rn(C[(size_t)i * ldc + j] * fx_scale);
+    T[(size_t)i * ldc + j] = (i == j) ? 0.0 : eq8_term(2, (double)acc * fx_inv, lgn, lgnn);
 }
 
 }  // namespace
@@ -1135,6 +1171,25 @@ int launch_logtab(pga_ctx *c, cudaStream_t s) {
     return PGA_OK;
 }
 
+// fold / label-sparse fixed point: S = 62 - ceil(log2(2 N^2 + 1)), so no
+// cluster sum of |C| <= 1 entries (|sum| <= 2 N^2) can overflow int64
+void fx_scale_of(int N, double *scale, double *inv) {
+    int bits = 0;
+    while ((1.0 * (1ull << bits)) < 2.0 * N * N + 1.0) ++bits;
+    *scale = ldexp(1.0, 62 - bits);
+    *inv = ldexp(1.0, bits - 62);
+}
+
+int launch_pairtab(pga_ctx *c, cudaStream_t s) {
+    if (!c->ptab) return PGA_OK;
+    double sc, inv;
+    fx_scale_of(c->N, &sc, &inv);
+    dim3 grid((unsigned)((c->N + 127) / 128), (unsigned)c->N);
+    k_pairtab<<<grid, 128, 0, s>>>(c->C, c->ldc, c->diag, c->N, sc, inv, c->lgtab, c->lgtab + (c->N + 1), c->ptab);
+    PGA_LAUNCHED();
+    return PGA_OK;
+}
+
 int fold_warps(int N) {
     const size_t per = 2 * (size_t)N * (sizeof(double) + sizeof(int32_t));   // NCF = 2 chromosomes per warp
     int w = (int)((size_t)(NSTAGE * STAGE_BYTES) / per);
@@ -1175,13 +1230,7 @@ int launch_fitness_range(pga_ctx *c, const FitBufs &b, int64_t begin, int64_t en
     a.cb0 = (int)(begin / CB);
     a.lgn = c->lgtab;
     a.lgnn = c->lgtab + (N + 1);
-    {
-        // S = 62 - ceil(log2(2 N^2 + 1)): |sum of V over a cluster| <= 2 N^2
-        int bits = 0;
-        while ((1.0 * (1ull << bits)) < 2.0 * N * N + 1.0) ++bits;
-        a.fx_scale = ldexp(1.0, 62 - bits);
-        a.fx_inv = ldexp(1.0, bits - 62);
-    }
+    fx_scale_of(N, &a.fx_scale, &a.fx_inv);   // |sum of V over a cluster| <= 2 N^2
     a.nCB = (int)((end - begin + CB - 1) / CB);
     a.fold_warps = fold_warps(N);
     a.P = P;
@@ -1199,7 +1248,7 @@ int launch_fitness_range(pga_ctx *c, const FitBufs &b, int64_t begin, int64_t en
     a.counters = c->counters;
     if (ev) PGA_CUDA(prof_record(ev[0], s));
     a.sflag = nullptr;
-    if (sparse_theta_eff(c) > 0.0 && N <= SPARSE_MAXN && c->sflag) {
+    if (sparse_theta_eff(c) > 0.0 && N <= SPARSE_MAXN && c->sflag && c->ptab) {
         // label-sparse pass first (f2); it flags the blocks it evaluated
         SparseArgs sp;
         sp.cm0 = b.cm0;
@@ -1228,17 +1277,17 @@ int launch_fitness_range(pga_ctx *c, const FitBufs &b, int64_t begin, int64_t en
         sp.fx_inv = a.fx_inv;
         sp.lgn = a.lgn;
         sp.lgnn = a.lgnn;
+        sp.ptab = c->ptab;
         sp.cc = c->cc_on ? c->cc : nullptr;
         sp.cc_mask = c->cc_mask;
         sp.cc_state = c->cc_state;
         sp.cc_keys = c->cc_keys;
-        k_fitness_sparse<<<(unsigned)a.nCB, SP_T, sparse_smem(N), s>>>(sp);
-        PGA_LAUNCHED();
+        PGA_LAUNCH_PDL(k_fitness_sparse, dim3((unsigned)a.nCB), dim3(SP_T), sparse_smem(N), s, sp);
         a.sflag = c->sflag;
     }
     if (ev) PGA_CUDA(prof_record(ev[1], s));   // dense kernel starts here
-    k_fitness<<<(unsigned)(a.nRT * a.nCB), FIT_THREADS, fitness_smem(N), s>>>(*b.tm0, *b.tm1, c->tmC, a);
-    PGA_LAUNCHED();
+    PGA_LAUNCH_PDL(k_fitness, dim3((unsigned)(a.nRT * a.nCB)), dim3(FIT_THREADS), fitness_smem(N), s, *b.tm0,
+                   *b.tm1, c->tmC, a);
     if (ev) PGA_CUDA(prof_record(ev[2], s));   // sweep and fold are one fused kernel
     return PGA_OK;
 }

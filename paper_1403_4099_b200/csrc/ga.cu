@@ -6,7 +6,7 @@
 // paper leaves open (readings Q7-Q21); the Philox stream layout makes every
 // operator bit-reproducible.
 #include <cuda_runtime.h>
-#include <cub/cub.cuh>
+#include <cub/block/block_radix_sort.cuh>
 
 #include "pga_internal.cuh"
 
@@ -161,6 +161,8 @@ k_stats(const double *__restrict__ L, int64_t P, const uint16_t *CM0, const uint
     __shared__ double sb[32], ss[32];
     __shared__ int si[32];
     __shared__ int s_improved, s_bi, s_last;
+    pdl_wait();
+    pdl_trigger();
     if (st->done) return;
     const int tid = threadIdx.x, lane = tid & 31;
     double best = -1.0, sum = 0.0;
@@ -238,30 +240,6 @@ k_stats(const double *__restrict__ L, int64_t P, const uint16_t *CM0, const uint
 // selection
 // ---------------------------------------------------------------------------
 
-// q_i = floor(2^B * w_i / w_max), w = 1/sqrt(rank) (RANK) or L (NONE)
-__global__ void k_weights(const double *__restrict__ L, const int32_t *__restrict__ order, int64_t P,
-                          int scaling, uint64_t *q, const int32_t *done) {
-    if (done && *done) return;
-    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= P) return;
-    const int i = order[r];
-    const int B = 62 - ceil_log2_d(P);
-    double w, wmax;
-    if (scaling == PGA_SCALE_RANK) {
-        w = 1.0 / sqrt((double)(r + 1));
-        wmax = 1.0;
-    } else {
-        w = L[i];
-        wmax = L[order[0]];
-    }
-    uint64_t qi = 0;
-    if (wmax > 0.0) {
-        const double x = w / wmax;
-        if (x > 0.0) qi = (uint64_t)floor(ldexp(x, B));
-    }
-    q[i] = qi;
-}
-
 // SUS (Q9) without a search: the M pointers start + m * step are sorted and
 // evenly spaced, so individual i (wheel segment [prefix[i-1], prefix[i])) owns
 // exactly the pointers m in [ceil((lo - start) / step), ceil((hi - start) /
@@ -272,30 +250,109 @@ __device__ __forceinline__ uint64_t sus_first(uint64_t x, uint64_t start, uint64
     return x <= start ? 0ull : (x - start + step - 1) / step;
 }
 
-__global__ void k_sus(const uint64_t *__restrict__ prefix, const double *__restrict__ L,
-                      const int32_t *__restrict__ order, int64_t P, int64_t M, int scaling,
-                      uint64_t seed, uint32_t gen, uint32_t island, int32_t *sel,
-                      const int32_t *done, const int32_t *gen_ptr, int32_t *sigma) {
+// ---------------------------------------------------------------------------
+// SUS for P > SMALL_GA_P without a library scan: two kernels over index
+// blocks of SCAN_T individuals.  k_qsum: q_i = floor(2^B w_i / w_max) in
+// index order (w from the rank the last merge level wrote, or from L) and
+// the block's sum.  k_sus2: the block's exclusive base (sum of the earlier
+// block sums) and the total Q from the block sums, an inclusive block scan
+// of q, and every individual's SUS pointer range (as k_sus), plus the mate
+// slots (Q10).  All integer (u64) arithmetic: the same prefix, bit for bit,
+// as any other summation order.
+// ---------------------------------------------------------------------------
+constexpr int SCAN_T = 1024;
+
+__device__ __forceinline__ uint64_t block_sum_u64(uint64_t v, uint64_t *ws) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, off);
+    __syncthreads();                      // ws may still be read from a previous call
+    if (lane == 0) ws[wid] = v;
+    __syncthreads();
+    uint64_t t = 0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += ws[k];
+    return t;
+}
+
+__global__ void __launch_bounds__(SCAN_T) k_qsum(const double *__restrict__ L, const int32_t *__restrict__ order,
+                                                 const int32_t *__restrict__ rank, int64_t P, int scaling,
+                                                 uint64_t *q, uint64_t *bsum, const int32_t *done) {
+    pdl_wait();
+    pdl_trigger();
     if (done && *done) return;
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= P && t >= M) return;
+    __shared__ uint64_t ws[SCAN_T / 32];
+    const int64_t i = (int64_t)blockIdx.x * SCAN_T + threadIdx.x;
+    uint64_t qi = 0;
+    if (i < P) {
+        const int B = 62 - ceil_log2_d(P);
+        double w, wmax;
+        if (scaling == PGA_SCALE_RANK) {
+            w = 1.0 / sqrt((double)(rank[i] + 1));
+            wmax = 1.0;
+        } else {
+            w = L[i];
+            wmax = L[order[0]];
+        }
+        if (wmax > 0.0) {
+            const double x = w / wmax;
+            if (x > 0.0) qi = (uint64_t)floor(ldexp(x, B));
+        }
+        q[i] = qi;
+    }
+    const uint64_t t = block_sum_u64(qi, ws);
+    if (threadIdx.x == 0) bsum[blockIdx.x] = t;
+}
+
+__global__ void __launch_bounds__(SCAN_T) k_sus2(const uint64_t *__restrict__ q, const uint64_t *__restrict__ bsum,
+                                                 int nbq, const double *__restrict__ L,
+                                                 const int32_t *__restrict__ order, int64_t P, int64_t M,
+                                                 int scaling, uint64_t seed, uint32_t gen, uint32_t island,
+                                                 int32_t *sel, const int32_t *done, const int32_t *gen_ptr,
+                                                 int32_t *sigma) {
+    pdl_wait();
+    pdl_trigger();
+    if (done && *done) return;
+    __shared__ uint64_t ws[SCAN_T / 32];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int64_t t = (int64_t)blockIdx.x * SCAN_T + tid;
     if (gen_ptr) gen = (uint32_t)*gen_ptr;
     if (sigma && t < M) sigma[t] = feistel_slot(t, M, seed, gen, island);   // mates fused (Q10)
     const double wmax = (scaling == PGA_SCALE_RANK) ? 1.0 : L[order[0]];
-    if (!(wmax > 0.0)) {  // all-zero fitness: uniform fallback
+    if (!(wmax > 0.0)) {   // all-zero fitness: uniform fallback; block-uniform
         if (t < M) {
             const U4 u = draw(seed, pga::TAG_SUS, island, gen, (uint32_t)t, 0u);
             sel[t] = (int32_t)scale_u32(u.x, (uint32_t)P);
         }
         return;
     }
+    // base of this block and the total Q from the block sums
+    uint64_t a = 0, b = 0;
+    for (int k = tid; k < nbq; k += SCAN_T) {
+        const uint64_t v = bsum[k];
+        b += v;
+        if (k < (int)blockIdx.x) a += v;
+    }
+    const uint64_t base = block_sum_u64(a, ws);
+    const uint64_t Q = block_sum_u64(b, ws);
+    // inclusive scan of q over the block
+    const uint64_t qi = t < P ? q[t] : 0ull;
+    uint64_t incl = qi;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint64_t o = __shfl_up_sync(0xFFFFFFFFu, incl, off);
+        if (lane >= off) incl += o;
+    }
+    __syncthreads();
+    if (lane == 31) ws[wid] = incl;
+    __syncthreads();
+    uint64_t wbase = 0;
+    for (int k = 0; k < wid; ++k) wbase += ws[k];
     if (t >= P) return;
-    const uint64_t Q = prefix[P - 1];
+    const uint64_t hi = base + wbase + incl, lo = hi - qi;
     const uint64_t step = Q / (uint64_t)M;
     const U4 u = draw(seed, pga::TAG_SUS, island, gen, 0u, 0xFFFFFFFFu);
     const uint64_t x = ((uint64_t)u.x << 32) | (uint64_t)u.y;
     const uint64_t start = __umul64hi(x, step);
-    const uint64_t lo = t ? prefix[t - 1] : 0ull, hi = prefix[t];
     const int64_t m0 = (int64_t)min(sus_first(lo, start, step), (uint64_t)M);
     const int64_t m1 = (int64_t)min(sus_first(hi, start, step), (uint64_t)M);
     for (int64_t m = m0; m < m1; ++m) sel[m] = (int32_t)t;
@@ -304,6 +361,8 @@ __global__ void k_sus(const uint64_t *__restrict__ prefix, const double *__restr
 __global__ void k_tournament(const double *__restrict__ L, int64_t P, int64_t M, int k,
                              uint64_t seed, uint32_t gen, uint32_t island, int32_t *sel,
                              const int32_t *done, const int32_t *gen_ptr, int32_t *sigma) {
+    pdl_wait();
+    pdl_trigger();
     if (done && *done) return;
     const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (m >= M) return;
@@ -345,6 +404,8 @@ __global__ void __launch_bounds__(SMALL_T)
 k_select_small(int what, const double *__restrict__ L, int P, int M, int selection, int tour_k, int scaling,
                uint64_t seed, uint32_t gen, uint32_t island, const int32_t *gen_ptr, int32_t *order,
                int32_t *sel, int32_t *sigma, const int32_t *done) {
+    pdl_wait();
+    pdl_trigger();
     if (done && *done) return;
     extern __shared__ __align__(16) unsigned char ssm[];
     using BRS0 = cub::BlockRadixSort<uint64_t, SMALL_T, SMALL_P / SMALL_T, uint32_t>;
@@ -525,6 +586,8 @@ constexpr int RUN = PGA_SORT_RUN, RUN_T = RUN / 2 < 1024 ? RUN / 2 : 1024;
 
 __global__ void __launch_bounds__(RUN_T)
 k_sort_runs(const double *__restrict__ L, int64_t P, uint64_t *keys, int32_t *idx, const int32_t *done) {
+    pdl_wait();
+    pdl_trigger();
     if (done && *done) return;
     __shared__ uint64_t sk[RUN];
     __shared__ uint32_t sv[RUN];
@@ -589,7 +652,10 @@ __device__ __forceinline__ bool key_before(uint64_t ka, uint32_t ia, uint64_t kb
 
 __global__ void __launch_bounds__(MERGE_T) k_merge_level(const uint64_t *__restrict__ ks,
                                                          const int32_t *__restrict__ is, int64_t P, int64_t w,
-                                                         uint64_t *kd, int32_t *id, const int32_t *done) {
+                                                         uint64_t *kd, int32_t *id, int32_t *rank_out,
+                                                         const int32_t *done) {
+    pdl_wait();
+    pdl_trigger();
     if (done && *done) return;
     __shared__ uint64_t sk[MERGE_CAP];
     __shared__ uint32_t si[MERGE_CAP];
@@ -657,6 +723,7 @@ __global__ void __launch_bounds__(MERGE_T) k_merge_level(const uint64_t *__restr
     const int64_t pos = blk + off + lo;
     if (kd) kd[pos] = ke;
     id[pos] = (int32_t)ie;
+    if (rank_out) rank_out[ie] = (int32_t)pos;   // last level: rank (0-based) of individual ie
 }
 
 static size_t select_small_smem() {
@@ -687,7 +754,24 @@ struct BreedArgs {
     uint32_t gen, island;
     const int32_t *done, *gen_ptr;
     const int32_t *gm_skip;            // != 0: the label-sparse pass owns the gene-major copy (f2)
+    pga::DevState *adv_st;             // GA: advance st->gen once the grid is done (null: hooks)
+    uint32_t *adv_ctr;                 // CTA counter for that (reset by the last CTA)
 };
+
+// The generation counter advances once the whole breed grid is done: the
+// last CTA to finish does it (every CTA read the generation at its start),
+// which replaces a separate one-thread k_advance launch.
+__device__ __forceinline__ void breed_advance(const BreedArgs &a) {
+    if (!a.adv_st) return;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(a.adv_ctr, 1u) == gridDim.x - 1) {
+            *a.adv_ctr = 0u;
+            if (!a.adv_st->done) a.adv_st->gen += 1;
+        }
+    }
+}
 
 
 __device__ __forceinline__ int parent_top(const BreedArgs &a, int64_t p) {
@@ -745,6 +829,8 @@ __device__ __forceinline__ ChildPlan plan_child(const BreedArgs &a, int64_t o, u
 
 template <bool HOOK>
 __global__ void __launch_bounds__(BW * 32, 3) k_breed(BreedArgs a) {
+    pdl_wait();
+    pdl_trigger();
     if (a.done && *a.done) return;
     extern __shared__ uint16_t sm16[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -847,6 +933,7 @@ __global__ void __launch_bounds__(BW * 32, 3) k_breed(BreedArgs a) {
             }
         }
     }
+    breed_advance(a);
 }
 
 // ---------------------------------------------------------------------------
@@ -885,6 +972,8 @@ static size_t breed2_smem(int N) {
 
 template <bool HOOK, int NB>
 __global__ void __launch_bounds__(BW * 32, NB <= 2 ? 3 : PGA_B2_MINB) k_breed2(BreedArgs a) {
+    pdl_wait();
+    pdl_trigger();
     if (a.done && *a.done) return;
     extern __shared__ __align__(16) unsigned char sm2[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1020,31 +1109,33 @@ __global__ void __launch_bounds__(BW * 32, NB <= 2 ? 3 : PGA_B2_MINB) k_breed2(B
                 }
             }
     }
-    if (!gm) return;   // sparse mode: k_fitness_sparse transposes dense blocks itself
-    __syncthreads();
-
-    // ---- phase 3: gene-major rows (BS children = 32 B per gene)
-    for (int e = threadIdx.x; e < N * (BS / 2); e += BW * 32) {
-        const int i = e / (BS / 2), pr = e - i * (BS / 2);
-        const int64_t oo = o0 + 2 * pr;
-        if (oo < a.P) {
-            const uint32_t two = *reinterpret_cast<const uint32_t *>(&tile[i * TS + 2 * pr]);
-            if (oo + 1 < a.P) *reinterpret_cast<uint32_t *>(&gm_out[(int64_t)i * a.Pcap + oo]) = two;
-            else gm_out[(int64_t)i * a.Pcap + oo] = (uint16_t)(two & 0xFFFF);
+    if (gm) {   // sparse mode: k_fitness_sparse transposes dense blocks itself
+        __syncthreads();
+        // ---- phase 3: gene-major rows (BS children = 32 B per gene)
+        for (int e = threadIdx.x; e < N * (BS / 2); e += BW * 32) {
+            const int i = e / (BS / 2), pr = e - i * (BS / 2);
+            const int64_t oo = o0 + 2 * pr;
+            if (oo < a.P) {
+                const uint32_t two = *reinterpret_cast<const uint32_t *>(&tile[i * TS + 2 * pr]);
+                if (oo + 1 < a.P) *reinterpret_cast<uint32_t *>(&gm_out[(int64_t)i * a.Pcap + oo]) = two;
+                else gm_out[(int64_t)i * a.Pcap + oo] = (uint16_t)(two & 0xFFFF);
+            }
         }
     }
+    breed_advance(a);
 }
 
 // one instantiation per chunk count NB = ceil(N / 128) (labels stay in registers)
 template <bool HOOK>
-static void launch_breed2(const BreedArgs &a, int64_t P, int N, cudaStream_t s) {
+static cudaError_t launch_breed2(const BreedArgs &a, int64_t P, int N, cudaStream_t s) {
     const unsigned grid = (unsigned)((P + BS - 1) / BS);
     const size_t sm = breed2_smem(N);
     switch ((N + GCH - 1) / GCH) {
-#define PGA_B2(nb) case nb: k_breed2<HOOK, nb><<<grid, BW * 32, sm, s>>>(a); break;
+#define PGA_B2(nb) case nb: return pga::launch_pdl(k_breed2<HOOK, nb>, dim3(grid), dim3(BW * 32), sm, s, a);
         PGA_B2(1) PGA_B2(2) PGA_B2(3) PGA_B2(4) PGA_B2(5) PGA_B2(6) PGA_B2(7) PGA_B2(8)
 #undef PGA_B2
     }
+    return cudaErrorInvalidValue;
 }
 
 template <bool HOOK>
@@ -1081,9 +1172,6 @@ __global__ void k_set_pop(const int32_t *__restrict__ lab, int64_t P, int N, int
     }
 }
 
-__global__ void k_advance(pga::DevState *st) {
-    if (!st->done) st->gen += 1;
-}
 
 // ---------------------------------------------------------------------------
 // migration (Q21).  Record: fp64 L | u16 top | u16 pad[3] | u16 labels[N],
@@ -1093,6 +1181,8 @@ __global__ void k_export(const double *__restrict__ L, const uint16_t *__restric
                          const int32_t *__restrict__ order, const uint16_t *CM0,
                          const uint16_t *CM1, const pga::DevState *st, int ldn, int N, int Em,
                          int64_t rec_bytes, unsigned char *out) {
+    pdl_wait();
+    pdl_trigger();
     const int r = blockIdx.x;
     if (r >= Em || st->done) return;   // stopped: the population is final (every island agrees, Q28)
     const uint16_t *CM = (st->gen & 1) ? CM1 : CM0;
@@ -1113,6 +1203,8 @@ __global__ void k_import(const unsigned char *__restrict__ in, int G, int Em, in
                          uint16_t *CM0, uint16_t *CM1, uint16_t *GM0, uint16_t *GM1,
                          const pga::DevState *st, int ldn, int N, int64_t Pcap) {
     __shared__ int chosen[256];
+    pdl_wait();
+    pdl_trigger();
     if (st->done) return;   // stopped: the population is final (every island agrees, Q28)
     const int total = G * Em;
     if (threadIdx.x == 0) {
@@ -1211,44 +1303,32 @@ int launch_stats(pga_ctx *c, int mode, cudaStream_t s) {
     int64_t g = (c->P + STATS_PER_CTA - 1) / STATS_PER_CTA;
     if (g > STATS_MAXG) g = STATS_MAXG;
     const int64_t per = (c->P + g - 1) / g;
-    k_stats<<<(unsigned)g, STATS_T, 0, s>>>(c->L, c->P, c->pop[0], c->pop[1], c->ldn, c->N, c->st,
-                                            c->best_labels, c->history, c->hist_cap, c->p.tol,
-                                            c->p.stall_gens, c->p.max_gens, mode, c->p.migrate_every,
-                                            c->stats_part, c->stats_ctr, per);
-    PGA_LAUNCHED();
+    PGA_LAUNCH_PDL(k_stats, dim3((unsigned)g), dim3(STATS_T), 0, s, (const double *)c->L, c->P,
+                   (const uint16_t *)c->pop[0], (const uint16_t *)c->pop[1], (int)c->ldn, (int)c->N, c->st,
+                   c->best_labels, c->history, (int)c->hist_cap, c->p.tol, (int)c->p.stall_gens,
+                   (int)c->p.max_gens, mode, (int)c->p.migrate_every, c->stats_part, c->stats_ctr, per);
     return PGA_OK;
 }
 
-size_t cub_tmp_needed(int64_t P) {
-    size_t a = 0, b = 0, d = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, a, (uint64_t *)nullptr, (uint64_t *)nullptr,
-                                    (int32_t *)nullptr, (int32_t *)nullptr, (int)P);
-    cub::DeviceScan::InclusiveSum(nullptr, b, (uint64_t *)nullptr, (uint64_t *)nullptr, (int)P);
-    cub::DeviceRadixSort::SortPairs(nullptr, d, (uint32_t *)nullptr, (uint32_t *)nullptr,
-                                    (int32_t *)nullptr, (int32_t *)nullptr, (int)(P + 1));
-    size_t m = a > b ? a : b;
-    return (m > d ? m : d) + 256;
-}
-
-// order = indices by (L desc, idx asc)
-static int sort_order(const double *L, int64_t P, int32_t *order, uint64_t *keys_in,
+// order = indices by (L desc, idx asc); rank[i] = position of individual i
+static int sort_order(const double *L, int64_t P, int32_t *order, int32_t *rank, uint64_t *keys_in,
                       uint64_t *keys_out, int32_t *idx_in, int32_t *idx_tmp, const int32_t *done,
                       cudaStream_t s) {
     const int nruns = (int)((P + RUN - 1) / RUN);
     uint64_t *kA = keys_out, *kB = keys_in;
     int32_t *iA = idx_in, *iB = idx_tmp;
-    k_sort_runs<<<nruns, RUN_T, 0, s>>>(L, P, kA, iA, done);
-    PGA_LAUNCHED();
+    PGA_LAUNCH_PDL(k_sort_runs, dim3(nruns), dim3(RUN_T), 0, s, L, P, kA, iA, done);
     const unsigned nb = (unsigned)((P + 255) / 256);
     if (nruns == 1) {   // one run: copy its indices out through a width-P "merge"
-        k_merge_level<<<nb, MERGE_T, 0, s>>>(kA, iA, P, P, nullptr, order, done);
-        PGA_LAUNCHED();
+        PGA_LAUNCH_PDL(k_merge_level, dim3(nb), dim3(MERGE_T), 0, s, (const uint64_t *)kA, (const int32_t *)iA,
+                       P, P, (uint64_t *)nullptr, order, rank, done);
         return PGA_OK;
     }
     for (int64_t w = RUN; w < P; w *= 2) {
         const bool last = 2 * w >= P;
-        k_merge_level<<<nb, MERGE_T, 0, s>>>(kA, iA, P, w, last ? nullptr : kB, last ? order : iB, done);
-        PGA_LAUNCHED();
+        PGA_LAUNCH_PDL(k_merge_level, dim3(nb), dim3(MERGE_T), 0, s, (const uint64_t *)kA, (const int32_t *)iA,
+                       P, w, last ? (uint64_t *)nullptr : kB, last ? order : iB, last ? rank : (int32_t *)nullptr,
+                       done);
         uint64_t *tk = kA;
         kA = kB;
         kB = tk;
@@ -1270,53 +1350,47 @@ int launch_select_small(int what, const double *L, int64_t P, const pga_params &
                         int32_t island, const int32_t *gen_ptr, int32_t *order, int32_t *sel,
                         int32_t *sigma, const int32_t *done, cudaStream_t s) {
     const int64_t M = 2 * ((P - p.elite + 1) / 2);
-    k_select_small<<<1, SMALL_T, select_small_smem(), s>>>(what, L, (int)P, (int)M, p.selection, p.tournament_k,
-                                                             p.scaling, p.seed, (uint32_t)gen, (uint32_t)island,
-                                                             gen_ptr, order, sel, sigma, done);
-    PGA_LAUNCHED();
+    PGA_LAUNCH_PDL(k_select_small, dim3(1), dim3(SMALL_T), select_small_smem(), s, what, L, (int)P, (int)M,
+                   (int)p.selection, (int)p.tournament_k, (int)p.scaling, p.seed, (uint32_t)gen, (uint32_t)island,
+                   gen_ptr, order, sel, sigma, done);
     return PGA_OK;
 }
 
+// Selection for P > SMALL_P (hooks) / P > SMALL_GA_P (GA): order (unless
+// `sorted`: the GA sorts in its own step), then tournament or SUS
+// (k_qsum + k_sus2) with the mate slots fused.  Scratch: rank (int32 [P]),
+// q (u64 [P]; also the sort's index double buffer), bsum (u64 [P / SCAN_T]).
 int run_select_ops(const double *L, int64_t P, const pga_params &p, int32_t gen, int32_t island,
                    int32_t *order, int32_t *sel, uint64_t *keys_in, uint64_t *keys_out,
-                   int32_t *idx_in, uint64_t *q, uint64_t *prefix, void *tmp, size_t tmp_bytes,
-                   const int32_t *done, cudaStream_t s, const int32_t *gen_ptr, bool sorted,
-                   int32_t *sigma) {
+                   int32_t *idx_in, int32_t *rank, uint64_t *q, uint64_t *bsum, const int32_t *done,
+                   cudaStream_t s, const int32_t *gen_ptr, bool sorted, int32_t *sigma) {
     const int64_t M = 2 * ((P - p.elite + 1) / 2);
-    const unsigned nb = (unsigned)((P + 255) / 256);
     if (!sorted && P <= SMALL_P)   // one CTA; mates go to scratch (q)
         return launch_select_small(3, L, P, p, gen, island, gen_ptr, order, sel,
                                    reinterpret_cast<int32_t *>(q), done, s);
     int rc;
     if (!sorted) {
-        rc = sort_order(L, P, order, keys_in, keys_out, idx_in, reinterpret_cast<int32_t *>(q), done, s);
+        rc = sort_order(L, P, order, rank, keys_in, keys_out, idx_in, reinterpret_cast<int32_t *>(q), done, s);
         if (rc) return rc;
     }
     if (p.selection == PGA_SEL_TOURNAMENT) {
-        k_tournament<<<(unsigned)((M + 255) / 256), 256, 0, s>>>(L, P, M, p.tournament_k, p.seed,
-                                                                (uint32_t)gen, (uint32_t)island,
-                                                                sel, done, gen_ptr, sigma);
-        PGA_LAUNCHED();
+        PGA_LAUNCH_PDL(k_tournament, dim3((unsigned)((M + 255) / 256)), dim3(256), 0, s, L, P, M,
+                       (int)p.tournament_k, p.seed, (uint32_t)gen, (uint32_t)island, sel, done, gen_ptr, sigma);
         return PGA_OK;
     }
-    k_weights<<<nb, 256, 0, s>>>(L, order, P, p.scaling, q, done);
-    PGA_LAUNCHED();
-    size_t tb = tmp_bytes;
-    PGA_CUDA(cub::DeviceScan::InclusiveSum(tmp, tb, q, prefix, (int)P, s));
-    count_launch();
-    k_sus<<<(unsigned)((max(P, M) + 255) / 256), 256, 0, s>>>(prefix, L, order, P, M, p.scaling, p.seed,
-                                                      (uint32_t)gen, (uint32_t)island, sel, done,
-                                                      gen_ptr, sigma);
-    PGA_LAUNCHED();
+    const int nbq = (int)((P + SCAN_T - 1) / SCAN_T);
+    PGA_LAUNCH_PDL(k_qsum, dim3(nbq), dim3(SCAN_T), 0, s, L, (const int32_t *)order, (const int32_t *)rank, P,
+                   (int)p.scaling, q, bsum, done);
+    const unsigned nbs = (unsigned)((max(P, M) + SCAN_T - 1) / SCAN_T);
+    PGA_LAUNCH_PDL(k_sus2, dim3(nbs), dim3(SCAN_T), 0, s, (const uint64_t *)q, (const uint64_t *)bsum, nbq, L,
+                   (const int32_t *)order, P, M, (int)p.scaling, p.seed, (uint32_t)gen, (uint32_t)island, sel,
+                   done, gen_ptr, sigma);
     return PGA_OK;
 }
 
-int run_mates(int64_t M, const pga_params &p, int32_t gen, int32_t island, uint32_t *k_in,
-              uint32_t *k_out, int32_t *m_in, int32_t *sigma, void *tmp, size_t tmp_bytes,
-              const int32_t *done, cudaStream_t s, const int32_t *gen_ptr) {
-    (void)k_in; (void)k_out; (void)m_in; (void)tmp; (void)tmp_bytes;
+int run_mates(int64_t M, const pga_params &p, int32_t gen, int32_t island, int32_t *sigma, cudaStream_t s) {
     k_mates<<<(unsigned)((M + 255) / 256), 256, 0, s>>>(M, p.seed, (uint32_t)gen, (uint32_t)island, sigma,
-                                                        done, gen_ptr);
+                                                        nullptr, nullptr);
     PGA_LAUNCHED();
     return PGA_OK;
 }
@@ -1354,9 +1428,9 @@ int launch_breed_hook(const int32_t *pop, const int32_t *top, const int32_t *ord
     a.island = (uint32_t)island;
     a.ldn = N;
     a.Pcap = P;
-    if (N <= BREED2_MAXN) launch_breed2<true>(a, P, N, s);
-    else k_breed<true><<<(unsigned)((P + BS - 1) / BS), BW * 32, breed_smem(N), s>>>(a);
-    PGA_LAUNCHED();
+    count_launch();
+    if (N <= BREED2_MAXN) PGA_CUDA(launch_breed2<true>(a, P, N, s));
+    else PGA_CUDA(launch_pdl(k_breed<true>, dim3((unsigned)((P + BS - 1) / BS)), dim3(BW * 32), breed_smem(N), s, a));
     return PGA_OK;
 }
 
@@ -1370,7 +1444,7 @@ int launch_sort_order(pga_ctx *c, cudaStream_t s) {
     if (small_select(c))
         return launch_select_small(1, c->L, c->P, c->p, 0, c->p.island, &c->st->gen, c->order, c->sel,
                                    c->sigma, &c->st->done, s);
-    return sort_order(c->L, c->P, c->order, c->keys_in, c->keys_out, c->idx_in,
+    return sort_order(c->L, c->P, c->order, c->rank, c->keys_in, c->keys_out, c->idx_in,
                       reinterpret_cast<int32_t *>(c->q), &c->st->done, s);
 }
 
@@ -1389,8 +1463,8 @@ int launch_select_breed(pga_ctx *c, cudaStream_t s) {
     } else {
         // selection with the Feistel mates fused into the same kernel
         rc = run_select_ops(c->L, c->P, p, 0, p.island, c->order, c->sel, c->keys_in, c->keys_out,
-                            c->idx_in, c->q, c->prefix, c->cub_tmp, c->cub_tmp_bytes, done, s,
-                            genp, true, c->sigma);
+                            c->idx_in, c->rank, c->q, c->keys_in /* free after the sort: block sums */,
+                            done, s, genp, true, c->sigma);
         if (rc) return rc;
         PGA_MARK(c, 5, s);
         PGA_MARK(c, 6, s);
@@ -1415,31 +1489,31 @@ int launch_select_breed(pga_ctx *c, cudaStream_t s) {
     // the gene-major copy is produced by the label-sparse pass while its
     // checks are live (it transposes exactly the blocks the dense sweep needs)
     a.gm_skip = (sparse_theta_eff(c) > 0.0 && c->N <= 640) ? c->sp_live : nullptr;
+    a.adv_st = c->st;           // the breed's last CTA advances the generation (no k_advance)
+    a.adv_ctr = c->breed_ctr;
+    count_launch();
     if (c->N <= BREED2_MAXN)
-        launch_breed2<false>(a, c->P, c->N, s);
+        PGA_CUDA(launch_breed2<false>(a, c->P, c->N, s));
     else
-        k_breed<false><<<(unsigned)((c->P + BS - 1) / BS), BW * 32, breed_smem(c->N), s>>>(a);
-    PGA_LAUNCHED();
+        PGA_CUDA(launch_pdl(k_breed<false>, dim3((unsigned)((c->P + BS - 1) / BS)), dim3(BW * 32),
+                            breed_smem(c->N), s, a));
     PGA_MARK(c, 7, s);
-    k_advance<<<1, 1, 0, s>>>(c->st);
-    PGA_LAUNCHED();
     return PGA_OK;
 }
 
 int launch_export(pga_ctx *c, void *dev_send, cudaStream_t s) {
-    k_export<<<c->p.migrants, 128, 0, s>>>(c->L, c->top, c->order, c->pop[0], c->pop[1], c->st,
-                                           c->ldn, c->N, c->p.migrants, c->mig_bytes / c->p.migrants,
-                                           (unsigned char *)dev_send);
-    PGA_LAUNCHED();
+    PGA_LAUNCH_PDL(k_export, dim3(c->p.migrants), dim3(128), 0, s, (const double *)c->L, (const uint16_t *)c->top,
+                   (const int32_t *)c->order, (const uint16_t *)c->pop[0], (const uint16_t *)c->pop[1],
+                   (const pga::DevState *)c->st, (int)c->ldn, (int)c->N, (int)c->p.migrants,
+                   (int64_t)(c->mig_bytes / c->p.migrants), (unsigned char *)dev_send);
     return PGA_OK;
 }
 
 int launch_import(pga_ctx *c, const void *dev_recv, int32_t G, cudaStream_t s) {
-    k_import<<<1, 256, 0, s>>>((const unsigned char *)dev_recv, G, c->p.migrants,
-                               c->mig_bytes / c->p.migrants, c->order, c->P, c->L, c->top,
-                               c->pop[0], c->pop[1], c->popT[0], c->popT[1], c->st, c->ldn, c->N,
-                               c->Pcap);
-    PGA_LAUNCHED();
+    PGA_LAUNCH_PDL(k_import, dim3(1), dim3(256), 0, s, (const unsigned char *)dev_recv, (int)G, (int)c->p.migrants,
+                   (int64_t)(c->mig_bytes / c->p.migrants), (const int32_t *)c->order, c->P, c->L, c->top,
+                   c->pop[0], c->pop[1], c->popT[0], c->popT[1], (const pga::DevState *)c->st, (int)c->ldn,
+                   (int)c->N, c->Pcap);
     return PGA_OK;
 }
 

@@ -38,6 +38,40 @@ int ensure_device(int dev);                  // api.cu: device present, made cur
         if ((c)->pev && (c)->prof_level >= 2) PGA_CUDA(::pga::prof_record((c)->pev[k], (s))); \
     } while (0)
 
+// Programmatic dependent launch (PDL): kernels of the generation sequence
+// are launched with cudaLaunchAttributeProgrammaticStreamSerialization, so a
+// kernel's launch and CTA rasterisation overlap the tail of the one before.
+// Every such kernel calls pdl_wait() (griddepcontrol.wait: blocks until the
+// preceding grid has completed and its memory is visible) before touching
+// global memory, then pdl_trigger() (griddepcontrol.launch_dependents) so
+// the next kernel may be scheduled.  Both are no-ops when the kernel was
+// launched without the attribute.  PGA_PDL=0 in the environment disables
+// the attribute (A/B measurement).
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
+
+#define PGA_LAUNCH_PDL(...)                                                \
+    do {                                                                   \
+        ::pga::count_launch();                                             \
+        cudaError_t _e = ::pga::launch_pdl(__VA_ARGS__);                   \
+        if (_e != cudaSuccess) return ::pga::cuda_fail(_e, "kernel launch");\
+    } while (0)
+
 #define PGA_LAUNCHED()                                                     \
     do {                                                                   \
         ::pga::count_launch();                                             \
@@ -122,6 +156,7 @@ struct pga_ctx {
     uint32_t cc_mask = 0;          // slots - 1
     uint32_t *cc_state = nullptr;  // device [4]: fill, clear request, CTA count
     uint64_t *cc_keys = nullptr;   // device [N][2] Zobrist keys
+    double *ptab = nullptr;        // [N][ldc] Eq. 8 term of each pair cluster (label-sparse pass, N <= 640)
     bool cc_on = true;
     // population: chromosome-major [Pcap][ldn] and gene-major [N][Pcap], double buffered
     uint16_t *pop[2] = {nullptr, nullptr};
@@ -131,14 +166,13 @@ struct pga_ctx {
     double *L = nullptr;   // [Pcap]
     uint16_t *top = nullptr;
     // selection scratch
-    uint64_t *keys_in = nullptr, *keys_out = nullptr;
+    uint64_t *keys_in = nullptr, *keys_out = nullptr;   // sort keys (double buffer); block sums after the sort
     int32_t *idx_in = nullptr, *order = nullptr;
-    uint64_t *q = nullptr, *prefix = nullptr;
+    int32_t *rank = nullptr;           // rank[i] = position of individual i in order (last merge level)
+    uint64_t *q = nullptr;             // SUS segment widths (index order); the sort's index buffer before
     int32_t *sel = nullptr;
-    uint32_t *mkeys_in = nullptr, *mkeys_out = nullptr;
-    int32_t *m_in = nullptr, *sigma = nullptr;
-    void *cub_tmp = nullptr;
-    size_t cub_tmp_bytes = 0;
+    int32_t *sigma = nullptr;
+    uint32_t *breed_ctr = nullptr;     // breed CTA counter (the last CTA advances the generation)
     // state
     pga::DevState *st = nullptr;
     uint16_t *best_labels = nullptr;   // [ldn]
@@ -197,6 +231,7 @@ int launch_pack(pga_ctx *c, const uint16_t *lab16, const int32_t *lab32, int64_t
                 uint16_t *CM, uint16_t *GM, cudaStream_t s);
 int prepare_fitness(int N);
 int launch_logtab(pga_ctx *c, cudaStream_t s);
+int launch_pairtab(pga_ctx *c, cudaStream_t s);   // after launch_logtab
 // ev (optional): 3 events recorded before the sweep, between sweep and
 // fold, and after the fold.
 int launch_fitness(pga_ctx *c, const FitBufs &b, int64_t P, double *L, uint16_t *top,
@@ -213,7 +248,6 @@ int launch_canonicalize_i32(int32_t *lab, int64_t P, int32_t N, cudaStream_t s);
 int launch_corr(const double *X, int32_t T, int32_t N, double *C, int32_t *status,
                 cudaStream_t s);
 
-size_t cub_tmp_needed(int64_t P);
 
 }  // namespace pga
 
@@ -221,6 +255,9 @@ size_t cub_tmp_needed(int64_t P);
 // Device helpers
 // ---------------------------------------------------------------------------
 namespace pgad {
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // Philox4x32-10 (Salmon et al. SC'11), the product's own implementation.
 struct U4 {
