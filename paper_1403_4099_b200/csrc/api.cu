@@ -156,6 +156,9 @@ void free_ctx(pga_ctx *c) {
     if (c->h_st) cudaFreeHost(c->h_st);
     for (cudaEvent_t e : c->prof_ev) cudaEventDestroy(e);
     if (c->join_ev) cudaEventDestroy(c->join_ev);
+    if (c->fork_ev) cudaEventDestroy(c->fork_ev);
+    if (c->join_side_ev) cudaEventDestroy(c->join_side_ev);
+    if (c->side) cudaStreamDestroy(c->side);
     if (c->stream) cudaStreamDestroy(c->stream);
 }
 
@@ -238,6 +241,7 @@ cudaEvent_t *prof_slot(pga_ctx *c) {
 // 7 breed end, 8 generation end.
 int phase_a(pga_ctx *c, int32_t g, int32_t *is_mig) {
     c->pev = prof_slot(c);
+    TRY(launch_mates_fork(c, c->stream));   // mate slots beside the fitness pass
     TRY(launch_fitness(c, ga_bufs(c), c->P, c->L, c->top, c->stream, c->pev));
     const bool mig = is_migration_gen(c, g);
     if (is_mig) *is_mig = mig ? 1 : 0;
@@ -247,6 +251,7 @@ int phase_a(pga_ctx *c, int32_t g, int32_t *is_mig) {
     } else {
         TRY(launch_stats(c, c->p.n_islands > 1 ? 1 : 0, c->stream));
     }
+    TRY(launch_mates_join(c, c->stream));
     PGA_MARK(c, 3, c->stream);
     return PGA_OK;
 }
@@ -418,6 +423,9 @@ int pga_create(const double *C, int32_t N, const pga_params *p, pga_ctx **out) {
     cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) return bail(cuda_fail(e, "cudaStreamCreate"));
     e = cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->join_side_ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
     if (e != cudaSuccess) return bail(cuda_fail(e, "cudaEventCreate"));
     const size_t cm = (size_t)c->Pcap * c->ldn, gm = (size_t)N * c->Pcap;
     int rc = 0;
@@ -656,7 +664,9 @@ int pga_rep_commit(pga_ctx *c, const double *L_dev, const uint16_t *top_dev) {
     PGA_CUDA(cudaSetDevice(c->device));
     PGA_CUDA(cudaMemcpyAsync(c->L, L_dev, sizeof(double) * c->P, cudaMemcpyDeviceToDevice, c->stream));
     PGA_CUDA(cudaMemcpyAsync(c->top, top_dev, sizeof(uint16_t) * c->P, cudaMemcpyDeviceToDevice, c->stream));
+    TRY(launch_mates_fork(c, c->stream));   // mate slots of this generation (phase_a does it on the GA path)
     TRY(launch_stats(c, 0, c->stream));
+    TRY(launch_mates_join(c, c->stream));
     PGA_MARK(c, 3, c->stream);
     return PGA_OK;
 }

@@ -6,6 +6,8 @@
 // paper leaves open (readings Q7-Q21); the Philox stream layout makes every
 // operator bit-reproducible.
 #include <cuda_runtime.h>
+#include <cooperative_groups.h>
+#include <cstdlib>
 #include <cub/block/block_radix_sort.cuh>
 
 #include "pga_internal.cuh"
@@ -726,6 +728,245 @@ __global__ void __launch_bounds__(MERGE_T) k_merge_level(const uint64_t *__restr
     if (rank_out) rank_out[ie] = (int32_t)pos;   // last level: rank (0-based) of individual ie
 }
 
+// ---------------------------------------------------------------------------
+// k_select_cluster (SMALL_GA_P < P <= CSEL_MAXP): isolate fittest, scaling
+// and selection of one island in ONE launch of a 16-CTA thread-block cluster
+// (distributed shared memory) -- what the multi-kernel path does with a run
+// sort, a merge tree, q sums and a scan (five or more latency-bound launches
+// at these sizes).  The mate slots are computed off the critical path (a
+// parallel graph branch, launch_mates_side).
+//   1. CTA c holds individuals [c R, (c + 1) R) (R a power of two <= CSEL_T,
+//      one per thread) and sorts them by (key = ~bits(L), index): a bitonic
+//      network, strides < 32 by warp shuffles, larger ones in shared memory.
+//   2. Global rank = local position + the number of items of every other
+//      run before it: the other runs are copied in (DSMEM, 16-byte vectors)
+//      and searched locally, all runs in lockstep (branch-free bisection).
+//   3. order[rank] = index, rank[index] = rank (global memory).
+//   4. SUS: q_i in index order from the rank (RANK) or L (NONE), a block
+//      scan, the CTA's base from the other CTAs' totals (DSMEM), pointer
+//      ranges per individual; or tournament.
+// The same integers as the multi-kernel path (bit-exact).
+// ---------------------------------------------------------------------------
+constexpr int CSEL_T = 512, CSEL_CL = 16, CSEL_MAXR = CSEL_T;
+constexpr int CSEL_MAXP = CSEL_CL * CSEL_MAXR;
+
+__host__ __device__ __forceinline__ int csel_run(int P) {
+    int r = 64;
+    while (r * CSEL_CL < P) r <<= 1;
+    return r;
+}
+
+static size_t csel_smem(int R) {
+    // own run: sk sL sx si srank; copies of the other runs' keys and indices
+    return (size_t)R * (8 + 8 + 8 + 4 + 4) + (size_t)(CSEL_CL - 1) * R * 12 + 256;
+}
+
+__device__ __forceinline__ void cs_exchange(uint64_t &k, uint32_t &v, int partner_lane_xor, bool keep_min) {
+    const uint64_t ok = __shfl_xor_sync(0xFFFFFFFFu, k, partner_lane_xor);
+    const uint32_t ov = __shfl_xor_sync(0xFFFFFFFFu, v, partner_lane_xor);
+    const bool other_less = kv_less(ok, ov, k, v);
+    if (other_less == keep_min) {
+        k = ok;
+        v = ov;
+    }
+}
+
+__global__ void __launch_bounds__(CSEL_T, 2)
+k_select_cluster(int what, const double *__restrict__ L, int P, int R, int M, int selection, int tour_k,
+                 int scaling, uint64_t seed, uint32_t gen, uint32_t island, const int32_t *gen_ptr,
+                 int32_t *order, int32_t *rank_out, int32_t *sel, const int32_t *done) {
+    namespace cg = cooperative_groups;
+    pdl_wait();
+    pdl_trigger();
+    if (done && *done) return;                     // grid-uniform
+    cg::cluster_group cl = cg::this_cluster();
+    const int c = (int)cl.block_rank();
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    extern __shared__ __align__(16) unsigned char csm[];
+    uint64_t *sk = reinterpret_cast<uint64_t *>(csm);          // [R] sorted keys
+    double *sL = reinterpret_cast<double *>(sk + R);           // [R] L by local index
+    uint64_t *sx = reinterpret_cast<uint64_t *>(sL + R);       // [R] exchange buffer (sort)
+    uint64_t *ok_ = sx + R;                                     // [(CL-1) R] other runs' keys
+    uint32_t *si = reinterpret_cast<uint32_t *>(ok_ + (CSEL_CL - 1) * R);   // [R] sorted indices
+    int32_t *srank = reinterpret_cast<int32_t *>(si + R);     // [R] global rank by local index
+    uint32_t *oi_ = reinterpret_cast<uint32_t *>(srank + R);  // [(CL-1) R] other runs' indices
+    __shared__ uint64_t ws[CSEL_T / 32];
+    __shared__ uint64_t s_tot, s_first_key;
+    __shared__ uint32_t s_first_idx;
+    if (gen_ptr) gen = (uint32_t)*gen_ptr;
+    const int base = c * R;
+    const bool act = tid < R;
+
+    // (1) load and sort the run: thread t holds position t
+    uint64_t k = ~0ull;
+    uint32_t v = 0xFFFFFFFFu;
+    if (act) {
+        const int i = base + tid;
+        double x = 0.0;
+        if (i < P) {
+            x = L[i];
+            if (x == 0.0) x = 0.0;
+            k = ~(uint64_t)__double_as_longlong(x);
+            v = (uint32_t)i;
+        }
+        sL[tid] = x;
+    }
+    for (int size = 2; size <= R; size <<= 1) {
+        const bool up = (tid & size) == 0;
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            const bool lower = (tid & stride) == 0;    // this thread holds the lower position
+            if (stride < 32) {
+                if (act) cs_exchange(k, v, stride, lower == up);
+                else { __shfl_xor_sync(0xFFFFFFFFu, k, stride); __shfl_xor_sync(0xFFFFFFFFu, v, stride); }
+            } else {
+                __syncthreads();
+                if (act) {
+                    sx[tid] = k;
+                    si[tid] = v;
+                }
+                __syncthreads();
+                if (act) {
+                    const uint64_t ok = sx[tid ^ stride];
+                    const uint32_t ov = si[tid ^ stride];
+                    if (kv_less(ok, ov, k, v) == (lower == up)) {
+                        k = ok;
+                        v = ov;
+                    }
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (act) {
+        sk[tid] = k;
+        si[tid] = v;
+    }
+    if (tid == 0) {
+        s_first_key = k;
+        s_first_idx = v;
+    }
+    cl.sync();                                     // every run sorted and visible
+
+    // (2) global ranks: copy the other runs (DSMEM, 16-byte vectors), then
+    // search all of them locally, in lockstep
+    {
+        const int nv = R / 2;                      // 16-byte vectors of keys per run
+        for (int j = tid; j < (CSEL_CL - 1) * nv; j += CSEL_T) {
+            const int r = j / nv, cr = r < c ? r : r + 1, q = j - r * nv;
+            reinterpret_cast<ulonglong2 *>(ok_ + r * R)[q] =
+                reinterpret_cast<const ulonglong2 *>(cl.map_shared_rank(sk, cr))[q];
+        }
+        const int nw = R / 4;                      // 16-byte vectors of indices per run
+        for (int j = tid; j < (CSEL_CL - 1) * nw; j += CSEL_T) {
+            const int r = j / nw, cr = r < c ? r : r + 1, q = j - r * nw;
+            reinterpret_cast<uint4 *>(oi_ + r * R)[q] = reinterpret_cast<const uint4 *>(cl.map_shared_rank(si, cr))[q];
+        }
+    }
+    __syncthreads();
+    if (act && v != 0xFFFFFFFFu) {                 // padding sorts last
+        int lo[CSEL_CL - 1];
+#pragma unroll
+        for (int r = 0; r < CSEL_CL - 1; ++r) lo[r] = 0;
+        // branch-free binary search for the first position not before (k, v)
+        for (int half = R >> 1; half > 0; half >>= 1) {
+#pragma unroll
+            for (int r = 0; r < CSEL_CL - 1; ++r) {
+                const int m = lo[r] + half - 1;
+                if (kv_less(ok_[r * R + m], oi_[r * R + m], k, v)) lo[r] += half;
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < CSEL_CL - 1; ++r)      // the last position (R - 1)
+            if (lo[r] == R - 1 && kv_less(ok_[r * R + R - 1], oi_[r * R + R - 1], k, v)) lo[r] = R;
+        int rank = tid;
+#pragma unroll
+        for (int r = 0; r < CSEL_CL - 1; ++r) rank += lo[r];
+        if (what & 1) order[rank] = (int32_t)v;
+        if (rank_out) rank_out[v] = rank;
+        srank[v - base] = rank;
+    }
+    __syncthreads();
+    if (!(what & 2)) {
+        cl.sync();                                 // no CTA leaves while others read its runs
+        return;
+    }
+
+    // (4) selection
+    if (selection == PGA_SEL_TOURNAMENT) {
+        for (int m = c * CSEL_T + tid; m < M; m += CSEL_CL * CSEL_T) {
+            const U4 u = draw(seed, pga::TAG_TOUR, island, gen, (uint32_t)m, 0u);
+            int best = (int)scale_u32(u.x, (uint32_t)P);
+            for (int t = 1; t < tour_k; ++t) {
+                const int cc = (int)scale_u32(word(u, t), (uint32_t)P);
+                if (L[cc] > L[best] || (L[cc] == L[best] && cc < best)) best = cc;
+            }
+            sel[m] = best;
+        }
+        cl.sync();
+        return;
+    }
+    // w_max: the globally first item (smallest key, then index) of the runs
+    double wmax = 1.0;
+    if (scaling != PGA_SCALE_RANK) {
+        uint64_t bk = ~0ull;
+        uint32_t bi = 0xFFFFFFFFu;
+        for (int r = 0; r < CSEL_CL; ++r) {
+            const uint64_t k_ = *cl.map_shared_rank(&s_first_key, r);
+            const uint32_t i_ = *cl.map_shared_rank(&s_first_idx, r);
+            if (kv_less(k_, i_, bk, bi)) {
+                bk = k_;
+                bi = i_;
+            }
+        }
+        wmax = L[bi];
+        if (wmax == 0.0) wmax = 0.0;
+    }
+    if (!(wmax > 0.0)) {                           // all-zero fitness: uniform fallback
+        for (int m = c * CSEL_T + tid; m < M; m += CSEL_CL * CSEL_T) {
+            const U4 u = draw(seed, pga::TAG_SUS, island, gen, (uint32_t)m, 0u);
+            sel[m] = (int32_t)scale_u32(u.x, (uint32_t)P);
+        }
+        cl.sync();
+        return;
+    }
+    const int B = 62 - ceil_log2_d(P);
+    uint64_t qi = 0;
+    if (act && base + tid < P) {
+        const double w = (scaling == PGA_SCALE_RANK) ? 1.0 / sqrt((double)(srank[tid] + 1)) : sL[tid];
+        const double x = w / wmax;
+        if (x > 0.0) qi = (uint64_t)floor(ldexp(x, B));
+    }
+    uint64_t incl = qi;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint64_t o = __shfl_up_sync(0xFFFFFFFFu, incl, off);
+        if (lane >= off) incl += o;
+    }
+    if (lane == 31) ws[wid] = incl;
+    __syncthreads();
+    uint64_t wbase = 0;
+    for (int kk = 0; kk < wid; ++kk) wbase += ws[kk];
+    if (tid == CSEL_T - 1) s_tot = wbase + incl;   // the CTA's total
+    cl.sync();                                     // totals visible
+    uint64_t cbase = 0, Q = 0;
+    for (int r = 0; r < CSEL_CL; ++r) {
+        const uint64_t t_ = *cl.map_shared_rank(&s_tot, r);
+        Q += t_;
+        if (r < c) cbase += t_;
+    }
+    if (act && base + tid < P) {
+        const uint64_t step = Q / (uint64_t)M;
+        const U4 u = draw(seed, pga::TAG_SUS, island, gen, 0u, 0xFFFFFFFFu);
+        const uint64_t x = ((uint64_t)u.x << 32) | (uint64_t)u.y;
+        const uint64_t start = __umul64hi(x, step);
+        const uint64_t hi = cbase + wbase + incl, lo = hi - qi;
+        const int64_t m0 = (int64_t)min(sus_first(lo, start, step), (uint64_t)M);
+        const int64_t m1 = (int64_t)min(sus_first(hi, start, step), (uint64_t)M);
+        for (int64_t m = m0; m < m1; ++m) sel[m] = base + tid;
+    }
+    cl.sync();                                     // no CTA leaves while others read its totals
+}
+
 static size_t select_small_smem() {
     using BRS = cub::BlockRadixSort<uint64_t, SMALL_T, SMALL_P / SMALL_T, uint32_t>;
     const size_t a = (size_t)SMALL_P * 8 > sizeof(typename BRS::TempStorage) ? (size_t)SMALL_P * 8
@@ -1250,6 +1491,14 @@ __global__ void k_import(const unsigned char *__restrict__ in, int G, int Em, in
 
 namespace pga {
 
+// A/B switches for measurement: getenv_flag(name, d) is d unless the variable
+// is set (then true for "1", false for "0").
+static bool getenv_flag(const char *name, bool d) {
+    const char *e = std::getenv(name);
+    if (!e || !e[0]) return d;
+    return e[0] != '0';
+}
+
 static size_t breed_smem(int N) { return ((size_t)2 * GCH * TS + (size_t)BS * breed_tab(N)) * sizeof(uint16_t); }
 
 static int breed_warps(int N) {
@@ -1342,6 +1591,37 @@ static int sort_order(const double *L, int64_t P, int32_t *order, int32_t *rank,
 int prepare_select_small() {
     PGA_CUDA(cudaFuncSetAttribute(k_select_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)select_small_smem()));
+    PGA_CUDA(cudaFuncSetAttribute(k_select_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)csel_smem(CSEL_MAXR)));
+    PGA_CUDA(cudaFuncSetAttribute(k_select_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    return PGA_OK;
+}
+
+// order/rank (what & 1) and/or selection + mates (what & 2) in one cluster
+// launch, SMALL_GA_P < P <= CSEL_MAXP
+static int launch_select_cluster(int what, const double *L, int64_t P, const pga_params &p,
+                                 const int32_t *gen_ptr, int32_t *order, int32_t *rank, int32_t *sel,
+                                 const int32_t *done, cudaStream_t s) {
+    const int64_t M = 2 * ((P - p.elite + 1) / 2);
+    const int R = csel_run((int)P);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CSEL_CL);
+    cfg.blockDim = dim3(CSEL_T);
+    cfg.dynamicSmemBytes = csel_smem(R);
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CSEL_CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    count_launch();
+    PGA_CUDA(cudaLaunchKernelEx(&cfg, k_select_cluster, what, L, (int)P, R, (int)M, (int)p.selection,
+                                (int)p.tournament_k, (int)p.scaling, p.seed, (uint32_t)0, (uint32_t)p.island,
+                                gen_ptr, order, rank, sel, done));
     return PGA_OK;
 }
 
@@ -1438,12 +1718,19 @@ int launch_breed_hook(const int32_t *pop, const int32_t *top, const int32_t *ord
 // path (run sort + merge tree, weights, scan, SUS, mates) is faster than the
 // single-CTA block radix sort (pga_op_select still uses it up to SMALL_P)
 constexpr int SMALL_GA_P = 1024;
-bool small_select(const pga_ctx *c) { return c->P <= SMALL_GA_P; }
+// order fused into the selection launch (one CTA up to SMALL_GA_P, one
+// cluster up to CSEL_MAXP); above, the run sort + merge tree is its own step
+bool small_select(const pga_ctx *c) {
+    return c->P <= SMALL_GA_P || (c->P <= CSEL_MAXP && !getenv_flag("PGA_NO_CSEL", false));
+}
 
 int launch_sort_order(pga_ctx *c, cudaStream_t s) {
-    if (small_select(c))
+    if (c->P <= SMALL_GA_P)
         return launch_select_small(1, c->L, c->P, c->p, 0, c->p.island, &c->st->gen, c->order, c->sel,
                                    c->sigma, &c->st->done, s);
+    if (small_select(c))
+        return launch_select_cluster(1, c->L, c->P, c->p, &c->st->gen, c->order, c->rank, c->sel,
+                                     &c->st->done, s);
     return sort_order(c->L, c->P, c->order, c->rank, c->keys_in, c->keys_out, c->idx_in,
                       reinterpret_cast<int32_t *>(c->q), &c->st->done, s);
 }
@@ -1454,17 +1741,23 @@ int launch_select_breed(pga_ctx *c, cudaStream_t s) {
     const int32_t *done = &c->st->done;
     const int32_t *genp = &c->st->gen;
     int rc;
-    if (small_select(c)) {
+    if (c->P <= SMALL_GA_P) {
         // one CTA: order + scaling + selection + mates
         rc = launch_select_small(3, c->L, c->P, p, 0, p.island, genp, c->order, c->sel, c->sigma, done, s);
         if (rc) return rc;
         PGA_MARK(c, 5, s);
         PGA_MARK(c, 6, s);
+    } else if (small_select(c)) {
+        // one cluster: order + scaling + selection + mates
+        rc = launch_select_cluster(3, c->L, c->P, p, genp, c->order, c->rank, c->sel, done, s);
+        if (rc) return rc;
+        PGA_MARK(c, 5, s);
+        PGA_MARK(c, 6, s);
     } else {
-        // selection with the Feistel mates fused into the same kernel
+        // selection (the mate slots come from the side branch, launch_mates_side)
         rc = run_select_ops(c->L, c->P, p, 0, p.island, c->order, c->sel, c->keys_in, c->keys_out,
                             c->idx_in, c->rank, c->q, c->keys_in /* free after the sort: block sums */,
-                            done, s, genp, true, c->sigma);
+                            done, s, genp, true, nullptr);
         if (rc) return rc;
         PGA_MARK(c, 5, s);
         PGA_MARK(c, 6, s);
@@ -1498,6 +1791,29 @@ int launch_select_breed(pga_ctx *c, cudaStream_t s) {
         PGA_CUDA(launch_pdl(k_breed<false>, dim3((unsigned)((c->P + BS - 1) / BS)), dim3(BW * 32),
                             breed_smem(c->N), s, a));
     PGA_MARK(c, 7, s);
+    return PGA_OK;
+}
+
+// Mate slots (Q10) depend only on (seed, generation, island): for P >
+// SMALL_GA_P they are computed on a side stream forked at the start of a
+// generation's evaluation and joined at its end, so the Feistel permutation
+// runs beside the fitness pass instead of on the selection's critical path.
+// (P <= SMALL_GA_P: k_select_small computes them itself.)
+int launch_mates_fork(pga_ctx *c, cudaStream_t s) {
+    if (c->P <= SMALL_GA_P) return PGA_OK;
+    const int64_t M = 2 * ((c->P - c->p.elite + 1) / 2);
+    PGA_CUDA(cudaEventRecord(c->fork_ev, s));
+    PGA_CUDA(cudaStreamWaitEvent(c->side, c->fork_ev, 0));
+    k_mates<<<(unsigned)((M + 255) / 256), 256, 0, c->side>>>(M, c->p.seed, 0u, (uint32_t)c->p.island, c->sigma,
+                                                               &c->st->done, &c->st->gen);
+    PGA_LAUNCHED();
+    PGA_CUDA(cudaEventRecord(c->join_side_ev, c->side));
+    return PGA_OK;
+}
+
+int launch_mates_join(pga_ctx *c, cudaStream_t s) {
+    if (c->P <= SMALL_GA_P) return PGA_OK;
+    PGA_CUDA(cudaStreamWaitEvent(s, c->join_side_ev, 0));
     return PGA_OK;
 }
 

@@ -133,6 +133,8 @@ struct pga_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
     cudaEvent_t join_ev = nullptr;   // joins a caller's stream to `stream` (pga_evaluate_device)
+    cudaStream_t side = nullptr;     // side branch of a generation (mate slots, launch_mates_fork)
+    cudaEvent_t fork_ev = nullptr, join_side_ev = nullptr;
     pga_params p{};
     int32_t N = 0;
     int32_t ldn = 0;       // padded gene stride of chromosome-major labels / V
@@ -243,6 +245,8 @@ int launch_stats(pga_ctx *c, int is_migration_check, cudaStream_t s);
 int launch_sort_order(pga_ctx *c, cudaStream_t s);
 int launch_select_breed(pga_ctx *c, cudaStream_t s);
 int launch_export(pga_ctx *c, void *dev_send, cudaStream_t s);
+int launch_mates_fork(pga_ctx *c, cudaStream_t s);
+int launch_mates_join(pga_ctx *c, cudaStream_t s);
 int launch_import(pga_ctx *c, const void *dev_recv, int32_t G, cudaStream_t s);
 int launch_canonicalize_i32(int32_t *lab, int64_t P, int32_t N, cudaStream_t s);
 int launch_corr(const double *X, int32_t T, int32_t N, double *C, int32_t *status,

@@ -91,6 +91,34 @@ def test_generation_lockstep_wide_N(pga, orc):
         pga.pga_destroy(ctx)
 
 
+@pytest.mark.parametrize("P,sel,scal,E", [(1025, 0, 0, 10), (1500, 0, 1, 7), (4096, 1, 0, 10),
+                                          (8192, 0, 0, 10), (16384, 0, 1, 0), (16383, 0, 0, 10)])
+def test_generation_lockstep_cluster_select(pga, orc, P, sel, scal, E):
+    """1024 < P <= 16384: order, scaling, selection and mates run in one
+    thread-block-cluster launch (k_select_cluster).  Generations in lockstep
+    with the oracle's operators: bit-exact populations given the GPU's L and
+    top, for SUS RANK / NONE and tournament, ragged P, E = 0 (M = P + 1 for
+    odd P - E)."""
+    C, _ = _corr(orc, workloads.CONFIGS["C3"])
+    N, gens = C.shape[0], 3
+    params = _par(pga, P, elite=E, selection=sel, scaling=scal, tournament_k=3, max_gens=gens + 1,
+                  tol=-1.0, p_mutation=0.02, seed=17)
+    op = orc.default_params(pop=P, elite=E, selection=sel, scaling=scal, tour_k=3, max_gens=gens + 1,
+                            tol=-1.0, p_m=0.02, seed=17)
+    ctx = pga.pga_create(C, params)
+    try:
+        pga.pga_init(ctx, 17)
+        pop, _ = pga.pga_get_population(ctx)
+        for g in range(gens):
+            pga.pga_generation(ctx)
+            nxt, L, top = pga.pga_get_population(ctx, with_top=True)
+            _assert_L(L, orc.evaluate(C, pop - 1, nthreads=NT)[0])
+            assert np.array_equal(nxt - 1, orc.step(op, pop - 1, L, top, gen=g)), g
+            pop = nxt
+    finally:
+        pga.pga_destroy(ctx)
+
+
 # ---------------------------------------------------------------------------
 # islands: the Q28 stall rule with tol >= 0, bit-exact after every import
 # ---------------------------------------------------------------------------
