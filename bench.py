@@ -273,6 +273,10 @@ def main():
     ap.add_argument("--stream", action="store_true",
                     help="F1 only: each step also computes the 1760 windows on the device from one "
                          "return stream (EWMA lambda=0.98 + RMT cleaning, SURVEY §8(f) f4)")
+    ap.add_argument("--fitness-only", action="store_true",
+                    help="a step is one fitness evaluation of the whole population (pga_evaluate_device over "
+                         "SURVEY §8(d)'s equal-thirds population mix); BASELINE configs[4] (C5) is stated "
+                         "this way")
     ap.add_argument("--config", default=CONFIG, choices=sorted(CFG_POP) + ["F1"],
                     help="workload (default C4, the config the metric is quoted on; F1 = the "
                          "batched GA over 1760 windows x 18 stocks, SURVEY §8(f))")
@@ -291,6 +295,8 @@ def main():
     P_TOTAL = CFG_POP[CONFIG]
     if args.impl == "reference":
         return run_reference(args)
+    if args.fitness_only:
+        return bench_fitness(args)
 
     import torch
     import torch.distributed as dist
@@ -556,6 +562,136 @@ def main():
                              "C2050; serial MATLAB 7.77 s), population 1000, <= 400 generations; at most "
                              "~5e5 fitness evaluations/s (BASELINE.md §1).  Other hardware, data and "
                              "workload: context, not a target.",
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def bench_fitness(args):
+    """Fitness-only throughput (BASELINE configs[4]: C5, N = 2000, P = 262144,
+    "fitness-eval-only throughput sweep"): a step is one pga_evaluate_device
+    over the whole population, the equal-thirds mix of SURVEY §8(d) (8192
+    base rows repeated under per-copy label permutations, built on the
+    device).  Weak scaling over ranks (each rank evaluates its own P)."""
+    import torch
+    import torch.distributed as dist
+    import paper_1403_4099_b200 as pga
+    rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    K, W = args.steps, args.warmup
+    X, planted = workloads.noh_returns(workloads.CONFIGS[CONFIG])
+    N = X.shape[1]
+    C = pga.pga_correlation(X, device=local)
+    P = P_TOTAL
+    base_P = min(P, 8192)
+    reps = (P + base_P - 1) // base_P
+    base = workloads.population_mix(SEED + rank, planted, base_P)
+    rng = np.random.default_rng(SEED + rank)
+    perms = np.stack([rng.permutation(N) for _ in range(reps)]).astype(np.int64)
+    ctx = pga.pga_create(C, pga.pga_params_default(pop_size=P, device=local))
+    db = torch.from_numpy(base.astype(np.int64)).cuda()
+    dp = torch.from_numpy(perms).cuda()
+    dl = torch.empty((P, N), dtype=torch.int16, device="cuda")
+    for t in range(reps):
+        n = min(base_P, P - t * base_P)
+        dl[t * base_P:t * base_P + n] = torch.gather(dp[t].expand(base_P, N), 1, db)[:n].to(torch.int16)
+    del db
+    # re-evaluating one population would let the cluster cache serve every
+    # large cluster from the previous step (memoised outputs): off here
+    pga.pga_set_cluster_cache(ctx, 0)
+    if args.sparse_theta is not None:
+        pga.pga_set_sparse_threshold(ctx, args.sparse_theta)
+    L = torch.zeros(P, dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream()
+    for _ in range(W):
+        pga.pga_evaluate_device(ctx, dl, L, stream=stream.cuda_stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(list(range(torch.cuda.device_count())) if world > 1 else [local])
+    if rank == 0:
+        clocks.start()
+        time.sleep(0.3)
+    b0, g0 = pga.pga_profile_sparse(ctx)
+    launches0 = pga.pga_launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for _ in range(K):
+        pga.pga_evaluate_device(ctx, dl, L, stream=stream.cuda_stream)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    launches = pga.pga_launch_count() - launches0
+    b1, g1 = pga.pga_profile_sparse(ctx)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    clk = clocks.stop() if rank == 0 else None
+    Lg = L.cpu().numpy()
+    ms_step = ms / K
+    nblk = (P + 31) // 32
+    sparse_frac = (b1 - b0) / float(nblk * K)
+    executed = N * (N - 1) / 2.0 * P
+    peaks = measured_peaks()
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    alu_peak = ALU_PAIRS_PER_CLK * SM_COUNT * sm_max * 1e6
+    hbm = float(peaks.get("hbm_gbs", 6542.7))
+    alg_bytes = P * (N * 2 + 8)
+    dense_rate = executed * (1.0 - sparse_frac) / (ms_step / 1000.0)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        import oracle as orc
+        orc.build()
+        Ch = orc.pearson(X)
+        idx = np.unique(np.concatenate([rng.choice(P, 1024, replace=False), [0, P - 1]]))
+        rows = np.stack([perms[i // base_P][base[i % base_P]] for i in idx]).astype(np.int32)
+        cores = os.cpu_count() or 1
+        t0 = time.perf_counter()
+        Lo, _ = orc.evaluate(Ch, rows, nthreads=cores)
+        dt = time.perf_counter() - t0
+        err = np.abs(Lg[idx] - Lo) / np.maximum(1.0, np.abs(Lo))
+        cpu = {"value": N * N * len(idx) / dt, "unit": "pair-updates/s", "cores": cores, "cpu_model": cpu_model(),
+               "kind": "oracle", "sample": "orc_evaluate of %d sampled rows of the same population on %d host "
+                                          "threads, %.1f s" % (len(idx), cores, dt),
+               "parity": {"rows": int(len(idx)), "max_rel_dL": float(err.max()), "tolerance": 1e-9,
+                          "pass": bool(err.max() <= 1e-9)}}
+    pga.pga_destroy(ctx)
+    if rank == 0:
+        line = {
+            "metric": "fitness evaluation throughput, nominal pair-updates/s (N^2 * P per evaluation)",
+            "value": float(N) * N * P * world / (ms_step / 1000.0), "unit": "pair-updates/s", "n_gpus": world,
+            "steps": K, "warmup": W, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (Noh-model returns, seed %d; Pearson C on device; equal-thirds label mix)"
+                    % workloads.CONFIGS[CONFIG].seed,
+            "config": {"workload": "%s fitness only: N=%d, P=%d per GPU, 1 step = 1 evaluation of the population"
+                                   % (CONFIG, N, P), "N": N, "population_per_gpu": P,
+                       "l2": "working set > L2 (labels %.0f MB per GPU); no flush" % (P * N * 2 / 1e6)},
+            "evals_per_s": P * world / (ms_step / 1000.0),
+            "sparse_block_fraction": sparse_frac,
+            "cluster_cache": "off (the same population is evaluated every step; cached terms would be memoised "
+                             "outputs)",
+            "roofline": {"bound": "alu", "kernel": "k_fitness (dense sweep; the label-sparse pass took %.1f%% "
+                                                   "of the blocks)" % (100 * sparse_frac),
+                         "achieved": dense_rate, "peak": alu_peak, "unit": "pair-updates/s",
+                         "frac": dense_rate / alu_peak,
+                         "traffic": None, "algorithmic_bytes": alg_bytes,
+                         "work_per_launch": "dense blocks x 32 chromosomes x N(N-1)/2 executed pair-updates",
+                         "peak_basis": "SURVEY §8(d): 32 pairs/clk/SM x 148 x %.0f MHz" % sm_max,
+                         "other_bounds": [{"bound": "hbm", "achieved_gbs": alg_bytes / (ms_step / 1000.0) / 1e9,
+                                           "peak_gbs": hbm,
+                                           "frac": alg_bytes / (ms_step / 1000.0) / 1e9 / hbm}],
+                         "measured": "CUDA events around K evaluate launches on the caller stream"},
+            "gpu_launches": int(launches), "clocks": clk, "cpu_baseline": cpu,
+            "parity": (cpu or {}).get("parity"),
+            "e2e": None,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -249,7 +249,7 @@ int pga_op_init(uint64_t seed, int32_t N, int64_t P, int64_t p_off, int32_t isla
  * label, L2 gathers of C for the pairs inside each cluster) and skipped by
  * the dense sweep.  The result is the same Eq. 5/6/8 value (within the
  * parity tolerance; deterministic).  theta in [0, 1]; 0 = always dense,
- * 1 = sparse whenever N <= 640; negative = automatic, the default: 0 for
+ * 1 = sparse whenever N <= 2048; negative = automatic, the default: 0 for
  * N < 160, else 0.25 with the cluster cache on (pga_set_cluster_cache) and
  * 0.04 with it off.  The
  * pass is cheaper than the dense sweep up to about 4% of the pairs when
@@ -259,7 +259,7 @@ int pga_op_init(uint64_t seed, int32_t N, int64_t P, int64_t p_off, int32_t isla
  * denser); pga_init / pga_set_population re-arm it.  Host only. */
 int pga_set_sparse_threshold(pga_ctx *ctx, double theta);
 
-/* Cluster cache of the label-sparse pass (on by default; N <= 640).  c_s
+/* Cluster cache of the label-sparse pass (on by default; N <= 2048).  c_s
  * (Eq. 6) depends only on the member set of cluster s, and a GA generation
  * repeats almost every cluster of the one before (elites are copied,
  * knowledge-based crossover transplants whole clusters, mutation moves a
@@ -274,7 +274,7 @@ int pga_set_cluster_cache(pga_ctx *ctx, int32_t on);
 
 /* Cluster-cache occupancy (measurement and tests; synchronises): slots
  * filled since the last clear, table size in slots (0 when the ctx has no
- * cache, N > 640), and how many times the table was cleared (a launch
+ * cache, N > 2048), and how many times the table was cleared (a launch
  * clears it when more than half the slots are filled).  Any pointer may be
  * NULL. */
 int pga_cache_stats(pga_ctx *ctx, int64_t *fill, int64_t *slots, int64_t *clears);

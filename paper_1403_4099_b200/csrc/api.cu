@@ -440,7 +440,7 @@ int pga_create(const double *C, int32_t N, const pga_params *p, pga_ctx **out) {
     if (!rc && cudaMemset(c->stats_ctr, 0, sizeof(uint32_t)) != cudaSuccess) rc = fail(PGA_EDEVICE, "memset stats_ctr");
     if (!rc && cudaMemset(c->sp_blocks, 0, 4 * sizeof(unsigned long long)) != cudaSuccess)
         rc = fail(PGA_EDEVICE, "memset sp_blocks");
-    if (!rc && N <= 640) {
+    if (!rc && N <= SPARSE_MAX_N) {
         // cluster cache: 64 slots per chromosome, 2^12 .. 2^22 slots (32 B each)
         uint32_t slots = 1u << 12;
         while (slots < (1u << 22) && (int64_t)slots < 64 * c->P) slots <<= 1;
@@ -637,7 +637,7 @@ int pga_set_sparse_threshold(pga_ctx *c, double theta) {
     const bool was_on = sparse_theta_eff(c) > 0.0;
     c->sparse_theta = theta < 0.0 ? -1.0 : theta;
     drop_graphs(c);   // the launch sequence depends on it
-    if (was_on && !(sparse_theta_eff(c) > 0.0) && c->has_pop && c->N <= 640) {
+    if (was_on && !(sparse_theta_eff(c) > 0.0) && c->has_pop && c->N <= SPARSE_MAX_N) {
         // the breed may have left the gene-major copy to the sparse pass
         PGA_CUDA(cudaSetDevice(c->device));
         TRY(launch_resync_gm(c, c->stream));

@@ -535,12 +535,13 @@ __global__ void k_resync_gm(const uint16_t *__restrict__ CM0, const uint16_t *__
 // is order-free), so the cache changes cost, never results, short of a
 // 128-bit key collision.
 // ---------------------------------------------------------------------------
-#ifndef PGA_SP_W
-#define PGA_SP_W 16
-#endif
-constexpr int SP_W = PGA_SP_W, SP_T = SP_W * 32;   // warps per CTA (a CTA owns one 32-chromosome block)
-constexpr int SPARSE_MAXN = 640;   // shared-memory footprint (sparse_smem) must fit one CTA
-constexpr int SP_LREG = SPARSE_MAXN / 64;   // label registers per lane (two 16-bit labels each)
+// Two instantiations of the pass (a CTA owns one 32-chromosome block; a
+// chromosome's labels stay in registers, LREG 32-bit words per lane):
+//   N <= SPARSE_SMALLN: 16 warps, LREG = 10, two CTAs per SM;
+//   N <= SPARSE_MAXN (C5's N = 2000): 8 warps, LREG = 32, one CTA per SM
+//   (the per-warp tables grow with N).
+constexpr int SPARSE_SMALLN = 640, SPARSE_MAXN = pga::SPARSE_MAX_N;
+__host__ __device__ __forceinline__ int sp_warps(int N) { return N <= SPARSE_SMALLN ? 16 : 8; }
 #ifndef PGA_CC_NMIN
 #define PGA_CC_NMIN 5
 #endif
@@ -668,12 +669,14 @@ __host__ __device__ __forceinline__ size_t sp_per_warp(int N) {
 }
 
 static size_t sparse_smem(int N) {
-    const size_t warps = (size_t)SP_W * sp_per_warp(N) + 64;
+    const size_t warps = (size_t)sp_warps(N) * sp_per_warp(N) + 64;
     const size_t tile = (size_t)N * (pga::CB + 2) * sizeof(uint16_t);   // dense-block transpose
     return warps > tile ? warps : tile;
 }
 
-__global__ void __launch_bounds__(SP_T, PGA_SP_MINB) k_fitness_sparse(SparseArgs a) {
+template <int LREG, int SPW>
+__global__ void __launch_bounds__(SPW * 32, SPW == 16 ? PGA_SP_MINB : 1) k_fitness_sparse(SparseArgs a) {
+    constexpr int SP_T = SPW * 32;
     pdl_wait();
     pdl_trigger();
     if (a.done && *a.done) return;
@@ -712,7 +715,7 @@ __global__ void __launch_bounds__(SP_T, PGA_SP_MINB) k_fitness_sparse(SparseArgs
     if (!skip1) {
 
     // ---- pass 1: cluster sizes and pair counts
-    for (int q = warp; q < pga::CB; q += SP_W) {
+    for (int q = warp; q < pga::CB; q += SPW) {
         const int64_t p = (int64_t)cb * pga::CB + q;
         for (int k = lane; k < W; k += 32) cq[k] = 0u;
         __syncwarp();
@@ -813,7 +816,7 @@ __global__ void __launch_bounds__(SP_T, PGA_SP_MINB) k_fitness_sparse(SparseArgs
     const double *C = a.C;
     const uint4 *keys4 = reinterpret_cast<const uint4 *>(a.cc_keys);
     uint16_t *ordm = reinterpret_cast<uint16_t *>(cq);
-    for (int q = warp; q < pga::CB; q += SP_W) {
+    for (int q = warp; q < pga::CB; q += SPW) {
         const int64_t p = (int64_t)cb * pga::CB + q;
         if (p >= a.P) break;
         for (int k = lane; k < W; k += 32) cq[k] = 0u;
@@ -823,15 +826,15 @@ __global__ void __launch_bounds__(SP_T, PGA_SP_MINB) k_fitness_sparse(SparseArgs
         // the chromosome's labels stay in registers for the passes over
         // them: gene 64 (k >> 1) + 2 lane + (k & 1) is half (k & 1) of
         // labr[k >> 1] (one aligned 32-bit load per gene pair; ldn is even)
-        uint32_t labr[SP_LREG];
+        uint32_t labr[LREG];
 #pragma unroll
-        for (int k = 0; k < SP_LREG; ++k) {
+        for (int k = 0; k < LREG; ++k) {
             const int i = 64 * k + 2 * lane;
             labr[k] = i < N ? *reinterpret_cast<const uint32_t *>(lab + i) : 0u;
         }
         // (1) counts; the count before a gene's increment is its slot
 #pragma unroll
-        for (int k = 0; k < 2 * SP_LREG; ++k) {
+        for (int k = 0; k < 2 * LREG; ++k) {
             const int i = 64 * (k >> 1) + 2 * lane + (k & 1);
             if (i < N) {
                 const uint32_t s = (labr[k >> 1] >> (16 * (k & 1))) & 0xFFFFu;
@@ -868,7 +871,7 @@ __global__ void __launch_bounds__(SP_T, PGA_SP_MINB) k_fitness_sparse(SparseArgs
         }
         __syncwarp();
         // (3) small clusters, one per lane: no walk, no queue
-        uint32_t nhit = 0, nsaved = 0, npair = 0;   // per chromosome: < 2^32 (N <= 640)
+        uint32_t nhit = 0, nsaved = 0, npair = 0;   // per chromosome: < 2^32 (N <= 2048)
         double fsum = 0.0, fbest = 0.0;
         int kbest = 0x7FFFFFFF;
         for (int j = lane; j < scnt; j += 32) {
@@ -907,7 +910,7 @@ __global__ void __launch_bounds__(SP_T, PGA_SP_MINB) k_fitness_sparse(SparseArgs
             }
             __syncwarp();
 #pragma unroll
-            for (int k = 0; k < 2 * SP_LREG; ++k) {
+            for (int k = 0; k < 2 * LREG; ++k) {
                 const int i = 64 * (k >> 1) + 2 * lane + (k & 1);
                 if (i >= N) continue;
                 const uint32_t om = ordm[(labr[k >> 1] >> (16 * (k & 1))) & 0xFFFFu];
@@ -969,7 +972,7 @@ __global__ void __launch_bounds__(SP_T, PGA_SP_MINB) k_fitness_sparse(SparseArgs
         // cluster is free: sums are exact)
         if (Nw > 0) {
 #pragma unroll
-            for (int k = 0; k < 2 * SP_LREG; ++k) {
+            for (int k = 0; k < 2 * LREG; ++k) {
                 const int i = 64 * (k >> 1) + 2 * lane + (k & 1);
                 if (i >= N) continue;
                 const uint32_t om = ordm[(labr[k >> 1] >> (16 * (k & 1))) & 0xFFFFu];
@@ -1206,9 +1209,12 @@ size_t fitness_smem(int N) {
 int prepare_fitness(int N) {
     PGA_CUDA(cudaFuncSetAttribute(k_fitness, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)fitness_smem(N)));
-    if (N <= SPARSE_MAXN)
-        PGA_CUDA(cudaFuncSetAttribute(k_fitness_sparse, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)sparse_smem(N)));
+    if (N <= SPARSE_SMALLN)
+        PGA_CUDA(cudaFuncSetAttribute(k_fitness_sparse<SPARSE_SMALLN / 64, 16>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sparse_smem(N)));
+    else if (N <= SPARSE_MAXN)
+        PGA_CUDA(cudaFuncSetAttribute(k_fitness_sparse<SPARSE_MAXN / 64, 8>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sparse_smem(N)));
     return PGA_OK;
 }
 
@@ -1282,7 +1288,12 @@ int launch_fitness_range(pga_ctx *c, const FitBufs &b, int64_t begin, int64_t en
         sp.cc_mask = c->cc_mask;
         sp.cc_state = c->cc_state;
         sp.cc_keys = c->cc_keys;
-        PGA_LAUNCH_PDL(k_fitness_sparse, dim3((unsigned)a.nCB), dim3(SP_T), sparse_smem(N), s, sp);
+        if (N <= SPARSE_SMALLN)
+            PGA_LAUNCH_PDL(k_fitness_sparse<SPARSE_SMALLN / 64, 16>, dim3((unsigned)a.nCB), dim3(16 * 32),
+                           sparse_smem(N), s, sp);
+        else
+            PGA_LAUNCH_PDL(k_fitness_sparse<SPARSE_MAXN / 64, 8>, dim3((unsigned)a.nCB), dim3(8 * 32),
+                           sparse_smem(N), s, sp);
         a.sflag = c->sflag;
     }
     if (ev) PGA_CUDA(prof_record(ev[1], s));   // dense kernel starts here

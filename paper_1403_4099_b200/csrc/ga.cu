@@ -1781,7 +1781,7 @@ int launch_select_breed(pga_ctx *c, cudaStream_t s) {
     a.gen_ptr = genp;
     // the gene-major copy is produced by the label-sparse pass while its
     // checks are live (it transposes exactly the blocks the dense sweep needs)
-    a.gm_skip = (sparse_theta_eff(c) > 0.0 && c->N <= 640) ? c->sp_live : nullptr;
+    a.gm_skip = (sparse_theta_eff(c) > 0.0 && c->N <= SPARSE_MAX_N) ? c->sp_live : nullptr;
     a.adv_st = c->st;           // the breed's last CTA advances the generation (no k_advance)
     a.adv_ctr = c->breed_ctr;
     count_launch();

@@ -86,6 +86,7 @@ enum : uint32_t {
 
 constexpr int PROF_EV = 9;     // phase marks per profiled generation
 constexpr int CB = 32;         // chromosomes per fitness CTA tile (one per lane)
+constexpr int SPARSE_MAX_N = 2048;   // largest N with a label-sparse pass (cluster cache, pair table)
 
 // Cluster-cache slot (k_fitness_sparse): exact fixed-point c_s of a member
 // set keyed by two 64-bit Zobrist words; k1 == 0 empty; chk validates.
@@ -154,11 +155,11 @@ struct pga_ctx {
     pga::GExec gx_eval[2];
     pga::GExec gx_breed;
     unsigned long long *sp_blocks = nullptr;  // device [4]: sparse blocks, gathers, cache hits, pairs saved (profiling)
-    pga::CCSlot *cc = nullptr;     // cluster cache table (N <= 640)
+    pga::CCSlot *cc = nullptr;     // cluster cache table (N <= SPARSE_MAX_N)
     uint32_t cc_mask = 0;          // slots - 1
     uint32_t *cc_state = nullptr;  // device [4]: fill, clear request, CTA count
     uint64_t *cc_keys = nullptr;   // device [N][2] Zobrist keys
-    double *ptab = nullptr;        // [N][ldc] Eq. 8 term of each pair cluster (label-sparse pass, N <= 640)
+    double *ptab = nullptr;        // [N][ldc] Eq. 8 term of each pair cluster (label-sparse pass, N <= SPARSE_MAX_N)
     bool cc_on = true;
     // population: chromosome-major [Pcap][ldn] and gene-major [N][Pcap], double buffered
     uint16_t *pop[2] = {nullptr, nullptr};

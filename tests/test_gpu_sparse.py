@@ -78,10 +78,12 @@ def test_sparse_threshold_validation(pga):
         pga.pga_destroy(ctx)
 
 
-@pytest.mark.parametrize("N,P", [(640, 100), (641, 64), (37, 33), (2, 5)])
+@pytest.mark.parametrize("N,P", [(640, 100), (641, 64), (1100, 40), (2048, 33), (2049, 32), (37, 33), (2, 5)])
 def test_sparse_edges_match_oracle(pga, orc, N, P):
-    """Largest N with a label-sparse pass (640), the first without (641),
-    ragged P (not a multiple of 32), N = 2: every path vs the oracle."""
+    """The two instantiations of the label-sparse pass (16 warps up to
+    N = 640, 8 warps with 32 label registers per lane up to 2048) at their
+    edges, the first N without a pass (2049), ragged P (not a multiple of
+    32), N = 2: every path vs the oracle."""
     rng = np.random.default_rng(N + P)
     X = rng.standard_normal((max(3 * N, 40), N))
     k = max(1, N // 6)
@@ -191,5 +193,31 @@ def test_switching_the_sparse_pass_off_mid_run(pga, orc):
         pga.pga_gen_evaluate(ctx)
         pop, L = pga.pga_get_population(ctx, P, N)
         _assert_L(L, orc.evaluate(C, pop - 1, nthreads=8)[0])
+    finally:
+        pga.pga_destroy(ctx)
+
+
+def test_sparse_pass_C5_ga_lockstep(pga, orc):
+    """N = 2000 (C5's stocks) GA generations with the automatic label-sparse
+    pass (early generations: every block sparse) and the cluster cache: L
+    matches the oracle and the bred population equals orc_step on the GPU's
+    L and top; the pass evaluated blocks."""
+    X, _ = workloads.noh_returns(workloads.CONFIGS["C5"])
+    C = orc.pearson(X)
+    N, P, gens = C.shape[0], 256, 4
+    params = pga.pga_params_default(pop_size=P, max_gens=gens + 1, tol=-1.0, p_mutation=2.0 / N, seed=21)
+    op = orc.default_params(pop=P, max_gens=gens + 1, tol=-1.0, p_m=2.0 / N, seed=21)
+    ctx = pga.pga_create(C, params)
+    try:
+        pga.pga_init(ctx, 21)
+        pop, _ = pga.pga_get_population(ctx)
+        for g in range(gens):
+            pga.pga_generation(ctx)
+            nxt, L, top = pga.pga_get_population(ctx, with_top=True)
+            _assert_L(L, orc.evaluate(C, pop - 1, nthreads=8)[0])
+            assert np.array_equal(nxt - 1, orc.step(op, pop - 1, L, top, gen=g)), g
+            pop = nxt
+        blocks, _ = pga.pga_profile_sparse(ctx)
+        assert blocks > 0
     finally:
         pga.pga_destroy(ctx)
