@@ -398,6 +398,14 @@ int pga_corr_stream(const double *X, int32_t T, int32_t N, double lambda, int32_
  * (for the bench's gpu_launches claim). */
 int64_t pga_launch_count(void);
 
+/* Device-side invariant checks (test infrastructure; the substitute for
+ * compute-sanitizer, which the GPU pool does not allow): in a library built
+ * with -DPGA_DEVICE_CHECKS, the number of index/range invariants of the hot
+ * kernels found violated so far in this process (0 = clean; synchronises
+ * with the device).  -1 in the product build (checks compiled out); -2 on a
+ * CUDA error. */
+int64_t pga_debug_violations(void);
+
 /* Kernel timing with CUDA events on the ctx's stream (measurement only).
  * pga_profile_enable(ctx, level): level 1 records, for every generation
  * launched through pga_gen_evaluate / pga_gen_breed, 3 events (fitness

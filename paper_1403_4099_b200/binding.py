@@ -81,6 +81,7 @@ _SIGS = {
                                ct.c_int32, ct.c_void_p]),
     "pga_launch_count": (ct.c_int64, []),
     "pga_get_dims": (ct.c_int, [ct.c_void_p, ct.c_void_p, ct.c_void_p, ct.c_void_p]),
+    "pga_debug_violations": (ct.c_int64, []),
     "pga_cache_stats": (ct.c_int, [ct.c_void_p, ct.c_void_p, ct.c_void_p, ct.c_void_p]),
     "pga_set_sparse_threshold": (ct.c_int, [ct.c_void_p, ct.c_double]),
     "pga_profile_sparse_blocks": (ct.c_int, [ct.c_void_p, ct.c_void_p]),
@@ -516,6 +517,11 @@ def pga_batch_op_step(params: pga_params, pop, L, top, gen: int):
     nxt = np.zeros_like(pop)
     _check(lib().pga_batch_op_step(B, N, ct.byref(params), _p(pop), _p(L), _p(top), gen, _p(nxt)))
     return nxt
+
+
+def pga_debug_violations() -> int:
+    """Device invariant violations so far (-1: product build, checks compiled out)."""
+    return lib().pga_debug_violations()
 
 
 def pga_launch_count() -> int:

@@ -11,6 +11,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpga.so")
+CHECK_LIB = os.path.join(HERE, "libpga_check.so")   # -DPGA_DEVICE_CHECKS (tests only)
 SOURCES = ["api.cu", "fitness.cu", "ga.cu", "corr.cu", "batch.cu", "stream.cu"]
 HEADERS = ["pga_internal.cuh", os.path.join("..", "..", "include", "pga.h")]
 
@@ -29,6 +30,21 @@ def _stale() -> bool:
     t = os.path.getmtime(LIB)
     deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS] + [os.path.abspath(__file__)]
     return any(os.path.getmtime(d) > t for d in deps)
+
+
+def _stale_lib(path) -> bool:
+    if not os.path.exists(path):
+        return True
+    t = os.path.getmtime(path)
+    deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS] + [os.path.abspath(__file__)]
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build_check(force: bool = False, verbose: bool = False) -> str:
+    """The device-check variant (test infrastructure, tests/test_gpu_checks.py)."""
+    if force or _stale_lib(CHECK_LIB):
+        build(force=True, verbose=verbose, out=CHECK_LIB, defines=("PGA_DEVICE_CHECKS",))
+    return CHECK_LIB
 
 
 def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:

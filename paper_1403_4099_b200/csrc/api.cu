@@ -63,6 +63,8 @@ int launch_set_pop(pga_ctx *c, const int32_t *lab32, int par, cudaStream_t s);
 int prepare_breed(int N);
 int prepare_select_small();
 bool small_select(const pga_ctx *c);
+long long viol_fitness();
+long long viol_ga();
 
 static int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
@@ -375,6 +377,12 @@ extern "C" {
 const char *pga_last_error(void) { return g_err.c_str(); }
 
 int64_t pga_launch_count(void) { return g_launches.load(); }
+
+int64_t pga_debug_violations(void) {
+    const long long a = viol_fitness(), b = viol_ga();
+    if (a < 0 || b < 0) return a < b ? a : b;
+    return a + b;
+}
 
 int pga_params_default(pga_params *o) {
     if (!o) return fail(PGA_EINVAL, "out is NULL");

@@ -840,6 +840,7 @@ __global__ void __launch_bounds__(SPW * 32, SPW == 16 ? PGA_SP_MINB : 1) k_fitne
                 const uint32_t s = (labr[k >> 1] >> (16 * (k & 1))) & 0xFFFFu;
                 kmax = max(kmax, s);
                 const uint32_t sh = 16 * (s & 1u);
+                PGA_DCHECK(s < (uint32_t)N);
                 const uint32_t slot = (atomicAdd(cq + (s >> 1), 1u << sh) >> sh) & 0xFFFFu;
                 if (slot < (uint32_t)SMALL_N) mem[SMALL_N * s + slot] = (uint16_t)i;
             }
@@ -859,11 +860,13 @@ __global__ void __launch_bounds__(SPW * 32, SPW == 16 ? PGA_SP_MINB : 1) k_fitne
             const unsigned be = __ballot_sync(0xFFFFFFFFu, el), bs = __ballot_sync(0xFFFFFFFFu, sm);
             if (el) {
                 const int ord = ecnt + __popc(be & lanemask_lt());
+                PGA_DCHECK(ord < E);
                 ordm[k] = (uint16_t)(ord | (n >= CC_NMIN ? 0x2000 : 0));
                 cn[ord] = (uint16_t)n;
                 clab[ord] = (uint16_t)k;
             } else if (k < K) {
                 ordm[k] = (uint16_t)(0x8000 | n);
+                PGA_DCHECK(!sm || scnt + __popc(bs & lanemask_lt()) <= N / 2);
                 if (sm) slist[scnt + __popc(bs & lanemask_lt())] = (uint16_t)k;
             }
             ecnt += __popc(be);
@@ -979,6 +982,7 @@ __global__ void __launch_bounds__(SPW * 32, SPW == 16 ? PGA_SP_MINB : 1) k_fitne
                 if (!(om & 0xC000u)) {
                     const uint32_t o = om & 0x1FFFu;
                     const uint32_t pos = atomicAdd(wen + o, 1u);
+                    PGA_DCHECK(o < (uint32_t)ecnt && pos < (uint32_t)Nw);
                     perm2[pos] = (uint32_t)i | (o << 16);
                 }
             }
@@ -1032,6 +1036,7 @@ __global__ void __launch_bounds__(SPW * 32, SPW == 16 ? PGA_SP_MINB : 1) k_fitne
             const int en31 = __shfl_sync(0xFFFFFFFFu, en, 31);
             const long long tot31 = __shfl_sync(0xFFFFFFFFu, tot, 31);
             carry = (o31 >= 0 && en31 > t0 + 32) ? tot31 : 0ll;
+            PGA_DCHECK(o < 0 || (o < ecnt && st >= 0 && en <= Nw && n >= WALK_N));
             if (o >= 0 && lane == lo && en <= t0 + 32) cval[o] = (double)tot * a.fx_inv;
         }
         __syncwarp();
@@ -1102,6 +1107,8 @@ __global__ void k_pairtab(const double *__restrict__ C, int ldc, const double *_
 }
 
 }  // namespace
+
+PGA_VIOL_READER(viol_fitness)
 
 namespace pga {
 

@@ -357,6 +357,7 @@ __global__ void __launch_bounds__(SCAN_T) k_sus2(const uint64_t *__restrict__ q,
     const uint64_t start = __umul64hi(x, step);
     const int64_t m0 = (int64_t)min(sus_first(lo, start, step), (uint64_t)M);
     const int64_t m1 = (int64_t)min(sus_first(hi, start, step), (uint64_t)M);
+    PGA_DCHECK(hi >= lo && hi <= Q);
     for (int64_t m = m0; m < m1; ++m) sel[m] = (int32_t)t;
 }
 
@@ -723,6 +724,7 @@ __global__ void __launch_bounds__(MERGE_T) k_merge_level(const uint64_t *__restr
     }
     if (!valid) return;
     const int64_t pos = blk + off + lo;
+    PGA_DCHECK(pos >= 0 && pos < P);
     if (kd) kd[pos] = ke;
     id[pos] = (int32_t)ie;
     if (rank_out) rank_out[ie] = (int32_t)pos;   // last level: rank (0-based) of individual ie
@@ -881,6 +883,7 @@ k_select_cluster(int what, const double *__restrict__ L, int P, int R, int M, in
         int rank = tid;
 #pragma unroll
         for (int r = 0; r < CSEL_CL - 1; ++r) rank += lo[r];
+        PGA_DCHECK(rank >= 0 && rank < P && (int)v - base >= 0 && (int)v - base < R);
         if (what & 1) order[rank] = (int32_t)v;
         if (rank_out) rank_out[v] = rank;
         srank[v - base] = rank;
@@ -1304,6 +1307,7 @@ __global__ void __launch_bounds__(BW * 32, NB <= 2 ? 3 : PGA_B2_MINB) k_breed2(B
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const int g0 = GCH * b + 64 * h + 2 * lane;
+                    PGA_DCHECK((w[b][h] & 0xFFFFu) <= (uint32_t)N && (w[b][h] >> 16) <= (uint32_t)N);
                     if (g0 < N) atomicMin(&fp[w[b][h] & 0xFFFFu], (uint32_t)g0);
                     if (g0 + 1 < N) atomicMin(&fp[w[b][h] >> 16], (uint32_t)(g0 + 1));
                 }
@@ -1488,6 +1492,8 @@ __global__ void k_import(const unsigned char *__restrict__ in, int G, int Em, in
 }
 
 }  // namespace
+
+PGA_VIOL_READER(viol_ga)
 
 namespace pga {
 

@@ -261,6 +261,35 @@ int launch_corr(const double *X, int32_t T, int32_t N, double *C, int32_t *statu
 // ---------------------------------------------------------------------------
 namespace pgad {
 
+// Device-side bounds checks (the sanitizer substitute: compute-sanitizer is
+// closed on the GPU pool).  A build with -DPGA_DEVICE_CHECKS counts every
+// violated index/range invariant of the hot kernels in a per-translation-
+// unit device counter that pga_debug_violations() sums; the product build
+// compiles the checks away.
+#ifdef PGA_DEVICE_CHECKS
+static __device__ unsigned int g_viol = 0u;
+#define PGA_DCHECK(c)                                  \
+    do {                                               \
+        if (!(c)) atomicAdd(&::pgad::g_viol, 1u);      \
+    } while (0)
+#define PGA_VIOL_READER(fn)                                                          \
+    namespace pga {                                                                  \
+    long long fn() {                                                                 \
+        unsigned int v = 0;                                                          \
+        if (cudaMemcpyFromSymbol(&v, ::pgad::g_viol, sizeof(v)) != cudaSuccess) return -2; \
+        return (long long)v;                                                         \
+    }                                                                                \
+    }
+#else
+#define PGA_DCHECK(c) \
+    do {              \
+    } while (0)
+#define PGA_VIOL_READER(fn) \
+    namespace pga {         \
+    long long fn() { return -1; } \
+    }
+#endif
+
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 

@@ -1,6 +1,9 @@
-"""Small invocations of every kernel family for compute-sanitizer (SURVEY §4
-layer 6): run as
-    compute-sanitizer --tool {memcheck,racecheck,synccheck,initcheck} python tools/sanitize.py
+"""Small invocations of every kernel family, checked against the oracle and,
+with the device-check build (PGA_LIB=paper_1403_4099_b200/libpga_check.so,
+-DPGA_DEVICE_CHECKS), against the hot kernels' index/range invariants
+(SURVEY §4 layer 6; compute-sanitizer itself is closed on the GPU pool, where
+it can also be run as
+    compute-sanitizer --tool {memcheck,racecheck,synccheck,initcheck} python tools/sanitize.py)
 Covers k_fitness (TMA sweep + last-CTA fold), k_fitness_sparse (counting
 sort, L2 gathers, cluster-cache CAS / relaxed loads, clear path), k_stats
 (multi-CTA last-CTA reduction), the order sort and merge levels, selection
@@ -66,6 +69,29 @@ def main():
         print("cache", pga.pga_cache_stats(ctx))
     finally:
         pga.pga_destroy(ctx)
+    # C4-size GA (N = 500): automatic label-sparse pass with the cache,
+    # cluster selection (P = 4096), and the N = 2000 instantiation of the pass
+    ctx = pga.pga_create(C4, pga.pga_params_default(pop_size=4096, p_mutation=0.004, tol=-1.0, seed=6))
+    try:
+        pga.pga_init(ctx, 6)
+        for _ in range(8):
+            pga.pga_gen_evaluate(ctx)
+            pga.pga_gen_breed(ctx)
+        pga.pga_gen_evaluate(ctx)
+        pop, L = pga.pga_get_population(ctx)
+        idx = np.arange(0, 4096, 97)
+        assert close(L[idx], orc.evaluate(C4, pop[idx] - 1)[0])
+    finally:
+        pga.pga_destroy(ctx)
+    X5, pl5 = workloads.noh_returns(workloads.CONFIGS["C5"])
+    C5 = orc.pearson(X5)
+    ctx = pga.pga_create(C5, pga.pga_params_default(pop_size=96, seed=8))
+    try:
+        lab5 = workloads.population_mix(9, pl5, 96)
+        pga.pga_set_sparse_threshold(ctx, 1.0)
+        assert close(pga.pga_evaluate(ctx, lab5 + 1), orc.evaluate(C5, lab5, nthreads=8)[0])
+    finally:
+        pga.pga_destroy(ctx)
     # small single-CTA selection path, k_stats with a stall stop
     C1, p1 = workloads.noh_returns(workloads.CONFIGS["C1"])
     C1 = orc.pearson(C1)
@@ -103,7 +129,10 @@ def main():
     Cs = pga.pga_corr_stream(Xs, warm=160, stride=20, q=0.0)
     assert np.isfinite(Cs).all()
     torch.cuda.synchronize()
-    print("sanitize workload ok")
+    v = pga.pga_debug_violations()
+    print("sanitize workload ok; device invariant violations: %d" % v)
+    if v > 0:
+        sys.exit(3)
 
 
 if __name__ == "__main__":
