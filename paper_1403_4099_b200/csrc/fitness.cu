@@ -9,6 +9,8 @@
 //            group sums, no float atomics -> deterministic), then Eq. 8 with
 //            readings Q1-Q3, L = 1/2 sum f_s and top = argmax f_s.
 #include <cuda_runtime.h>
+#include <algorithm>
+#include <cstdlib>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_fp16.h>
@@ -97,6 +99,7 @@ constexpr int LAB_BYTES = KC * pga::CB * 2;
 constexpr int CST_BYTES = KC * RT * 8;
 constexpr int STAGE_BYTES = LAB_BYTES + CST_BYTES;
 constexpr int FIT_THREADS = (CW + 1) * 32;
+constexpr int FIT_BLOCKS_PER_CTA_MIN = 1024;   // chromosome blocks from which a k_fitness CTA sweeps a whole block
 static_assert(KC % WR == 0, "a warp's rows must not straddle two chunks");
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -134,6 +137,7 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *tm, in
 
 struct FitArgs {
     int N, ldn, nRT, nCB, fold_warps;
+    int F, cpb;                     // row tiles per CTA, CTAs per chromosome block (cpb = ceil(nRT / F))
     int cb0;                        // first chromosome block (shard offset / 32)
     double fx_scale, fx_inv;        // fold fixed point: 2^S and 2^-S
     const double *lgn, *lgnn;       // log n, log(n^2 - n), n = 0..N (Q30)
@@ -313,7 +317,7 @@ k_fitness(const __grid_constant__ CUtensorMap tmLab0, const __grid_constant__ CU
     {   // both exit tests from one round trip (independent loads): with every
         // block evaluated label-sparsely, this is all a CTA does
         const int32_t dn = a.done ? __ldg(a.done) : 0;
-        const uint8_t sf = a.sflag ? a.sflag[a.cb0 + (int)(blockIdx.x / a.nRT)] : (uint8_t)0;
+        const uint8_t sf = a.sflag ? a.sflag[a.cb0 + (int)(blockIdx.x / a.cpb)] : (uint8_t)0;
         if (dn | sf) return;   // stopped, or done by k_fitness_sparse
     }
     const int par = (a.gen && (*a.gen & 1)) ? 1 : 0;
@@ -326,9 +330,8 @@ k_fitness(const __grid_constant__ CUtensorMap tmLab0, const __grid_constant__ CU
     __shared__ int s_last;
 
     const int N = a.N;
-    const int cb = a.cb0 + (int)(blockIdx.x / a.nRT), rt = blockIdx.x - (blockIdx.x / a.nRT) * a.nRT;
-    const int i0 = rt * RT;
-    const int nchunks = (N - i0 + KC - 1) / KC;
+    const int cb = a.cb0 + (int)(blockIdx.x / a.cpb);
+    const int rt_lo = (int)(blockIdx.x % a.cpb) * a.F, rt_hi = min(a.nRT, rt_lo + a.F);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
     if (tid == 0) {
@@ -340,12 +343,22 @@ k_fitness(const __grid_constant__ CUtensorMap tmLab0, const __grid_constant__ CU
     }
     __syncthreads();
 
+    // The CTA sweeps row tiles rt_lo .. rt_hi-1 of its chromosome block in
+    // turn (F > 1 keeps the grid near the resident-CTA count when the block
+    // count is large, so a launch whose blocks all went label-sparse costs
+    // few CTA launches).  Stage s / phase of chunk kk continue across tiles.
+    int kk0 = 0;
+    for (int rt = rt_lo; rt < rt_hi; ++rt) {
+    const int i0 = rt * RT;
+    const int nchunks = (N - i0 + KC - 1) / KC;
+
     if (warp == CW) {
         // ---------------- producer ----------------
         if (lane == 0) {
             for (int k = 0; k < nchunks; ++k) {
-                const int s = k % NSTAGE;
-                if (k >= NSTAGE) mbar_wait(&empty[s], (uint32_t)((k / NSTAGE - 1) & 1));
+                const int kk = kk0 + k;
+                const int s = kk % NSTAGE;
+                if (kk >= NSTAGE) mbar_wait(&empty[s], (uint32_t)((kk / NSTAGE - 1) & 1));
                 unsigned char *st = smem + s * STAGE_BYTES;
                 mbar_expect_tx(&full[s], STAGE_BYTES);
                 tma_load_2d(st, tmLab, cb * pga::CB, i0 + k * KC, &full[s]);
@@ -367,8 +380,9 @@ k_fitness(const __grid_constant__ CUtensorMap tmLab0, const __grid_constant__ CU
         const int kw = lw / KC, lw0 = lw - kw * KC;
         uint32_t rl[WR];
         for (int k = 0; k < nchunks; ++k) {
-            const int s = k % NSTAGE;
-            mbar_wait(&full[s], (uint32_t)((k / NSTAGE) & 1));
+            const int kk = kk0 + k;
+            const int s = kk % NSTAGE;
+            mbar_wait(&full[s], (uint32_t)((kk / NSTAGE) & 1));
             const unsigned char *st = smem + s * STAGE_BYTES;
             const uint16_t *labs = reinterpret_cast<const uint16_t *>(st) + lane;
             const double *cst = reinterpret_cast<const double *>(st + LAB_BYTES) + lw;
@@ -420,13 +434,15 @@ k_fitness(const __grid_constant__ CUtensorMap tmLab0, const __grid_constant__ CU
             }
         }
     }
+    kk0 += nchunks;
+    }   // row tiles
 
     // ---------------- fused fold (last CTA of the chromosome block) ----------------
     __syncthreads();
     if (tid == 0) {
         __threadfence();
         const unsigned prev = atomicAdd(&a.counters[cb], 1u);
-        s_last = (prev == (unsigned)(a.nRT - 1));
+        s_last = (prev == (unsigned)(a.cpb - 1));
     }
     __syncthreads();
     if (!s_last) return;
@@ -1304,7 +1320,21 @@ int launch_fitness_range(pga_ctx *c, const FitBufs &b, int64_t begin, int64_t en
         a.sflag = c->sflag;
     }
     if (ev) PGA_CUDA(prof_record(ev[1], s));   // dense kernel starts here
-    PGA_LAUNCH_PDL(k_fitness, dim3((unsigned)(a.nRT * a.nCB)), dim3(FIT_THREADS), fitness_smem(N), s, *b.tm0,
+    {
+        // row tiles per CTA: a whole chromosome block per CTA (all nRT tiles,
+        // cpb = 1) when there are enough blocks to fill the GPU (>= 1024:
+        // C4, C5), else one tile per CTA.  Every CTA of a block exits at once
+        // when the block went label-sparse, so in GA generations where the
+        // sparse pass took every block this launch costs nCB instead of
+        // nRT * nCB empty CTAs (C4: 8.2 instead of 22.5 us); a dense sweep
+        // runs the same either way (C4: 1.447 vs 1.443 ms; uneven splits,
+        // e.g. 6 + 2 tiles, measured slower: 1.58 ms).
+        int F = a.nCB >= FIT_BLOCKS_PER_CTA_MIN ? a.nRT : 1;
+        if (const char *e = std::getenv("PGA_FIT_F")) F = std::max(1, std::min(a.nRT, std::atoi(e)));
+        a.F = F;
+        a.cpb = (a.nRT + F - 1) / F;
+    }
+    PGA_LAUNCH_PDL(k_fitness, dim3((unsigned)(a.cpb * a.nCB)), dim3(FIT_THREADS), fitness_smem(N), s, *b.tm0,
                    *b.tm1, c->tmC, a);
     if (ev) PGA_CUDA(prof_record(ev[2], s));   // sweep and fold are one fused kernel
     return PGA_OK;
