@@ -235,6 +235,11 @@ int pga_op_breed(const int32_t *pop, const int32_t *top, const int32_t *order,
                  const pga_params *p, int32_t gen, int32_t island, int64_t p_off,
                  int32_t *next_out);
 
+/* The label-sparse pass's table-driven natural log (fitness.cu fast_ln) of
+ * x[0..n) (host, positive normal values) -> out[n] (host), with the ctx's
+ * table; pins its accuracy against libm in the tests. */
+int pga_op_fast_ln(pga_ctx *ctx, const double *x, int64_t n, double *out);
+
 /* First-occurrence canonical form (Q7), in place, labels [P][N] 0-based < 2N. */
 int pga_op_canonicalize(int32_t *labels, int64_t P, int32_t N, int32_t device);
 

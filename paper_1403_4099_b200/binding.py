@@ -82,6 +82,7 @@ _SIGS = {
     "pga_launch_count": (ct.c_int64, []),
     "pga_get_dims": (ct.c_int, [ct.c_void_p, ct.c_void_p, ct.c_void_p, ct.c_void_p]),
     "pga_debug_violations": (ct.c_int64, []),
+    "pga_op_fast_ln": (ct.c_int, [ct.c_void_p, ct.c_void_p, ct.c_int64, ct.c_void_p]),
     "pga_cache_stats": (ct.c_int, [ct.c_void_p, ct.c_void_p, ct.c_void_p, ct.c_void_p]),
     "pga_set_sparse_threshold": (ct.c_int, [ct.c_void_p, ct.c_double]),
     "pga_profile_sparse_blocks": (ct.c_int, [ct.c_void_p, ct.c_void_p]),
@@ -372,6 +373,14 @@ def pga_op_breed(pop, top, order, sel, sigma, params: pga_params, gen=0, island=
                               _p(_c(sel, np.int32)), _p(_c(sigma, np.int32)), ct.byref(params),
                               gen, island, p_off, _p(nxt)))
     return nxt
+
+
+def pga_op_fast_ln(ctx, x):
+    """The sparse pass's table-driven ln (test hook)."""
+    x = _c(x, np.float64)
+    out = np.zeros_like(x)
+    _check(lib().pga_op_fast_ln(ctx, _p(x), x.size, _p(out)))
+    return out
 
 
 def pga_op_canonicalize(labels, device: int = 0):

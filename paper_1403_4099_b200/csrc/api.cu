@@ -64,6 +64,7 @@ int prepare_breed(int N);
 int prepare_select_small();
 bool small_select(const pga_ctx *c);
 long long viol_fitness();
+int launch_fast_ln(const double *x, int64_t n, const double *lgtab, int N, double *out, cudaStream_t s);
 long long viol_ga();
 
 static int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
@@ -439,7 +440,7 @@ int pga_create(const double *C, int32_t N, const pga_params *p, pga_ctx **out) {
     int rc = 0;
     rc = rc ? rc : dalloc(&c->C, (size_t)N * c->ldc);
     rc = rc ? rc : dalloc(&c->diag, (size_t)N);
-    rc = rc ? rc : dalloc(&c->lgtab, (size_t)2 * (N + 1));
+    rc = rc ? rc : dalloc(&c->lgtab, (size_t)2 * (N + 1) + 2 * LN_TAB);
     rc = rc ? rc : dalloc(&c->sflag, (size_t)(c->Pcap / CB + 1));
     rc = rc ? rc : dalloc(&c->sp_live, (size_t)6);
     rc = rc ? rc : dalloc(&c->sp_blocks, (size_t)4);
@@ -1044,6 +1045,23 @@ int pga_op_breed(const int32_t *pop, const int32_t *top, const int32_t *order, i
     TRY(launch_breed_hook(dpop, dtop, dord, P, N, dsel, dsig, *p, gen, island, p_off, dnext, 0));
     PGA_CUDA(cudaDeviceSynchronize());
     PGA_CUDA(cudaMemcpy(next_out, dnext, sizeof(int32_t) * P * N, cudaMemcpyDeviceToHost));
+    return PGA_OK;
+}
+
+int pga_op_fast_ln(pga_ctx *c, const double *x, int64_t n, double *out) {
+    if (!c || !x || !out) return fail(PGA_EINVAL, "NULL argument");
+    if (n < 1) return fail(PGA_EINVAL, "n must be >= 1");
+    for (int64_t i = 0; i < n; ++i)
+        if (!(x[i] >= 2.2250738585072014e-308) || !std::isfinite(x[i])) return fail(PGA_EINVAL, "x must be positive normal");
+    PGA_CUDA(cudaSetDevice(c->device));
+    HookBufs hb;
+    double *dx, *dy;
+    TRY(hb.get(&dx, (size_t)n));
+    TRY(hb.get(&dy, (size_t)n));
+    PGA_CUDA(cudaMemcpy(dx, x, sizeof(double) * n, cudaMemcpyHostToDevice));
+    TRY(launch_fast_ln(dx, n, c->lgtab, c->N, dy, c->stream));
+    PGA_CUDA(cudaStreamSynchronize(c->stream));
+    PGA_CUDA(cudaMemcpy(out, dy, sizeof(double) * n, cudaMemcpyDeviceToHost));
     return PGA_OK;
 }
 

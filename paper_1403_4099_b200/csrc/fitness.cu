@@ -247,6 +247,17 @@ __device__ __forceinline__ double eq8_term(int n, double c, const double *__rest
     return (__ldg(lgn + n) - log(ch)) + (nd - 1.0) * (__ldg(lgnn + n) - log(n2 - ch));
 }
 
+// The same summand with the table-driven log (label-sparse pass): its
+// clusters all have c > n >= 2 and n^2 - c >= 1e-9, positive normals.
+__device__ __forceinline__ double eq8_term_fast(int n, double c, const double *__restrict__ lgn,
+                                                const double *__restrict__ lgnn,
+                                                const double2 *__restrict__ lnt) {
+    if (!(c > (double)n)) return 0.0;
+    const double nd = (double)n, n2 = nd * nd;
+    const double ch = fmin(c, n2 - 1e-9);
+    return (__ldg(lgn + n) - fast_ln(ch, lnt)) + (nd - 1.0) * (__ldg(lgnn + n) - fast_ln(n2 - ch, lnt));
+}
+
 // Fold (warp-wide) of NC chromosomes at once (independent chains -> ILP):
 // lane per gene; n_s by a shared-memory integer atomic, and c_s = sum of V_i
 // over the cluster accumulated in 64-bit fixed point (V * 2^S, S = 62 -
@@ -660,6 +671,7 @@ struct SparseArgs {
     int nblocks;
     double fx_scale, fx_inv;
     const double *lgn, *lgnn;
+    const double2 *lnt;           // fast_ln table (after lgn, lgnn in the ctx's lgtab)
     const double *ptab;           // [N][ldc] Eq. 8 term of every pair cluster {i, j} (k_pairtab)
     pga::CCSlot *cc;              // cluster cache (null = off)
     uint32_t cc_mask;             // slots - 1
@@ -909,7 +921,7 @@ __global__ void __launch_bounds__(SPW * 32, SPW == 16 ? PGA_SP_MINB : 1) k_fitne
                     2 * (__double2ll_rn(__ldg(C + (size_t)g0 * a.ldc + g1) * a.fx_scale) +
                          __double2ll_rn(__ldg(C + (size_t)g0 * a.ldc + g2) * a.fx_scale) +
                          __double2ll_rn(__ldg(C + (size_t)g1 * a.ldc + g2) * a.fx_scale));
-                f = eq8_term(n, (double)acc * a.fx_inv, a.lgn, a.lgnn);
+                f = eq8_term_fast(n, (double)acc * a.fx_inv, a.lgn, a.lgnn, a.lnt);
                 npair += 3;
             }
             fsum += f;
@@ -1065,7 +1077,7 @@ __global__ void __launch_bounds__(SPW * 32, SPW == 16 ? PGA_SP_MINB : 1) k_fitne
             if (nh & 0x8000u) {
                 f = __longlong_as_double((long long)cent[o].x);
             } else {
-                f = eq8_term((int)nh, cval[o], a.lgn, a.lgnn);
+                f = eq8_term_fast((int)nh, cval[o], a.lgn, a.lgnn, a.lnt);
                 if (use_cache && nh >= (uint32_t)CC_NMIN) {
                     const ulonglong2 e = cent[o];
                     cc_insert(a.cc, a.cc_mask, a.cc_state, e.x, e.y, nh, __double_as_longlong(f));
@@ -1114,12 +1126,12 @@ __global__ void __launch_bounds__(SPW * 32, SPW == 16 ? PGA_SP_MINB : 1) k_fitne
 // same eq8_term -- identical to what a walk of that pair would give.
 __global__ void k_pairtab(const double *__restrict__ C, int ldc, const double *__restrict__ diag, int N,
                           double fx_scale, double fx_inv, const double *__restrict__ lgn,
-                          const double *__restrict__ lgnn, double *T) {
+                          const double *__restrict__ lgnn, const double2 *__restrict__ lnt, double *T) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y;
     if (j >= N) return;
     const long long acc = __double2ll_rn(diag[i] * fx_scale) + __double2ll_rn(diag[j] * fx_scale) +
                           2 * __double2ll_rn(C[(size_t)i * ldc + j] * fx_scale);
-    T[(size_t)i * ldc + j] = (i == j) ? 0.0 : eq8_term(2, (double)acc * fx_inv, lgn, lgnn);
+    T[(size_t)i * ldc + j] = (i == j) ? 0.0 : eq8_term_fast(2, (double)acc * fx_inv, lgn, lgnn, lnt);
 }
 
 }  // namespace
@@ -1186,13 +1198,24 @@ int make_c_tmap(CUtensorMap *tm, const double *C, int N, int ldc) {
 
 __global__ void k_logtab(int N, double *t) {
     const int n = blockIdx.x * blockDim.x + threadIdx.x;
+    if (n < LN_TAB) {   // fast_ln table: ln c_j, 1 / c_j
+        const double c = 1.0 + (n + 0.5) / (double)LN_TAB;
+        t[2 * (N + 1) + 2 * n] = log(c);
+        t[2 * (N + 1) + 2 * n + 1] = 1.0 / c;
+    }
     if (n > N) return;
     t[n] = n >= 1 ? log((double)n) : 0.0;
     t[N + 1 + n] = n >= 2 ? log((double)n * n - n) : 0.0;
 }
 
+// Test hook kernel: fast_ln of x[0..n) (tests/test_gpu_checks.py).
+__global__ void k_fast_ln(const double *x, int64_t n, const double *tab, double *out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = fast_ln(x[i], reinterpret_cast<const double2 *>(tab));
+}
+
 int launch_logtab(pga_ctx *c, cudaStream_t s) {
-    k_logtab<<<(c->N + 1 + 255) / 256, 256, 0, s>>>(c->N, c->lgtab);
+    k_logtab<<<(std::max(c->N + 1, LN_TAB) + 255) / 256, 256, 0, s>>>(c->N, c->lgtab);
     PGA_LAUNCHED();
     return PGA_OK;
 }
@@ -1206,12 +1229,19 @@ void fx_scale_of(int N, double *scale, double *inv) {
     *inv = ldexp(1.0, bits - 62);
 }
 
+int launch_fast_ln(const double *x, int64_t n, const double *lgtab, int N, double *out, cudaStream_t s) {
+    k_fast_ln<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(x, n, lgtab + 2 * (N + 1), out);
+    PGA_LAUNCHED();
+    return PGA_OK;
+}
+
 int launch_pairtab(pga_ctx *c, cudaStream_t s) {
     if (!c->ptab) return PGA_OK;
     double sc, inv;
     fx_scale_of(c->N, &sc, &inv);
     dim3 grid((unsigned)((c->N + 127) / 128), (unsigned)c->N);
-    k_pairtab<<<grid, 128, 0, s>>>(c->C, c->ldc, c->diag, c->N, sc, inv, c->lgtab, c->lgtab + (c->N + 1), c->ptab);
+    k_pairtab<<<grid, 128, 0, s>>>(c->C, c->ldc, c->diag, c->N, sc, inv, c->lgtab, c->lgtab + (c->N + 1),
+                                   reinterpret_cast<const double2 *>(c->lgtab + 2 * (c->N + 1)), c->ptab);
     PGA_LAUNCHED();
     return PGA_OK;
 }
@@ -1306,6 +1336,7 @@ int launch_fitness_range(pga_ctx *c, const FitBufs &b, int64_t begin, int64_t en
         sp.fx_inv = a.fx_inv;
         sp.lgn = a.lgn;
         sp.lgnn = a.lgnn;
+        sp.lnt = reinterpret_cast<const double2 *>(c->lgtab + 2 * (N + 1));
         sp.ptab = c->ptab;
         sp.cc = c->cc_on ? c->cc : nullptr;
         sp.cc_mask = c->cc_mask;

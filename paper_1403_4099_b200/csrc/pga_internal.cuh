@@ -86,6 +86,7 @@ enum : uint32_t {
 
 constexpr int PROF_EV = 9;     // phase marks per profiled generation
 constexpr int CB = 32;         // chromosomes per fitness CTA tile (one per lane)
+constexpr int LN_TAB = 128;    // table-driven log: c_j = 1 + (j + 1/2) / 128
 constexpr int SPARSE_MAX_N = 2048;   // largest N with a label-sparse pass (cluster cache, pair table)
 
 // Cluster-cache slot (k_fitness_sparse): exact fixed-point c_s of a member
@@ -145,7 +146,8 @@ struct pga_ctx {
     // correlation matrix
     double *C = nullptr;
     double *diag = nullptr;
-    double *lgtab = nullptr;  // [2 (N+1)]: log n, log(n^2 - n) for the Eq. 8 fold (Q30)
+    double *lgtab = nullptr;  // [2 (N+1)]: log n, log(n^2 - n) for the Eq. 8 fold (Q30); then
+                              // [2 LN_TAB] {ln c_j, 1 / c_j} of the table-driven log (fast_ln)
     uint8_t *sflag = nullptr; // [Pcap / CB]: block evaluated by the label-sparse pass (f2)
     double sparse_theta = -1.0;   // < 0: automatic (sparse_theta_eff)
     int32_t *sp_live = nullptr;  // device [6]: sparse-pass hysteresis (see k_fitness_sparse)
@@ -336,6 +338,30 @@ __device__ __forceinline__ unsigned lanemask_lt() {
     unsigned m;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
     return m;
+}
+
+// Natural log of a positive normal x, table-driven (the label-sparse pass's
+// Eq. 8 terms): x = 2^e m, m in [1, 2); c = 1 + (j + 1/2)/128 for the top 7
+// mantissa bits j; r = m (1/c) - 1 (one rounding, |r| < 2^-8);
+// ln x = e ln 2 + ln c + log1p(r), log1p by its degree-7 Taylor polynomial
+// (truncation < r^8/8 < 7e-21).  tab[2j] = ln c (libm), tab[2j+1] = 1/c.
+// Absolute error ~2e-16 (a few ulp of the result), 17 instructions instead
+// of the library's ~45; pinned against libm by tests/test_gpu_checks.py.
+__device__ __forceinline__ double fast_ln(double x, const double2 *__restrict__ tab) {
+    const long long b = __double_as_longlong(x);
+    const int e = (int)(b >> 52) - 1023;
+    const int j = (int)((b >> 45) & (pga::LN_TAB - 1));
+    const double m = __longlong_as_double((b & 0x000FFFFFFFFFFFFFll) | 0x3FF0000000000000ll);
+    const double2 t = __ldg(tab + j);
+    const double r = fma(m, t.y, -1.0);
+    double p = fma(r, 1.0 / 7.0, -1.0 / 6.0);
+    p = fma(p, r, 1.0 / 5.0);
+    p = fma(p, r, -1.0 / 4.0);
+    p = fma(p, r, 1.0 / 3.0);
+    p = fma(p, r, -1.0 / 2.0);
+    p = fma(p, r, 1.0);
+    const double lnm = fma(p, r, t.x);
+    return fma((double)e, 0.69314718055994530942, fma((double)e, 2.3190468138462996e-17, lnm));
 }
 
 // Summand of Eq. 8 for one cluster with readings Q2/Q3.

@@ -71,3 +71,24 @@ def test_atomic_kernels_bit_identical_run_to_run(pga, orc, cfg, P, theta):
     a, b = out
     for x, y in zip(a, b):
         assert np.array_equal(np.asarray(x), np.asarray(y))
+
+
+def test_fast_ln_matches_libm(pga):
+    """The label-sparse pass's table-driven ln (fitness.cu fast_ln) against
+    numpy's correctly rounded log over the range the Eq. 8 terms use
+    (c in (2, 4.2e6), n^2 - c down to 1e-9): a few ulp of the result, far
+    inside the 1e-9 max(1, |L|) parity bound."""
+    rng = np.random.default_rng(5)
+    x = np.concatenate([np.exp(rng.uniform(np.log(1e-9), np.log(5e6), 200000)),
+                        2.0 ** np.arange(-30, 23), np.nextafter(2.0 ** np.arange(-30, 23), 0),
+                        1.0 + (np.arange(129) / 128.0), 1.0 + (np.arange(128) + 0.5) / 128.0,
+                        np.array([1.0, 2.0, 3.0, 1e-9, 4.2e6])])
+    ctx = pga.pga_create(np.eye(4), pga.pga_params_default(pop_size=4, elite=1))
+    try:
+        got = pga.pga_op_fast_ln(ctx, x)
+    finally:
+        pga.pga_destroy(ctx)
+    want = np.log(x)
+    err = np.abs(got - want)
+    assert err.max() <= 4e-16 * np.maximum(1.0, np.abs(want)).max()
+    assert (err <= 8 * np.spacing(np.maximum(np.abs(want), 1e-300)) + 3e-16).all()
