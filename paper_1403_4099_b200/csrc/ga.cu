@@ -585,8 +585,23 @@ k_select_small(int what, const double *__restrict__ L, int P, int M, int selecti
 #define PGA_SORT_RUN 1024
 #endif
 // bitonic runs in shared memory (RUN * 12 B); 1024 measured best of 1024..4096
-constexpr int RUN = PGA_SORT_RUN, RUN_T = RUN / 2 < 1024 ? RUN / 2 : 1024;
+constexpr int RUN = PGA_SORT_RUN, RUN_T = RUN;   // one thread per item
+static_assert(RUN <= 1024, "one CTA thread per run item");
 
+// compare-exchange of a bitonic stage with the partner lane (stride < 32):
+// keep the smaller (key, index) when keep_min, else the larger
+__device__ __forceinline__ void cs_exchange(uint64_t &k, uint32_t &v, int partner_lane_xor, bool keep_min) {
+    const uint64_t ok = __shfl_xor_sync(0xFFFFFFFFu, k, partner_lane_xor);
+    const uint32_t ov = __shfl_xor_sync(0xFFFFFFFFu, v, partner_lane_xor);
+    const bool other_less = kv_less(ok, ov, k, v);
+    if (other_less == keep_min) {
+        k = ok;
+        v = ov;
+    }
+}
+
+// One thread per item: bitonic stages with stride < 32 run as warp shuffles
+// (no barrier), larger strides exchange through shared memory.
 __global__ void __launch_bounds__(RUN_T)
 k_sort_runs(const double *__restrict__ L, int64_t P, uint64_t *keys, int32_t *idx, const int32_t *done) {
     pdl_wait();
@@ -595,44 +610,38 @@ k_sort_runs(const double *__restrict__ L, int64_t P, uint64_t *keys, int32_t *id
     __shared__ uint64_t sk[RUN];
     __shared__ uint32_t sv[RUN];
     const int tid = threadIdx.x;
-    const int64_t base = (int64_t)blockIdx.x * RUN;
-    for (int t = tid; t < RUN; t += RUN_T) {
-        const int64_t i = base + t;
-        if (i < P) {
-            double x = L[i];
-            if (x == 0.0) x = 0.0;
-            sk[t] = ~(uint64_t)__double_as_longlong(x);
-            sv[t] = (uint32_t)i;
-        } else {
-            sk[t] = ~0ull;
-            sv[t] = 0xFFFFFFFFu;
-        }
+    const int64_t i = (int64_t)blockIdx.x * RUN + tid;
+    uint64_t k = ~0ull;
+    uint32_t v = 0xFFFFFFFFu;
+    if (i < P) {
+        double x = L[i];
+        if (x == 0.0) x = 0.0;
+        k = ~(uint64_t)__double_as_longlong(x);
+        v = (uint32_t)i;
     }
-    __syncthreads();
-    for (int size = 2; size <= RUN; size <<= 1)
+    for (int size = 2; size <= RUN; size <<= 1) {
+        const bool up = (tid & size) == 0;
         for (int stride = size >> 1; stride > 0; stride >>= 1) {
-#pragma unroll
-            for (int r = 0; r < RUN / (2 * RUN_T); ++r) {
-                const int t = tid + r * RUN_T;
-                const int i = 2 * t - (t & (stride - 1)), j = i + stride;
-                const bool up = (i & size) == 0;
-                const uint64_t ki = sk[i], kj = sk[j];
-                const uint32_t vi = sv[i], vj = sv[j];
-                if (kv_less(kj, vj, ki, vi) == up) {
-                    sk[i] = kj;
-                    sk[j] = ki;
-                    sv[i] = vj;
-                    sv[j] = vi;
+            const bool lower = (tid & stride) == 0;
+            if (stride < 32) {
+                cs_exchange(k, v, stride, lower == up);
+            } else {
+                __syncthreads();
+                sk[tid] = k;
+                sv[tid] = v;
+                __syncthreads();
+                const uint64_t ok = sk[tid ^ stride];
+                const uint32_t ov = sv[tid ^ stride];
+                if (kv_less(ok, ov, k, v) == (lower == up)) {
+                    k = ok;
+                    v = ov;
                 }
             }
-            __syncthreads();
         }
-    for (int t = tid; t < RUN; t += RUN_T) {
-        const int64_t o = base + t;
-        if (o < P) {
-            keys[o] = sk[t];
-            idx[o] = (int32_t)sv[t];
-        }
+    }
+    if (i < P) {
+        keys[i] = k;
+        idx[i] = (int32_t)v;
     }
 }
 
@@ -653,77 +662,108 @@ __device__ __forceinline__ bool key_before(uint64_t ka, uint32_t ia, uint64_t kb
     return ka < kb || (ka == kb && ia < ib);
 }
 
+// WAY-way merge level (WAY = 2 or 4): runs of width w are merged in groups
+// of WAY into runs of width WAY * w.  An item's new position = group start +
+// its offset in its own run + the number of items before it in each sibling
+// run.  All siblings are searched at once: their samples are staged in one
+// round trip, then their windows in a second one.
+template <int WAY>
 __global__ void __launch_bounds__(MERGE_T) k_merge_level(const uint64_t *__restrict__ ks,
                                                          const int32_t *__restrict__ is, int64_t P, int64_t w,
                                                          uint64_t *kd, int32_t *id, int32_t *rank_out,
                                                          const int32_t *done) {
+    constexpr int NSIB = WAY - 1, CAP = MERGE_CAP / (WAY == 2 ? 1 : 2);
     pdl_wait();
     pdl_trigger();
     if (done && *done) return;
-    __shared__ uint64_t sk[MERGE_CAP];
-    __shared__ uint32_t si[MERGE_CAP];
-    __shared__ int64_t s_lo, s_hi;
+    __shared__ uint64_t sk[NSIB][CAP];
+    __shared__ uint32_t si[NSIB][CAP];
+    __shared__ int64_t s_lo[NSIB], s_hi[NSIB];
     const int tid = threadIdx.x;
     const int64_t c0 = (int64_t)blockIdx.x * MERGE_T;
     if (c0 >= P) return;
     const int64_t g = c0 + tid;
     const bool valid = g < P;
-    const int64_t blk = c0 / (2 * w) * (2 * w);
-    const bool left = c0 - blk < w;
-    const int64_t sib = left ? blk + w : blk;
-    const int64_t off = (left ? c0 - blk : c0 - blk - w) + tid;
-    const int64_t slen = max((int64_t)0, min(w, P - sib));
+    const int64_t blk = c0 / (WAY * w) * (WAY * w);
+    const int q = (int)((c0 - blk) / w);                     // own run in the group
+    const int64_t off = c0 - blk - (int64_t)q * w + tid;
     const int64_t last = min((int64_t)MERGE_T, P - c0) - 1;   // last valid thread
     const uint64_t ke = valid ? ks[g] : ~0ull;
     const uint32_t ie = valid ? (uint32_t)is[g] : 0xFFFFFFFFu;
-    const uint64_t *sk_g = ks + sib;
-    const int32_t *si_g = is + sib;
-
-    // (1) window [lo, hi) of the rank from the sibling's MS-sample
-    int64_t lo = 0, hi = slen;
-    const int64_t ns = (slen + MERGE_MS - 1) / MERGE_MS;
-    if (ns > 0 && ns <= MERGE_CAP) {
-        for (int64_t j = tid; j < ns; j += MERGE_T) {
-            sk[j] = __ldg(sk_g + j * MERGE_MS);
-            si[j] = (uint32_t)__ldg(si_g + j * MERGE_MS);
-        }
-        __syncthreads();
-        int64_t a = 0, b = ns;                        // samples before the item
-        while (a < b) {
-            const int64_t m = (a + b) >> 1;
-            if (key_before(sk[m], si[m], ke, ie)) a = m + 1;
-            else b = m;
-        }
-        lo = a > 0 ? (a - 1) * MERGE_MS + 1 : 0;
-        hi = min(slen, a * MERGE_MS);
-        __syncthreads();                              // samples read: the buffer is reused
+    int64_t sib[NSIB], slen[NSIB], ns[NSIB], lo[NSIB], hi[NSIB];
+#pragma unroll
+    for (int j = 0; j < NSIB; ++j) {
+        const int r = j < q ? j : j + 1;
+        sib[j] = blk + (int64_t)r * w;
+        slen[j] = max((int64_t)0, min(w, P - sib[j]));
+        ns[j] = (slen[j] + MERGE_MS - 1) / MERGE_MS;
+        lo[j] = 0;
+        hi[j] = slen[j];
     }
-    // (2) the CTA's span of windows, staged when it fits
-    if (tid == 0) s_lo = lo;
-    if (tid == last) s_hi = hi;
+    // (1) samples of every sibling, one round trip
+#pragma unroll
+    for (int j = 0; j < NSIB; ++j)
+        if (ns[j] > 0 && ns[j] <= CAP)
+            for (int64_t t = tid; t < ns[j]; t += MERGE_T) {
+                sk[j][t] = __ldg(ks + sib[j] + t * MERGE_MS);
+                si[j][t] = (uint32_t)__ldg(is + sib[j] + t * MERGE_MS);
+            }
     __syncthreads();
-    const int64_t Lo = s_lo, Hi = s_hi;
-    if (!valid) lo = hi = Lo;                         // beyond P: no search
-    if (Hi - Lo <= MERGE_CAP) {
-        for (int64_t p = Lo + tid; p < Hi; p += MERGE_T) {
-            sk[p - Lo] = __ldg(sk_g + p);
-            si[p - Lo] = (uint32_t)__ldg(si_g + p);
+#pragma unroll
+    for (int j = 0; j < NSIB; ++j)
+        if (ns[j] > 0 && ns[j] <= CAP) {
+            int64_t a = 0, b = ns[j];                 // samples before the item
+            while (a < b) {
+                const int64_t m = (a + b) >> 1;
+                if (key_before(sk[j][m], si[j][m], ke, ie)) a = m + 1;
+                else b = m;
+            }
+            lo[j] = a > 0 ? (a - 1) * MERGE_MS + 1 : 0;
+            hi[j] = min(slen[j], a * MERGE_MS);
         }
-        __syncthreads();
-        while (lo < hi) {
-            const int64_t m = (lo + hi) >> 1;
-            if (key_before(sk[m - Lo], si[m - Lo], ke, ie)) lo = m + 1;
-            else hi = m;
+    __syncthreads();                                  // samples read: the buffers are reused
+    // (2) the CTA's span of windows in every sibling, staged when it fits
+#pragma unroll
+    for (int j = 0; j < NSIB; ++j) {
+        if (tid == 0) s_lo[j] = lo[j];
+        if (tid == last) s_hi[j] = hi[j];
+    }
+    __syncthreads();
+    int64_t Lo[NSIB], Hi[NSIB];
+#pragma unroll
+    for (int j = 0; j < NSIB; ++j) {
+        Lo[j] = s_lo[j];
+        Hi[j] = s_hi[j];
+        if (!valid) lo[j] = hi[j] = Lo[j];            // beyond P: no search
+        if (Hi[j] - Lo[j] <= CAP)
+            for (int64_t p = Lo[j] + tid; p < Hi[j]; p += MERGE_T) {
+                sk[j][p - Lo[j]] = __ldg(ks + sib[j] + p);
+                si[j][p - Lo[j]] = (uint32_t)__ldg(is + sib[j] + p);
+            }
+    }
+    __syncthreads();
+    int64_t pos = blk + off;
+#pragma unroll
+    for (int j = 0; j < NSIB; ++j) {
+        int64_t l = lo[j], h = hi[j];
+        if (Hi[j] - Lo[j] <= CAP) {
+            while (l < h) {
+                const int64_t m = (l + h) >> 1;
+                if (key_before(sk[j][m - Lo[j]], si[j][m - Lo[j]], ke, ie)) l = m + 1;
+                else h = m;
+            }
+        } else {
+            const uint64_t *k_g = ks + sib[j];
+            const int32_t *i_g = is + sib[j];
+            while (l < h) {
+                const int64_t m = (l + h) >> 1;
+                if (key_before(__ldg(k_g + m), (uint32_t)__ldg(i_g + m), ke, ie)) l = m + 1;
+                else h = m;
+            }
         }
-    } else {
-        while (lo < hi) {
-            const int64_t m = (lo + hi) >> 1;
-            if (key_before(__ldg(sk_g + m), (uint32_t)__ldg(si_g + m), ke, ie)) lo = m + 1;
-            else hi = m;
-        }
+        pos += l;
     }
     if (!valid) return;
-    const int64_t pos = blk + off + lo;
     PGA_DCHECK(pos >= 0 && pos < P);
     if (kd) kd[pos] = ke;
     id[pos] = (int32_t)ie;
@@ -761,16 +801,6 @@ __host__ __device__ __forceinline__ int csel_run(int P) {
 static size_t csel_smem(int R) {
     // own run: sk sL sx si srank; copies of the other runs' keys and indices
     return (size_t)R * (8 + 8 + 8 + 4 + 4) + (size_t)(CSEL_CL - 1) * R * 12 + 256;
-}
-
-__device__ __forceinline__ void cs_exchange(uint64_t &k, uint32_t &v, int partner_lane_xor, bool keep_min) {
-    const uint64_t ok = __shfl_xor_sync(0xFFFFFFFFu, k, partner_lane_xor);
-    const uint32_t ov = __shfl_xor_sync(0xFFFFFFFFu, v, partner_lane_xor);
-    const bool other_less = kv_less(ok, ov, k, v);
-    if (other_less == keep_min) {
-        k = ok;
-        v = ov;
-    }
 }
 
 __global__ void __launch_bounds__(CSEL_T, 2)
@@ -1575,15 +1605,24 @@ static int sort_order(const double *L, int64_t P, int32_t *order, int32_t *rank,
     PGA_LAUNCH_PDL(k_sort_runs, dim3(nruns), dim3(RUN_T), 0, s, L, P, kA, iA, done);
     const unsigned nb = (unsigned)((P + 255) / 256);
     if (nruns == 1) {   // one run: copy its indices out through a width-P "merge"
-        PGA_LAUNCH_PDL(k_merge_level, dim3(nb), dim3(MERGE_T), 0, s, (const uint64_t *)kA, (const int32_t *)iA,
+        PGA_LAUNCH_PDL(k_merge_level<2>, dim3(nb), dim3(MERGE_T), 0, s, (const uint64_t *)kA, (const int32_t *)iA,
                        P, P, (uint64_t *)nullptr, order, rank, done);
         return PGA_OK;
     }
-    for (int64_t w = RUN; w < P; w *= 2) {
-        const bool last = 2 * w >= P;
-        PGA_LAUNCH_PDL(k_merge_level, dim3(nb), dim3(MERGE_T), 0, s, (const uint64_t *)kA, (const int32_t *)iA,
-                       P, w, last ? (uint64_t *)nullptr : kB, last ? order : iB, last ? rank : (int32_t *)nullptr,
-                       done);
+    // 4-way levels while two more doublings are needed, a 2-way level last
+    // (P = 65536: three levels instead of six)
+    for (int64_t w = RUN; w < P;) {
+        const int way = (2 * w < P) ? 4 : 2;
+        const bool last = (int64_t)way * w >= P;
+        if (way == 4)
+            PGA_LAUNCH_PDL(k_merge_level<4>, dim3(nb), dim3(MERGE_T), 0, s, (const uint64_t *)kA,
+                           (const int32_t *)iA, P, w, last ? (uint64_t *)nullptr : kB, last ? order : iB,
+                           last ? rank : (int32_t *)nullptr, done);
+        else
+            PGA_LAUNCH_PDL(k_merge_level<2>, dim3(nb), dim3(MERGE_T), 0, s, (const uint64_t *)kA,
+                           (const int32_t *)iA, P, w, last ? (uint64_t *)nullptr : kB, last ? order : iB,
+                           last ? rank : (int32_t *)nullptr, done);
+        w *= way;
         uint64_t *tk = kA;
         kA = kB;
         kB = tk;
