@@ -843,6 +843,13 @@ def bench_f1(args):
         if args.stream:
             Xp = torch.from_numpy(Xs).pin_memory()
         ke = max(1, min(K, 3))
+        # one untimed call first: the host path's first call also creates the
+        # stream-ordered memory pool (~80 ms once per process)
+        if args.stream:
+            pga.pga_batch_run(pga.pga_corr_stream(Xp.numpy(), lam=0.98, warm=T, stride=stride, q=0.0,
+                                                  device=local), params)
+        else:
+            pga.pga_batch_run(Cp.numpy(), params)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(ke):

@@ -1353,14 +1353,17 @@ int launch_fitness_range(pga_ctx *c, const FitBufs &b, int64_t begin, int64_t en
     if (ev) PGA_CUDA(prof_record(ev[1], s));   // dense kernel starts here
     {
         // row tiles per CTA: a whole chromosome block per CTA (all nRT tiles,
-        // cpb = 1) when there are enough blocks to fill the GPU (>= 1024:
-        // C4, C5), else one tile per CTA.  Every CTA of a block exits at once
+        // cpb = 1) when the label-sparse pass runs before this launch and
+        // there are enough blocks to fill the GPU (>= 1024: C4, C5), else one
+        // tile per CTA (a dense-only launch keeps the tiles of a block
+        // concurrent, so their fold scratch V stays in L2: ncu DRAM 140 MB per
+        // C4 launch with one tile per CTA, 185 MB with whole blocks).  Every CTA of a block exits at once
         // when the block went label-sparse, so in GA generations where the
         // sparse pass took every block this launch costs nCB instead of
         // nRT * nCB empty CTAs (C4: 8.2 instead of 22.5 us); a dense sweep
         // runs the same either way (C4: 1.447 vs 1.443 ms; uneven splits,
         // e.g. 6 + 2 tiles, measured slower: 1.58 ms).
-        int F = a.nCB >= FIT_BLOCKS_PER_CTA_MIN ? a.nRT : 1;
+        int F = (a.sflag && a.nCB >= FIT_BLOCKS_PER_CTA_MIN) ? a.nRT : 1;
         if (const char *e = std::getenv("PGA_FIT_F")) F = std::max(1, std::min(a.nRT, std::atoi(e)));
         a.F = F;
         a.cpb = (a.nRT + F - 1) / F;

@@ -1,0 +1,7 @@
+O=gpurun_out/r02s; mkdir -p $O
+timeout 1800 python -m pytest tests -m gpu -q -x > $O/pytest.log 2>&1; echo "rc=$?" >> $O/pytest.log
+timeout 600 python bench.py --steps 100 --warmup 5 --no-cpu --no-e2e > $O/c4.json 2>> $O/bench.err
+timeout 600 python bench.py --steps 200 --warmup 5 --no-cpu --no-e2e --island-load 8 > $O/il8.json 2>> $O/bench.err
+timeout 600 python bench.py --steps 200 --warmup 5 --no-cpu --no-e2e --island-load 4 > $O/il4.json 2>> $O/bench.err
+timeout 600 python bench.py --steps 200 --warmup 5 --no-cpu --no-e2e --island-load 2 > $O/il2.json 2>> $O/bench.err
+timeout 900 /usr/local/cuda/bin/ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv --log-file $O/launches_c4.csv python bench.py --steps 3 --warmup 3 --no-cpu --no-e2e > $O/ncu.log 2>&1

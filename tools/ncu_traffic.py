@@ -31,8 +31,8 @@ METRICS = {
     "launch__block_size": "block",
     "sm__cycles_elapsed.avg.per_second": "sm_clock_hz",
 }
-UNIT = {"Mbyte": 1e6, "Kbyte": 1e3, "Gbyte": 1e9, "byte": 1.0, "usecond": 1.0, "msecond": 1e3,
-        "nsecond": 1e-3, "Ghz": 1e9, "Mhz": 1e6, "hz": 1.0}
+UNIT = {"Mbyte": 1e6, "Kbyte": 1e3, "Gbyte": 1e9, "byte": 1.0, "usecond": 1.0, "us": 1.0, "msecond": 1e3,
+        "ms": 1e3, "nsecond": 1e-3, "ns": 1e-3, "Ghz": 1e9, "Mhz": 1e6, "hz": 1.0, "GHz": 1e9, "MHz": 1e6}
 
 
 def read(rep):
