@@ -267,34 +267,59 @@ __device__ __forceinline__ double eq8_term_fast(int n, double c, const double *_
 // per V, 6e-14 at N = 500) is below the fp64 summation error it replaces.
 // Then Eq. 8 (Q1-Q3) for labels up to the chromosome's largest.
 template <int NC>
-__device__ __forceinline__ void fold_multi(const uint16_t *const (&lab)[NC], const double *const (&v)[NC],
+__device__ __forceinline__ void fold_multi(const uint16_t *const (&lab)[NC], int64_t lstride,
+                                           const double *const (&v)[NC],
                                            int N, double *const (&cs)[NC], int32_t *const (&ns)[NC],
                                            int lane, double *const (&L_out)[NC],
                                            uint16_t *const (&top_out)[NC], double scale, double inv_scale,
                                            const double *__restrict__ lgn, const double *__restrict__ lgnn) {
     // cs / ns were zeroed by the caller (all-zero bits == integer 0)
-    // software pipeline: loads of chunk c+2 are issued while chunk c folds
+    // software pipeline: loads of chunk c+2 are issued while chunk c folds.
+    // Gene-major labels of two adjacent chromosomes (p even, p + 1) are one
+    // aligned 32-bit word per gene: one load for the pair.
+    const bool pair = (NC == 2) && lstride != 1 && lab[NC - 1] == lab[0] + 1;
+    auto ld = [&](int q, int i) -> uint32_t {
+        if (i >= N) return 0u;
+        if (pair) {
+            const uint32_t w = *reinterpret_cast<const uint32_t *>(lab[0] + i * lstride);
+            return q ? (w >> 16) : (w & 0xFFFFu);
+        }
+        return (uint32_t)lab[q][i * lstride];
+    };
     uint32_t s_n1[NC], s_n2[NC];
     double v_n1[NC], v_n2[NC];
+    if (pair) {
+        const uint32_t w1 = lane < N ? *reinterpret_cast<const uint32_t *>(lab[0] + lane * lstride) : 0u;
+        const uint32_t w2 = 32 + lane < N ? *reinterpret_cast<const uint32_t *>(lab[0] + (32 + lane) * lstride) : 0u;
+        s_n1[0] = w1 & 0xFFFFu;
+        s_n1[NC - 1] = w1 >> 16;
+        s_n2[0] = w2 & 0xFFFFu;
+        s_n2[NC - 1] = w2 >> 16;
+    } else {
+#pragma unroll
+        for (int q = 0; q < NC; ++q) {
+            s_n1[q] = ld(q, lane);
+            s_n2[q] = ld(q, 32 + lane);
+        }
+    }
 #pragma unroll
     for (int q = 0; q < NC; ++q) {
-        const int i1 = lane, i2 = 32 + lane;
-        s_n1[q] = (i1 < N) ? (uint32_t)lab[q][i1] : 0u;
-        v_n1[q] = (i1 < N) ? __ldcg(v[q] + i1) : 0.0;
-        s_n2[q] = (i2 < N) ? (uint32_t)lab[q][i2] : 0u;
-        v_n2[q] = (i2 < N) ? __ldcg(v[q] + i2) : 0.0;
+        v_n1[q] = (lane < N) ? __ldcg(v[q] + lane) : 0.0;
+        v_n2[q] = (32 + lane < N) ? __ldcg(v[q] + 32 + lane) : 0.0;
     }
     uint32_t kmax = 0;
     for (int base = 0; base < N; base += 32) {
         const bool valid = base + lane < N;
+        const int i3 = base + 64 + lane;
+        uint32_t w3 = 0u;
+        if (pair && i3 < N) w3 = *reinterpret_cast<const uint32_t *>(lab[0] + i3 * lstride);
 #pragma unroll
         for (int q = 0; q < NC; ++q) {
             const uint32_t s = s_n1[q];
             const double x = v_n1[q];
             s_n1[q] = s_n2[q];
             v_n1[q] = v_n2[q];
-            const int i3 = base + 64 + lane;
-            s_n2[q] = (i3 < N) ? (uint32_t)lab[q][i3] : 0u;
+            s_n2[q] = pair ? (q ? (w3 >> 16) : (w3 & 0xFFFFu)) : ld(q, i3);
             v_n2[q] = (i3 < N) ? __ldcg(v[q] + i3) : 0.0;
             if (valid) {
                 kmax = max(kmax, s);
@@ -465,7 +490,10 @@ k_fitness(const __grid_constant__ CUtensorMap tmLab0, const __grid_constant__ CU
     if (warp < a.fold_warps) {
         // NCF chromosomes per warp per pass (independent chains -> ILP)
         constexpr int NCF = 2;
-        const uint16_t *CM = par ? a.cm1 : a.cm0;
+        // labels from the gene-major copy the sweep streamed (its 64-byte
+        // rows of this block are in L2/L1), not a second DRAM read of the
+        // chromosome-major copy
+        const uint16_t *GM = par ? a.gm1 : a.gm0;
         double *csb = reinterpret_cast<double *>(smem) + (size_t)warp * NCF * N;
         int32_t *nsb = reinterpret_cast<int32_t *>(reinterpret_cast<double *>(smem) + (size_t)a.fold_warps * NCF * N) +
                        (size_t)warp * NCF * N;
@@ -481,7 +509,7 @@ k_fitness(const __grid_constant__ CUtensorMap tmLab0, const __grid_constant__ CU
 #pragma unroll
             for (int c = 0; c < NCF; ++c) {
                 const int64_t pc = (p + c < a.P) ? p + c : p;   // duplicate work at an odd tail
-                lab[c] = CM + pc * a.ldn;
+                lab[c] = GM + pc;
                 vv[c] = a.V + pc * a.ldn;
                 cs[c] = csb + c * N;
                 ns[c] = nsb + c * N;
@@ -495,7 +523,7 @@ k_fitness(const __grid_constant__ CUtensorMap tmLab0, const __grid_constant__ CU
                 for (int k = lane; k < N * NCF / 2; k += 32) n2[k] = make_uint2(0u, 0u);
                 __syncwarp();
             }
-            fold_multi<NCF>(lab, vv, N, cs, ns, lane, Lo, to, a.fx_scale, a.fx_inv, a.lgn, a.lgnn);
+            fold_multi<NCF>(lab, a.Pcap, vv, N, cs, ns, lane, Lo, to, a.fx_scale, a.fx_inv, a.lgn, a.lgnn);
             // V of these chromosomes is dead: drop its L2 lines without a
             // DRAM write-back (rows are 128-byte aligned, ldn % 16 == 0)
 #pragma unroll
