@@ -151,7 +151,7 @@ void free_ctx(pga_ctx *c) {
                     c->stats_part, c->stats_ctr,
                     c->cc_keys, c->ptab, c->pop[0], c->pop[1], c->popT[0], c->popT[1], c->V, c->L,
                     c->top, c->keys_in, c->keys_out, c->idx_in, c->order, c->q, c->rank,
-                    c->sel, c->sigma, c->breed_ctr, c->st,
+                    c->sel, c->sigma, c->breed_ctr, c->mmask, c->st,
                     c->best_labels, c->history, c->stage_i32, c->evCM, c->evGM, c->evL,
                     c->counters};
     for (void *p : ptrs)
@@ -491,6 +491,7 @@ int pga_create(const double *C, int32_t N, const pga_params *p, pga_ctx **out) {
     rc = rc ? rc : dalloc(&c->sel, (size_t)c->Pcap + 2);
     rc = rc ? rc : dalloc(&c->sigma, (size_t)c->Pcap + 2);
     rc = rc ? rc : dalloc(&c->breed_ctr, (size_t)1);
+    rc = rc ? rc : dalloc(&c->mmask, (size_t)c->Pcap * ((N + 31) / 32));
     rc = rc ? rc : dalloc(&c->st, 1);
     rc = rc ? rc : dalloc(&c->best_labels, (size_t)c->ldn);
     rc = rc ? rc : dalloc(&c->counters, (size_t)(c->Pcap / CB));

@@ -380,6 +380,34 @@ __global__ void k_tournament(const double *__restrict__ L, int64_t P, int64_t M,
     sel[m] = best;
 }
 
+// Mutation masks of one generation (Q13, Q27): gene i of child slot o
+// mutates iff Philox(MUT; i >> 2, p_off + o)[i & 3] < thr(p_m) -- the same
+// draws the breed would make, one bit per gene, [Pcap][mw] 32-bit words,
+// thread per word (8 Philox blocks).  They depend only on (seed, generation,
+// island, slot), so the GA computes them on its side stream beside the
+// fitness pass (launch_mates_fork); elites (o < E) are never mutated.
+__global__ void k_mutmask(uint64_t seed, uint32_t island, const int32_t *gen_ptr, const int32_t *done, int64_t P,
+                          int N, int E, int64_t p_off, uint64_t thr_m, int mw, uint32_t *mask) {
+    if (done && *done) return;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t o = t / mw;
+    const int w = (int)(t - o * mw);
+    if (o >= P || o < E) return;
+    const uint32_t gen = (uint32_t)*gen_ptr;
+    const uint32_t og = (uint32_t)(p_off + o);
+    uint32_t bits = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int blk = 8 * w + k;
+        if (4 * blk < N) {
+            const U4 u = draw(seed, pga::TAG_MUT, island, gen, (uint32_t)blk, og);
+            bits |= (((uint64_t)u.x < thr_m ? 1u : 0u) | ((uint64_t)u.y < thr_m ? 2u : 0u) |
+                     ((uint64_t)u.z < thr_m ? 4u : 0u) | ((uint64_t)u.w < thr_m ? 8u : 0u)) << (4 * k);
+        }
+    }
+    mask[o * mw + w] = bits;
+}
+
 // Mate pairing (Q10): sigma = keyed Feistel permutation of the M slots
 // (4 rounds, round function Philox(PERM; R, round)[0], cycle-walking).
 __global__ void k_mates(int64_t M, uint64_t seed, uint32_t gen, uint32_t island, int32_t *sigma,
@@ -1028,6 +1056,8 @@ struct BreedArgs {
     uint32_t gen, island;
     const int32_t *done, *gen_ptr;
     const int32_t *gm_skip;            // != 0: the label-sparse pass owns the gene-major copy (f2)
+    const uint32_t *mmask;             // GA, P > SMALL_GA_P: precomputed mutation masks [Pcap][mw] (k_mutmask)
+    int mw;                            // words per child: ceil(N / 32)
     pga::DevState *adv_st;             // GA: advance st->gen once the grid is done (null: hooks)
     uint32_t *adv_ctr;                 // CTA counter for that (reset by the last CTA)
 };
@@ -1151,9 +1181,14 @@ __global__ void __launch_bounds__(BW * 32, 3) k_breed(BreedArgs a) {
             // mutation mask of genes base+4*lane .. base+4*lane+3
             uint32_t mbits = 0;
             if (p.valid && p.mutate && base + 4 * lane < N) {
-                const U4 u = draw(a.seed, pga::TAG_MUT, a.island, gen, (uint32_t)((base >> 2) + lane), p.og);
-                mbits = ((uint64_t)u.x < a.thr_m ? 1u : 0u) | ((uint64_t)u.y < a.thr_m ? 2u : 0u) |
-                        ((uint64_t)u.z < a.thr_m ? 4u : 0u) | ((uint64_t)u.w < a.thr_m ? 8u : 0u);
+                if (a.mmask) {
+                    const uint32_t wv = a.mmask[(o0 + slot) * a.mw + (base >> 5) + (lane >> 3)];
+                    mbits = (wv >> (4 * (lane & 7))) & 0xFu;
+                } else {
+                    const U4 u = draw(a.seed, pga::TAG_MUT, a.island, gen, (uint32_t)((base >> 2) + lane), p.og);
+                    mbits = ((uint64_t)u.x < a.thr_m ? 1u : 0u) | ((uint64_t)u.y < a.thr_m ? 2u : 0u) |
+                            ((uint64_t)u.z < a.thr_m ? 4u : 0u) | ((uint64_t)u.w < a.thr_m ? 8u : 0u);
+                }
             }
             uint32_t sv[GCH / 32];
             unsigned mm[GCH / 32];
@@ -1293,9 +1328,14 @@ __global__ void __launch_bounds__(BW * 32, NB <= 2 ? 3 : PGA_B2_MINB) k_breed2(B
         }
         uint32_t mbits = 0;
         if (p.valid && p.mutate && b0 + 4 * lane < N) {
-            const U4 u = draw(a.seed, pga::TAG_MUT, a.island, gen, (uint32_t)((b0 >> 2) + lane), p.og);
-            mbits = ((uint64_t)u.x < a.thr_m ? 1u : 0u) | ((uint64_t)u.y < a.thr_m ? 2u : 0u) |
-                    ((uint64_t)u.z < a.thr_m ? 4u : 0u) | ((uint64_t)u.w < a.thr_m ? 8u : 0u);
+            if (a.mmask) {   // precomputed beside the fitness pass (k_mutmask)
+                const uint32_t wv = a.mmask[o * a.mw + (b0 >> 5) + (lane >> 3)];
+                mbits = (wv >> (4 * (lane & 7))) & 0xFu;
+            } else {
+                const U4 u = draw(a.seed, pga::TAG_MUT, a.island, gen, (uint32_t)((b0 >> 2) + lane), p.og);
+                mbits = ((uint64_t)u.x < a.thr_m ? 1u : 0u) | ((uint64_t)u.y < a.thr_m ? 2u : 0u) |
+                        ((uint64_t)u.z < a.thr_m ? 4u : 0u) | ((uint64_t)u.w < a.thr_m ? 8u : 0u);
+            }
         }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -1534,6 +1574,14 @@ static bool getenv_flag(const char *name, bool d) {
     if (!e || !e[0]) return d;
     return e[0] != '0';
 }
+
+// Mutation masks precomputed on the side stream, beside the fitness pass,
+// only while that pass leaves SMs idle (P <= MUTMASK_MAXP: an 8-GPU island of
+// C4).  At C4's P = 65536 the pass fills the GPU and the mask kernel steals its
+// issue slots: 0.5498 vs 0.5285 ms per generation (breed -11 us, sparse pass
+// +31 us); at P = 8192 0.1315 vs 0.1328 ms.  PGA_NO_MUTMASK=1 / =0 forces it.
+constexpr int64_t MUTMASK_MAXP = 8192;
+static bool mutmask_use(int64_t P) { return getenv_flag("PGA_MUTMASK_FORCE", false) || (P <= MUTMASK_MAXP && !getenv_flag("PGA_NO_MUTMASK", false)); }
 
 static size_t breed_smem(int N) { return ((size_t)2 * GCH * TS + (size_t)BS * breed_tab(N)) * sizeof(uint16_t); }
 
@@ -1828,6 +1876,10 @@ int launch_select_breed(pga_ctx *c, cudaStream_t s) {
     // checks are live (it transposes exactly the blocks the dense sweep needs)
     a.gm_skip = (sparse_theta_eff(c) > 0.0 && c->N <= SPARSE_MAX_N) ? c->sp_live : nullptr;
     a.adv_st = c->st;           // the breed's last CTA advances the generation (no k_advance)
+    if (!(c->P <= SMALL_GA_P) && c->mmask && mutmask_use(c->P)) {   // masks from the side stream
+        a.mmask = c->mmask;
+        a.mw = (c->N + 31) / 32;
+    }
     a.adv_ctr = c->breed_ctr;
     count_launch();
     if (c->N <= BREED2_MAXN)
@@ -1852,6 +1904,17 @@ int launch_mates_fork(pga_ctx *c, cudaStream_t s) {
     k_mates<<<(unsigned)((M + 255) / 256), 256, 0, c->side>>>(M, c->p.seed, 0u, (uint32_t)c->p.island, c->sigma,
                                                                &c->st->done, &c->st->gen);
     PGA_LAUNCHED();
+    if (c->mmask && mutmask_use(c->P)) {
+        BreedArgs t{};
+        fill_breed(t, c->p, c->P, c->N);
+        const int mw = (c->N + 31) / 32;
+        const int64_t nth = c->P * (int64_t)mw;
+        k_mutmask<<<(unsigned)((nth + 255) / 256), 256, 0, c->side>>>(c->p.seed, (uint32_t)c->p.island, &c->st->gen,
+                                                                       &c->st->done, c->P, c->N, c->p.elite,
+                                                                       (int64_t)c->p.island * c->P, t.thr_m, mw,
+                                                                       c->mmask);
+        PGA_LAUNCHED();
+    }
     PGA_CUDA(cudaEventRecord(c->join_side_ev, c->side));
     return PGA_OK;
 }

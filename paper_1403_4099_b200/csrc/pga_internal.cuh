@@ -178,6 +178,7 @@ struct pga_ctx {
     int32_t *sel = nullptr;
     int32_t *sigma = nullptr;
     uint32_t *breed_ctr = nullptr;     // breed CTA counter (the last CTA advances the generation)
+    uint32_t *mmask = nullptr;         // mutation masks of the generation [Pcap][ceil(N/32)] (k_mutmask)
     // state
     pga::DevState *st = nullptr;
     uint16_t *best_labels = nullptr;   // [ldn]
