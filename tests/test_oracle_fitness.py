@@ -141,6 +141,33 @@ def test_clamp_near_perfect_correlation(orc):
                               rel=1e-6)
 
 
+def test_clamp_region_properties(orc):
+    """Q3 pinned by properties a wrong clamp would break, not by retyping it:
+    (a) the term is constant for c in [n^2 - 1e-9, n^2] (the clamp is active
+    exactly there); (b) it is continuous at the clamp boundary from below;
+    (c) it increases strictly in c on (n, n^2 - 1e-9) (a dropped term or a
+    sign error in either log breaks this); (d) for a pair the clamped value
+    equals the pair closed form -ln(1 - rho^2) at rho = 1 - 5e-10 (c = 2 + 2 rho
+    = 4 - 1e-9), independent of Eq. 8's algebra."""
+    for n in (2, 3, 5, 40):
+        n2 = float(n * n)
+        top = orc.cluster_term(n, n2)
+        for c in (n2 - 1e-9, n2 - 5e-10, n2 - 1e-12, n2):
+            assert orc.cluster_term(n, c) == top
+        # below the boundary the second log is ~(n-1) ln(1/(n^2 - c)): the gap to
+        # the clamped value is ~(n-1) d / 1e-9 for small d, so it vanishes
+        d3 = max(1e-13, 8 * np.spacing(n2))      # resolvable below n^2 - 1e-9
+        below = [orc.cluster_term(n, n2 - 1e-9 - d) for d in (1e-7, 1e-11, d3)]
+        gaps = [top - b for b in below]
+        assert all(g > 0 for g in gaps) and gaps[0] > gaps[1] > gaps[2]
+        assert gaps[1] < 0.02 * (n - 1) and gaps[2] < 2.0 * (n - 1) * d3 / 1e-9
+        cs = np.linspace(n + 1e-3, n2 - 2e-9, 200)
+        f = [orc.cluster_term(n, float(c)) for c in cs]
+        assert all(b > a for a, b in zip(f, f[1:]))
+    rho = 1.0 - 5e-10
+    assert orc.cluster_term(2, 4.0) == pytest.approx(-math.log1p(-rho * rho), rel=1e-7)
+
+
 @pytest.mark.parametrize("seed", range(6))
 def test_cross_oracle_one_hot(orc, seed):
     """Eq. 5/6 double loop vs numpy diag(Z^T C Z)."""
