@@ -7,9 +7,10 @@ with it.  The arithmetic lives in ``oracle.c`` (plain fp64 C, each function
 citing PAPER.md); this module only marshals arguments through ctypes, and
 ``npref.py`` holds an independent numpy one-hot formulation used as a pin.
 
-Parity-unpinned items: the c_s -> n_s^2 clamp region (Q3)
-and the knowledge-based crossover's fidelity to the (unavailable) thesis
-operator (Q12).
+Parity-unpinned items: GPU-vs-oracle parity inside the
+c_s -> n_s^2 clamp region (Q3; the oracle's clamp itself is pinned by
+properties) and the knowledge-based crossover's fidelity to the
+(unavailable) thesis operator (Q12).
 """
 from __future__ import annotations
 
