@@ -184,7 +184,7 @@ def run_reference(args):
     N = C.shape[0]
     K, W = args.steps, args.warmup
     # size each step so the whole run stays within ~3 minutes
-    budget = 150.0 / max(1, K + W)
+    budget = float(os.environ.get("PGA_REF_BUDGET_S", "150")) / max(1, K + W)
     P = 256
     pop = orc.canonicalize(workloads.population_mix(SEED, planted, P))
     params = orc.default_params(pop=P, elite=10, p_m=2.0 / N, tol=-1.0, seed=SEED)
