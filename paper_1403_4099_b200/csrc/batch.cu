@@ -35,6 +35,11 @@ using namespace pgad;
 
 constexpr int BT = 256, BNW = BT / 32;   // threads per CTA (one CTA per matrix)
 constexpr int BMAX_N = 32, BMAX_P = 2048;
+// C row stride in shared memory: 32 doubles, so C[j][lane] sits in bank pair
+// lane mod 16 whatever row j a lane's cluster walk is on -- the lanes of
+// different clusters (different j) no longer collide (round 1: 33% of the
+// kernel's shared wavefronts were bank-conflict excess, profiles/r01l_full.md)
+constexpr int BLDC = 32;
 constexpr int TAB = 36;                  // per-thread canonicalisation table (labels 0..N)
 constexpr int EB = 8;                    // chromosomes per warp per evaluation batch
 
@@ -60,7 +65,7 @@ __host__ __device__ inline BLayout b_layout(int N, int P, int M) {
     l.oL = 0;
     size_t o = al16((size_t)8 * P);
     if (o < (size_t)BT * TAB) o = al16((size_t)BT * TAB);
-    l.oC = o;     o += al16((size_t)8 * N * N);
+    l.oC = o;     o += al16((size_t)8 * N * BLDC);   // rows padded to BLDC doubles (conflict-free, see b_evaluate)
     l.oVal = o;   o += al16((size_t)4 * n2);
     l.oRank = o;  o += al16((size_t)2 * P);
     l.oSel = o;   o += al16((size_t)2 * M);
@@ -192,7 +197,7 @@ __device__ __forceinline__ void b_evaluate(const BSmem &s, const uint8_t *pop, i
             const unsigned m = __match_any_sync(0xFFFFFFFFu, lab);
             double V = 0.0;                         // V_i = sum_{j in s_i} C_ji (ascending j)
             if (valid)
-                for (unsigned mm = m; mm; mm &= mm - 1) V += s.C[(__ffs(mm) - 1) * N + lane];
+                for (unsigned mm = m; mm; mm &= mm - 1) V += s.C[(__ffs(mm) - 1) * BLDC + lane];
             Vw[lane] = V;
             __syncwarp();
             const int n = __popc(m);
@@ -437,7 +442,7 @@ __global__ void __launch_bounds__(BT, 3) k_batch(BArgs a) {
     const uint64_t seed = a.seed + (uint64_t)b;
 
     if (a.mode != MODE_STEP)
-        for (int t = tid; t < N * N; t += BT) s.C[t] = a.C[(size_t)b * N * N + t];
+        for (int t = tid; t < N * N; t += BT) s.C[(t / N) * BLDC + t % N] = a.C[(size_t)b * N * N + t];
     if (a.mode == MODE_RUN) {
         b_init(a, s, ldb, seed);
     } else {

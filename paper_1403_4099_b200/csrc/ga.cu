@@ -1567,6 +1567,9 @@ PGA_VIOL_READER(viol_ga)
 
 namespace pga {
 
+// k_select_cluster can be co-scheduled on this device (prepare_select_small)
+static bool g_csel_ok = false;
+
 // A/B switches for measurement: getenv_flag(name, d) is d unless the variable
 // is set (then true for "1", false for "0").
 static bool getenv_flag(const char *name, bool d) {
@@ -1687,6 +1690,23 @@ int prepare_select_small() {
     PGA_CUDA(cudaFuncSetAttribute(k_select_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)csel_smem(CSEL_MAXR)));
     PGA_CUDA(cudaFuncSetAttribute(k_select_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    {   // can a 16-CTA cluster of this size be co-scheduled on this device?  If
+        // not (a smaller part, MIG), the multi-kernel path serves these P.
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(CSEL_CL);
+        cfg.blockDim = dim3(CSEL_T);
+        cfg.dynamicSmemBytes = csel_smem(CSEL_MAXR);
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = CSEL_CL;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int nc = 0;
+        g_csel_ok = cudaOccupancyMaxActiveClusters(&nc, k_select_cluster, &cfg) == cudaSuccess && nc > 0;
+        (void)cudaGetLastError();
+    }
     return PGA_OK;
 }
 
@@ -1814,7 +1834,7 @@ constexpr int SMALL_GA_P = 1024;
 // order fused into the selection launch (one CTA up to SMALL_GA_P, one
 // cluster up to CSEL_MAXP); above, the run sort + merge tree is its own step
 bool small_select(const pga_ctx *c) {
-    return c->P <= SMALL_GA_P || (c->P <= CSEL_MAXP && !getenv_flag("PGA_NO_CSEL", false));
+    return c->P <= SMALL_GA_P || (c->P <= CSEL_MAXP && g_csel_ok && !getenv_flag("PGA_NO_CSEL", false));
 }
 
 int launch_sort_order(pga_ctx *c, cudaStream_t s) {
