@@ -140,7 +140,8 @@ void drop_graph(GExec &g) {
 void drop_graphs(pga_ctx *c) {
     drop_graph(c->gx_eval[0]);
     drop_graph(c->gx_eval[1]);
-    drop_graph(c->gx_breed);
+    drop_graph(c->gx_breed[0]);
+    drop_graph(c->gx_breed[1]);
 }
 
 void free_ctx(pga_ctx *c) {
@@ -161,6 +162,8 @@ void free_ctx(pga_ctx *c) {
     if (c->join_ev) cudaEventDestroy(c->join_ev);
     if (c->fork_ev) cudaEventDestroy(c->fork_ev);
     if (c->join_side_ev) cudaEventDestroy(c->join_side_ev);
+    if (c->fit_ev) cudaEventDestroy(c->fit_ev);
+    if (c->stats_ev) cudaEventDestroy(c->stats_ev);
     if (c->side) cudaStreamDestroy(c->side);
     if (c->stream) cudaStreamDestroy(c->stream);
 }
@@ -251,18 +254,32 @@ int phase_a(pga_ctx *c, int32_t g, int32_t *is_mig) {
     if (mig) {
         TRY(launch_sort_order(c, c->stream));
         c->pending_migration = true;
+        PGA_MARK(c, 3, c->stream);
     } else {
-        TRY(launch_stats(c, c->p.n_islands > 1 ? 1 : 0, c->stream));
+        // statistics / termination on the side stream, concurrent with the
+        // selection on the main stream: both only read L (the breed skips a
+        // generation the statistics stop); joined before phase A ends
+        PGA_CUDA(cudaEventRecord(c->fit_ev, c->stream));
+        PGA_CUDA(cudaStreamWaitEvent(c->side, c->fit_ev, 0));
+        TRY(launch_stats(c, c->p.n_islands > 1 ? 1 : 0, c->side));
+        PGA_CUDA(cudaEventRecord(c->stats_ev, c->side));
+        TRY(launch_select(c, c->stream));
+        PGA_CUDA(cudaStreamWaitEvent(c->stream, c->stats_ev, 0));
+        PGA_MARK(c, 3, c->stream);
     }
     TRY(launch_mates_join(c, c->stream));
-    PGA_MARK(c, 3, c->stream);
     return PGA_OK;
 }
 
-int phase_b(pga_ctx *c) {
-    if (!small_select(c)) TRY(launch_sort_order(c, c->stream));   // small P: fused in selection
+// Phase B.  fresh: phase A of this generation already selected (non-migration
+// generations); otherwise (after a migration import or a replicated commit)
+// the selection runs here.
+int phase_b(pga_ctx *c, bool fresh) {
+    if (!fresh) TRY(launch_select(c, c->stream));
     PGA_MARK(c, 4, c->stream);
-    TRY(launch_select_breed(c, c->stream));
+    PGA_MARK(c, 5, c->stream);
+    PGA_MARK(c, 6, c->stream);
+    TRY(launch_breed(c, c->stream));
     if (c->pev) {
         PGA_CUDA(prof_record(c->pev[8], c->stream));
         c->prof_used += PROF_EV;
@@ -329,12 +346,12 @@ int launch_graph(pga_ctx *c, GExec &g) {
 int run_one_generation(pga_ctx *c, GExec &g, bool use_graph) {
     if (!use_graph) {
         TRY(phase_a(c, 0, nullptr));
-        return phase_b(c);
+        return phase_b(c, true);
     }
     if (!g.x)
         TRY(capture_graph(c, &g, [&] {
             int rc = phase_a(c, 0, nullptr);
-            return rc ? rc : phase_b(c);
+            return rc ? rc : phase_b(c, true);
         }));
     return launch_graph(c, g);
 }
@@ -434,6 +451,8 @@ int pga_create(const double *C, int32_t N, const pga_params *p, pga_ctx **out) {
     e = cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->join_side_ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->fit_ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->stats_ev, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
     if (e != cudaSuccess) return bail(cuda_fail(e, "cudaEventCreate"));
     const size_t cm = (size_t)c->Pcap * c->ldn, gm = (size_t)N * c->Pcap;
@@ -621,6 +640,7 @@ int pga_init(pga_ctx *c, uint64_t seed) {
     c->has_pop = true;
     c->host_gen = 0;
     c->pending_migration = false;
+    c->sel_fresh = false;
     return PGA_OK;
 }
 
@@ -637,6 +657,7 @@ int pga_gen_evaluate(pga_ctx *c, int32_t *is_migration) {
     TRY(launch_graph(c, g));
     c->pev = prof_slot(c);   // this generation's slot (null unless profiling)
     c->pending_migration = mig;
+    c->sel_fresh = !mig;     // phase A selected beside its statistics
     if (is_migration) *is_migration = mig ? 1 : 0;
     return PGA_OK;
 }
@@ -677,6 +698,7 @@ int pga_rep_commit(pga_ctx *c, const double *L_dev, const uint16_t *top_dev) {
     TRY(launch_mates_fork(c, c->stream));   // mate slots of this generation (phase_a does it on the GA path)
     TRY(launch_stats(c, 0, c->stream));
     TRY(launch_mates_join(c, c->stream));
+    c->sel_fresh = false;    // phase B selects from the committed L
     PGA_MARK(c, 3, c->stream);
     return PGA_OK;
 }
@@ -687,8 +709,10 @@ int pga_gen_breed(pga_ctx *c) {
     if (c->pending_migration) return fail(PGA_ESTATE, "migration pending: call pga_import_migrants");
     PGA_CUDA(cudaSetDevice(c->device));
     const bool profiled = c->pev != nullptr;   // phase_b clears it while being captured
-    if (!c->gx_breed.x) TRY(capture_graph(c, &c->gx_breed, [&] { return phase_b(c); }));
-    TRY(launch_graph(c, c->gx_breed));
+    const int f = c->sel_fresh ? 1 : 0;
+    if (!c->gx_breed[f].x) TRY(capture_graph(c, &c->gx_breed[f], [&] { return phase_b(c, f == 1); }));
+    TRY(launch_graph(c, c->gx_breed[f]));
+    c->sel_fresh = false;
     if (profiled) c->prof_used += PROF_EV;   // as phase_b does in plain launches
     c->pev = nullptr;
     c->host_gen += 1;
@@ -914,6 +938,7 @@ int pga_set_population(pga_ctx *c, const int32_t *labels, int32_t generation) {
     c->has_pop = true;
     c->host_gen = generation;
     c->pending_migration = false;
+    c->sel_fresh = false;
     return PGA_OK;
 }
 
@@ -938,6 +963,7 @@ int pga_import_migrants(pga_ctx *c, const void *dev_recv, int32_t n_islands) {
     TRY(launch_import(c, dev_recv, n_islands, c->stream));
     TRY(launch_stats(c, 2, c->stream));
     c->pending_migration = false;
+    c->sel_fresh = false;    // L changed: phase B selects
     return PGA_OK;
 }
 

@@ -1848,33 +1848,40 @@ int launch_sort_order(pga_ctx *c, cudaStream_t s) {
                       reinterpret_cast<int32_t *>(c->q), &c->st->done, s);
 }
 
-// Phase B of a generation, after launch_sort_order.
-int launch_select_breed(pga_ctx *c, cudaStream_t s) {
+// Isolate fittest + scaling + selection of a generation (Alg. 1):
+// one CTA up to SMALL_GA_P, one thread-block cluster up to CSEL_MAXP, else the
+// run sort + merge tree, then SUS (or tournament).  The mate slots come from
+// the side stream (launch_mates_fork) for P > SMALL_GA_P.
+int launch_select(pga_ctx *c, cudaStream_t s) {
     const pga_params &p = c->p;
     const int32_t *done = &c->st->done;
     const int32_t *genp = &c->st->gen;
     int rc;
     if (c->P <= SMALL_GA_P) {
-        // one CTA: order + scaling + selection + mates
         rc = launch_select_small(3, c->L, c->P, p, 0, p.island, genp, c->order, c->sel, c->sigma, done, s);
         if (rc) return rc;
-        PGA_MARK(c, 5, s);
-        PGA_MARK(c, 6, s);
     } else if (small_select(c)) {
-        // one cluster: order + scaling + selection + mates
         rc = launch_select_cluster(3, c->L, c->P, p, genp, c->order, c->rank, c->sel, done, s);
         if (rc) return rc;
-        PGA_MARK(c, 5, s);
-        PGA_MARK(c, 6, s);
     } else {
-        // selection (the mate slots come from the side branch, launch_mates_side)
+        rc = sort_order(c->L, c->P, c->order, c->rank, c->keys_in, c->keys_out, c->idx_in,
+                        reinterpret_cast<int32_t *>(c->q), done, s);
+        if (rc) return rc;
         rc = run_select_ops(c->L, c->P, p, 0, p.island, c->order, c->sel, c->keys_in, c->keys_out,
                             c->idx_in, c->rank, c->q, c->keys_in /* free after the sort: block sums */,
                             done, s, genp, true, nullptr);
         if (rc) return rc;
-        PGA_MARK(c, 5, s);
-        PGA_MARK(c, 6, s);
     }
+    return PGA_OK;
+}
+
+// Crossover, mutation, canonicalisation, replacement (Alg. 1) from
+// the selection launch_select left in order / sel / sigma; the last CTA
+// advances the generation.
+int launch_breed(pga_ctx *c, cudaStream_t s) {
+    const pga_params &p = c->p;
+    const int32_t *done = &c->st->done;
+    const int32_t *genp = &c->st->gen;
     BreedArgs a{};
     fill_breed(a, p, c->P, c->N);
     a.cm_in0 = c->pop[0];

@@ -137,6 +137,7 @@ struct pga_ctx {
     cudaEvent_t join_ev = nullptr;   // joins a caller's stream to `stream` (pga_evaluate_device)
     cudaStream_t side = nullptr;     // side branch of a generation (mate slots, launch_mates_fork)
     cudaEvent_t fork_ev = nullptr, join_side_ev = nullptr;
+    cudaEvent_t fit_ev = nullptr, stats_ev = nullptr;   // statistics on the side stream beside the selection
     pga_params p{};
     int32_t N = 0;
     int32_t ldn = 0;       // padded gene stride of chromosome-major labels / V
@@ -155,7 +156,8 @@ struct pga_ctx {
     // pga_gen_breed; dropped whenever a setting that changes the launch
     // sequence does (drop_graphs)
     pga::GExec gx_eval[2];
-    pga::GExec gx_breed;
+    pga::GExec gx_breed[2];        // [1]: selection already done in phase A (sel_fresh)
+    bool sel_fresh = false;        // the last phase A selected concurrently with its statistics
     unsigned long long *sp_blocks = nullptr;  // device [4]: sparse blocks, gathers, cache hits, pairs saved (profiling)
     pga::CCSlot *cc = nullptr;     // cluster cache table (N <= SPARSE_MAX_N)
     uint32_t cc_mask = 0;          // slots - 1
@@ -247,7 +249,8 @@ int launch_fitness_range(pga_ctx *c, const FitBufs &b, int64_t begin, int64_t en
 int launch_init(pga_ctx *c, uint64_t seed, cudaStream_t s);
 int launch_stats(pga_ctx *c, int is_migration_check, cudaStream_t s);
 int launch_sort_order(pga_ctx *c, cudaStream_t s);
-int launch_select_breed(pga_ctx *c, cudaStream_t s);
+int launch_select(pga_ctx *c, cudaStream_t s);   // order + scaling + selection
+int launch_breed(pga_ctx *c, cudaStream_t s);    // crossover .. replacement + advance
 int launch_export(pga_ctx *c, void *dev_send, cudaStream_t s);
 int launch_mates_fork(pga_ctx *c, cudaStream_t s);
 int launch_mates_join(pga_ctx *c, cudaStream_t s);
