@@ -817,7 +817,8 @@ __global__ void __launch_bounds__(MERGE_T) k_merge_level(const uint64_t *__restr
 //      ranges per individual; or tournament.
 // The same integers as the multi-kernel path (bit-exact).
 // ---------------------------------------------------------------------------
-constexpr int CSEL_T = 512, CSEL_CL = 16, CSEL_MAXR = CSEL_T;
+constexpr int CSEL_T = 1024, CSEL_CL = 16, CSEL_MAXR = CSEL_T / 2;   // >= 2 threads per item in the rank search
+constexpr int CSEL_RPT = (CSEL_CL - 1 + 1) / 2;                       // other runs per search thread (at most)
 constexpr int CSEL_MAXP = CSEL_CL * CSEL_MAXR;
 
 __host__ __device__ __forceinline__ int csel_run(int P) {
@@ -827,11 +828,11 @@ __host__ __device__ __forceinline__ int csel_run(int P) {
 }
 
 static size_t csel_smem(int R) {
-    // own run: sk sL sx si srank; copies of the other runs' keys and indices
-    return (size_t)R * (8 + 8 + 8 + 4 + 4) + (size_t)(CSEL_CL - 1) * R * 12 + 256;
+    // own run: sk sL sx si srank spos; copies of the other runs' keys and indices
+    return (size_t)R * (8 + 8 + 8 + 4 + 4 + 4) + (size_t)(CSEL_CL - 1) * R * 12 + 256;
 }
 
-__global__ void __launch_bounds__(CSEL_T, 2)
+__global__ void __launch_bounds__(CSEL_T, 1)
 k_select_cluster(int what, const double *__restrict__ L, int P, int R, int M, int selection, int tour_k,
                  int scaling, uint64_t seed, uint32_t gen, uint32_t island, const int32_t *gen_ptr,
                  int32_t *order, int32_t *rank_out, int32_t *sel, const int32_t *done) {
@@ -850,6 +851,7 @@ k_select_cluster(int what, const double *__restrict__ L, int P, int R, int M, in
     uint32_t *si = reinterpret_cast<uint32_t *>(ok_ + (CSEL_CL - 1) * R);   // [R] sorted indices
     int32_t *srank = reinterpret_cast<int32_t *>(si + R);     // [R] global rank by local index
     uint32_t *oi_ = reinterpret_cast<uint32_t *>(srank + R);  // [(CL-1) R] other runs' indices
+    int32_t *spos = reinterpret_cast<int32_t *>(oi_ + (CSEL_CL - 1) * R);   // [R] global rank accumulators
     __shared__ uint64_t ws[CSEL_T / 32];
     __shared__ uint64_t s_tot, s_first_key;
     __shared__ uint32_t s_first_idx;
@@ -922,25 +924,42 @@ k_select_cluster(int what, const double *__restrict__ L, int P, int R, int M, in
             reinterpret_cast<uint4 *>(oi_ + r * R)[q] = reinterpret_cast<const uint4 *>(cl.map_shared_rank(si, cr))[q];
         }
     }
+    for (int t = tid; t < R; t += CSEL_T) spos[t] = t;   // own position
     __syncthreads();
-    if (act && v != 0xFFFFFFFFu) {                 // padding sorts last
-        int lo[CSEL_CL - 1];
+    {   // thread t searches for item t % R in the runs t / R, t / R + tpi, ...
+        const int tpi = CSEL_T / R, it = tid % R, h = tid / R;
+        const uint64_t ke = sk[it];
+        const uint32_t ve = si[it];
+        if (ve != 0xFFFFFFFFu) {                   // padding sorts last
+            int lo[CSEL_RPT];
 #pragma unroll
-        for (int r = 0; r < CSEL_CL - 1; ++r) lo[r] = 0;
-        // branch-free binary search for the first position not before (k, v)
-        for (int half = R >> 1; half > 0; half >>= 1) {
+            for (int q = 0; q < CSEL_RPT; ++q) lo[q] = 0;
+            // branch-free binary search for the first position not before (ke, ve)
+            for (int half = R >> 1; half > 0; half >>= 1) {
 #pragma unroll
-            for (int r = 0; r < CSEL_CL - 1; ++r) {
-                const int m = lo[r] + half - 1;
-                if (kv_less(ok_[r * R + m], oi_[r * R + m], k, v)) lo[r] += half;
+                for (int q = 0; q < CSEL_RPT; ++q) {
+                    const int r = h + q * tpi;
+                    if (r < CSEL_CL - 1) {
+                        const int m = lo[q] + half - 1;
+                        if (kv_less(ok_[r * R + m], oi_[r * R + m], ke, ve)) lo[q] += half;
+                    }
+                }
             }
+            int sum = 0;
+#pragma unroll
+            for (int q = 0; q < CSEL_RPT; ++q) {
+                const int r = h + q * tpi;
+                if (r < CSEL_CL - 1) {
+                    if (lo[q] == R - 1 && kv_less(ok_[r * R + R - 1], oi_[r * R + R - 1], ke, ve)) lo[q] = R;
+                    sum += lo[q];
+                }
+            }
+            atomicAdd(spos + it, sum);
         }
-#pragma unroll
-        for (int r = 0; r < CSEL_CL - 1; ++r)      // the last position (R - 1)
-            if (lo[r] == R - 1 && kv_less(ok_[r * R + R - 1], oi_[r * R + R - 1], k, v)) lo[r] = R;
-        int rank = tid;
-#pragma unroll
-        for (int r = 0; r < CSEL_CL - 1; ++r) rank += lo[r];
+    }
+    __syncthreads();
+    if (act && v != 0xFFFFFFFFu) {
+        const int rank = spos[tid];
         PGA_DCHECK(rank >= 0 && rank < P && (int)v - base >= 0 && (int)v - base < R);
         if (what & 1) order[rank] = (int32_t)v;
         if (rank_out) rank_out[v] = rank;
