@@ -1075,6 +1075,7 @@ struct BreedArgs {
     uint32_t gen, island;
     const int32_t *done, *gen_ptr;
     const int32_t *gm_skip;            // != 0: the label-sparse pass owns the gene-major copy (f2)
+    RoundKeys rk;                      // Philox round keys of `seed` (in the parameter constant bank)
     const uint32_t *mmask;             // GA, P > SMALL_GA_P: precomputed mutation masks [Pcap][mw] (k_mutmask)
     int mw;                            // words per child: ceil(N / 32)
     pga::DevState *adv_st;             // GA: advance st->gen once the grid is done (null: hooks)
@@ -1135,7 +1136,7 @@ __device__ __forceinline__ ChildPlan plan_child(const BreedArgs &a, int64_t o, u
     const int64_t ia = a.sel[a.sigma[2 * k]], ib = a.sel[a.sigma[2 * k + 1]];
     c.pa = child ? ib : ia;   // the parent whose genes the child keeps
     c.pb = child ? ia : ib;   // the other parent
-    const U4 x = draw(a.seed, pga::TAG_XO, a.island, gen, (uint32_t)k, 0u);
+    const U4 x = draw_rk(a.rk, pga::TAG_XO, a.island, gen, (uint32_t)k, 0u);
     c.kb_top = -1;
     if ((uint64_t)x.x >= a.thr_c) {
         c.mode = 0;
@@ -1204,7 +1205,7 @@ __global__ void __launch_bounds__(BW * 32, 3) k_breed(BreedArgs a) {
                     const uint32_t wv = a.mmask[(o0 + slot) * a.mw + (base >> 5) + (lane >> 3)];
                     mbits = (wv >> (4 * (lane & 7))) & 0xFu;
                 } else {
-                    const U4 u = draw(a.seed, pga::TAG_MUT, a.island, gen, (uint32_t)((base >> 2) + lane), p.og);
+                    const U4 u = draw_rk(a.rk, pga::TAG_MUT, a.island, gen, (uint32_t)((base >> 2) + lane), p.og);
                     mbits = ((uint64_t)u.x < a.thr_m ? 1u : 0u) | ((uint64_t)u.y < a.thr_m ? 2u : 0u) |
                             ((uint64_t)u.z < a.thr_m ? 4u : 0u) | ((uint64_t)u.w < a.thr_m ? 8u : 0u);
                 }
@@ -1223,7 +1224,7 @@ __global__ void __launch_bounds__(BW * 32, 3) k_breed(BreedArgs a) {
                     if (i >= p.cut) s = gb[sc];
                 }
                 if (valid && ((mb >> (lane & 3)) & 1u)) {
-                    const U4 v = draw(a.seed, pga::TAG_MUTV, a.island, gen, (uint32_t)(i >> 2), p.og);
+                    const U4 v = draw_rk(a.rk, pga::TAG_MUTV, a.island, gen, (uint32_t)(i >> 2), p.og);
                     s = scale_u32(word(v, i & 3), (uint32_t)N);
                 }
                 sv[sc] = s;
@@ -1351,7 +1352,7 @@ __global__ void __launch_bounds__(BW * 32, NB <= 2 ? 3 : PGA_B2_MINB) k_breed2(B
                 const uint32_t wv = a.mmask[o * a.mw + (b0 >> 5) + (lane >> 3)];
                 mbits = (wv >> (4 * (lane & 7))) & 0xFu;
             } else {
-                const U4 u = draw(a.seed, pga::TAG_MUT, a.island, gen, (uint32_t)((b0 >> 2) + lane), p.og);
+                const U4 u = draw_rk(a.rk, pga::TAG_MUT, a.island, gen, (uint32_t)((b0 >> 2) + lane), p.og);
                 mbits = ((uint64_t)u.x < a.thr_m ? 1u : 0u) | ((uint64_t)u.y < a.thr_m ? 2u : 0u) |
                         ((uint64_t)u.z < a.thr_m ? 4u : 0u) | ((uint64_t)u.w < a.thr_m ? 8u : 0u);
             }
@@ -1374,7 +1375,7 @@ __global__ void __launch_bounds__(BW * 32, NB <= 2 ? 3 : PGA_B2_MINB) k_breed2(B
                 s[e] = x;
             }
             if (p.valid && mb) {
-                const U4 v = draw(a.seed, pga::TAG_MUTV, a.island, gen, (uint32_t)(g0 >> 2), p.og);
+                const U4 v = draw_rk(a.rk, pga::TAG_MUTV, a.island, gen, (uint32_t)(g0 >> 2), p.og);
 #pragma unroll
                 for (int e = 0; e < 2; ++e)
                     if ((mb >> e) & 1u) s[e] = scale_u32(word(v, (g0 + e) & 3), (uint32_t)N);
@@ -1813,6 +1814,7 @@ static void fill_breed(BreedArgs &a, const pga_params &p, int64_t P, int N) {
     a.N = N;
     a.E = p.elite;
     a.seed = p.seed;
+    a.rk = round_keys(p.seed);
     a.island = (uint32_t)p.island;
     auto thr = [](double x) -> uint64_t {
         if (x >= 1.0) return (uint64_t)1 << 32;

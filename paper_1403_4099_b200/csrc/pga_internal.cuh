@@ -324,6 +324,47 @@ __device__ __forceinline__ U4 philox(uint32_t c0, uint32_t c1, uint32_t c2, uint
     return U4{c0, c1, c2, c3};
 }
 
+// Philox4x32-10 with the 10 round keys precomputed (rk[2r], rk[2r+1] =
+// key + r * (0x9E3779B9, 0xBB67AE85), the same modular sums philox() forms
+// round by round).  When rk lives in a kernel's parameter struct the XORs
+// take it straight from the constant bank: 4 instead of 6 instructions per
+// round in the breed's per-gene mutation draws.
+struct RoundKeys {
+    uint32_t k[20];
+};
+
+inline RoundKeys round_keys(uint64_t seed) {
+    RoundKeys r;
+    uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+    for (int i = 0; i < 10; ++i) {
+        r.k[2 * i] = k0;
+        r.k[2 * i + 1] = k1;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    return r;
+}
+
+__device__ __forceinline__ U4 philox_rk(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, const RoundKeys &rk) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint64_t p0 = (uint64_t)0xD2511F53u * c0;
+        const uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
+        const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ rk.k[2 * r];
+        const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ rk.k[2 * r + 1];
+        c0 = n0;
+        c1 = (uint32_t)p1;
+        c2 = n2;
+        c3 = (uint32_t)p0;
+    }
+    return U4{c0, c1, c2, c3};
+}
+
+__device__ __forceinline__ U4 draw_rk(const RoundKeys &rk, uint32_t tag, uint32_t island, uint32_t gen,
+                                      uint32_t c0, uint32_t c1) {
+    return philox_rk(c0, c1, gen, tag | (island << 8), rk);
+}
+
 // counter = (c0, c1, gen, tag | island << 8), key = (seed_lo, seed_hi)
 __device__ __forceinline__ U4 draw(uint64_t seed, uint32_t tag, uint32_t island, uint32_t gen,
                                     uint32_t c0, uint32_t c1) {
