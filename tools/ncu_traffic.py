@@ -45,7 +45,10 @@ def read(rep):
         d = dict(zip(hdr, r))
         u = dict(zip(hdr, units))
         name = d["Kernel Name"]
-        name = name.split("(")[0].replace("<unnamed>::", "").strip()
+        # kernel name without namespace, "void " and template arguments
+        # (bench.py looks kernels up by their plain names)
+        name = name.split("(")[0].replace("<unnamed>::", "").replace("void ", "").strip()
+        name = name.split("<")[0]
         rec = {}
         for m, k in METRICS.items():
             if m not in d or d[m] in ("", "n/a"):
