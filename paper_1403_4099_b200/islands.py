@@ -99,8 +99,14 @@ class IslandRunner:
         return mig
 
     def run(self, gens):
-        for _ in range(gens):
+        """Up to `gens` generations; stops once the engine reports termination
+        (Q28: every island decides identically, so all ranks stop together).
+        Returns the generations stepped."""
+        for g in range(gens):
             self.step()
+            if self.e.state().get("done"):
+                return g + 1
+        return gens
 
     def global_best(self):
         """(best L, labels) over all islands: (L desc, island asc)."""

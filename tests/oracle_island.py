@@ -28,13 +28,28 @@ class OracleIsland:
         self.best_ever = -1.0
         self.best_labels = np.zeros(self.N, np.int32)
         self.history = []
+        self.stall, self.prev, self.done = 0, 0.0, False
 
-    def _stats(self):
+    def _stats(self, migration=False):
         b = int(np.argmax(self.L))
         self.history.append(float(self.L[b]))
         if self.L[b] > self.best_ever:
             self.best_ever = float(self.L[b])
             self.best_labels = self.pop[b].copy()
+        # termination (Q28 for islands: the stall test runs at migration
+        # generations only, on the island's post-import best, which is the
+        # global best; Q16 for one island)
+        best = float(self.L[b])
+        if self.G == 1:
+            if self.gen > 0:
+                self.stall = self.stall + 1 if best - self.prev < self.p.tol else 0
+            self.prev = best
+        elif migration:
+            if self.gen + 1 > self.p.migrate_every:
+                self.stall = self.stall + self.p.migrate_every if best - self.prev < self.p.tol else 0
+            self.prev = best
+        if (self.p.tol >= 0 and self.stall >= self.p.stall_gens) or self.gen + 1 >= self.p.max_gens:
+            self.done = True
 
     def gen_evaluate(self):
         self.L, self.top = orc.evaluate(self.C, self.pop)
@@ -83,15 +98,18 @@ class OracleIsland:
             self.pop[w] = lab
             self.L[w] = L
             self.top[w] = t
-        self._stats()
+        self._stats(migration=True)
 
     def gen_breed(self):
+        if self.done:                       # the device breed is a no-op once done
+            return
         self.pop = orc.step(self.p, self.pop, self.L, self.top, self.gen, island=self.island,
                             p_off=self.island * self.P)
         self.gen += 1
 
     def state(self):
-        return dict(generation=self.gen, best_L=self.best_ever, best_labels=self.best_labels + 1)
+        return dict(generation=self.gen, best_L=self.best_ever, best_labels=self.best_labels + 1,
+                    done=int(self.done))
 
 
 class OracleReplica:

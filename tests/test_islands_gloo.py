@@ -23,7 +23,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, out_path, gens):
+def _worker(rank, world, port, out_path, gens, tol=-1.0, stall=50):
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -36,12 +36,12 @@ def _worker(rank, world, port, out_path, gens):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     X, planted = workloads.noh_returns(workloads.CONFIGS["C1"])
     C = orc.pearson(X)
-    params = orc.default_params(pop=48, max_gens=gens, tol=-1.0, n_islands=world,
+    params = orc.default_params(pop=48, max_gens=gens, tol=tol, stall_gens=stall, n_islands=world,
                                 migrate_every=4, migrants=5, seed=77)
     eng = OracleIsland(C, params, rank, world)
     runner = IslandRunner(eng)
     eng.init(77)
-    runner.run(gens)
+    stepped = runner.run(gens)
     bestL, best, isl = runner.global_best()
     # per-generation global best = max over islands
     import torch
@@ -50,7 +50,8 @@ def _worker(rank, world, port, out_path, gens):
     dist.all_gather(parts, h)
     if rank == 0:
         json.dump({"history": torch.stack(parts).max(0).values.tolist(), "best_L": bestL,
-                   "exchanges": runner.exchanges}, open(out_path, "w"))
+                   "exchanges": runner.exchanges, "stepped": stepped,
+                   "generation": eng.state()["generation"]}, open(out_path, "w"))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -68,5 +69,25 @@ def test_two_islands_gloo_matches_oracle(tmp_path):
     ref = orc.run(C, orc.default_params(pop=48, max_gens=gens, tol=-1.0, n_islands=2,
                                         migrate_every=4, migrants=5, seed=77))
     assert res["exchanges"] == gens // 4
+    assert np.array_equal(np.array(res["history"]), ref["history"])
+    assert res["best_L"] == ref["best_L"]
+
+
+def test_two_islands_gloo_stall_termination_matches_oracle(tmp_path):
+    """Live tolerance (Q28): both ranks stop at the generation orc_run's
+    two-island rule gives, with the same per-generation global best."""
+    import oracle as orc
+    import workloads
+    gens, tol, stall = 200, 1e-5, 8
+    out = str(tmp_path / "res.json")
+    mp.start_processes(_worker, args=(2, _free_port(), out, gens, tol, stall), nprocs=2, join=True,
+                       start_method="spawn")
+    res = json.load(open(out))
+    X, _ = workloads.noh_returns(workloads.CONFIGS["C1"])
+    C = orc.pearson(X)
+    ref = orc.run(C, orc.default_params(pop=48, max_gens=gens, tol=tol, stall_gens=stall, n_islands=2,
+                                        migrate_every=4, migrants=5, seed=77))
+    assert ref["reason"] == 1 and ref["gens_run"] < gens
+    assert res["stepped"] == ref["gens_run"]
     assert np.array_equal(np.array(res["history"]), ref["history"])
     assert res["best_L"] == ref["best_L"]
