@@ -269,7 +269,7 @@ def main():
                          "SURVEY §8(f) f3)")
     ap.add_argument("--sparse-theta", type=float, default=None,
                     help="label-sparse threshold (pga_set_sparse_threshold; default: the library's automatic "
-                         "choice, 0.25 with the cluster cache at N >= 160; 0 = dense sweep only)")
+                         "choice, 0.25 with the cluster cache at N >= 64; 0 = dense sweep only)")
     ap.add_argument("--stream", action="store_true",
                     help="F1 only: each step also computes the 1760 windows on the device from one "
                          "return stream (EWMA lambda=0.98 + RMT cleaning, SURVEY §8(f) f4)")

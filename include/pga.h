@@ -255,7 +255,7 @@ int pga_op_init(uint64_t seed, int32_t N, int64_t P, int64_t p_off, int32_t isla
  * the dense sweep.  The result is the same Eq. 5/6/8 value (within the
  * parity tolerance; deterministic).  theta in [0, 1]; 0 = always dense,
  * 1 = sparse whenever N <= 2048; negative = automatic, the default: 0 for
- * N < 160, else 0.25 with the cluster cache on (pga_set_cluster_cache) and
+ * N < 64, else 0.25 with the cluster cache on (pga_set_cluster_cache) and
  * 0.04 with it off.  The
  * pass is cheaper than the dense sweep up to about 4% of the pairs when
  * every pair is gathered, and up to a quarter when most clusters are cache

@@ -804,7 +804,7 @@ __global__ void __launch_bounds__(MERGE_T) k_merge_level(const uint64_t *__restr
 // (distributed shared memory) -- what the multi-kernel path does with a run
 // sort, a merge tree, q sums and a scan (five or more latency-bound launches
 // at these sizes).  The mate slots are computed off the critical path (a
-// parallel graph branch, launch_mates_side).
+// parallel graph branch, launch_mates_fork).
 //   1. CTA c holds individuals [c R, (c + 1) R) (R a power of two <= CSEL_T,
 //      one per thread) and sorts them by (key = ~bits(L), index): a bitonic
 //      network, strides < 32 by warp shuffles, larger ones in shared memory.

@@ -212,12 +212,13 @@ struct pga_ctx {
 };
 
 // Label-sparse threshold in effect: the caller's, else automatic: off below
-// N = 160 (the dense sweep is cheaper there: C1-C3 measured), 0.25 with the
-// cluster cache (hits make a sparse block cheap up to a quarter of the dense
-// pairs) and 0.04 without it.
+// N = 64 (the dense sweep is cheaper there: C1 0.056 vs 0.058, C2 0.060 vs
+// 0.077 ms per generation; round 2's pass wins from C3's N = 100 up: 0.071 vs
+// 0.090 ms over 2000 generations), 0.25 with the cluster cache (hits make a
+// sparse block cheap up to a quarter of the dense pairs) and 0.04 without it.
 inline double sparse_theta_eff(const pga_ctx *c) {
     if (c->sparse_theta >= 0.0) return c->sparse_theta;
-    if (c->N < 160) return 0.0;
+    if (c->N < 64) return 0.0;
     return (c->cc && c->cc_on) ? 0.25 : 0.04;
 }
 

@@ -324,7 +324,7 @@ def test_C4_full_size_midrun_sample(pga, orc):
 @pytest.mark.parametrize("cfg,P,W,gens", [("C4", 2048, 2, 6), ("C3", 1024, 3, 8)])
 def test_replicated_default_theta_lockstep(pga, orc, cfg, P, W, gens):
     """Replicas with the library's automatic threshold (the label-sparse
-    pass on for N >= 160, as bench --mode replicated runs it), stepped in
+    pass on for N >= 64, as bench --mode replicated runs it), stepped in
     sequence on one GPU: every generation the gathered L matches the
     oracle, every replica holds the same population, and it equals orc_step
     on the gathered L and top."""
@@ -368,7 +368,7 @@ def test_replicated_default_theta_lockstep(pga, orc, cfg, P, W, gens):
     finally:
         for r in reps:
             r.close()
-    if N >= 160:
+    if N >= 64:
         assert sparse_seen > 0
 
 
