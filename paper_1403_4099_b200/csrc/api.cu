@@ -62,6 +62,7 @@ int launch_breed_hook(const int32_t *pop, const int32_t *top, const int32_t *ord
 int launch_set_pop(pga_ctx *c, const int32_t *lab32, int par, cudaStream_t s);
 int prepare_breed(int N);
 int prepare_select_small();
+int prepare_rank_sel(pga_ctx *c);
 bool small_select(const pga_ctx *c);
 long long viol_fitness();
 int launch_fast_ln(const double *x, int64_t n, const double *lgtab, int N, double *out, cudaStream_t s);
@@ -151,7 +152,7 @@ void free_ctx(pga_ctx *c) {
     void *ptrs[] = {c->C, c->diag, c->lgtab, c->sflag, c->sp_live, c->sp_blocks, c->cc, c->cc_state,
                     c->stats_part, c->stats_ctr,
                     c->cc_keys, c->ptab, c->pop[0], c->pop[1], c->popT[0], c->popT[1], c->V, c->L,
-                    c->top, c->keys_in, c->keys_out, c->idx_in, c->order, c->q, c->rank,
+                    c->top, c->keys_in, c->keys_out, c->idx_in, c->order, c->q, c->rank, c->rc_acc, c->rc_qtab,
                     c->sel, c->sigma, c->breed_ctr, c->mmask, c->st,
                     c->best_labels, c->history, c->stage_i32, c->evCM, c->evGM, c->evL,
                     c->counters};
@@ -507,6 +508,10 @@ int pga_create(const double *C, int32_t N, const pga_params *p, pga_ctx **out) {
     rc = rc ? rc : dalloc(&c->order, (size_t)c->Pcap);
     rc = rc ? rc : dalloc(&c->q, (size_t)c->Pcap);
     rc = rc ? rc : dalloc(&c->rank, (size_t)c->Pcap);
+    if (c->Pcap > 1024 && c->Pcap <= RANKC_MAXP) {
+        rc = rc ? rc : dalloc(&c->rc_acc, (size_t)c->Pcap + 64);
+        rc = rc ? rc : dalloc(&c->rc_qtab, (size_t)c->Pcap);
+    }
     rc = rc ? rc : dalloc(&c->sel, (size_t)c->Pcap + 2);
     rc = rc ? rc : dalloc(&c->sigma, (size_t)c->Pcap + 2);
     rc = rc ? rc : dalloc(&c->breed_ctr, (size_t)1);
@@ -517,6 +522,8 @@ int pga_create(const double *C, int32_t N, const pga_params *p, pga_ctx **out) {
     if (rc) return bail(rc);
     e = cudaMemsetAsync(c->counters, 0, sizeof(uint32_t) * (size_t)(c->Pcap / CB), c->stream);
     if (e == cudaSuccess) e = cudaMemsetAsync(c->breed_ctr, 0, sizeof(uint32_t), c->stream);
+    if (e == cudaSuccess && c->rc_acc)
+        e = cudaMemsetAsync(c->rc_acc, 0, sizeof(int32_t) * ((size_t)c->Pcap + 64), c->stream);
     if (e != cudaSuccess) return bail(cuda_fail(e, "cudaMemset counters"));
     e = cudaMallocHost((void **)&c->h_st, sizeof(DevState));
     if (e != cudaSuccess) return bail(fail(PGA_ENOMEM, "cudaMallocHost failed"));
@@ -542,6 +549,7 @@ int pga_create(const double *C, int32_t N, const pga_params *p, pga_ctx **out) {
     rc = prepare_fitness(N);
     if (!rc) rc = launch_logtab(c, c->stream);
     if (!rc) rc = launch_pairtab(c, c->stream);
+    if (!rc) rc = prepare_rank_sel(c);
     if (!rc && cudaStreamSynchronize(c->stream) != cudaSuccess) rc = cuda_fail(cudaGetLastError(), "log table");
     if (!rc) rc = prepare_breed(N);
     if (!rc) rc = prepare_select_small();

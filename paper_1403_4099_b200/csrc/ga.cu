@@ -305,7 +305,8 @@ __global__ void __launch_bounds__(SCAN_T) k_qsum(const double *__restrict__ L, c
     if (threadIdx.x == 0) bsum[blockIdx.x] = t;
 }
 
-__global__ void __launch_bounds__(SCAN_T) k_sus2(const uint64_t *__restrict__ q, const uint64_t *__restrict__ bsum,
+template <int T>
+__global__ void __launch_bounds__(T) k_sus2(const uint64_t *__restrict__ q, const uint64_t *__restrict__ bsum,
                                                  int nbq, const double *__restrict__ L,
                                                  const int32_t *__restrict__ order, int64_t P, int64_t M,
                                                  int scaling, uint64_t seed, uint32_t gen, uint32_t island,
@@ -314,9 +315,9 @@ __global__ void __launch_bounds__(SCAN_T) k_sus2(const uint64_t *__restrict__ q,
     pdl_wait();
     pdl_trigger();
     if (done && *done) return;
-    __shared__ uint64_t ws[SCAN_T / 32];
+    __shared__ uint64_t ws[T / 32];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const int64_t t = (int64_t)blockIdx.x * SCAN_T + tid;
+    const int64_t t = (int64_t)blockIdx.x * T + tid;
     if (gen_ptr) gen = (uint32_t)*gen_ptr;
     if (sigma && t < M) sigma[t] = feistel_slot(t, M, seed, gen, island);   // mates fused (Q10)
     const double wmax = (scaling == PGA_SCALE_RANK) ? 1.0 : L[order[0]];
@@ -329,7 +330,7 @@ __global__ void __launch_bounds__(SCAN_T) k_sus2(const uint64_t *__restrict__ q,
     }
     // base of this block and the total Q from the block sums
     uint64_t a = 0, b = 0;
-    for (int k = tid; k < nbq; k += SCAN_T) {
+    for (int k = tid; k < nbq; k += T) {
         const uint64_t v = bsum[k];
         b += v;
         if (k < (int)blockIdx.x) a += v;
@@ -430,6 +431,7 @@ constexpr int SMALL_P = 4096, SMALL_T = 1024;
 __device__ __forceinline__ bool kv_less(uint64_t ka, uint32_t va, uint64_t kb, uint32_t vb) {
     return ka < kb || (ka == kb && va < vb);
 }
+
 
 __global__ void __launch_bounds__(SMALL_T)
 k_select_small(int what, const double *__restrict__ L, int P, int M, int selection, int tour_k, int scaling,
@@ -626,6 +628,198 @@ __device__ __forceinline__ void cs_exchange(uint64_t &k, uint32_t &v, int partne
         k = ok;
         v = ov;
     }
+}
+
+// ---------------------------------------------------------------------------
+// Isolate fittest + rank scaling (Alg. 1) for SMALL_GA_P < P <=
+// RANKC_MAXP, spread over the whole GPU.  The position of i in the (L desc,
+// index asc) order is the number of j before it.  CTA (x, y) sorts chunk y
+// of RS_T individuals in shared memory (bitonic, one item per thread) and
+// each of the RS_TILE individuals i of tile x counts the chunk's items before
+// it by a binary search; the counts are added into acc[i] (integer atomics:
+// the sum is order-free).  The last CTA of tile x to finish (threadfence +
+// per-tile counter) reads and re-zeroes acc, writes rank and order and,
+// for SUS with rank scaling (Table 3), forms q_i = qtab[rank_i] =
+// floor(2^B / sqrt(rank_i + 1)), publishes the tile's sum, waits until all
+// tiles have published theirs (the finalising CTAs are running: at most
+// RS_MAXTILES of them wait, every other CTA has finished or will), and
+// writes the tile's SUS pointer ranges from its base, Q and a block scan --
+// the exact u64 prefix of k_qsum + k_sus2, without their launches.  A sort of a few thousand items in one CTA or one
+// cluster is a chain of dependent steps on a handful of SMs; here each CTA's
+// chain is one 512-item sort and two 10-step searches per thread.
+// ---------------------------------------------------------------------------
+#ifndef PGA_RS_T
+#define PGA_RS_T 512
+#endif
+constexpr int RS_T = PGA_RS_T, RS_TILE = 1024, RS_IPT = RS_TILE / RS_T;   // chunk RS_T, tile RS_TILE
+constexpr int RS_MAXTILES = 32;   // per-tile counters, then the SUS arrive / depart counters
+static_assert(pga::RANKC_MAXP <= (int64_t)RS_TILE * RS_MAXTILES, "tile counters");
+
+__device__ __forceinline__ uint64_t order_key(double x) {
+    if (x == 0.0) x = 0.0;   // -0 ties +0
+    return ~(uint64_t)__double_as_longlong(x);
+}
+
+__global__ void __launch_bounds__(RS_T) k_rank_sel(const double *__restrict__ L, int P,
+                                                   const uint64_t *__restrict__ qtab, int32_t *__restrict__ acc,
+                                                   uint32_t *ctr, int32_t *__restrict__ order,
+                                                   int32_t *__restrict__ rank, bool q, uint64_t *bsum, int M,
+                                                   uint64_t seed, uint32_t island, const int32_t *gen_ptr,
+                                                   int32_t *__restrict__ sel) {
+    // no early exit on the done flag: the statistics may raise it during
+    // this launch (side stream), and every CTA must reach the counter
+    pdl_wait();
+    pdl_trigger();
+    __shared__ uint64_t sk[RS_T];
+    __shared__ uint32_t sv[RS_T];
+    __shared__ uint64_t ws[RS_T / 32];
+    __shared__ int s_last;
+    const int tid = threadIdx.x;
+    // ---- this CTA's chunk, sorted by (key, index)
+    {
+        const int j = blockIdx.y * RS_T + tid;
+        uint64_t k = ~0ull;
+        uint32_t v = 0xFFFFFFFFu;   // padding: after every individual
+        if (j < P) {
+            k = order_key(L[j]);
+            v = (uint32_t)j;
+        }
+        for (int size = 2; size <= RS_T; size <<= 1) {
+            const bool up = (tid & size) == 0;
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                const bool lower = (tid & stride) == 0;
+                if (stride < 32) {
+                    cs_exchange(k, v, stride, lower == up);
+                } else {
+                    __syncthreads();
+                    sk[tid] = k;
+                    sv[tid] = v;
+                    __syncthreads();
+                    const uint64_t ok = sk[tid ^ stride];
+                    const uint32_t ov = sv[tid ^ stride];
+                    if (kv_less(ok, ov, k, v) == (lower == up)) {
+                        k = ok;
+                        v = ov;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        sk[tid] = k;
+        sv[tid] = v;
+        __syncthreads();
+    }
+    // ---- items of the chunk before individual i: lower bound of (key_i, i)
+#pragma unroll
+    for (int k = 0; k < RS_IPT; ++k) {
+        const int i = blockIdx.x * RS_TILE + k * RS_T + tid;
+        if (i < P) {
+            const uint64_t ki = order_key(L[i]);
+            int lo = 0;   // lower bound in [0, RS_T]
+#pragma unroll
+            for (int h = RS_T / 2; h > 0; h >>= 1)
+                if (kv_less(sk[lo + h - 1], sv[lo + h - 1], ki, (uint32_t)i)) lo += h;
+            lo += (int)kv_less(sk[lo], sv[lo], ki, (uint32_t)i);   // lo <= RS_T - 1 here
+            if (lo) atomicAdd(acc + i, lo);
+        }
+    }
+    // ---- the last CTA of tile x (all chunks counted): rank, order, q_i and
+    // the tile's sum of q (k_sus2 scans the tile sums); accumulators and
+    // counter re-zeroed
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(ctr + blockIdx.x, 1u) == gridDim.y - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    uint64_t qs = 0, qk[RS_IPT];
+#pragma unroll
+    for (int k = 0; k < RS_IPT; ++k) {
+        qk[k] = 0;
+        const int i = blockIdx.x * RS_TILE + k * RS_T + tid;
+        if (i < P) {
+            const int32_t r = __ldcg(acc + i);
+            PGA_DCHECK(r >= 0 && r < P);
+            acc[i] = 0;
+            rank[i] = r;
+            order[r] = i;
+            if (q) {
+                qk[k] = qtab[r];
+                qs += qk[k];
+            }
+        }
+    }
+    if (tid == 0) ctr[blockIdx.x] = 0u;
+    if (!q) return;
+    // ---- SUS (as k_sus2): publish the tile's sum of q, wait for every
+    // tile's (the nb finalising CTAs are running: their tiles' other CTAs
+    // have finished), then the tile's base, Q, a block scan of q in index
+    // order and each individual's pointer range
+    const int nb = (int)gridDim.x;
+    uint32_t *arrive = ctr + RS_MAXTILES, *depart = arrive + 1;
+    const uint64_t tsum = block_sum_u64(qs, ws);
+    if (tid == 0) {
+        bsum[blockIdx.x] = tsum;
+        __threadfence();
+        atomicAdd(arrive, 1u);
+        while (*reinterpret_cast<volatile uint32_t *>(arrive) < (uint32_t)nb) __nanosleep(64);
+        __threadfence();
+    }
+    __syncthreads();
+    uint64_t a = 0, b = 0;
+    for (int k = tid; k < nb; k += RS_T) {
+        const uint64_t v = __ldcg(bsum + k);
+        b += v;
+        if (k < (int)blockIdx.x) a += v;
+    }
+    const uint64_t base = block_sum_u64(a, ws);
+    const uint64_t Q = block_sum_u64(b, ws);
+    if (tid == 0 && atomicAdd(depart, 1u) == (uint32_t)nb - 1) {   // the last to read arrive
+        *arrive = 0u;
+        *depart = 0u;
+    }
+    const uint32_t gen = (uint32_t)*gen_ptr;
+    const uint64_t step = Q / (uint64_t)M;
+    const U4 u = draw(seed, pga::TAG_SUS, island, gen, 0u, 0xFFFFFFFFu);
+    const uint64_t start = __umul64hi(((uint64_t)u.x << 32) | (uint64_t)u.y, step);
+    const int lane = tid & 31, wid = tid >> 5;
+    uint64_t run = base;
+#pragma unroll
+    for (int k = 0; k < RS_IPT; ++k) {
+        const int i = blockIdx.x * RS_TILE + k * RS_T + tid;
+        uint64_t incl = qk[k];
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint64_t o = __shfl_up_sync(0xFFFFFFFFu, incl, off);
+            if (lane >= off) incl += o;
+        }
+        __syncthreads();
+        if (lane == 31) ws[wid] = incl;
+        __syncthreads();
+        uint64_t wb = 0, tot = 0;
+        for (int w = 0; w < RS_T / 32; ++w) {
+            const uint64_t t = ws[w];
+            if (w < wid) wb += t;
+            tot += t;
+        }
+        if (i < P) {
+            const uint64_t hi = run + wb + incl, lo = hi - qk[k];
+            const int m0 = (int)min(sus_first(lo, start, step), (uint64_t)M);
+            const int m1 = (int)min(sus_first(hi, start, step), (uint64_t)M);
+            for (int m = m0; m < m1; ++m) sel[m] = i;
+        }
+        run += tot;
+    }
+}
+
+// q by rank for k_rank_sel: qtab[r] = floor(2^B / sqrt(r + 1)) (k_qsum's
+// formula with w_max = 1), B = 62 - ceil(log2 P)
+__global__ void k_qtab(int P, uint64_t *qtab) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= P) return;
+    const int B = 62 - ceil_log2_d(P);
+    const double x = 1.0 / sqrt((double)(r + 1));
+    qtab[r] = x > 0.0 ? (uint64_t)floor(ldexp(x, B)) : 0ull;
 }
 
 // One thread per item: bitonic stages with stride < 32 run as warp shuffles
@@ -1795,7 +1989,7 @@ int run_select_ops(const double *L, int64_t P, const pga_params &p, int32_t gen,
     PGA_LAUNCH_PDL(k_qsum, dim3(nbq), dim3(SCAN_T), 0, s, L, (const int32_t *)order, (const int32_t *)rank, P,
                    (int)p.scaling, q, bsum, done);
     const unsigned nbs = (unsigned)((max(P, M) + SCAN_T - 1) / SCAN_T);
-    PGA_LAUNCH_PDL(k_sus2, dim3(nbs), dim3(SCAN_T), 0, s, (const uint64_t *)q, (const uint64_t *)bsum, nbq, L,
+    PGA_LAUNCH_PDL(k_sus2<SCAN_T>, dim3(nbs), dim3(SCAN_T), 0, s, (const uint64_t *)q, (const uint64_t *)bsum, nbq, L,
                    (const int32_t *)order, P, M, (int)p.scaling, p.seed, (uint32_t)gen, (uint32_t)island, sel,
                    done, gen_ptr, sigma);
     return PGA_OK;
@@ -1857,11 +2051,31 @@ constexpr int SMALL_GA_P = 1024;
 bool small_select(const pga_ctx *c) {
     return c->P <= SMALL_GA_P || (c->P <= CSEL_MAXP && g_csel_ok && !getenv_flag("PGA_NO_CSEL", false));
 }
+// Rank + selection in one launch (k_rank_sel) for SMALL_GA_P < P <= RANKC_MAXP
+static bool rankc_use(const pga_ctx *c) {
+    return c->P > SMALL_GA_P && c->P <= pga::RANKC_MAXP && c->rc_acc && !getenv_flag("PGA_NO_RANKC", false);
+}
+int prepare_rank_sel(pga_ctx *c) {
+    if (!c->rc_acc) return PGA_OK;
+    k_qtab<<<(unsigned)((c->P + 255) / 256), 256, 0, c->stream>>>((int)c->P, c->rc_qtab);
+    PGA_CUDA(cudaGetLastError());
+    return PGA_OK;
+}
+static int launch_rank_sel(pga_ctx *c, bool sus, cudaStream_t s) {
+    const int P = (int)c->P, M = (int)(2 * ((c->P - c->p.elite + 1) / 2));
+    const unsigned nb = (unsigned)((P + RS_TILE - 1) / RS_TILE), nc = (unsigned)((P + RS_T - 1) / RS_T);
+    PGA_LAUNCH_PDL(k_rank_sel, dim3(nb, nc), dim3(RS_T), 0, s, (const double *)c->L, P,
+                   (const uint64_t *)c->rc_qtab, c->rc_acc, reinterpret_cast<uint32_t *>(c->rc_acc + c->Pcap),
+                   c->order, c->rank, sus, c->keys_in, M, c->p.seed, (uint32_t)c->p.island,
+                   (const int32_t *)&c->st->gen, c->sel);
+    return PGA_OK;
+}
 
 int launch_sort_order(pga_ctx *c, cudaStream_t s) {
     if (c->P <= SMALL_GA_P)
         return launch_select_small(1, c->L, c->P, c->p, 0, c->p.island, &c->st->gen, c->order, c->sel,
                                    c->sigma, &c->st->done, s);
+    if (rankc_use(c)) return launch_rank_sel(c, false, s);
     if (small_select(c))
         return launch_select_cluster(1, c->L, c->P, c->p, &c->st->gen, c->order, c->rank, c->sel,
                                      &c->st->done, s);
@@ -1881,6 +2095,17 @@ int launch_select(pga_ctx *c, cudaStream_t s) {
     if (c->P <= SMALL_GA_P) {
         rc = launch_select_small(3, c->L, c->P, p, 0, p.island, genp, c->order, c->sel, c->sigma, done, s);
         if (rc) return rc;
+    } else if (rankc_use(c)) {
+        // SUS with rank scaling (Table 3) completes in the launch; otherwise
+        // it leaves order / rank to the tournament or fitness-scaled SUS
+        const bool fused = p.selection == PGA_SEL_SUS && p.scaling == PGA_SCALE_RANK;
+        rc = launch_rank_sel(c, fused, s);
+        if (rc) return rc;
+        if (!fused) {
+            rc = run_select_ops(c->L, c->P, p, 0, p.island, c->order, c->sel, c->keys_in, c->keys_out,
+                                c->idx_in, c->rank, c->q, c->keys_in, done, s, genp, true, nullptr);
+            if (rc) return rc;
+        }
     } else if (small_select(c)) {
         rc = launch_select_cluster(3, c->L, c->P, p, genp, c->order, c->rank, c->sel, done, s);
         if (rc) return rc;

@@ -88,6 +88,8 @@ constexpr int PROF_EV = 9;     // phase marks per profiled generation
 constexpr int CB = 32;         // chromosomes per fitness CTA tile (one per lane)
 constexpr int LN_TAB = 128;    // table-driven log: c_j = 1 + (j + 1/2) / 128
 constexpr int SPARSE_MAX_N = 2048;   // largest N with a label-sparse pass (cluster cache, pair table)
+// rank + selection in one launch (k_rank_sel) for 1024 < P <= RANKC_MAXP
+constexpr int64_t RANKC_MAXP = 16384;
 
 // Cluster-cache slot (k_fitness_sparse): exact fixed-point c_s of a member
 // set keyed by two 64-bit Zobrist words; k1 == 0 empty; chk validates.
@@ -176,6 +178,8 @@ struct pga_ctx {
     uint64_t *keys_in = nullptr, *keys_out = nullptr;   // sort keys (double buffer); block sums after the sort
     int32_t *idx_in = nullptr, *order = nullptr;
     int32_t *rank = nullptr;           // rank[i] = position of individual i in order (last merge level)
+    int32_t *rc_acc = nullptr;         // k_rank_sel rank accumulators [Pcap] (zero between launches) + CTA counter
+    uint64_t *rc_qtab = nullptr;       // k_rank_sel q by rank [Pcap]
     uint64_t *q = nullptr;             // SUS segment widths (index order); the sort's index buffer before
     int32_t *sel = nullptr;
     int32_t *sigma = nullptr;
