@@ -263,6 +263,7 @@ int phase_a(pga_ctx *c, int32_t g, int32_t *is_mig) {
         PGA_CUDA(cudaEventRecord(c->fit_ev, c->stream));
         PGA_CUDA(cudaStreamWaitEvent(c->side, c->fit_ev, 0));
         TRY(launch_stats(c, c->p.n_islands > 1 ? 1 : 0, c->side));
+        if (mutmask_late(c)) TRY(launch_mutmask(c, c->side));   // read by this generation's breed
         PGA_CUDA(cudaEventRecord(c->stats_ev, c->side));
         TRY(launch_select(c, c->stream));
         PGA_CUDA(cudaStreamWaitEvent(c->stream, c->stats_ev, 0));
@@ -280,7 +281,7 @@ int phase_b(pga_ctx *c, bool fresh) {
     PGA_MARK(c, 4, c->stream);
     PGA_MARK(c, 5, c->stream);
     PGA_MARK(c, 6, c->stream);
-    TRY(launch_breed(c, c->stream));
+    TRY(launch_breed(c, c->stream, fresh));
     if (c->pev) {
         PGA_CUDA(prof_record(c->pev[8], c->stream));
         c->prof_used += PROF_EV;

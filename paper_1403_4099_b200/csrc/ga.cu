@@ -387,7 +387,7 @@ __global__ void k_tournament(const double *__restrict__ L, int64_t P, int64_t M,
 // thread per word (8 Philox blocks).  They depend only on (seed, generation,
 // island, slot), so the GA computes them on its side stream beside the
 // fitness pass (launch_mates_fork); elites (o < E) are never mutated.
-__global__ void k_mutmask(uint64_t seed, uint32_t island, const int32_t *gen_ptr, const int32_t *done, int64_t P,
+__global__ void k_mutmask(RoundKeys rk, uint32_t island, const int32_t *gen_ptr, const int32_t *done, int64_t P,
                           int N, int E, int64_t p_off, uint64_t thr_m, int mw, uint32_t *mask) {
     if (done && *done) return;
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -401,7 +401,7 @@ __global__ void k_mutmask(uint64_t seed, uint32_t island, const int32_t *gen_ptr
     for (int k = 0; k < 8; ++k) {
         const int blk = 8 * w + k;
         if (4 * blk < N) {
-            const U4 u = draw(seed, pga::TAG_MUT, island, gen, (uint32_t)blk, og);
+            const U4 u = draw_rk(rk, pga::TAG_MUT, island, gen, (uint32_t)blk, og);
             bits |= (((uint64_t)u.x < thr_m ? 1u : 0u) | ((uint64_t)u.y < thr_m ? 2u : 0u) |
                      ((uint64_t)u.z < thr_m ? 4u : 0u) | ((uint64_t)u.w < thr_m ? 8u : 0u)) << (4 * k);
         }
@@ -2124,7 +2124,7 @@ int launch_select(pga_ctx *c, cudaStream_t s) {
 // Crossover, mutation, canonicalisation, replacement (Alg. 1) from
 // the selection launch_select left in order / sel / sigma; the last CTA
 // advances the generation.
-int launch_breed(pga_ctx *c, cudaStream_t s) {
+int launch_breed(pga_ctx *c, cudaStream_t s, bool late_masks) {
     const pga_params &p = c->p;
     const int32_t *done = &c->st->done;
     const int32_t *genp = &c->st->gen;
@@ -2149,7 +2149,8 @@ int launch_breed(pga_ctx *c, cudaStream_t s) {
     // checks are live (it transposes exactly the blocks the dense sweep needs)
     a.gm_skip = (sparse_theta_eff(c) > 0.0 && c->N <= SPARSE_MAX_N) ? c->sp_live : nullptr;
     a.adv_st = c->st;           // the breed's last CTA advances the generation (no k_advance)
-    if (!(c->P <= SMALL_GA_P) && c->mmask && mutmask_use(c->P)) {   // masks from the side stream
+    if (!(c->P <= SMALL_GA_P) && c->mmask && (mutmask_use(c->P) || (late_masks && mutmask_late(c)))) {
+        // masks from the side stream
         a.mmask = c->mmask;
         a.mw = (c->N + 31) / 32;
     }
@@ -2169,6 +2170,26 @@ int launch_breed(pga_ctx *c, cudaStream_t s) {
 // generation's evaluation and joined at its end, so the Feistel permutation
 // runs beside the fitness pass instead of on the selection's critical path.
 // (P <= SMALL_GA_P: k_select_small computes them itself.)
+// the generation's mutation masks (the breed's per-gene MUT draws) on s
+int launch_mutmask(pga_ctx *c, cudaStream_t s) {
+    BreedArgs t{};
+    fill_breed(t, c->p, c->P, c->N);
+    const int mw = (c->N + 31) / 32;
+    const int64_t nth = c->P * (int64_t)mw;
+    k_mutmask<<<(unsigned)((nth + 255) / 256), 256, 0, s>>>(t.rk, (uint32_t)c->p.island, &c->st->gen, &c->st->done,
+                                                            c->P, c->N, c->p.elite, (int64_t)c->p.island * c->P,
+                                                            t.thr_m, mw, c->mmask);
+    PGA_LAUNCHED();
+    return PGA_OK;
+}
+
+// For P > MUTMASK_MAXP the masks are computed beside the statistics and the
+// selection of a non-migration generation (latency-bound sort / scan launches
+// that leave most SMs idle), and the breed of that generation reads them.
+bool mutmask_late(const pga_ctx *c) {
+    return c->mmask && c->P > MUTMASK_MAXP && c->P > SMALL_GA_P && !getenv_flag("PGA_NO_MUTMASK_LATE", false);
+}
+
 int launch_mates_fork(pga_ctx *c, cudaStream_t s) {
     if (c->P <= SMALL_GA_P) return PGA_OK;
     const int64_t M = 2 * ((c->P - c->p.elite + 1) / 2);
@@ -2178,15 +2199,8 @@ int launch_mates_fork(pga_ctx *c, cudaStream_t s) {
                                                                &c->st->done, &c->st->gen);
     PGA_LAUNCHED();
     if (c->mmask && mutmask_use(c->P)) {
-        BreedArgs t{};
-        fill_breed(t, c->p, c->P, c->N);
-        const int mw = (c->N + 31) / 32;
-        const int64_t nth = c->P * (int64_t)mw;
-        k_mutmask<<<(unsigned)((nth + 255) / 256), 256, 0, c->side>>>(c->p.seed, (uint32_t)c->p.island, &c->st->gen,
-                                                                       &c->st->done, c->P, c->N, c->p.elite,
-                                                                       (int64_t)c->p.island * c->P, t.thr_m, mw,
-                                                                       c->mmask);
-        PGA_LAUNCHED();
+        const int rc = launch_mutmask(c, c->side);
+        if (rc) return rc;
     }
     PGA_CUDA(cudaEventRecord(c->join_side_ev, c->side));
     return PGA_OK;

@@ -255,7 +255,9 @@ int launch_init(pga_ctx *c, uint64_t seed, cudaStream_t s);
 int launch_stats(pga_ctx *c, int is_migration_check, cudaStream_t s);
 int launch_sort_order(pga_ctx *c, cudaStream_t s);
 int launch_select(pga_ctx *c, cudaStream_t s);   // order + scaling + selection
-int launch_breed(pga_ctx *c, cudaStream_t s);    // crossover .. replacement + advance
+int launch_breed(pga_ctx *c, cudaStream_t s, bool late_masks);   // crossover .. replacement + advance
+int launch_mutmask(pga_ctx *c, cudaStream_t s);   // the breed's mutation masks (k_mutmask)
+bool mutmask_late(const pga_ctx *c);              // masks beside stats + selection (P > 8192)
 int launch_export(pga_ctx *c, void *dev_send, cudaStream_t s);
 int launch_mates_fork(pga_ctx *c, cudaStream_t s);
 int launch_mates_join(pga_ctx *c, cudaStream_t s);
