@@ -1515,6 +1515,16 @@ __global__ void __launch_bounds__(BW * 32, NB <= 2 ? 3 : PGA_B2_MINB) k_breed2(B
     const int64_t o0 = (int64_t)blockIdx.x * BS;
     const int slot = warp;
     const int64_t o = o0 + slot;
+    // precomputed mutation-mask words (k_mutmask) depend only on the child
+    // index: their loads are issued before the plan's dependent chain
+    // (sigma -> sel -> parent labels) instead of after it
+    uint32_t mwv[NB];
+    {
+        const bool mw_on = a.mmask && o < a.P && o >= a.E && a.thr_m != 0;
+#pragma unroll
+        for (int b = 0; b < NB; ++b)
+            mwv[b] = (mw_on && GCH * b + 4 * lane < N) ? a.mmask[o * a.mw + ((GCH * b) >> 5) + (lane >> 3)] : 0u;
+    }
     const ChildPlan p = plan_child(a, o, gen);
 
     // ---- phase 1: crossover + mutation -> pre-canonical pair words.  Both
@@ -1542,9 +1552,8 @@ __global__ void __launch_bounds__(BW * 32, NB <= 2 ? 3 : PGA_B2_MINB) k_breed2(B
         }
         uint32_t mbits = 0;
         if (p.valid && p.mutate && b0 + 4 * lane < N) {
-            if (a.mmask) {   // precomputed beside the fitness pass (k_mutmask)
-                const uint32_t wv = a.mmask[o * a.mw + (b0 >> 5) + (lane >> 3)];
-                mbits = (wv >> (4 * (lane & 7))) & 0xFu;
+            if (a.mmask) {   // precomputed on the side stream (k_mutmask)
+                mbits = (mwv[b] >> (4 * (lane & 7))) & 0xFu;
             } else {
                 const U4 u = draw_rk(a.rk, pga::TAG_MUT, a.island, gen, (uint32_t)((b0 >> 2) + lane), p.og);
                 mbits = ((uint64_t)u.x < a.thr_m ? 1u : 0u) | ((uint64_t)u.y < a.thr_m ? 2u : 0u) |
