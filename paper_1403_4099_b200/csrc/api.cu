@@ -158,7 +158,7 @@ void free_ctx(pga_ctx *c) {
                     c->counters};
     for (void *p : ptrs)
         if (p) cudaFree(p);
-    if (c->h_st) cudaFreeHost(c->h_st);
+    delete c->h_st;
     for (cudaEvent_t e : c->prof_ev) cudaEventDestroy(e);
     if (c->join_ev) cudaEventDestroy(c->join_ev);
     if (c->fork_ev) cudaEventDestroy(c->fork_ev);
@@ -526,8 +526,9 @@ int pga_create(const double *C, int32_t N, const pga_params *p, pga_ctx **out) {
     if (e == cudaSuccess && c->rc_acc)
         e = cudaMemsetAsync(c->rc_acc, 0, sizeof(int32_t) * ((size_t)c->Pcap + 64), c->stream);
     if (e != cudaSuccess) return bail(cuda_fail(e, "cudaMemset counters"));
-    e = cudaMallocHost((void **)&c->h_st, sizeof(DevState));
-    if (e != cudaSuccess) return bail(fail(PGA_ENOMEM, "cudaMallocHost failed"));
+    // host copy of the device state: pageable (every read of it follows a
+    // stream synchronisation; cudaMallocHost cost ~9 ms per context)
+    c->h_st = new DevState();
     // population buffers: zero so padding chromosomes hold valid labels
     for (int b = 0; b < 2; ++b) {
         e = cudaMemsetAsync(c->pop[b], 0, sizeof(uint16_t) * cm, c->stream);

@@ -205,7 +205,7 @@ struct pga_ctx {
     bool has_pop = false;
     bool pending_migration = false;
     int32_t host_gen = 0;              // host-side count of launched generations
-    // pinned host
+    // host copy of the device state (pageable; read after a stream sync)
     pga::DevState *h_st = nullptr;
     // profiling (pga_profile_enable): per generation 4 events
     bool prof = false;

@@ -125,6 +125,44 @@ def test_generation_lockstep_cluster_select(pga, orc, P, sel, scal, E, path, mon
         pga.pga_destroy(ctx)
 
 
+@pytest.mark.parametrize("path", ["rank_count", "cluster_or_sort"])
+@pytest.mark.parametrize("P,kind", [(2048, "identical"), (5000, "singletons"), (12000, "two_values")])
+def test_generation_lockstep_selection_ties(pga, orc, P, kind, path, monkeypatch):
+    """Selection with massive L ties (1024 < P <= 16384): every individual
+    the same chromosome (all L equal), every individual all singletons (L =
+    0 everywhere: the sort key equals the padding key of k_rank_sel's
+    chunks), or two distinct chromosomes alternating.  The order must break
+    ties by index across chunks and tiles; one generation in lockstep with
+    orc_step (bit-exact), by rank counting and by the cluster / sort path."""
+    if path != "rank_count":
+        monkeypatch.setenv("PGA_NO_RANKC", "1")
+    C, planted = _corr(orc, workloads.CONFIGS["C3"])
+    N = C.shape[0]
+    if kind == "identical":
+        pop = np.tile(planted, (P, 1))
+    elif kind == "singletons":
+        pop = np.tile(np.arange(N), (P, 1))
+    else:
+        alt = orc.canonicalize(np.where(np.arange(N) % 2 == 0, planted, 0)[None, :])[0]
+        pop = np.where((np.arange(P) % 2 == 0)[:, None], planted[None, :], alt[None, :])
+    pop = pop.astype(np.int32)
+    params = _par(pga, P, max_gens=4, tol=-1.0, p_mutation=0.02, seed=23)
+    op = orc.default_params(pop=P, max_gens=4, tol=-1.0, p_m=0.02, seed=23)
+    ctx = pga.pga_create(C, params)
+    try:
+        pga.pga_init(ctx, 23)
+        pga.pga_set_population(ctx, pop + 1, 0)
+        pga.pga_generation(ctx)
+        nxt, L, top = pga.pga_get_population(ctx, with_top=True)
+        Lo = orc.evaluate(C, pop, nthreads=NT)[0]
+        _assert_L(L, Lo)
+        if kind == "singletons":
+            assert np.all(L == 0.0)
+        assert np.array_equal(nxt - 1, orc.step(op, pop, L, top, gen=0))
+    finally:
+        pga.pga_destroy(ctx)
+
+
 # ---------------------------------------------------------------------------
 # islands: the Q28 stall rule with tol >= 0, bit-exact after every import
 # ---------------------------------------------------------------------------
