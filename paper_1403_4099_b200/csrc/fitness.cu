@@ -238,17 +238,9 @@ __device__ __forceinline__ void eq8_tables(double *cs, int32_t *ns, int K, int l
 
 // Summand of Eq. 8 (Q1-Q3) for a cluster of n >= 2 members with intra-
 // cluster sum c: 0 unless c > n (Q2); c clamped to n^2 - 1e-9 (Q3); the
-// integer logs from the table (Q30).
-__device__ __forceinline__ double eq8_term(int n, double c, const double *__restrict__ lgn,
-                                           const double *__restrict__ lgnn) {
-    if (!(c > (double)n)) return 0.0;
-    const double nd = (double)n, n2 = nd * nd;
-    const double ch = fmin(c, n2 - 1e-9);
-    return (__ldg(lgn + n) - log(ch)) + (nd - 1.0) * (__ldg(lgnn + n) - log(n2 - ch));
-}
-
-// The same summand with the table-driven log (label-sparse pass): its
-// clusters all have c > n >= 2 and n^2 - c >= 1e-9, positive normals.
+// integer logs from the table (Q30), ln by the table-driven fast_ln (the
+// label-sparse pass: its clusters all have c > n >= 2 and n^2 - c >= 1e-9,
+// positive normals).
 __device__ __forceinline__ double eq8_term_fast(int n, double c, const double *__restrict__ lgn,
                                                 const double *__restrict__ lgnn,
                                                 const double2 *__restrict__ lnt) {
@@ -615,12 +607,6 @@ constexpr int WALK_N = 4;
 constexpr int SMALL_N = WALK_N - 1;   // members recorded per label
 static_assert(CC_NMIN >= WALK_N, "cacheable clusters are in the walk class");
 __host__ __device__ __forceinline__ int cc_entries(int N) { return N / WALK_N + 1; }
-
-__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t *p) {
-    uint64_t v;
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
 
 // slot: k1 claimed by CAS (0 = empty); k2, v and chk = cc_mix(k1, k2, v, n)
 // are then written once.  A reader takes the slot only if k1, k2 and the
@@ -1151,7 +1137,7 @@ __global__ void __launch_bounds__(SPW * 32, SPW == 16 ? PGA_SP_MINB : 1) k_fitne
 
 // Eq. 8 term of every pair cluster {i, j} (the label-sparse pass's n = 2
 // clusters): c = C_ii + C_jj + 2 C_ij in the pass's fixed point, then the
-// same eq8_term -- identical to what a walk of that pair would give.
+// same eq8_term_fast -- identical to what a walk of that pair would give.
 __global__ void k_pairtab(const double *__restrict__ C, int ldc, const double *__restrict__ diag, int N,
                           double fx_scale, double fx_inv, const double *__restrict__ lgn,
                           const double *__restrict__ lgnn, const double2 *__restrict__ lnt, double *T) {

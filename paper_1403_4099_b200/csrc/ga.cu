@@ -166,7 +166,7 @@ k_stats(const double *__restrict__ L, int64_t P, const uint16_t *CM0, const uint
     pdl_wait();
     pdl_trigger();
     if (st->done) return;
-    const int tid = threadIdx.x, lane = tid & 31;
+    const int tid = threadIdx.x;
     double best = -1.0, sum = 0.0;
     int bi = 0x7FFFFFFF;
     const int64_t lo = (int64_t)blockIdx.x * per, hi = min(P, lo + per);
