@@ -1,5 +1,5 @@
 # Round-2 bench lines and captures -> gpurun_out/final/
-O=gpurun_out/final2; mkdir -p $O
+O=gpurun_out/final3; mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/smi.txt 2>&1
 for c in C1 C2 C3; do
   timeout 600 python bench.py --config $c --steps 500 --warmup 5 > $O/bench_$c.json 2> $O/bench_$c.err
@@ -21,3 +21,4 @@ timeout 900 /usr/local/cuda/bin/ncu --set full --import-source on --clock-contro
 timeout 900 /usr/local/cuda/bin/ncu --set full --clock-control none -k regex:"k_fitness\b|k_fitness\(" --launch-skip 8 --launch-count 1 -o $O/c4_dense python bench.py --steps 3 --warmup 5 --no-cpu --no-e2e --sparse-theta 0 > $O/ncu_dense.log 2>&1
 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.txt 2>&1
 timeout 600 /usr/local/cuda/bin/ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file $O/launches_il8.csv python bench.py --steps 3 --warmup 3 --no-cpu --no-e2e --island-load 8 > $O/ncu_il8.log 2>&1
+timeout 1800 python -m pytest tests/ -q -x -m gpu > $O/pytest_gpu.log 2>&1; echo "rc=$?" >> $O/pytest_gpu.log
