@@ -22,3 +22,17 @@ def orc():
     import oracle
     oracle.build()
     return oracle
+
+
+def pytest_sessionfinish(session, exitstatus):
+    """Under the device-check build (PGA_LIB=.../libpga_check.so, see
+    tests/test_gpu_checks.py) the whole GPU suite must leave the device
+    invariant counters at zero."""
+    lib = os.environ.get("PGA_LIB", "")
+    if not lib.endswith("libpga_check.so") or exitstatus != 0:
+        return
+    import paper_1403_4099_b200 as pga
+    v = pga.pga_debug_violations()
+    print("\ndevice invariant violations over the session: %d" % v)
+    if v:
+        session.exitstatus = 1
