@@ -542,9 +542,12 @@ def main():
                                     "cache on) are evaluated label-sparsely and skipped by k_fitness; "
                                     "clusters of >= 5 genes come from the cluster cache when an earlier "
                                     "generation had the same member set, the rest are gathered from L2"},
-            "phase_ms_per_generation": {k: round(v, 4) for k, v in phases.items()
-                                        if k != "fitness_fold_fused"},
-            "phase_note": "diagnostic pass after the timed region (phase events add ~3 us/gen)",
+            "phase_ms_per_generation": {("stats_order_selection" if k == "stats" else k): round(v, 4)
+                                        for k, v in phases.items() if k != "fitness_fold_fused"},
+            "phase_note": "diagnostic pass after the timed region (phase events add ~3 us/gen); in "
+                          "non-migration generations the order sort and the selection run in phase A "
+                          "beside the statistics (side stream), so their time is in "
+                          "stats_order_selection and order_sort/selection/mates show only the marks",
             "roofline": rl_main,
             "roofline_other": rl_other,
             "gpu_launches": int(launches),

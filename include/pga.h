@@ -434,9 +434,10 @@ int pga_profile_sparse(pga_ctx *ctx, int64_t *sparse_blocks, int64_t *gathered);
 int pga_profile_cache(pga_ctx *ctx, int64_t *hits, int64_t *saved);
 
 /* Level-2 profiling: per-phase AVERAGE milliseconds, ms[PGA_PROF_PHASES]:
- * 0 dense fitness kernel (sweep + fused fold), 1 label-sparse pre-pass, 2 statistics/termination,
- * 3 order sort, 4 scaling+selection, 5 mate pairing, 6 breed, 7 advance (fused into the
- * breed's last CTA since round 2: ~0). */
+ * 0 dense fitness kernel (sweep + fused fold), 1 label-sparse pre-pass, 2 statistics/termination
+ * (in non-migration generations also the order sort and the selection, which run beside the
+ * statistics since round 2), 3 order sort, 4 scaling+selection, 5 mate pairing (~0 then: only
+ * the phase marks), 6 breed, 7 advance (fused into the breed's last CTA since round 2: ~0). */
 #define PGA_PROF_PHASES 8
 int pga_profile_phases(pga_ctx *ctx, double *ms, int32_t *count);
 
