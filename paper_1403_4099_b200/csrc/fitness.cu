@@ -141,6 +141,7 @@ struct FitArgs {
     int cb0;                        // first chromosome block (shard offset / 32)
     double fx_scale, fx_inv;        // fold fixed point: 2^S and 2^-S
     const double *lgn, *lgnn;       // log n, log(n^2 - n), n = 0..N (Q30)
+    const double2 *lnt;             // fast_ln table (after lgn, lgnn in the ctx's lgtab)
     const uint8_t *sflag;           // per chromosome block: 1 = already evaluated label-sparsely
     int64_t P, Pcap;
     const double *diag;
@@ -183,11 +184,13 @@ __device__ __forceinline__ void pairs16(uint32_t caddr, uint32_t w, const uint32
 // non-zero summands, Q2) are compacted to the front of cs/ns in label order
 // (ns keeps n | label << 16), then the summands are taken lane-parallel as
 // (log n - log c) + (n-1)(log(n^2-n) - log(n^2-c)) with the integer logs from
-// the table (Q30: no divisions), c clamped to n^2 - 1e-9 (Q3); L = half the
-// sum; top = label of the largest summand (smallest label on ties).
+// the table (Q30: no divisions) and the two real logs by the table-driven
+// fast_ln (as the label-sparse pass; c > n >= 2 and n^2 - c >= 1e-9 here),
+// c clamped to n^2 - 1e-9 (Q3); L = half the sum; top = label of the
+// largest summand (smallest label on ties).
 __device__ __forceinline__ void eq8_tables(double *cs, int32_t *ns, int K, int lane, double inv_scale,
                                            const double *__restrict__ lgn, const double *__restrict__ lgnn,
-                                           double *L_out, uint16_t *top_out) {
+                                           const double2 *__restrict__ lnt, double *L_out, uint16_t *top_out) {
     int M = 0;
     for (int k0 = 0; k0 < K; k0 += 32) {
         const int k = k0 + lane;
@@ -213,7 +216,7 @@ __device__ __forceinline__ void eq8_tables(double *cs, int32_t *ns, int K, int l
         const int n = nk & 0xFFFF;
         const double nd = (double)n, n2 = nd * nd;
         const double ch = fmin(cs[j], n2 - 1e-9);
-        const double f = (__ldg(lgn + n) - log(ch)) + (nd - 1.0) * (__ldg(lgnn + n) - log(n2 - ch));
+        const double f = (__ldg(lgn + n) - fast_ln(ch, lnt)) + (nd - 1.0) * (__ldg(lgnn + n) - fast_ln(n2 - ch, lnt));
         fsum += f;
         if (f > fbest) {
             fbest = f;
@@ -264,7 +267,8 @@ __device__ __forceinline__ void fold_multi(const uint16_t *const (&lab)[NC], int
                                            int N, double *const (&cs)[NC], int32_t *const (&ns)[NC],
                                            int lane, double *const (&L_out)[NC],
                                            uint16_t *const (&top_out)[NC], double scale, double inv_scale,
-                                           const double *__restrict__ lgn, const double *__restrict__ lgnn) {
+                                           const double *__restrict__ lgn, const double *__restrict__ lgnn,
+                                           const double2 *__restrict__ lnt) {
     // cs / ns were zeroed by the caller (all-zero bits == integer 0)
     // software pipeline: loads of chunk c+2 are issued while chunk c folds.
     // Gene-major labels of two adjacent chromosomes (p even, p + 1) are one
@@ -333,7 +337,7 @@ __device__ __forceinline__ void fold_multi(const uint16_t *const (&lab)[NC], int
     const int K = (int)min(kmax + 1u, (uint32_t)N);
 #pragma unroll
     for (int q = 0; q < NC; ++q)
-        eq8_tables(cs[q], ns[q], K, lane, inv_scale, lgn, lgnn, L_out[q], top_out[q]);
+        eq8_tables(cs[q], ns[q], K, lane, inv_scale, lgn, lgnn, lnt, L_out[q], top_out[q]);
     __syncwarp();
 }
 
@@ -515,7 +519,7 @@ k_fitness(const __grid_constant__ CUtensorMap tmLab0, const __grid_constant__ CU
                 for (int k = lane; k < N * NCF / 2; k += 32) n2[k] = make_uint2(0u, 0u);
                 __syncwarp();
             }
-            fold_multi<NCF>(lab, a.Pcap, vv, N, cs, ns, lane, Lo, to, a.fx_scale, a.fx_inv, a.lgn, a.lgnn);
+            fold_multi<NCF>(lab, a.Pcap, vv, N, cs, ns, lane, Lo, to, a.fx_scale, a.fx_inv, a.lgn, a.lgnn, a.lnt);
             // V of these chromosomes is dead: drop its L2 lines without a
             // DRAM write-back (rows are 128-byte aligned, ldn % 16 == 0)
 #pragma unroll
@@ -1303,6 +1307,7 @@ int launch_fitness_range(pga_ctx *c, const FitBufs &b, int64_t begin, int64_t en
     a.cb0 = (int)(begin / CB);
     a.lgn = c->lgtab;
     a.lgnn = c->lgtab + (N + 1);
+    a.lnt = reinterpret_cast<const double2 *>(c->lgtab + 2 * (N + 1));
     fx_scale_of(N, &a.fx_scale, &a.fx_inv);   // |sum of V over a cluster| <= 2 N^2
     a.nCB = (int)((end - begin + CB - 1) / CB);
     a.fold_warps = fold_warps(N);
