@@ -969,8 +969,9 @@ def e2e_run(pga, torch, dist, C, params, world, K, planted, theta=None):
     d2h = 56 + 2 * N          # DevState + best labels (u16)
     return {"value": value, "unit": "pair-updates/s", "h2d_bytes_per_step": N * N * 8 / K,
             "d2h_bytes_per_step": d2h, "steps": K, "seconds": dt,
-            "includes": "pga_create from pinned host C + init + K generations + per-step state "
-                        "read + final global best gather"}
+            "includes": "pga_create from pinned host C (device buffers from the library's memory "
+                        "pool, which keeps the pages of the timed run's destroyed context) + init + K "
+                        "generations + per-step state read + final global best gather"}
 
 
 if __name__ == "__main__":

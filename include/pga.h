@@ -77,7 +77,10 @@ int pga_params_default(pga_params *out);
  * (row-major fp64, host) to the device and allocates the population.
  * C must be exactly symmetric, |C_ii - 1| <= 1e-12, |C_ij| <= 1 + 1e-9,
  * finite (Eq. 7; reading Q4); otherwise PGA_EINVAL.  2 <= N <= 16384.
- * The ctx owns its copy of C; the caller's buffer may be freed on return. */
+ * The ctx owns its copy of C; the caller's buffer may be freed on return.
+ * Device buffers come from a per-device memory pool of the library that keeps
+ * up to PGA_POOL_KEEP_MB (environment, default 4096) MiB of memory freed by
+ * pga_destroy mapped for later contexts in the process. */
 int pga_create(const double *C, int32_t N, const pga_params *p, pga_ctx **out);
 
 /* The ctx's sizes (host only, no device call): N, pop_size (this island's

@@ -1,4 +1,5 @@
 #include <cstdlib>
+#include <mutex>
 // api.cu — the C ABI declared in include/pga.h.  Argument validation, the
 // per-island runtime (buffers, stream, CUDA graph of one generation) and the
 // host<->device marshalling.  Every step of the method runs in the kernels of
@@ -129,6 +130,40 @@ int ensure_device(int dev) {
 
 using namespace pga;
 
+// Device buffers of the ABI come from a per-device memory pool of the
+// library that keeps up to PGA_POOL_KEEP_MB (default 4096) MiB of freed
+// memory mapped for later allocations in the process: a context created
+// after an earlier one was destroyed reuses its pages instead of mapping
+// new ones (cudaMalloc of C4's ~0.7 GB costs 15-40 ms).  Allocation and free
+// are made synchronous, like cudaMalloc / cudaFree.
+cudaMemPool_t pga::lib_pool(int *err) {
+    static std::mutex mu;
+    static cudaMemPool_t pools[64] = {};
+    int dev = 0;
+    *err = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+        *err = 1;
+        return nullptr;
+    }
+    std::lock_guard<std::mutex> lk(mu);
+    if (!pools[dev]) {
+        cudaMemPoolProps pr = {};
+        pr.allocType = cudaMemAllocationTypePinned;
+        pr.location.type = cudaMemLocationTypeDevice;
+        pr.location.id = dev;
+        if (cudaMemPoolCreate(&pools[dev], &pr) != cudaSuccess) {
+            pools[dev] = nullptr;
+            *err = 1;
+            return nullptr;
+        }
+        uint64_t keep = 4096ull << 20;
+        if (const char *e = std::getenv("PGA_POOL_KEEP_MB")) keep = std::strtoull(e, nullptr, 10) << 20;
+        cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    return pools[dev];
+}
+
+
 namespace {
 
 
@@ -145,6 +180,8 @@ void drop_graphs(pga_ctx *c) {
     drop_graph(c->gx_breed[1]);
 }
 
+static void dfree(void *p);
+
 void free_ctx(pga_ctx *c) {
     if (!c) return;
     cudaSetDevice(c->device);
@@ -156,8 +193,7 @@ void free_ctx(pga_ctx *c) {
                     c->sel, c->sigma, c->breed_ctr, c->mmask, c->st,
                     c->best_labels, c->history, c->stage_i32, c->evCM, c->evGM, c->evL,
                     c->counters};
-    for (void *p : ptrs)
-        if (p) cudaFree(p);
+    for (void *p : ptrs) dfree(p);
     delete c->h_st;
     for (cudaEvent_t e : c->prof_ev) cudaEventDestroy(e);
     if (c->join_ev) cudaEventDestroy(c->join_ev);
@@ -171,9 +207,21 @@ void free_ctx(pga_ctx *c) {
 
 template <typename T>
 int dalloc(T **p, size_t count) {
-    cudaError_t e = cudaMalloc((void **)p, sizeof(T) * (count ? count : 1));
-    if (e != cudaSuccess) return fail(PGA_ENOMEM, std::string("cudaMalloc failed: ") + cudaGetErrorString(e));
+    int perr = 0;
+    cudaMemPool_t pool = lib_pool(&perr);
+    if (perr) return fail(PGA_EDEVICE, "device memory pool unavailable");
+    cudaError_t e = cudaMallocFromPoolAsync((void **)p, sizeof(T) * (count ? count : 1), pool, 0);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(0);
+    if (e != cudaSuccess) return fail(PGA_ENOMEM, std::string("device allocation failed: ") + cudaGetErrorString(e));
     return PGA_OK;
+}
+
+// the counterpart of dalloc (waits for the device, as cudaFree does)
+static void dfree(void *p) {
+    if (!p) return;
+    cudaDeviceSynchronize();
+    cudaFreeAsync(p, 0);
+    cudaStreamSynchronize(0);
 }
 
 #define TRY(x)                 \
@@ -209,7 +257,7 @@ int ensure_history(pga_ctx *c, int32_t n) {
     if (c->history) {
         PGA_CUDA(cudaMemcpyAsync(h, c->history, sizeof(double) * c->hist_cap, cudaMemcpyDeviceToDevice, c->stream));
         PGA_CUDA(cudaStreamSynchronize(c->stream));
-        cudaFree(c->history);
+        dfree(c->history);
     }
     c->history = h;
     c->hist_cap = n;
@@ -365,7 +413,7 @@ void to_one_based(const std::vector<uint16_t> &src, int32_t *dst, size_t n) {
 struct HookBufs {
     std::vector<void *> ptrs;
     ~HookBufs() {
-        for (void *p : ptrs) cudaFree(p);
+        for (void *p : ptrs) dfree(p);
     }
     template <typename T>
     int get(T **p, size_t n) {
@@ -1000,9 +1048,9 @@ int pga_correlation(const double *returns, int32_t T, int32_t N, double *C_out, 
             if (e != cudaSuccess) rc = cuda_fail(e, "pga_correlation");
         }
     }
-    cudaFree(X);
-    cudaFree(C);
-    cudaFree(st);
+    dfree(X);
+    dfree(C);
+    dfree(st);
     cudaStreamDestroy(s);
     if (!rc && hst) rc = fail(PGA_ENUMERIC, "zero-variance or non-finite column in returns");
     return rc;

@@ -671,7 +671,7 @@ int pga_batch_run(const double *C, int32_t B, int32_t N, const pga_params *p, in
     const size_t nC = (size_t)B * N * N, nH = history ? (size_t)B * p->max_gens : 0;
     unsigned char *blob = nullptr;
     const size_t bytes = sizeof(double) * (nC + B + nH) + sizeof(int32_t) * ((size_t)B * N + 2 * (size_t)B) + 64;
-    PGA_CUDA(cudaMallocAsync((void **)&blob, bytes, st));
+    PGA_CUDA(pga::pool_malloc_async((void **)&blob, bytes, st));
     struct BlobGuard {
         void *p;
         cudaStream_t s;

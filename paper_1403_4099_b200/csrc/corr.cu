@@ -120,9 +120,9 @@ int launch_corr(const double *X, int32_t T, int32_t N, double *C, int32_t *statu
     const int Npad = (N + GT - 1) / GT * GT;
     const int Tpad = (T + GK - 1) / GK * GK;
     double *mean = nullptr, *inv = nullptr, *Z = nullptr;
-    PGA_CUDA(cudaMallocAsync(&mean, sizeof(double) * N, s));
-    PGA_CUDA(cudaMallocAsync(&inv, sizeof(double) * N, s));
-    PGA_CUDA(cudaMallocAsync(&Z, sizeof(double) * (size_t)Npad * Tpad, s));
+    PGA_CUDA(pga::pool_malloc_async((void **)&mean, sizeof(double) * N, s));
+    PGA_CUDA(pga::pool_malloc_async((void **)&inv, sizeof(double) * N, s));
+    PGA_CUDA(pga::pool_malloc_async((void **)&Z, sizeof(double) * (size_t)Npad * Tpad, s));
     k_colstats<<<(N + 127) / 128, 128, 0, s>>>(X, T, N, mean, inv, status);
     PGA_LAUNCHED();
     PGA_CUDA(cudaMemsetAsync(Z, 0, sizeof(double) * (size_t)Npad * Tpad, s));

@@ -253,6 +253,14 @@ int launch_fitness_range(pga_ctx *c, const FitBufs &b, int64_t begin, int64_t en
                          uint16_t *top, cudaStream_t s, cudaEvent_t *ev = nullptr);
 int launch_init(pga_ctx *c, uint64_t seed, cudaStream_t s);
 int launch_stats(pga_ctx *c, int is_migration_check, cudaStream_t s);
+// the library's per-device memory pool (api.cu dalloc); *err != 0 if unavailable
+cudaMemPool_t lib_pool(int *err);
+// stream-ordered scratch from that pool
+inline cudaError_t pool_malloc_async(void **p, size_t bytes, cudaStream_t s) {
+    int err = 0;
+    cudaMemPool_t pool = lib_pool(&err);
+    return err ? cudaMallocAsync(p, bytes, s) : cudaMallocFromPoolAsync(p, bytes, pool, s);
+}
 int launch_sort_order(pga_ctx *c, cudaStream_t s);
 int launch_select(pga_ctx *c, cudaStream_t s);   // order + scaling + selection
 int launch_breed(pga_ctx *c, cudaStream_t s, bool late_masks);   // crossover .. replacement + advance

@@ -300,7 +300,7 @@ int pga_corr_stream(const double *X, int32_t T, int32_t N, double lambda, int32_
         // stream-ordered scratch: no device-wide synchronisation
         cudaStream_t st = (cudaStream_t)stream;
         double *R = nullptr;
-        PGA_CUDA(cudaMallocAsync((void **)&R, sizeof(double) * ((size_t)B * N * N + 1), st));
+        PGA_CUDA(pga::pool_malloc_async((void **)&R, sizeof(double) * ((size_t)B * N * N + 1), st));
         int rc = launch_stream(X, T, N, lambda, warm, stride, qq, clean, C_out, status, R, st);
         cudaFreeAsync(R, st);
         return rc;
@@ -317,7 +317,7 @@ int pga_corr_stream(const double *X, int32_t T, int32_t N, double lambda, int32_
     } guard{st};
     const size_t nX = (size_t)T * N, nR = (size_t)B * N * N;
     unsigned char *blob = nullptr;
-    PGA_CUDA(cudaMallocAsync((void **)&blob, sizeof(double) * (nX + 2 * nR) + 64, st));
+    PGA_CUDA(pga::pool_malloc_async((void **)&blob, sizeof(double) * (nX + 2 * nR) + 64, st));
     struct BlobGuard {
         void *p;
         cudaStream_t s;
