@@ -635,7 +635,7 @@ __device__ __forceinline__ void cs_exchange(uint64_t &k, uint32_t &v, int partne
 // RANKC_MAXP, spread over the whole GPU.  The position of i in the (L desc,
 // index asc) order is the number of j before it.  CTA (x, y) sorts chunk y
 // of RS_T individuals in shared memory (bitonic, one item per thread) and
-// each of the RS_TILE individuals i of tile x counts the chunk's items before
+// each of the RS_T * IPT individuals i of tile x counts the chunk's items before
 // it by a binary search; the counts are added into acc[i] (integer atomics:
 // the sum is order-free).  The last CTA of tile x to finish (threadfence +
 // per-tile counter) reads and re-zeroes acc, writes rank and order and,
@@ -646,20 +646,24 @@ __device__ __forceinline__ void cs_exchange(uint64_t &k, uint32_t &v, int partne
 // writes the tile's SUS pointer ranges from its base, Q and a block scan --
 // the exact u64 prefix of k_qsum + k_sus2, without their launches.  A sort of a few thousand items in one CTA or one
 // cluster is a chain of dependent steps on a handful of SMs; here each CTA's
-// chain is one 512-item sort and two 10-step searches per thread.
+// chain is one 512-item sort and one or two 10-step searches per thread.
 // ---------------------------------------------------------------------------
 #ifndef PGA_RS_T
 #define PGA_RS_T 512
 #endif
-constexpr int RS_T = PGA_RS_T, RS_TILE = 1024, RS_IPT = RS_TILE / RS_T;   // chunk RS_T, tile RS_TILE
+// chunk RS_T; tile RS_T * IPT individuals: IPT = 1 up to P = 8192 (16 x 16
+// CTAs keep every SM busy: island-load 8 0.1130 -> 0.1111 ms), IPT = 2
+// above (fewer chunk sorts: island-load 4 0.1921 -> 0.1810 ms)
+constexpr int RS_T = PGA_RS_T;
 constexpr int RS_MAXTILES = 32;   // per-tile counters, then the SUS arrive / depart counters
-static_assert(pga::RANKC_MAXP <= (int64_t)RS_TILE * RS_MAXTILES, "tile counters");
+static_assert(pga::RANKC_MAXP <= (int64_t)RS_T * 2 * RS_MAXTILES, "tile counters");
 
 __device__ __forceinline__ uint64_t order_key(double x) {
     if (x == 0.0) x = 0.0;   // -0 ties +0
     return ~(uint64_t)__double_as_longlong(x);
 }
 
+template <int RS_IPT>
 __global__ void __launch_bounds__(RS_T) k_rank_sel(const double *__restrict__ L, int P,
                                                    const uint64_t *__restrict__ qtab, int32_t *__restrict__ acc,
                                                    uint32_t *ctr, int32_t *__restrict__ order,
@@ -668,6 +672,7 @@ __global__ void __launch_bounds__(RS_T) k_rank_sel(const double *__restrict__ L,
                                                    int32_t *__restrict__ sel) {
     // no early exit on the done flag: the statistics may raise it during
     // this launch (side stream), and every CTA must reach the counter
+    constexpr int RS_TILE = RS_T * RS_IPT;
     pdl_wait();
     pdl_trigger();
     __shared__ uint64_t sk[RS_T];
@@ -2072,11 +2077,18 @@ int prepare_rank_sel(pga_ctx *c) {
 }
 static int launch_rank_sel(pga_ctx *c, bool sus, cudaStream_t s) {
     const int P = (int)c->P, M = (int)(2 * ((c->P - c->p.elite + 1) / 2));
-    const unsigned nb = (unsigned)((P + RS_TILE - 1) / RS_TILE), nc = (unsigned)((P + RS_T - 1) / RS_T);
-    PGA_LAUNCH_PDL(k_rank_sel, dim3(nb, nc), dim3(RS_T), 0, s, (const double *)c->L, P,
-                   (const uint64_t *)c->rc_qtab, c->rc_acc, reinterpret_cast<uint32_t *>(c->rc_acc + c->Pcap),
-                   c->order, c->rank, sus, c->keys_in, M, c->p.seed, (uint32_t)c->p.island,
-                   (const int32_t *)&c->st->gen, c->sel);
+    const int ipt = P <= 8192 ? 1 : 2, tile = RS_T * ipt;
+    const unsigned nb = (unsigned)((P + tile - 1) / tile), nc = (unsigned)((P + RS_T - 1) / RS_T);
+    if (ipt == 1)
+        PGA_LAUNCH_PDL(k_rank_sel<1>, dim3(nb, nc), dim3(RS_T), 0, s, (const double *)c->L, P,
+                       (const uint64_t *)c->rc_qtab, c->rc_acc, reinterpret_cast<uint32_t *>(c->rc_acc + c->Pcap),
+                       c->order, c->rank, sus, c->keys_in, M, c->p.seed, (uint32_t)c->p.island,
+                       (const int32_t *)&c->st->gen, c->sel);
+    else
+        PGA_LAUNCH_PDL(k_rank_sel<2>, dim3(nb, nc), dim3(RS_T), 0, s, (const double *)c->L, P,
+                       (const uint64_t *)c->rc_qtab, c->rc_acc, reinterpret_cast<uint32_t *>(c->rc_acc + c->Pcap),
+                       c->order, c->rank, sus, c->keys_in, M, c->p.seed, (uint32_t)c->p.island,
+                       (const int32_t *)&c->st->gen, c->sel);
     return PGA_OK;
 }
 
