@@ -373,7 +373,7 @@ int capture_graph(pga_ctx *c, GExec *g, F fn) {
                 if (base + k < c->prof_ev.size() && c->prof_ev[base + k] == ev) g->evn.emplace_back(nd, k);
         }
     }
-    e = cudaGraphInstantiate(&g->x, g->g, 0);
+    e = cudaGraphInstantiate(&g->x, g->g, c->use_prio ? cudaGraphInstantiateFlagUseNodePriority : 0);
     if (e != cudaSuccess) {
         drop_graph(*g);
         return cuda_fail(e, "cudaGraphInstantiate");
@@ -496,14 +496,22 @@ int pga_create(const double *C, int32_t N, const pga_params *p, pga_ctx **out) {
         delete c;
         return rc;
     };
-    cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    // stream priorities: the side branch (mate slots, statistics, mutation
+    // masks) yields SM slots to the generation's critical path
+    int prio_lo = 0, prio_hi = 0;
+    {
+        const char *np = std::getenv("PGA_NO_PRIO");
+        if (!(np && np[0] && np[0] != '0')) cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+        c->use_prio = prio_lo != prio_hi;
+    }
+    cudaError_t e = cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio_hi);
     if (e != cudaSuccess) return bail(cuda_fail(e, "cudaStreamCreate"));
     e = cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->join_side_ev, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->fit_ev, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->stats_ev, cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_lo);
     if (e != cudaSuccess) return bail(cuda_fail(e, "cudaEventCreate"));
     const size_t cm = (size_t)c->Pcap * c->ldn, gm = (size_t)N * c->Pcap;
     int rc = 0;

@@ -138,6 +138,7 @@ struct pga_ctx {
     cudaStream_t stream = nullptr;
     cudaEvent_t join_ev = nullptr;   // joins a caller's stream to `stream` (pga_evaluate_device)
     cudaStream_t side = nullptr;     // side branch of a generation (mate slots, launch_mates_fork)
+    bool use_prio = false;           // main stream high priority, side stream low (PGA_NO_PRIO=1: off)
     cudaEvent_t fork_ev = nullptr, join_side_ev = nullptr;
     cudaEvent_t fit_ev = nullptr, stats_ev = nullptr;   // statistics on the side stream beside the selection
     pga_params p{};
