@@ -17,7 +17,9 @@
  *   orc_cluster_stats     pinned (numpy one-hot diag(Z^T C Z); closed forms)
  *   orc_log_likelihood    pinned (closed forms: pair, triple, planted block;
  *                         singleton/identity zeros; brute-force argmax)
- *                         -- parity unpinned near the c_s -> n_s^2 clamp (Q3)
+ *                         -- GPU parity unpinned near the c_s -> n_s^2 clamp
+ *                            (Q3); the clamp itself is pinned by properties
+ *                            (tests/test_oracle_fitness.py)
  *   orc_canonicalize      pinned (idempotence, first-occurrence invariants)
  *   orc_brute_force       pinned (Bell numbers 1..10)
  *   orc_select / mates    pinned (SUS worked examples S:153-155, expected-copies
