@@ -428,8 +428,24 @@ __global__ void k_mates(int64_t M, uint64_t seed, uint32_t gen, uint32_t island,
 // ---------------------------------------------------------------------------
 constexpr int SMALL_P = 4096, SMALL_T = 1024;
 
+// (ka, va) < (kb, vb) lexicographically = the 96-bit number ka:va below
+// kb:vb: the borrow out of one subtraction chain (4 instructions instead of
+// two 64-bit compares, an equality test and the index compare)
 __device__ __forceinline__ bool kv_less(uint64_t ka, uint32_t va, uint64_t kb, uint32_t vb) {
+#ifdef PGA_KV_PLAIN
     return ka < kb || (ka == kb && va < vb);
+#else
+    uint32_t r;
+    asm("{\n\t.reg .u32 t;\n\t"
+        "sub.cc.u32 t, %1, %4;\n\t"
+        "subc.cc.u32 t, %2, %5;\n\t"
+        "subc.cc.u32 t, %3, %6;\n\t"
+        "subc.u32 %0, 0, 0;\n\t}"
+        : "=r"(r)
+        : "r"(va), "r"((uint32_t)ka), "r"((uint32_t)(ka >> 32)), "r"(vb), "r"((uint32_t)kb),
+          "r"((uint32_t)(kb >> 32)));
+    return r != 0u;
+#endif
 }
 
 
@@ -886,7 +902,7 @@ constexpr int MERGE_T = 256, MERGE_MS = 64, MERGE_CAP = 2048;
 static_assert(RUN % MERGE_T == 0, "a CTA of the merge must lie in one run");
 
 __device__ __forceinline__ bool key_before(uint64_t ka, uint32_t ia, uint64_t kb, uint32_t ib) {
-    return ka < kb || (ka == kb && ia < ib);
+    return kv_less(ka, ia, kb, ib);
 }
 
 // WAY-way merge level (WAY = 2 or 4): runs of width w are merged in groups
