@@ -921,24 +921,24 @@ __global__ void __launch_bounds__(MERGE_T) k_merge_level(const uint64_t *__restr
     if (done && *done) return;
     __shared__ uint64_t sk[NSIB][CAP];
     __shared__ uint32_t si[NSIB][CAP];
-    __shared__ int64_t s_lo[NSIB], s_hi[NSIB];
+    __shared__ int s_lo[NSIB], s_hi[NSIB];   // positions fit 32 bits (P <= 2^31)
     const int tid = threadIdx.x;
-    const int64_t c0 = (int64_t)blockIdx.x * MERGE_T;
+    const int c0 = (int)blockIdx.x * MERGE_T;
     if (c0 >= P) return;
-    const int64_t g = c0 + tid;
+    const int g = c0 + tid;
     const bool valid = g < P;
-    const int64_t blk = c0 / (WAY * w) * (WAY * w);
-    const int q = (int)((c0 - blk) / w);                     // own run in the group
-    const int64_t off = c0 - blk - (int64_t)q * w + tid;
-    const int64_t last = min((int64_t)MERGE_T, P - c0) - 1;   // last valid thread
+    const int W = (int)w, blk = c0 / (WAY * W) * (WAY * W), Pi = (int)P;
+    const int q = (c0 - blk) / W;                            // own run in the group
+    const int off = c0 - blk - q * W + tid;
+    const int last = min(MERGE_T, Pi - c0) - 1;            // last valid thread
     const uint64_t ke = valid ? ks[g] : ~0ull;
     const uint32_t ie = valid ? (uint32_t)is[g] : 0xFFFFFFFFu;
-    int64_t sib[NSIB], slen[NSIB], ns[NSIB], lo[NSIB], hi[NSIB];
+    int sib[NSIB], slen[NSIB], ns[NSIB], lo[NSIB], hi[NSIB];
 #pragma unroll
     for (int j = 0; j < NSIB; ++j) {
         const int r = j < q ? j : j + 1;
-        sib[j] = blk + (int64_t)r * w;
-        slen[j] = max((int64_t)0, min(w, P - sib[j]));
+        sib[j] = blk + r * W;
+        slen[j] = max(0, min(W, Pi - sib[j]));
         ns[j] = (slen[j] + MERGE_MS - 1) / MERGE_MS;
         lo[j] = 0;
         hi[j] = slen[j];
@@ -947,7 +947,7 @@ __global__ void __launch_bounds__(MERGE_T) k_merge_level(const uint64_t *__restr
 #pragma unroll
     for (int j = 0; j < NSIB; ++j)
         if (ns[j] > 0 && ns[j] <= CAP)
-            for (int64_t t = tid; t < ns[j]; t += MERGE_T) {
+            for (int t = tid; t < ns[j]; t += MERGE_T) {
                 sk[j][t] = __ldg(ks + sib[j] + t * MERGE_MS);
                 si[j][t] = (uint32_t)__ldg(is + sib[j] + t * MERGE_MS);
             }
@@ -955,9 +955,9 @@ __global__ void __launch_bounds__(MERGE_T) k_merge_level(const uint64_t *__restr
 #pragma unroll
     for (int j = 0; j < NSIB; ++j)
         if (ns[j] > 0 && ns[j] <= CAP) {
-            int64_t a = 0, b = ns[j];                 // samples before the item
+            int a = 0, b = ns[j];                     // samples before the item
             while (a < b) {
-                const int64_t m = (a + b) >> 1;
+                const int m = (a + b) >> 1;
                 if (key_before(sk[j][m], si[j][m], ke, ie)) a = m + 1;
                 else b = m;
             }
@@ -972,26 +972,26 @@ __global__ void __launch_bounds__(MERGE_T) k_merge_level(const uint64_t *__restr
         if (tid == last) s_hi[j] = hi[j];
     }
     __syncthreads();
-    int64_t Lo[NSIB], Hi[NSIB];
+    int Lo[NSIB], Hi[NSIB];
 #pragma unroll
     for (int j = 0; j < NSIB; ++j) {
         Lo[j] = s_lo[j];
         Hi[j] = s_hi[j];
         if (!valid) lo[j] = hi[j] = Lo[j];            // beyond P: no search
         if (Hi[j] - Lo[j] <= CAP)
-            for (int64_t p = Lo[j] + tid; p < Hi[j]; p += MERGE_T) {
+            for (int p = Lo[j] + tid; p < Hi[j]; p += MERGE_T) {
                 sk[j][p - Lo[j]] = __ldg(ks + sib[j] + p);
                 si[j][p - Lo[j]] = (uint32_t)__ldg(is + sib[j] + p);
             }
     }
     __syncthreads();
-    int64_t pos = blk + off;
+    int pos = blk + off;
 #pragma unroll
     for (int j = 0; j < NSIB; ++j) {
-        int64_t l = lo[j], h = hi[j];
+        int l = lo[j], h = hi[j];
         if (Hi[j] - Lo[j] <= CAP) {
             while (l < h) {
-                const int64_t m = (l + h) >> 1;
+                const int m = (l + h) >> 1;
                 if (key_before(sk[j][m - Lo[j]], si[j][m - Lo[j]], ke, ie)) l = m + 1;
                 else h = m;
             }
@@ -999,7 +999,7 @@ __global__ void __launch_bounds__(MERGE_T) k_merge_level(const uint64_t *__restr
             const uint64_t *k_g = ks + sib[j];
             const int32_t *i_g = is + sib[j];
             while (l < h) {
-                const int64_t m = (l + h) >> 1;
+                const int m = (l + h) >> 1;
                 if (key_before(__ldg(k_g + m), (uint32_t)__ldg(i_g + m), ke, ie)) l = m + 1;
                 else h = m;
             }
