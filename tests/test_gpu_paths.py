@@ -93,13 +93,15 @@ def test_generation_lockstep_wide_N(pga, orc):
 
 @pytest.mark.parametrize("path", ["rank_count", "cluster_or_sort"])
 @pytest.mark.parametrize("P,sel,scal,E", [(1025, 0, 0, 10), (1500, 0, 1, 7), (4096, 1, 0, 10),
-                                          (8192, 0, 0, 10), (16384, 0, 1, 0), (16383, 0, 0, 10)])
+                                          (8192, 0, 0, 10), (16384, 0, 1, 0), (16383, 0, 0, 10),
+                                          (20001, 0, 0, 10), (20000, 0, 1, 10)])
 def test_generation_lockstep_cluster_select(pga, orc, P, sel, scal, E, path, monkeypatch):
     """1024 < P <= 16384: order, scaling and selection by rank counting in
     one launch (k_rank_sel: chunk sorts + binary searches, per-tile
     finalisers, fused SUS; the default there) or, with PGA_NO_RANKC=1, in
     one thread-block-cluster launch (k_select_cluster, P <= 8192) / the run
-    sort + merge tree (P > 8192).
+    sort + merge tree (P > 8192); P > 16384: the run sort + merge tree on
+    both (path is then moot).
     Generations in lockstep with the oracle's operators: bit-exact
     populations given the GPU's L and top, for SUS RANK / NONE and
     tournament, ragged P, E = 0 (M = P + 1 for odd P - E)."""
