@@ -695,6 +695,7 @@ struct SparseArgs {
     uint32_t cc_mask;             // slots - 1
     uint32_t *cc_state;           // [0] fill, [1] clear request, [2] CTA count, [3] clears done
     const uint64_t *cc_keys;      // [N][2] Zobrist keys
+    uint32_t stage_off;           // != 0: keys and fixed-point diagonal staged in shared memory at this offset
 };
 
 __host__ __device__ __forceinline__ int sp_words(int N) { return (N + 2) / 2; }   // packed u16 counters for labels 0..N
@@ -718,6 +719,25 @@ static size_t sparse_smem(int N) {
     const size_t warps = (size_t)sp_warps(N) * sp_per_warp(N) + 64;
     const size_t tile = (size_t)N * (pga::CB + 2) * sizeof(uint16_t);   // dense-block transpose
     return warps > tile ? warps : tile;
+}
+
+// Staged per CTA after the warps' tables (when it costs no occupancy): the
+// Zobrist keys (16 B per gene) and the fixed-point diagonal (8 B per gene),
+// read by every cacheable gene's XOR and every walked / triple cluster.
+static size_t sparse_stage_off(int N) { return ((size_t)sp_warps(N) * sp_per_warp(N) + 64 + 15) & ~(size_t)15; }
+static size_t sparse_smem_staged(int N) {
+    const size_t st = sparse_stage_off(N) + 24 * (size_t)N;
+    const size_t base = sparse_smem(N);
+    return st > base ? st : base;
+}
+static bool sparse_stage_ok(int N) {
+    if (std::getenv("PGA_NO_SP_STAGE")) return false;
+    const size_t smem_sm = 228 * 1024, per_cta_extra = 1024, max_cta = 227 * 1024;
+    const size_t a = sparse_smem(N), b = sparse_smem_staged(N);
+    if (b > max_cta) return false;
+    if ((size_t)N * (pga::CB + 2) * sizeof(uint16_t) > sparse_stage_off(N)) return false;   // transpose tile
+    const size_t ca = std::min<size_t>(2, smem_sm / (a + per_cta_extra)), cb = std::min<size_t>(2, smem_sm / (b + per_cta_extra));
+    return cb >= ca;
 }
 
 template <int LREG, int SPW>
@@ -757,6 +777,14 @@ __global__ void __launch_bounds__(SPW * 32, SPW == 16 ? PGA_SP_MINB : 1) k_fitne
     const bool cc_clear = a.cc && *reinterpret_cast<volatile uint32_t *>(a.cc_state + 1) != 0u;
     const bool use_cache = a.cc && !cc_clear;
     if (tid == 0) s_maxp = 0u;
+    const bool stage = a.stage_off != 0u;
+    uint4 *skeys = reinterpret_cast<uint4 *>(sps + a.stage_off);
+    long long *sdfx = reinterpret_cast<long long *>(skeys + N);
+    if (stage) {
+        if (a.cc)
+            for (int i = tid; i < N; i += SP_T) skeys[i] = __ldg(reinterpret_cast<const uint4 *>(a.cc_keys) + i);
+        for (int i = tid; i < N; i += SP_T) sdfx[i] = __double2ll_rn(__ldg(a.diag + i) * a.fx_scale);
+    }
     __syncthreads();
     if (!skip1) {
 
@@ -933,9 +961,13 @@ __global__ void __launch_bounds__(SPW * 32, SPW == 16 ? PGA_SP_MINB : 1) k_fitne
                 npair += 1;
             } else {
                 const int g2 = mem[SMALL_N * sl + 2];
+                const long long dsum =
+                    stage ? sdfx[g0] + sdfx[g1] + sdfx[g2]
+                          : __double2ll_rn(__ldg(a.diag + g0) * a.fx_scale) +
+                                __double2ll_rn(__ldg(a.diag + g1) * a.fx_scale) +
+                                __double2ll_rn(__ldg(a.diag + g2) * a.fx_scale);
                 const long long acc =
-                    __double2ll_rn(__ldg(a.diag + g0) * a.fx_scale) + __double2ll_rn(__ldg(a.diag + g1) * a.fx_scale) +
-                    __double2ll_rn(__ldg(a.diag + g2) * a.fx_scale) +
+                    dsum +
                     2 * (__double2ll_rn(__ldg(C + (size_t)g0 * a.ldc + g1) * a.fx_scale) +
                          __double2ll_rn(__ldg(C + (size_t)g0 * a.ldc + g2) * a.fx_scale) +
                          __double2ll_rn(__ldg(C + (size_t)g1 * a.ldc + g2) * a.fx_scale));
@@ -966,7 +998,7 @@ __global__ void __launch_bounds__(SPW * 32, SPW == 16 ? PGA_SP_MINB : 1) k_fitne
                 if ((om & 0xA000u) == 0x2000u) {
                     const uint32_t o = om & 0x1FFFu;
                     uint32_t *h = (lane & 1) ? cent2 + 4 * o : reinterpret_cast<uint32_t *>(cent + o);
-                    const uint4 kk = __ldg(keys4 + i);
+                    const uint4 kk = stage ? skeys[i] : __ldg(keys4 + i);
                     atomicXor(h, kk.x);
                     atomicXor(h + 1, kk.y);
                     atomicXor(h + 2, kk.z);
@@ -1054,7 +1086,7 @@ __global__ void __launch_bounds__(SPW * 32, SPW == 16 ? PGA_SP_MINB : 1) k_fitne
                 const int av = t - st;
                 if (av == 0) npair += (uint32_t)(n * (n - 1) / 2);   // C pairs gathered, once per cluster
                 const double *Cg = C + (size_t)g * a.ldc;
-                acc = __double2ll_rn(__ldg(a.diag + g) * a.fx_scale);
+                acc = stage ? sdfx[g] : __double2ll_rn(__ldg(a.diag + g) * a.fx_scale);
                 const int h = (n - 1) >> 1;
                 int bidx = av;
 #pragma unroll 4
@@ -1282,10 +1314,12 @@ int prepare_fitness(int N) {
                                   (int)fitness_smem(N)));
     if (N <= SPARSE_SMALLN)
         PGA_CUDA(cudaFuncSetAttribute(k_fitness_sparse<SPARSE_SMALLN / 64, 16>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sparse_smem(N)));
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(sparse_stage_ok(N) ? sparse_smem_staged(N) : sparse_smem(N))));
     else if (N <= SPARSE_MAXN)
         PGA_CUDA(cudaFuncSetAttribute(k_fitness_sparse<SPARSE_MAXN / 64, 8>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sparse_smem(N)));
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(sparse_stage_ok(N) ? sparse_smem_staged(N) : sparse_smem(N))));
     return PGA_OK;
 }
 
@@ -1361,12 +1395,15 @@ int launch_fitness_range(pga_ctx *c, const FitBufs &b, int64_t begin, int64_t en
         sp.cc_mask = c->cc_mask;
         sp.cc_state = c->cc_state;
         sp.cc_keys = c->cc_keys;
+        const bool stg = sparse_stage_ok(N);
+        sp.stage_off = stg ? (uint32_t)sparse_stage_off(N) : 0u;
+        const size_t sp_smem = stg ? sparse_smem_staged(N) : sparse_smem(N);
         if (N <= SPARSE_SMALLN)
             PGA_LAUNCH_PDL(k_fitness_sparse<SPARSE_SMALLN / 64, 16>, dim3((unsigned)a.nCB), dim3(16 * 32),
-                           sparse_smem(N), s, sp);
+                           sp_smem, s, sp);
         else
             PGA_LAUNCH_PDL(k_fitness_sparse<SPARSE_MAXN / 64, 8>, dim3((unsigned)a.nCB), dim3(8 * 32),
-                           sparse_smem(N), s, sp);
+                           sp_smem, s, sp);
         a.sflag = c->sflag;
     }
     if (ev) PGA_CUDA(prof_record(ev[1], s));   // dense kernel starts here
