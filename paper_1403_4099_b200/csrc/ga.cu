@@ -898,7 +898,10 @@ k_sort_runs(const double *__restrict__ L, int64_t P, uint64_t *keys, int32_t *id
 // shared memory and each item finishes its search there.  Spans too large
 // to stage fall back to searches in global memory.  The result is the same
 // permutation as a plain per-item binary search.
-constexpr int MERGE_T = 256, MERGE_MS = 64, MERGE_CAP = 2048;
+#ifndef PGA_MERGE_T
+#define PGA_MERGE_T 256
+#endif
+constexpr int MERGE_T = PGA_MERGE_T, MERGE_MS = 64, MERGE_CAP = 2048;
 static_assert(RUN % MERGE_T == 0, "a CTA of the merge must lie in one run");
 
 __device__ __forceinline__ bool key_before(uint64_t ka, uint32_t ia, uint64_t kb, uint32_t ib) {
@@ -1898,7 +1901,7 @@ static int sort_order(const double *L, int64_t P, int32_t *order, int32_t *rank,
     uint64_t *kA = keys_out, *kB = keys_in;
     int32_t *iA = idx_in, *iB = idx_tmp;
     PGA_LAUNCH_PDL(k_sort_runs, dim3(nruns), dim3(RUN_T), 0, s, L, P, kA, iA, done);
-    const unsigned nb = (unsigned)((P + 255) / 256);
+    const unsigned nb = (unsigned)((P + MERGE_T - 1) / MERGE_T);
     if (nruns == 1) {   // one run: copy its indices out through a width-P "merge"
         PGA_LAUNCH_PDL(k_merge_level<2>, dim3(nb), dim3(MERGE_T), 0, s, (const uint64_t *)kA, (const int32_t *)iA,
                        P, P, (uint64_t *)nullptr, order, rank, done);
