@@ -1,0 +1,9 @@
+# run length 256 / 512 / 1024 (default) for the C4 order sort
+O=gpurun_out/r03x; mkdir -p $O
+PGA_LIB=paper_1403_4099_b200/libpga_r256.so timeout 900 python -m pytest tests/test_gpu_paths.py tests/test_gpu_parity.py -q -x -k "cluster_select or op_select" > $O/pytest_r256.log 2>&1; echo "rc=$?" >> $O/pytest_r256.log
+for r in 1 2 3; do
+  for v in base r512 r256; do
+    L=paper_1403_4099_b200/libpga.so; [ $v != base ] && L=paper_1403_4099_b200/libpga_$v.so
+    PGA_LIB=$L timeout 300 python bench.py --steps 100 --warmup 5 --no-cpu --no-e2e > $O/c4_${v}_$r.json 2>> $O/bench.err
+  done
+done
