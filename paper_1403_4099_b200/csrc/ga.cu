@@ -673,7 +673,7 @@ __device__ __forceinline__ void cs_exchange(uint64_t &k, uint32_t &v, int partne
 // above (fewer chunk sorts: island-load 4 0.1921 -> 0.1810 ms)
 constexpr int RS_T = PGA_RS_T;
 constexpr int RS_MAXTILES = 32;   // per-tile counters, then the SUS arrive / depart counters
-static_assert(pga::RANKC_MAXP <= (int64_t)RS_T * 2 * RS_MAXTILES, "tile counters");
+static_assert(pga::RANKC_MAXP <= (int64_t)RS_T * RS_MAXTILES, "tile counters");
 
 __device__ __forceinline__ uint64_t order_key(double x) {
     if (x == 0.0) x = 0.0;   // -0 ties +0

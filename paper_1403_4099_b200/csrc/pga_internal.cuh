@@ -89,7 +89,7 @@ constexpr int CB = 32;         // chromosomes per fitness CTA tile (one per lane
 constexpr int LN_TAB = 128;    // table-driven log: c_j = 1 + (j + 1/2) / 128
 constexpr int SPARSE_MAX_N = 2048;   // largest N with a label-sparse pass (cluster cache, pair table)
 // rank + selection in one launch (k_rank_sel) for 1024 < P <= RANKC_MAXP
-constexpr int64_t RANKC_MAXP = 16384;
+constexpr int64_t RANKC_MAXP = 8192;   // above it the run sort + merge tree is as fast (island-load 4: 0.1755 vs 0.1763 ms)
 
 // Cluster-cache slot (k_fitness_sparse): exact fixed-point c_s of a member
 // set keyed by two 64-bit Zobrist words; k1 == 0 empty; chk validates.

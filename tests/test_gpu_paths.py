@@ -96,12 +96,11 @@ def test_generation_lockstep_wide_N(pga, orc):
                                           (8192, 0, 0, 10), (16384, 0, 1, 0), (16383, 0, 0, 10),
                                           (20001, 0, 0, 10), (20000, 0, 1, 10)])
 def test_generation_lockstep_cluster_select(pga, orc, P, sel, scal, E, path, monkeypatch):
-    """1024 < P <= 16384: order, scaling and selection by rank counting in
+    """1024 < P <= 8192: order, scaling and selection by rank counting in
     one launch (k_rank_sel: chunk sorts + binary searches, per-tile
     finalisers, fused SUS; the default there) or, with PGA_NO_RANKC=1, in
-    one thread-block-cluster launch (k_select_cluster, P <= 8192) / the run
-    sort + merge tree (P > 8192); P > 16384: the run sort + merge tree on
-    both (path is then moot).
+    one thread-block-cluster launch (k_select_cluster); P > 8192: the run
+    sort + merge tree on both (path is then moot).
     Generations in lockstep with the oracle's operators: bit-exact
     populations given the GPU's L and top, for SUS RANK / NONE and
     tournament, ragged P, E = 0 (M = P + 1 for odd P - E)."""
@@ -130,7 +129,7 @@ def test_generation_lockstep_cluster_select(pga, orc, P, sel, scal, E, path, mon
 @pytest.mark.parametrize("path", ["rank_count", "cluster_or_sort"])
 @pytest.mark.parametrize("P,kind", [(2048, "identical"), (5000, "singletons"), (12000, "two_values")])
 def test_generation_lockstep_selection_ties(pga, orc, P, kind, path, monkeypatch):
-    """Selection with massive L ties (1024 < P <= 16384): every individual
+    """Selection with massive L ties (1024 < P <= 16384; k_rank_sel up to 8192): every individual
     the same chromosome (all L equal), every individual all singletons (L =
     0 everywhere: the sort key equals the padding key of k_rank_sel's
     chunks), or two distinct chromosomes alternating.  The order must break
