@@ -540,7 +540,7 @@ def main():
                             "note": "SURVEY §8(f) f2: blocks of 32 chromosomes whose clusters need <= 25% "
                                     "of the dense pair updates (automatic threshold with the cluster "
                                     "cache on) are evaluated label-sparsely and skipped by k_fitness; "
-                                    "clusters of >= 5 genes come from the cluster cache when an earlier "
+                                    "clusters of >= 4 genes come from the cluster cache when an earlier "
                                     "generation had the same member set, the rest are gathered from L2"},
             "phase_ms_per_generation": {("stats_order_selection" if k == "stats" else k): round(v, 4)
                                         for k, v in phases.items() if k != "fitness_fold_fused"},
