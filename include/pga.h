@@ -271,7 +271,7 @@ int pga_set_sparse_threshold(pga_ctx *ctx, double theta);
  * (Eq. 6) depends only on the member set of cluster s, and a GA generation
  * repeats almost every cluster of the one before (elites are copied,
  * knowledge-based crossover transplants whole clusters, mutation moves a
- * few genes).  Clusters with at least 5 members are keyed by two 64-bit
+ * few genes).  Clusters with at least 4 members are keyed by two 64-bit
  * Zobrist sums of their members plus n_s, and their exact 64-bit
  * fixed-point c_s is kept in a device hash table (64 slots per chromosome,
  * 2^12..2^22 slots of 32 B; cleared by the pass itself when half full).  A
