@@ -1,5 +1,5 @@
 # Round-2 bench lines and captures -> gpurun_out/final/
-O=gpurun_out/final9; mkdir -p $O
+O=gpurun_out/final10; mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/smi.txt 2>&1
 for c in C1 C2 C3; do
   timeout 600 python bench.py --config $c --steps 500 --warmup 5 > $O/bench_$c.json 2> $O/bench_$c.err
