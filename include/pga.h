@@ -274,7 +274,7 @@ int pga_set_sparse_threshold(pga_ctx *ctx, double theta);
  * few genes).  Clusters with at least 4 members are keyed by two 64-bit
  * Zobrist sums of their members plus n_s, and their exact 64-bit
  * fixed-point c_s is kept in a device hash table (64 slots per chromosome,
- * PGA_CC_PER overrides; 2^12..2^23 slots of 32 B; cleared by the pass itself when half full).  A
+ * PGA_CC_PER overrides; 2^12..2^22 slots of 32 B; cleared by the pass itself when half full).  A
  * hit replaces the cluster's n_s(n_s-1)/2 gathers.  Results are
  * bit-identical with the cache on or off (a wrong hit needs a 128-bit key
  * collision).  on: 0 = off, else on.  Host only. */

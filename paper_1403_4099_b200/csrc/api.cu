@@ -527,15 +527,19 @@ int pga_create(const double *C, int32_t N, const pga_params *p, pga_ctx **out) {
     if (!rc && cudaMemset(c->sp_blocks, 0, 4 * sizeof(unsigned long long)) != cudaSuccess)
         rc = fail(PGA_EDEVICE, "memset sp_blocks");
     if (!rc && N <= SPARSE_MAX_N) {
-        // cluster cache: 2^12 .. 2^23 slots (32 B each)
+        // cluster cache: 2^12 .. 2^22 slots (32 B each; 2^23 with PGA_CC_PER)
         uint32_t slots = 1u << 12;
         // 64 slots per chromosome (C4: 2^22 slots): fewer clears up to a few
         // hundred generations (20: 0.479 vs 0.498 ms, 100: 0.4666 vs 0.4698
         // against 32); 32 (2^21 slots, L2-resident) wins on long runs (1000
         // generations: 0.5238 vs 0.5420).  PGA_CC_PER overrides.
         int64_t per = 64;
-        if (const char *e = std::getenv("PGA_CC_PER")) per = std::max<int64_t>(1, std::atoll(e));
-        while (slots < (1u << 23) && (int64_t)slots < per * c->P) slots <<= 1;
+        uint32_t cap = 1u << 22;
+        if (const char *e = std::getenv("PGA_CC_PER")) {
+            per = std::max<int64_t>(1, std::atoll(e));
+            cap = 1u << 23;
+        }
+        while (slots < cap && (int64_t)slots < per * c->P) slots <<= 1;
         c->cc_mask = slots - 1u;
         rc = rc ? rc : dalloc(&c->cc, (size_t)slots);
         rc = rc ? rc : dalloc(&c->cc_state, (size_t)4);
